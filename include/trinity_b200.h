@@ -1,0 +1,127 @@
+/*
+ * trinity_b200.h -- C-ABI of the B200-native Trinity vector-search pool.
+ *
+ * Plain pointers and sizes only.  Each entry point replaces one reference
+ * interface (citations are path:line under the reference's pkg/src/trinity/);
+ * the reference is pure Python, so the "FFI" a maintainer binds is ctypes --
+ * see INTEGRATION.md for the binding and for the Python shim that keeps the
+ * reference's API (paper_2512_02281_b200/).
+ *
+ * Status codes: TRI_OK, TRI_EINVAL (-> ValueError: bad shape / k / dim /
+ * non-finite input, the reference's ann_graph.py:131-134, engine.py:158-163),
+ * TRI_EINTERNAL (-> RuntimeError: internal consistency, engine.py:196-198,
+ * 249-250), TRI_ECUDA (CUDA failure).  tri_last_error() returns the message of
+ * the calling thread's last failure.
+ *
+ * Handles own their device memory.  Functions without the _dev suffix take
+ * HOST buffers and synchronise the stream before returning; _dev functions
+ * take DEVICE buffers (per-query k / nprobe stay host arrays) and are
+ * asynchronous on `stream` (NULL = the handle's own stream).  A handle is
+ * single-owner: the reference's engine is a single-owner stepper
+ * (engine.py:313-319) and so is every handle here.
+ *
+ * Numerics: returned distances are float64 squared L2 computed in the
+ * reference's exact operation order (bit-identical to
+ * ann_graph.rowwise_sq_dists); ids are ordered by (dist, id) as
+ * ann_graph.py:136.  Candidates are generated in fp32 and certified (see
+ * DESIGN.md); uncertified queries are recomputed exactly on the device.
+ */
+#ifndef TRINITY_B200_H
+#define TRINITY_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TRI_OK 0
+#define TRI_EINVAL 1
+#define TRI_EINTERNAL 2
+#define TRI_ECUDA 3
+
+#define TRI_MAX_K 1638 /* largest k (or nprobe) the device path accepts */
+
+typedef struct tri_store tri_store;
+typedef struct tri_ivf tri_ivf;
+
+/* Library ------------------------------------------------------------------ */
+const char* tri_last_error(void);
+int tri_version(void);
+int tri_device_count(int32_t* count);
+/* Debug/test knobs: "force_fixup" (1 = treat every query as uncertified),
+ * "kp_extra" (extra over-fetch added to k). */
+int tri_set_option(const char* name, int64_t value);
+
+/* Vector store: replaces ann_graph.VectorStore (ann_graph.py:21-48).
+ * x is n x d row-major float32 on the host; no float64 copy is kept. */
+int tri_store_create(const float* x, int64_t n, int32_t d, int32_t device, tri_store** out);
+int tri_store_destroy(tri_store* s);
+int tri_store_info(const tri_store* s, int64_t* n, int32_t* d, double* max_norm);
+/* Global id of row 0 (shards of a larger database). */
+int tri_store_set_id_offset(tri_store* s, int64_t id_offset);
+
+/* Exact kNN: replaces ann_graph.brute_force_knn (ann_graph.py:124-137),
+ * batched with a per-query k.  q: B x d float64.  Outputs B x ldo, row i holds
+ * k[i] results sorted by (dist, id). */
+int tri_knn_bruteforce(tri_store* s, const double* q, int32_t B, const int32_t* k, int32_t ldo, int64_t* ids,
+                       double* dists, void* stream);
+int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32_t* k, int32_t ldo, int64_t* ids,
+                           double* dists, void* stream);
+
+/* Row distances: replaces ann_graph.rowwise_sq_dists (ann_graph.py:97-105)
+ * for the rows of the store named by `rows` (host buffers). */
+int tri_rowwise_sq_dists(tri_store* s, const double* q, const int64_t* rows, int64_t n, double* out, void* stream);
+
+/* Fixed-shape distance batch: replaces engine.execute_distance_batch
+ * (engine.py:229-256).  Task i pairs query row owner[i] of `queries`
+ * (n_queries x d float64) with store row cand[i]; returns TRI_EINTERNAL if a
+ * candidate is out of range (engine.py:249-250).  Host buffers. */
+int tri_distance_tasks(tri_store* s, const int32_t* owner, const int64_t* cand, int32_t n_tasks,
+                       const double* queries, int32_t n_queries, double* out, void* stream);
+
+/* IVF-Flat (new component; the reference has no IVF).
+ * train: GPU Lloyd k-means from the host-chosen init rows, `iters` updates.
+ * create: from a shared artifact (fp32 centroids + the list id of each row),
+ * `id_offset` = global id of the store's row 0 (shards). */
+int tri_ivf_train(tri_store* s, int32_t nlist, int32_t iters, const int64_t* init_rows, tri_ivf** out);
+int tri_ivf_create(tri_store* s, const float* centroids, int32_t nlist, const int32_t* assign, int64_t id_offset,
+                   tri_ivf** out);
+int tri_ivf_destroy(tri_ivf* v);
+int tri_ivf_info(const tri_ivf* v, int32_t* nlist, int64_t* n, int32_t* d);
+/* centroids: nlist x d float32; assign: n int32 (either may be NULL). */
+int tri_ivf_export(tri_ivf* v, float* centroids, int32_t* assign);
+int tri_ivf_list_sizes(tri_ivf* v, int64_t* sizes);
+
+/* Ragged batched IVF search: query i wants k[i] results over its nprobe[i]
+ * closest lists (coarse step = exact kNN over the centroids).  This is the
+ * continuous-batch entry: prefill (large k / nprobe) and decode (small)
+ * queries share one launch sequence.  Outputs B x ldo; rows shorter than
+ * k[i] (probed lists hold fewer vectors) are padded with id -1. */
+int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe, int32_t ldo,
+                   int64_t* ids, double* dists, void* stream);
+int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe,
+                       int32_t ldo, int64_t* ids, double* dists, void* stream);
+/* Probed list ids of the last search (B x ld, host), for inspection. */
+int tri_ivf_last_probes(tri_ivf* v, int64_t* probes, int32_t ld);
+/* Queries of the last search that needed the exact fix-up (host int). */
+int tri_ivf_last_fixups(tri_ivf* v, int32_t* n);
+int tri_store_last_fixups(tri_store* s, int32_t* n);
+/* Profiling: when enabled, CUDA events bracket the list-scan kernel. */
+int tri_ivf_set_profiling(tri_ivf* v, int32_t on);
+int tri_ivf_scan_time(tri_ivf* v, double* total_ms, int32_t* launches);
+/* Algorithmic bytes of the last search's list scan: every probed list read
+ * once (d*4 + 4 bytes per vector).  Also returns the number of scanned
+ * (query, vector) pairs. */
+int tri_ivf_last_scan_bytes(tri_ivf* v, int64_t* bytes, int64_t* pairs);
+
+/* Exact merge of G per-shard result lists (device buffers, G x B x k_in,
+ * id -1 = empty) into the global top-k_out by (dist, id). */
+int tri_merge_topk(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t k_out,
+                   double* out_dists, int64_t* out_ids, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRINITY_B200_H */

@@ -1,0 +1,215 @@
+"""CPU oracle for the Trinity vector-search hot path.
+
+TEST INFRASTRUCTURE ONLY.  Nothing in ``paper_2512_02281_b200`` imports this
+module; only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may call it, and only as the
+checker or as the timed CPU baseline -- never as the product path.
+
+It restates, in numpy, the reference's algorithm for the path named by
+BASELINE.json (citations are ``path:line`` under the read-only reference
+``pkg/src/trinity/``):
+
+* ``sq_dists``            <- ``ann_graph.rowwise_sq_dists``  (ann_graph.py:97-105)
+* ``pair_distance``       <- ``ann_graph.distance``          (ann_graph.py:113-121)
+* ``exact_knn``           <- ``ann_graph.brute_force_knn``   (ann_graph.py:124-137)
+* ``ivf_search``          <- composition of the two above: the
+  reference has no IVF, so the IVF oracle is built from its primitives with the
+  same (dist, id) tie semantics.
+* ``merge_shards``        <- (dist, id) lexicographic merge, the tie rule of
+  ann_graph.py:8-9 applied to per-shard lists.
+
+Parity pin: ``tests/golden/`` holds vectors produced by importing the reference
+itself (``tests/golden/make_golden.py``); ``tests/test_oracle_golden.py`` checks
+this module against them bit-for-bit.
+
+Summation order.  The reference's distance is ``np.einsum("ij,ij->i", diff,
+diff)`` on float64.  numpy evaluates that contraction with its SSE2 baseline
+kernel: two float64 lanes, the row walked in blocks of 8 elements whose four
+2-lane sub-blocks are accumulated in *reverse* order, unfused multiply then
+add, a 2-lane tail, and finally ``lane0 + lane1``.  ``sq_dist_scalar_order``
+spells that order out in pure Python; the CUDA re-rank kernel implements the
+same order, which is why GPU distances are bit-identical to the reference's.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+# ----------------------------------------------------------------------------
+# distances
+
+
+def sq_dists(query64: np.ndarray, rows64: np.ndarray) -> np.ndarray:
+    """Squared L2 from one float64 query to each float64 row (ann_graph.py:97-105)."""
+    delta = query64 - rows64
+    return np.einsum("ij,ij->i", delta, delta)
+
+
+def sq_dist_scalar_order(q64, x64) -> float:
+    """The exact float64 operation order numpy's einsum uses for one row.
+
+    Slow pure-Python statement of the order the GPU re-rank kernel follows
+    (see module docstring); used by tests to pin that order against numpy.
+    """
+    d = len(q64)
+    lane = [0.0, 0.0]
+    i = 0
+    while d - i >= 8:
+        for sub in (3, 2, 1, 0):
+            for ln in (0, 1):
+                t = float(q64[i + 2 * sub + ln]) - float(x64[i + 2 * sub + ln])
+                lane[ln] = t * t + lane[ln]
+        i += 8
+    while i < d:
+        for ln in (0, 1):
+            if i + ln < d:
+                t = float(q64[i + ln]) - float(x64[i + ln])
+                lane[ln] = t * t + lane[ln]
+        i += 2
+    return lane[0] + lane[1]
+
+
+def pair_distance(a, b) -> float:
+    """Checked single-pair squared distance (ann_graph.py:113-121)."""
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    if a.shape != b.shape:
+        raise ValueError(f"dimension mismatch: {a.shape} vs {b.shape}")
+    if not (np.isfinite(a).all() and np.isfinite(b).all()):
+        raise ValueError("vectors must be finite")
+    return float(sq_dists(a, b.reshape(1, -1))[0])
+
+
+def _chunked_sq_dists(q64: np.ndarray, data32: np.ndarray, rows=None, chunk: int = 65536) -> np.ndarray:
+    """sq_dists over (a subset of) a float32 matrix without a full float64 copy.
+
+    Equal bit-for-bit to one big call: the reference's per-row reduction does
+    not depend on how many rows share the call (ann_graph.py:98-103).
+    """
+    n = data32.shape[0] if rows is None else len(rows)
+    out = np.empty(n, dtype=np.float64)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        block = data32[s:e] if rows is None else data32[rows[s:e]]
+        out[s:e] = sq_dists(q64, block.astype(np.float64))
+    return out
+
+
+def _lex_topk(dists: np.ndarray, ids: np.ndarray, k: int):
+    """k smallest by (dist, id), the rule of ann_graph.py:136."""
+    order = np.lexsort((ids, dists))[:k]
+    return ids[order].astype(np.int64), dists[order]
+
+
+# ----------------------------------------------------------------------------
+# exact kNN
+
+
+def exact_knn(data32: np.ndarray, query, k: int):
+    """brute_force_knn restated (ann_graph.py:124-137): (ids int64[k], dists f64[k])."""
+    q = np.asarray(query, dtype=np.float64).ravel()
+    n, d = data32.shape
+    if q.shape[0] != d:
+        raise ValueError(f"query dim {q.shape[0]} != store dim {d}")
+    if not 1 <= k <= n:
+        raise ValueError(f"k must be in [1, {n}], got {k}")
+    dists = _chunked_sq_dists(q, data32)
+    return _lex_topk(dists, np.arange(n, dtype=np.int64), k)
+
+
+def exact_knn_batch(data32: np.ndarray, queries, ks):
+    """exact_knn per row of ``queries``; ``ks`` is an int or one k per query."""
+    queries = np.asarray(queries)
+    ks = np.broadcast_to(np.asarray(ks, dtype=np.int64), (queries.shape[0],))
+    return [exact_knn(data32, queries[i], int(ks[i])) for i in range(queries.shape[0])]
+
+
+# ----------------------------------------------------------------------------
+# IVF-Flat (composed from the reference primitives)
+
+
+class IVFArtifact:
+    """Shared index artifact: fp32 centroids + the list id of every vector.
+
+    The GPU index and this oracle consume the same artifact, so parity checks
+    isolate search from training.  Lists hold global ids in ascending order.
+    """
+
+    def __init__(self, centroids: np.ndarray, assign: np.ndarray):
+        self.centroids = np.ascontiguousarray(centroids, dtype=np.float32)
+        self.assign = np.ascontiguousarray(assign, dtype=np.int32)
+        nlist = self.centroids.shape[0]
+        order = np.argsort(self.assign, kind="stable")
+        counts = np.bincount(self.assign, minlength=nlist)
+        self.offsets = np.zeros(nlist + 1, dtype=np.int64)
+        np.cumsum(counts, out=self.offsets[1:])
+        self.list_ids = order.astype(np.int64)  # ascending id inside every list
+
+    @property
+    def nlist(self) -> int:
+        return self.centroids.shape[0]
+
+    def members(self, lst: int) -> np.ndarray:
+        return self.list_ids[self.offsets[lst]:self.offsets[lst + 1]]
+
+
+def coarse_probe(art: IVFArtifact, query, nprobe: int) -> np.ndarray:
+    """Probed list ids: brute_force_knn over the centroids (ann_graph.py:124-137)."""
+    ids, _ = exact_knn(art.centroids, query, nprobe)
+    return ids
+
+
+def ivf_search(data32: np.ndarray, art: IVFArtifact, query, k: int, nprobe: int):
+    """Exact top-k over the union of the nprobe closest lists.
+
+    Coarse step = brute_force_knn over centroids; fine step = the probed
+    lists' ids in ascending order, rowwise_sq_dists, then lexsort by
+    (dist, id) -- identical tie semantics to ann_graph.py:136.  Returns fewer
+    than k results when the probed lists hold fewer than k vectors.
+    """
+    q = np.asarray(query, dtype=np.float64).ravel()
+    probes = coarse_probe(art, q, nprobe)
+    cand = np.sort(np.concatenate([art.members(int(p)) for p in probes]))
+    if cand.size == 0:
+        return np.empty(0, np.int64), np.empty(0, np.float64)
+    dists = _chunked_sq_dists(q, data32, rows=cand)
+    return _lex_topk(dists, cand, min(k, cand.size))
+
+
+def kmeans(data32: np.ndarray, nlist: int, iters: int, seed: int):
+    """Small Lloyd k-means used to make CPU-test artifacts (no reference exists).
+
+    Centroids start from a seeded sample of rows; empty clusters keep their
+    previous centroid.  Not the GPU trainer -- only an artifact source.
+    """
+    rng = np.random.Generator(np.random.Philox(seed))
+    n = data32.shape[0]
+    cent = data32[np.sort(rng.choice(n, size=nlist, replace=False))].astype(np.float64)
+    x64 = data32.astype(np.float64)
+    xn = np.einsum("ij,ij->i", x64, x64)
+    assign = np.zeros(n, dtype=np.int32)
+    for _ in range(iters + 1):
+        cn = np.einsum("ij,ij->i", cent, cent)
+        d = xn[:, None] + cn[None, :] - 2.0 * (x64 @ cent.T)
+        assign = np.argmin(d, axis=1).astype(np.int32)
+        if _ == iters:
+            break
+        sums = np.zeros_like(cent)
+        np.add.at(sums, assign, x64)
+        cnt = np.bincount(assign, minlength=nlist)
+        nz = cnt > 0
+        cent[nz] = sums[nz] / cnt[nz, None]
+    return IVFArtifact(cent.astype(np.float32), assign)
+
+
+# ----------------------------------------------------------------------------
+# shard merge
+
+
+def merge_shards(parts, k: int):
+    """Merge per-shard (ids, dists) lists into the global top-k by (dist, id)."""
+    ids = np.concatenate([np.asarray(p[0], dtype=np.int64) for p in parts])
+    dists = np.concatenate([np.asarray(p[1], dtype=np.float64) for p in parts])
+    keep = ids >= 0
+    ids, dists = ids[keep], dists[keep]
+    return _lex_topk(dists, ids, min(k, ids.size))

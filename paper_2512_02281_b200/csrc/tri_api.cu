@@ -1,0 +1,1088 @@
+// C-ABI of libtrinity_b200: handles, host-side planning and launch sequences.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/trinity_b200.h"
+#include "tri_internal.h"
+
+using namespace tri;
+
+namespace {
+
+thread_local std::string g_err;
+long long g_force_fixup = 0;
+long long g_kp_extra = 0;
+constexpr int kSmemLimit = 225 * 1024;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(TRI_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+#define TRY(expr)            \
+  do {                       \
+    int _rc = (expr);        \
+    if (_rc != TRI_OK) return _rc; \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+int ensure(DevBuf& b, size_t bytes) {
+  if (bytes <= b.cap && b.p) return TRI_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+  CU(cudaMalloc(&b.p, want));
+  b.cap = want;
+  return TRI_OK;
+}
+
+void release(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+int ensure_host(HostBuf& b, size_t bytes) {
+  if (bytes <= b.cap && b.p) return TRI_OK;
+  if (b.p) cudaFreeHost(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+  CU(cudaMallocHost(&b.p, want));
+  b.cap = want;
+  return TRI_OK;
+}
+
+int kp_for(int k) {
+  long long want = (long long)k + std::max<long long>(16, k / 4) + g_kp_extra;
+  int kp = kMinKp;
+  while (kp < want) kp <<= 1;
+  return kp;
+}
+
+int cls_of(int kp) {
+  int c = 0;
+  while ((kMinKp << c) < kp) ++c;
+  return c;
+}
+
+int sm_count(int device) {
+  int v = 148;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  return v;
+}
+
+// Relative error constant of the fp32 dot-form candidate distance:
+// |approx - exact| <= c * (|q| + |x|)^2 with c = gamma_d + 6u.
+double bound_const(int d) {
+  const double u = std::ldexp(1.0, -24);
+  const double gd = d * u / (1.0 - d * u);
+  return gd + 6.0 * u;
+}
+
+// Per-search scratch shared by the brute-force and IVF pipelines.
+struct Workspace {
+  DevBuf q64, Q32, qn32, qn64, flags, plan, part, merged, out_ids, out_d;
+  HostBuf h_plan;
+  // cached host plan (brute force)
+  std::vector<int> plan_k;
+  int plan_B = -1;
+  long long plan_n = -1;
+  int n_items = 0, grid = 0, gmax = 0, cap = 0, kp_max = 0, k_max = 0;
+  size_t off_items = 0, off_members = 0, plan_bytes = 0;
+  long long part_keys = 0;
+  int last_fixups = 0;
+  void free_all() {
+    for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &out_ids, &out_d}) release(*b);
+    if (h_plan.p) cudaFreeHost(h_plan.p);
+    h_plan.p = nullptr;
+  }
+};
+
+}  // namespace
+
+struct tri_store {
+  int device = 0;
+  long long n = 0;
+  int d = 0, dp = 0, qld = 0;
+  long long id_offset = 0;
+  float* X = nullptr;
+  float* xnorm = nullptr;
+  double xmax = 0.0;
+  cudaStream_t own = nullptr;
+  Workspace ws;
+};
+
+struct tri_ivf {
+  int device = 0;
+  long long n = 0;
+  int d = 0, dp = 0, qld = 0, nlist = 0;
+  long long id_offset = 0;
+  float* Xl = nullptr;
+  float* xnl = nullptr;
+  long long* ids = nullptr;
+  long long* list_off = nullptr;
+  int* list_by_size = nullptr;
+  int* assign = nullptr;  // per original row (store order)
+  double xmax = 0.0;
+  std::vector<long long> h_off;
+  tri_store* cstore = nullptr;  // centroids as a vector store (coarse step)
+  cudaStream_t own = nullptr;
+  Workspace ws;
+  DevBuf probes, probe_d, counts, fill, mbase, items, members, counters, meta;
+  HostBuf h_meta;
+  int last_B = 0, last_npmax = 0;
+  std::vector<int> last_np;
+  bool prof = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double scan_ms = 0.0;
+  int scan_launches = 0;
+  bool pending_event = false;
+};
+
+namespace {
+
+cudaStream_t pick(void* stream, cudaStream_t own) { return stream ? static_cast<cudaStream_t>(stream) : own; }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int check_queries(const double* q, long long count) {
+  for (long long i = 0; i < count; ++i)
+    if (!std::isfinite(q[i])) return fail(TRI_EINVAL, "query must be finite");
+  return TRI_OK;
+}
+
+// Create a store from device-resident rows (row stride ldx floats).
+int store_from_device(const float* Xdev, long long ldx, long long n, int d, int device, tri_store** out) {
+  tri_store* s = new tri_store();
+  s->device = device;
+  s->n = n;
+  s->d = d;
+  s->dp = (d + 3) & ~3;
+  s->qld = (d + 15) & ~15;
+  cudaError_t e = cudaMalloc(&s->X, (size_t)n * s->dp * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&s->xnorm, (size_t)n * sizeof(float));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->own, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemset2DAsync(s->X, s->dp * sizeof(float), 0, s->dp * sizeof(float), n, s->own);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(s->X, s->dp * sizeof(float), Xdev, ldx * sizeof(float), d * sizeof(float), n,
+                          cudaMemcpyDeviceToDevice, s->own);
+  unsigned long long* xm = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&xm, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemsetAsync(xm, 0, sizeof(unsigned long long), s->own);
+  if (e == cudaSuccess) e = launch_norms(s->X, n, d, s->dp, s->xnorm, xm, s->own);
+  unsigned long long bits = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&bits, xm, sizeof(bits), cudaMemcpyDeviceToHost, s->own);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->own);
+  if (xm) cudaFree(xm);
+  if (e != cudaSuccess) {
+    tri_store_destroy(s);
+    return fail(TRI_ECUDA, "store creation failed: %s", cudaGetErrorString(e));
+  }
+  std::memcpy(&s->xmax, &bits, sizeof(double));
+  *out = s;
+  return TRI_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Brute-force plan: queries grouped by capacity class, the rows cut into
+// ranges so that (#ranges x #groups) work items fill the GPU; items are
+// range-major so CTAs running concurrently share rows through L2.
+
+int plan_bruteforce(tri_store* s, int B, const int* k, cudaStream_t st) {
+  Workspace& w = s->ws;
+  if (w.plan_B == B && w.plan_n == s->n && (int)w.plan_k.size() == B &&
+      std::equal(w.plan_k.begin(), w.plan_k.end(), k))
+    return TRI_OK;
+  std::vector<int> kp(B), cls(B);
+  int kp_max = kMinKp, k_max = 1;
+  for (int i = 0; i < B; ++i) {
+    kp[i] = kp_for(k[i]);
+    cls[i] = cls_of(kp[i]);
+    kp_max = std::max(kp_max, kp[i]);
+    k_max = std::max(k_max, k[i]);
+  }
+  const int cap = 2 * kp_max;
+  const int gmax = scan_gmax(s->qld, cap, kSmemLimit);
+  if (gmax < 1) return fail(TRI_EINVAL, "dimension %d too large for the device scan", s->d);
+  // groups: consecutive same-class queries in index order
+  std::vector<std::vector<int>> groups;
+  for (int c = 0; c < kNumCls; ++c) {
+    std::vector<int> cur;
+    for (int i = 0; i < B; ++i)
+      if (cls[i] == c) {
+        cur.push_back(i);
+        if ((int)cur.size() == gmax) {
+          groups.push_back(cur);
+          cur.clear();
+        }
+      }
+    if (!cur.empty()) groups.push_back(cur);
+  }
+  const int nsm = sm_count(s->device);
+  const long long max_ranges = std::max<long long>(1, (s->n + 511) / 512);
+  long long nr = std::max<long long>(1, (3LL * nsm + (long long)groups.size() - 1) / (long long)groups.size());
+  nr = std::min(nr, max_ranges);
+  long long R = (s->n + nr - 1) / nr;
+  R = ((R + 511) / 512) * 512;
+  nr = (s->n + R - 1) / R;
+  // sizes
+  std::vector<QueryMeta> meta(B);
+  long long off = 0;
+  for (int i = 0; i < B; ++i) {
+    meta[i].k = k[i];
+    meta[i].kp = kp[i];
+    meta[i].n_slots = (int)nr;
+    meta[i].cls = cls[i];
+    meta[i].part_off = off;
+    meta[i].n_total = s->n;
+    off += nr * kp[i];
+  }
+  const long long n_items = nr * (long long)groups.size();
+  const long long n_members = nr * (long long)B;
+  w.off_items = ((size_t)B * sizeof(QueryMeta) + 255) & ~(size_t)255;
+  w.off_members = w.off_items + (((size_t)n_items * sizeof(WorkItem) + 255) & ~(size_t)255);
+  size_t counters_off = w.off_members + (((size_t)n_members * sizeof(Member) + 255) & ~(size_t)255);
+  w.plan_bytes = counters_off + 256;
+  TRY(ensure_host(w.h_plan, w.plan_bytes));
+  TRY(ensure(w.plan, w.plan_bytes));
+  unsigned char* h = static_cast<unsigned char*>(w.h_plan.p);
+  std::memcpy(h, meta.data(), B * sizeof(QueryMeta));
+  WorkItem* items = reinterpret_cast<WorkItem*>(h + w.off_items);
+  Member* members = reinterpret_cast<Member*>(h + w.off_members);
+  long long it = 0, mb = 0;
+  for (long long r = 0; r < nr; ++r) {
+    for (const auto& g : groups) {
+      WorkItem wi;
+      wi.row_begin = r * R;
+      wi.row_count = (int)std::min<long long>(R, s->n - r * R);
+      wi.member_begin = (int)mb;
+      wi.member_count = (int)g.size();
+      wi.kp = kp[g[0]];
+      wi.pad0 = 0;
+      wi.pad1 = 0;
+      items[it++] = wi;
+      for (int q : g) {
+        Member m;
+        m.q = q;
+        m.pad = (int)r;
+        m.slot = meta[q].part_off + r * kp[q];
+        members[mb++] = m;
+      }
+    }
+  }
+  int* ctr = reinterpret_cast<int*>(h + counters_off);
+  ctr[0] = (int)n_items;
+  CU(cudaMemcpyAsync(w.plan.p, h, w.plan_bytes, cudaMemcpyHostToDevice, st));
+  CU(cudaStreamSynchronize(st));  // h_plan is reused by the next plan
+  w.plan_B = B;
+  w.plan_n = s->n;
+  w.plan_k.assign(k, k + B);
+  w.n_items = (int)n_items;
+  w.grid = (int)std::min<long long>(n_items, nsm);
+  w.gmax = gmax;
+  w.cap = cap;
+  w.kp_max = kp_max;
+  w.k_max = k_max;
+  w.part_keys = off;
+  return TRI_OK;
+}
+
+int ensure_query_bufs(Workspace& w, int B, int d, int qld) {
+  TRY(ensure(w.q64, (size_t)B * d * sizeof(double)));
+  TRY(ensure(w.Q32, (size_t)B * qld * sizeof(float)));
+  TRY(ensure(w.qn32, (size_t)B * sizeof(float)));
+  TRY(ensure(w.qn64, (size_t)B * sizeof(double)));
+  TRY(ensure(w.flags, (size_t)(B + 64) * sizeof(int)));
+  return TRI_OK;
+}
+
+// Run the brute-force pipeline on prepared queries (Q32/qn32/qn64 in `qw`,
+// fp64 queries at q64dev).  Results to device ids/dists with row stride ldo.
+int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int B, const int* k, int ldo,
+                    long long* ids, double* dists, cudaStream_t st) {
+  Workspace& w = s->ws;
+  TRY(plan_bruteforce(s, B, k, st));
+  TRY(ensure(w.part, (size_t)w.part_keys * sizeof(unsigned long long)));
+  TRY(ensure(w.merged, (size_t)B * w.kp_max * sizeof(unsigned long long)));
+  TRY(ensure(w.flags, (size_t)(B + 64) * sizeof(int)));
+  unsigned char* plan = static_cast<unsigned char*>(w.plan.p);
+  const QueryMeta* meta = reinterpret_cast<const QueryMeta*>(plan);
+  int* ctr = reinterpret_cast<int*>(plan + w.plan_bytes - 256);
+  int* n_flag = w.flags.as<int>();
+  int* flag_list = n_flag + 64;
+  CU(cudaMemsetAsync(ctr + 1, 0, sizeof(int), st));
+  CU(cudaMemsetAsync(n_flag, 0, sizeof(int), st));
+
+  ScanLaunch sl;
+  sl.X = s->X;
+  sl.ldx = s->dp;
+  sl.xnorm = s->xnorm;
+  sl.Q = qw.Q32.as<float>();
+  sl.qld = s->qld;
+  sl.qnorm = qw.qn32.as<float>();
+  sl.items = reinterpret_cast<const WorkItem*>(plan + w.off_items);
+  sl.n_items = ctr;
+  sl.counter = ctr + 1;
+  sl.members = reinterpret_cast<const Member*>(plan + w.off_members);
+  sl.part = w.part.as<unsigned long long>();
+  sl.dp = s->dp;
+  sl.gmax = w.gmax;
+  sl.cap = w.cap;
+  sl.grid = w.grid;
+  CU(launch_scan(sl, st));
+  CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
+                  st));
+  RerankLaunch rr;
+  rr.merged = w.merged.as<unsigned long long>();
+  rr.ld_merged = w.kp_max;
+  rr.meta = meta;
+  rr.q64 = q64dev;
+  rr.d = s->d;
+  rr.qn64 = qw.qn64.as<double>();
+  rr.X = s->X;
+  rr.ldx = s->dp;
+  rr.idmap = nullptr;
+  rr.id_offset = s->id_offset;
+  rr.xmax = s->xmax;
+  rr.cbound = g_force_fixup ? 1e30 : bound_const(s->d);
+  rr.out_ids = ids;
+  rr.out_d = dists;
+  rr.ldo = ldo;
+  rr.n_flag = n_flag;
+  rr.flag_list = flag_list;
+  rr.B = B;
+  rr.kp_max = w.kp_max;
+  CU(launch_rerank(rr, st));
+  FixupLaunch fx;
+  fx.n_flag = n_flag;
+  fx.flag_list = flag_list;
+  fx.meta = meta;
+  fx.q64 = q64dev;
+  fx.d = s->d;
+  fx.X = s->X;
+  fx.ldx = s->dp;
+  fx.n_rows = s->n;
+  fx.probes = nullptr;
+  fx.ld_probes = 0;
+  fx.nprobe = nullptr;
+  fx.list_off = nullptr;
+  fx.idmap = nullptr;
+  fx.id_offset = s->id_offset;
+  fx.out_ids = ids;
+  fx.out_d = dists;
+  fx.ldo = ldo;
+  fx.B = B;
+  fx.k_max = w.k_max;
+  CU(launch_fixup(fx, st));
+  return TRI_OK;
+}
+
+int validate_k(const int* k, int B, long long limit, const char* what) {
+  for (int i = 0; i < B; ++i) {
+    if (k[i] < 1 || k[i] > limit) return fail(TRI_EINVAL, "%s must be in [1, %lld], got %d", what, limit, k[i]);
+    if (k[i] > TRI_MAX_K) return fail(TRI_EINVAL, "%s=%d exceeds the device limit %d", what, k[i], TRI_MAX_K);
+  }
+  return TRI_OK;
+}
+
+int prep_queries(Workspace& w, const double* q64dev, int B, int d, int qld, cudaStream_t st) {
+  CU(launch_prep(q64dev, B, d, w.Q32.as<float>(), qld, w.qn32.as<float>(), w.qn64.as<double>(), nullptr, st));
+  return TRI_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* tri_last_error(void) { return g_err.c_str(); }
+
+int tri_version(void) { return 1; }
+
+int tri_device_count(int32_t* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(TRI_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *count = c;
+  return TRI_OK;
+}
+
+int tri_set_option(const char* name, int64_t value) {
+  if (!name) return fail(TRI_EINVAL, "option name is NULL");
+  if (!std::strcmp(name, "force_fixup")) g_force_fixup = value;
+  else if (!std::strcmp(name, "kp_extra")) g_kp_extra = value;
+  else return fail(TRI_EINVAL, "unknown option '%s'", name);
+  return TRI_OK;
+}
+
+int tri_store_create(const float* x, int64_t n, int32_t d, int32_t device, tri_store** out) {
+  if (!out) return fail(TRI_EINVAL, "out is NULL");
+  if (n < 1 || d < 1) return fail(TRI_EINVAL, "vector store must be a nonempty 2-D matrix, got shape (%lld, %d)",
+                                  (long long)n, d);
+  if (n >= (1LL << 31)) return fail(TRI_EINVAL, "stores hold < 2^31 rows per device");
+  for (long long i = 0; i < n * (long long)d; ++i)
+    if (!std::isfinite(x[i])) return fail(TRI_EINVAL, "vector store entries must all be finite");
+  CU(cudaSetDevice(device));
+  float* tmp = nullptr;
+  CU(cudaMalloc(&tmp, (size_t)n * d * sizeof(float)));
+  cudaError_t e = cudaMemcpy(tmp, x, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(tmp);
+    return fail(TRI_ECUDA, "upload: %s", cudaGetErrorString(e));
+  }
+  int rc = store_from_device(tmp, d, n, d, device, out);
+  cudaFree(tmp);
+  return rc;
+}
+
+int tri_store_destroy(tri_store* s) {
+  if (!s) return TRI_OK;
+  DeviceGuard g(s->device);
+  if (s->own) cudaStreamSynchronize(s->own);
+  if (s->X) cudaFree(s->X);
+  if (s->xnorm) cudaFree(s->xnorm);
+  s->ws.free_all();
+  if (s->own) cudaStreamDestroy(s->own);
+  delete s;
+  return TRI_OK;
+}
+
+int tri_store_info(const tri_store* s, int64_t* n, int32_t* d, double* max_norm) {
+  if (!s) return fail(TRI_EINVAL, "store is NULL");
+  if (n) *n = s->n;
+  if (d) *d = s->d;
+  if (max_norm) *max_norm = s->xmax;
+  return TRI_OK;
+}
+
+int tri_store_set_id_offset(tri_store* s, int64_t id_offset) {
+  if (!s) return fail(TRI_EINVAL, "store is NULL");
+  s->id_offset = id_offset;
+  return TRI_OK;
+}
+
+int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32_t* k, int32_t ldo, int64_t* ids,
+                           double* dists, void* stream) {
+  if (!s) return fail(TRI_EINVAL, "store is NULL");
+  if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
+  if (B == 0) return TRI_OK;
+  TRY(validate_k(k, B, s->n, "k"));
+  int km = *std::max_element(k, k + B);
+  if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
+  DeviceGuard g(s->device);
+  cudaStream_t st = pick(stream, s->own);
+  TRY(ensure_query_bufs(s->ws, B, s->d, s->qld));
+  TRY(prep_queries(s->ws, q, B, s->d, s->qld, st));
+  return bruteforce_core(s, s->ws, q, B, k, ldo, reinterpret_cast<long long*>(ids), dists, st);
+}
+
+int tri_knn_bruteforce(tri_store* s, const double* q, int32_t B, const int32_t* k, int32_t ldo, int64_t* ids,
+                       double* dists, void* stream) {
+  if (!s) return fail(TRI_EINVAL, "store is NULL");
+  if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
+  if (B == 0) return TRI_OK;
+  TRY(validate_k(k, B, s->n, "k"));
+  int km = *std::max_element(k, k + B);
+  if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
+  TRY(check_queries(q, (long long)B * s->d));
+  DeviceGuard g(s->device);
+  cudaStream_t st = pick(stream, s->own);
+  Workspace& w = s->ws;
+  TRY(ensure_query_bufs(w, B, s->d, s->qld));
+  TRY(ensure(w.out_ids, (size_t)B * ldo * sizeof(long long)));
+  TRY(ensure(w.out_d, (size_t)B * ldo * sizeof(double)));
+  CU(cudaMemcpyAsync(w.q64.p, q, (size_t)B * s->d * sizeof(double), cudaMemcpyHostToDevice, st));
+  TRY(prep_queries(w, w.q64.as<double>(), B, s->d, s->qld, st));
+  TRY(bruteforce_core(s, w, w.q64.as<double>(), B, k, ldo, w.out_ids.as<long long>(), w.out_d.as<double>(), st));
+  CU(cudaMemcpyAsync(ids, w.out_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(dists, w.out_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&w.last_fixups, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return TRI_OK;
+}
+
+int tri_store_last_fixups(tri_store* s, int32_t* n) {
+  if (!s || !n) return fail(TRI_EINVAL, "NULL argument");
+  DeviceGuard g(s->device);
+  int v = 0;
+  if (s->ws.flags.p) {
+    CU(cudaStreamSynchronize(s->own));
+    CU(cudaMemcpy(&v, s->ws.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  *n = v;
+  return TRI_OK;
+}
+
+int tri_rowwise_sq_dists(tri_store* s, const double* q, const int64_t* rows, int64_t n, double* out, void* stream) {
+  if (!s) return fail(TRI_EINVAL, "store is NULL");
+  if (n < 0 || n > (1LL << 30)) return fail(TRI_EINVAL, "bad row count %lld", (long long)n);
+  if (n == 0) return TRI_OK;
+  std::vector<int32_t> owner(n, 0);
+  return tri_distance_tasks(s, owner.data(), rows, (int32_t)n, q, 1, out, stream);
+}
+
+int tri_distance_tasks(tri_store* s, const int32_t* owner, const int64_t* cand, int32_t n_tasks,
+                       const double* queries, int32_t n_queries, double* out, void* stream) {
+  if (!s) return fail(TRI_EINVAL, "store is NULL");
+  if (n_tasks < 0 || n_queries < 0) return fail(TRI_EINVAL, "negative size");
+  if (n_tasks == 0) return TRI_OK;
+  for (int i = 0; i < n_tasks; ++i)
+    if (owner[i] < 0 || owner[i] >= n_queries) return fail(TRI_EINVAL, "task %d owner %d out of range", i, owner[i]);
+  DeviceGuard g(s->device);
+  cudaStream_t st = pick(stream, s->own);
+  auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  const size_t qb = (size_t)n_queries * s->d * sizeof(double);
+  const size_t o_c = al(qb), o_o = o_c + al((size_t)n_tasks * sizeof(long long));
+  const size_t o_out = o_o + al((size_t)n_tasks * sizeof(int));
+  const size_t total = o_out + al((size_t)n_tasks * sizeof(double));
+  DevBuf& buf = s->ws.merged;  // reuse a scratch buffer
+  TRY(ensure(buf, total));
+  unsigned char* base = buf.as<unsigned char>();
+  double* dq = reinterpret_cast<double*>(base);
+  long long* dc = reinterpret_cast<long long*>(base + o_c);
+  int* dow = reinterpret_cast<int*>(base + o_o);
+  double* dout = reinterpret_cast<double*>(base + o_out);
+  TRY(ensure(s->ws.flags, 64 * sizeof(int)));
+  int* derr = s->ws.flags.as<int>() + 1;
+  CU(cudaMemcpyAsync(dq, queries, qb, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dc, cand, (size_t)n_tasks * sizeof(long long), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dow, owner, (size_t)n_tasks * sizeof(int), cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(derr, 0, sizeof(int), st));
+  CU(launch_distance_tasks(dow, dc, n_tasks, dq, s->d, s->X, s->dp, s->n, dout, derr, st));
+  int herr = 0;
+  CU(cudaMemcpyAsync(out, dout, (size_t)n_tasks * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (herr) {
+    for (int i = 0; i < n_tasks; ++i)
+      if (cand[i] < 0 || cand[i] >= s->n)
+        return fail(TRI_EINTERNAL, "candidate id %lld out of range [0, %lld)", (long long)cand[i], s->n);
+    return fail(TRI_EINTERNAL, "candidate out of range");
+  }
+  return TRI_OK;
+}
+
+// ---------------------------------------------------------------------------
+// IVF
+
+static int ivf_layout(tri_ivf* v, const float* X, long long ldx, const long long* perm_dev, cudaStream_t st) {
+  const long long n = v->n;
+  CU(cudaMalloc(&v->Xl, (size_t)n * v->dp * sizeof(float)));
+  CU(cudaMalloc(&v->xnl, (size_t)n * sizeof(float)));
+  CU(cudaMalloc(&v->ids, (size_t)n * sizeof(long long)));
+  CU(launch_gather_rows(X, ldx, perm_dev, n, v->dp, v->Xl, st));
+  unsigned long long* xm = nullptr;
+  CU(cudaMalloc(&xm, sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(xm, 0, sizeof(unsigned long long), st));
+  CU(launch_norms(v->Xl, n, v->d, v->dp, v->xnl, xm, st));
+  CU(cudaMemcpyAsync(v->ids, perm_dev, (size_t)n * sizeof(long long), cudaMemcpyDeviceToDevice, st));
+  unsigned long long bits = 0;
+  CU(cudaMemcpyAsync(&bits, xm, sizeof(bits), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  cudaFree(xm);
+  std::memcpy(&v->xmax, &bits, sizeof(double));
+  // list order by descending size (ties: smaller list id first)
+  std::vector<int> order(v->nlist);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return (v->h_off[a + 1] - v->h_off[a]) > (v->h_off[b + 1] - v->h_off[b]);
+  });
+  CU(cudaMalloc(&v->list_by_size, (size_t)v->nlist * sizeof(int)));
+  CU(cudaMemcpy(v->list_by_size, order.data(), (size_t)v->nlist * sizeof(int), cudaMemcpyHostToDevice));
+  return TRI_OK;
+}
+
+static tri_ivf* ivf_new(tri_store* s, int nlist) {
+  tri_ivf* v = new tri_ivf();
+  v->device = s->device;
+  v->n = s->n;
+  v->d = s->d;
+  v->dp = s->dp;
+  v->qld = s->qld;
+  v->nlist = nlist;
+  v->id_offset = s->id_offset;
+  return v;
+}
+
+static int ivf_finish(tri_ivf* v, tri_store* s, const float* Cdev, const int* assign_dev, cudaStream_t st) {
+  // counts -> offsets (host) -> ordered members -> layout
+  DevBuf cnt;
+  TRY(ensure(cnt, (size_t)v->nlist * sizeof(int)));
+  CU(launch_counts(assign_dev, v->n, v->nlist, cnt.as<int>(), st));
+  std::vector<int> hc(v->nlist);
+  CU(cudaMemcpyAsync(hc.data(), cnt.p, (size_t)v->nlist * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  release(cnt);
+  v->h_off.assign(v->nlist + 1, 0);
+  for (int l = 0; l < v->nlist; ++l) v->h_off[l + 1] = v->h_off[l] + hc[l];
+  CU(cudaMalloc(&v->list_off, (size_t)(v->nlist + 1) * sizeof(long long)));
+  CU(cudaMemcpy(v->list_off, v->h_off.data(), (size_t)(v->nlist + 1) * sizeof(long long), cudaMemcpyHostToDevice));
+  DevBuf perm;
+  TRY(ensure(perm, (size_t)v->n * sizeof(long long)));
+  CU(launch_list_members(assign_dev, v->n, v->nlist, v->list_off, perm.as<long long>(), st));
+  TRY(ivf_layout(v, s->X, s->dp, perm.as<long long>(), st));
+  release(perm);
+  if (v->id_offset) {
+    // ids are global: add the shard offset on the host-free path
+    std::vector<long long> h(v->n);
+    CU(cudaMemcpy(h.data(), v->ids, (size_t)v->n * sizeof(long long), cudaMemcpyDeviceToHost));
+    for (auto& x : h) x += v->id_offset;
+    CU(cudaMemcpy(v->ids, h.data(), (size_t)v->n * sizeof(long long), cudaMemcpyHostToDevice));
+  }
+  CU(cudaMalloc(&v->assign, (size_t)v->n * sizeof(int)));
+  CU(cudaMemcpyAsync(v->assign, assign_dev, (size_t)v->n * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  TRY(store_from_device(Cdev, v->dp, v->nlist, v->d, v->device, &v->cstore));
+  CU(cudaStreamCreateWithFlags(&v->own, cudaStreamNonBlocking));
+  CU(cudaEventCreate(&v->ev0));
+  CU(cudaEventCreate(&v->ev1));
+  CU(cudaStreamSynchronize(st));
+  return TRI_OK;
+}
+
+int tri_ivf_train(tri_store* s, int32_t nlist, int32_t iters, const int64_t* init_rows, tri_ivf** out) {
+  if (!s || !out || !init_rows) return fail(TRI_EINVAL, "NULL argument");
+  if (nlist < 1 || nlist > s->n) return fail(TRI_EINVAL, "nlist must be in [1, %lld], got %d", s->n, nlist);
+  if (iters < 0) return fail(TRI_EINVAL, "iters must be >= 0");
+  for (int i = 0; i < nlist; ++i)
+    if (init_rows[i] < 0 || init_rows[i] >= s->n) return fail(TRI_EINVAL, "init row %lld out of range", (long long)init_rows[i]);
+  DeviceGuard g(s->device);
+  cudaStream_t st = s->own;
+  tri_ivf* v = ivf_new(s, nlist);
+  DevBuf C, cn, asg, cnt, perm, off, xm, initd;
+  auto cleanup = [&]() {
+    for (DevBuf* b : {&C, &cn, &asg, &cnt, &perm, &off, &xm, &initd}) release(*b);
+  };
+  int rc = TRI_OK;
+  do {
+    if ((rc = ensure(C, (size_t)nlist * s->dp * sizeof(float)))) break;
+    if ((rc = ensure(cn, (size_t)nlist * sizeof(float)))) break;
+    if ((rc = ensure(asg, (size_t)s->n * sizeof(int)))) break;
+    if ((rc = ensure(cnt, (size_t)nlist * sizeof(int)))) break;
+    if ((rc = ensure(perm, (size_t)s->n * sizeof(long long)))) break;
+    if ((rc = ensure(off, (size_t)(nlist + 1) * sizeof(long long)))) break;
+    if ((rc = ensure(xm, sizeof(unsigned long long)))) break;
+    if ((rc = ensure(initd, (size_t)nlist * sizeof(long long)))) break;
+    cudaError_t e = cudaMemcpyAsync(initd.p, init_rows, (size_t)nlist * sizeof(long long), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = launch_gather_rows(s->X, s->dp, initd.as<long long>(), nlist, s->dp, C.as<float>(), st);
+    std::vector<int> hc(nlist);
+    std::vector<long long> ho(nlist + 1);
+    for (int it = 0; it <= iters && e == cudaSuccess; ++it) {
+      e = cudaMemsetAsync(xm.p, 0, sizeof(unsigned long long), st);
+      if (e == cudaSuccess) e = launch_norms(C.as<float>(), nlist, s->d, s->dp, cn.as<float>(), xm.as<unsigned long long>(), st);
+      if (e == cudaSuccess)
+        e = launch_assign(s->X, s->n, s->d, s->dp, C.as<float>(), nlist, s->dp, cn.as<float>(), asg.as<int>(), st);
+      if (it == iters) break;
+      if (e == cudaSuccess) e = launch_counts(asg.as<int>(), s->n, nlist, cnt.as<int>(), st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), cnt.p, (size_t)nlist * sizeof(int), cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) break;
+      ho[0] = 0;
+      for (int l = 0; l < nlist; ++l) ho[l + 1] = ho[l] + hc[l];
+      e = cudaMemcpyAsync(off.p, ho.data(), (size_t)(nlist + 1) * sizeof(long long), cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = launch_list_members(asg.as<int>(), s->n, nlist, off.as<long long>(), perm.as<long long>(), st);
+      if (e == cudaSuccess)
+        e = launch_centroid_update(s->X, s->dp, s->d, perm.as<long long>(), off.as<long long>(), nlist, C.as<float>(), s->dp, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // ho is reused
+    }
+    if (e != cudaSuccess) {
+      rc = fail(TRI_ECUDA, "k-means: %s", cudaGetErrorString(e));
+      break;
+    }
+    rc = ivf_finish(v, s, C.as<float>(), asg.as<int>(), st);
+  } while (0);
+  cleanup();
+  if (rc != TRI_OK) {
+    tri_ivf_destroy(v);
+    return rc;
+  }
+  *out = v;
+  return TRI_OK;
+}
+
+int tri_ivf_create(tri_store* s, const float* centroids, int32_t nlist, const int32_t* assign, int64_t id_offset,
+                   tri_ivf** out) {
+  if (!s || !out || !centroids || !assign) return fail(TRI_EINVAL, "NULL argument");
+  if (nlist < 1) return fail(TRI_EINVAL, "nlist must be >= 1");
+  for (long long i = 0; i < s->n; ++i)
+    if (assign[i] < 0 || assign[i] >= nlist) return fail(TRI_EINVAL, "assign[%lld]=%d out of range", i, assign[i]);
+  for (long long i = 0; i < (long long)nlist * s->d; ++i)
+    if (!std::isfinite(centroids[i])) return fail(TRI_EINVAL, "centroids must be finite");
+  DeviceGuard g(s->device);
+  cudaStream_t st = s->own;
+  tri_ivf* v = ivf_new(s, nlist);
+  v->id_offset = id_offset;
+  DevBuf C, asg;
+  int rc = ensure(C, (size_t)nlist * s->dp * sizeof(float));
+  if (!rc) rc = ensure(asg, (size_t)s->n * sizeof(int));
+  if (!rc) {
+    cudaError_t e = cudaMemset2DAsync(C.p, s->dp * sizeof(float), 0, s->dp * sizeof(float), nlist, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(C.p, s->dp * sizeof(float), centroids, s->d * sizeof(float), s->d * sizeof(float), nlist,
+                            cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(asg.p, assign, (size_t)s->n * sizeof(int), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) rc = fail(TRI_ECUDA, "upload: %s", cudaGetErrorString(e));
+  }
+  if (!rc) rc = ivf_finish(v, s, C.as<float>(), asg.as<int>(), st);
+  release(C);
+  release(asg);
+  if (rc) {
+    tri_ivf_destroy(v);
+    return rc;
+  }
+  *out = v;
+  return TRI_OK;
+}
+
+int tri_ivf_destroy(tri_ivf* v) {
+  if (!v) return TRI_OK;
+  DeviceGuard g(v->device);
+  if (v->own) cudaStreamSynchronize(v->own);
+  for (void* p : {(void*)v->Xl, (void*)v->xnl, (void*)v->ids, (void*)v->list_off, (void*)v->list_by_size,
+                  (void*)v->assign})
+    if (p) cudaFree(p);
+  v->ws.free_all();
+  for (DevBuf* b : {&v->probes, &v->probe_d, &v->counts, &v->fill, &v->mbase, &v->items, &v->members, &v->counters,
+                    &v->meta})
+    release(*b);
+  if (v->h_meta.p) cudaFreeHost(v->h_meta.p);
+  if (v->cstore) tri_store_destroy(v->cstore);
+  if (v->ev0) cudaEventDestroy(v->ev0);
+  if (v->ev1) cudaEventDestroy(v->ev1);
+  if (v->own) cudaStreamDestroy(v->own);
+  delete v;
+  return TRI_OK;
+}
+
+int tri_ivf_info(const tri_ivf* v, int32_t* nlist, int64_t* n, int32_t* d) {
+  if (!v) return fail(TRI_EINVAL, "index is NULL");
+  if (nlist) *nlist = v->nlist;
+  if (n) *n = v->n;
+  if (d) *d = v->d;
+  return TRI_OK;
+}
+
+int tri_ivf_export(tri_ivf* v, float* centroids, int32_t* assign) {
+  if (!v) return fail(TRI_EINVAL, "index is NULL");
+  DeviceGuard g(v->device);
+  if (centroids)
+    CU(cudaMemcpy2D(centroids, v->d * sizeof(float), v->cstore->X, v->dp * sizeof(float), v->d * sizeof(float),
+                    v->nlist, cudaMemcpyDeviceToHost));
+  if (assign) CU(cudaMemcpy(assign, v->assign, (size_t)v->n * sizeof(int), cudaMemcpyDeviceToHost));
+  return TRI_OK;
+}
+
+int tri_ivf_list_sizes(tri_ivf* v, int64_t* sizes) {
+  if (!v || !sizes) return fail(TRI_EINVAL, "NULL argument");
+  for (int l = 0; l < v->nlist; ++l) sizes[l] = v->h_off[l + 1] - v->h_off[l];
+  return TRI_OK;
+}
+
+int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe,
+                       int32_t ldo, int64_t* ids, double* dists, void* stream) {
+  if (!v) return fail(TRI_EINVAL, "index is NULL");
+  if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
+  if (B == 0) return TRI_OK;
+  TRY(validate_k(k, B, (long long)1 << 40, "k"));
+  TRY(validate_k(nprobe, B, v->nlist, "nprobe"));
+  int km = *std::max_element(k, k + B);
+  if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
+  DeviceGuard g(v->device);
+  cudaStream_t st = pick(stream, v->own);
+  Workspace& w = v->ws;
+  const int npmax = *std::max_element(nprobe, nprobe + B);
+  TRY(ensure_query_bufs(w, B, v->d, v->qld));
+  TRY(prep_queries(w, q, B, v->d, v->qld, st));
+
+  // 1. coarse step: exact top-nprobe centroids per query
+  TRY(ensure(v->probes, (size_t)B * npmax * sizeof(long long)));
+  TRY(ensure(v->probe_d, (size_t)B * npmax * sizeof(double)));
+  TRY(bruteforce_core(v->cstore, w, q, B, nprobe, npmax, v->probes.as<long long>(), v->probe_d.as<double>(), st));
+
+  // 2. host-side per-query plan (k, kp, slots) -> device
+  std::vector<int> kp(B);
+  int kp_max = kMinKp, k_max = 1;
+  long long part_keys = 0, members = 0;
+  TRY(ensure_host(v->h_meta, (size_t)B * (sizeof(QueryMeta) + sizeof(int)) + 64));
+  QueryMeta* hm = static_cast<QueryMeta*>(v->h_meta.p);
+  int* hnp = reinterpret_cast<int*>(hm + B);
+  for (int i = 0; i < B; ++i) {
+    kp[i] = kp_for(k[i]);
+    kp_max = std::max(kp_max, kp[i]);
+    k_max = std::max(k_max, k[i]);
+    hm[i].k = k[i];
+    hm[i].kp = kp[i];
+    hm[i].n_slots = nprobe[i];
+    hm[i].cls = cls_of(kp[i]);
+    hm[i].part_off = part_keys;
+    hm[i].n_total = 0;
+    hnp[i] = nprobe[i];
+    part_keys += (long long)nprobe[i] * kp[i];
+    members += nprobe[i];
+  }
+  const int cap = 2 * kp_max;
+  const int gmax = scan_gmax(v->qld, cap, kSmemLimit);
+  if (gmax < 1) return fail(TRI_EINVAL, "dimension %d too large for the device scan", v->d);
+  TRY(ensure(v->meta, (size_t)B * (sizeof(QueryMeta) + sizeof(int)) + 64));
+  CU(cudaMemcpyAsync(v->meta.p, v->h_meta.p, (size_t)B * (sizeof(QueryMeta) + sizeof(int)), cudaMemcpyHostToDevice, st));
+  QueryMeta* dmeta = v->meta.as<QueryMeta>();
+  int* dnp = reinterpret_cast<int*>(dmeta + B);
+  TRY(ensure(w.part, (size_t)part_keys * sizeof(unsigned long long)));
+  TRY(ensure(w.merged, (size_t)B * kp_max * sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(w.part.p, 0xff, (size_t)part_keys * sizeof(unsigned long long), st));
+  size_t cbytes = (size_t)v->nlist * kNumCls * sizeof(int);
+  TRY(ensure(v->counts, cbytes));
+  TRY(ensure(v->fill, cbytes));
+  TRY(ensure(v->mbase, cbytes));
+  TRY(ensure(v->items, (size_t)members * sizeof(WorkItem)));
+  TRY(ensure(v->members, (size_t)members * sizeof(Member)));
+  TRY(ensure(v->counters, 64 * sizeof(int)));
+  int* ctr = v->counters.as<int>();
+  CU(cudaMemsetAsync(ctr, 0, 4 * sizeof(int), st));
+
+  // 3. device packer
+  PackLaunch pk;
+  pk.probes = v->probes.as<long long>();
+  pk.ld_probes = npmax;
+  pk.nprobe = dnp;
+  pk.meta = dmeta;
+  pk.B = B;
+  pk.list_off = v->list_off;
+  pk.list_by_size = v->list_by_size;
+  pk.nlist = v->nlist;
+  pk.counts = v->counts.as<int>();
+  pk.fill = v->fill.as<int>();
+  pk.member_base = v->mbase.as<int>();
+  pk.items = v->items.as<WorkItem>();
+  pk.n_items = ctr;
+  pk.members = v->members.as<Member>();
+  pk.gmax = gmax;
+  CU(launch_pack(pk, st));
+
+  // 4. list scan (persistent, one CTA per SM)
+  ScanLaunch sl;
+  sl.X = v->Xl;
+  sl.ldx = v->dp;
+  sl.xnorm = v->xnl;
+  sl.Q = w.Q32.as<float>();
+  sl.qld = v->qld;
+  sl.qnorm = w.qn32.as<float>();
+  sl.items = v->items.as<WorkItem>();
+  sl.n_items = ctr;
+  sl.counter = ctr + 1;
+  sl.members = v->members.as<Member>();
+  sl.part = w.part.as<unsigned long long>();
+  sl.dp = v->dp;
+  sl.gmax = gmax;
+  sl.cap = cap;
+  sl.grid = (int)std::min<long long>(sm_count(v->device), members);
+  if (v->prof) CU(cudaEventRecord(v->ev0, st));
+  CU(launch_scan(sl, st));
+  if (v->prof) {
+    CU(cudaEventRecord(v->ev1, st));
+    v->pending_event = true;
+  }
+
+  // 5. merge, exact re-rank, certified fix-up
+  CU(launch_merge(w.part.as<unsigned long long>(), dmeta, w.merged.as<unsigned long long>(), kp_max, B, kp_max, st));
+  int* n_flag = w.flags.as<int>();
+  int* flag_list = n_flag + 64;
+  CU(cudaMemsetAsync(n_flag, 0, sizeof(int), st));
+  RerankLaunch rr;
+  rr.merged = w.merged.as<unsigned long long>();
+  rr.ld_merged = kp_max;
+  rr.meta = dmeta;
+  rr.q64 = q;
+  rr.d = v->d;
+  rr.qn64 = w.qn64.as<double>();
+  rr.X = v->Xl;
+  rr.ldx = v->dp;
+  rr.idmap = v->ids;
+  rr.id_offset = 0;
+  rr.xmax = v->xmax;
+  rr.cbound = g_force_fixup ? 1e30 : bound_const(v->d);
+  rr.out_ids = reinterpret_cast<long long*>(ids);
+  rr.out_d = dists;
+  rr.ldo = ldo;
+  rr.n_flag = n_flag;
+  rr.flag_list = flag_list;
+  rr.B = B;
+  rr.kp_max = kp_max;
+  CU(launch_rerank(rr, st));
+  FixupLaunch fx;
+  fx.n_flag = n_flag;
+  fx.flag_list = flag_list;
+  fx.meta = dmeta;
+  fx.q64 = q;
+  fx.d = v->d;
+  fx.X = v->Xl;
+  fx.ldx = v->dp;
+  fx.n_rows = v->n;
+  fx.probes = v->probes.as<long long>();
+  fx.ld_probes = npmax;
+  fx.nprobe = dnp;
+  fx.list_off = v->list_off;
+  fx.idmap = v->ids;
+  fx.id_offset = 0;
+  fx.out_ids = reinterpret_cast<long long*>(ids);
+  fx.out_d = dists;
+  fx.ldo = ldo;
+  fx.B = B;
+  fx.k_max = k_max;
+  CU(launch_fixup(fx, st));
+  v->last_B = B;
+  v->last_npmax = npmax;
+  v->last_np.assign(nprobe, nprobe + B);
+  return TRI_OK;
+}
+
+int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe, int32_t ldo,
+                   int64_t* ids, double* dists, void* stream) {
+  if (!v) return fail(TRI_EINVAL, "index is NULL");
+  if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
+  if (B == 0) return TRI_OK;
+  TRY(check_queries(q, (long long)B * v->d));
+  DeviceGuard g(v->device);
+  cudaStream_t st = pick(stream, v->own);
+  Workspace& w = v->ws;
+  int km = 0;
+  for (int i = 0; i < B; ++i) km = std::max(km, k[i]);
+  if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
+  TRY(ensure(w.q64, (size_t)B * v->d * sizeof(double)));
+  TRY(ensure(w.out_ids, (size_t)B * ldo * sizeof(long long)));
+  TRY(ensure(w.out_d, (size_t)B * ldo * sizeof(double)));
+  CU(cudaMemcpyAsync(w.q64.p, q, (size_t)B * v->d * sizeof(double), cudaMemcpyHostToDevice, st));
+  TRY(tri_ivf_search_dev(v, w.q64.as<double>(), B, k, nprobe, ldo, reinterpret_cast<int64_t*>(w.out_ids.p),
+                         w.out_d.as<double>(), st));
+  CU(cudaMemcpyAsync(ids, w.out_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(dists, w.out_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return TRI_OK;
+}
+
+int tri_ivf_last_probes(tri_ivf* v, int64_t* probes, int32_t ld) {
+  if (!v || !probes) return fail(TRI_EINVAL, "NULL argument");
+  if (ld < v->last_npmax) return fail(TRI_EINVAL, "ld=%d < nprobe max %d", ld, v->last_npmax);
+  DeviceGuard g(v->device);
+  CU(cudaDeviceSynchronize());
+  std::vector<long long> h((size_t)v->last_B * v->last_npmax);
+  if (!h.empty())
+    CU(cudaMemcpy(h.data(), v->probes.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < v->last_B; ++i)
+    for (int j = 0; j < ld; ++j)
+      probes[(long long)i * ld + j] = j < v->last_np[i] ? h[(size_t)i * v->last_npmax + j] : -1;
+  return TRI_OK;
+}
+
+int tri_ivf_last_fixups(tri_ivf* v, int32_t* n) {
+  if (!v || !n) return fail(TRI_EINVAL, "NULL argument");
+  DeviceGuard g(v->device);
+  CU(cudaDeviceSynchronize());
+  int a = 0, b = 0;
+  if (v->ws.flags.p) CU(cudaMemcpy(&a, v->ws.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (v->cstore && v->cstore->ws.flags.p) CU(cudaMemcpy(&b, v->cstore->ws.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
+  *n = a + b;
+  return TRI_OK;
+}
+
+int tri_ivf_set_profiling(tri_ivf* v, int32_t on) {
+  if (!v) return fail(TRI_EINVAL, "index is NULL");
+  v->prof = on != 0;
+  v->scan_ms = 0.0;
+  v->scan_launches = 0;
+  v->pending_event = false;
+  return TRI_OK;
+}
+
+int tri_ivf_scan_time(tri_ivf* v, double* total_ms, int32_t* launches) {
+  if (!v) return fail(TRI_EINVAL, "index is NULL");
+  DeviceGuard g(v->device);
+  if (v->pending_event) {
+    CU(cudaEventSynchronize(v->ev1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, v->ev0, v->ev1));
+    v->scan_ms += ms;
+    v->scan_launches += 1;
+    v->pending_event = false;
+  }
+  if (total_ms) *total_ms = v->scan_ms;
+  if (launches) *launches = v->scan_launches;
+  return TRI_OK;
+}
+
+int tri_ivf_last_scan_bytes(tri_ivf* v, int64_t* bytes, int64_t* pairs) {
+  if (!v) return fail(TRI_EINVAL, "index is NULL");
+  std::vector<int64_t> pr((size_t)v->last_B * std::max(1, v->last_npmax));
+  TRY(tri_ivf_last_probes(v, pr.data(), std::max(1, v->last_npmax)));
+  std::vector<char> hit(v->nlist, 0);
+  long long pp = 0;
+  for (int i = 0; i < v->last_B; ++i)
+    for (int j = 0; j < v->last_np[i]; ++j) {
+      long long l = pr[(size_t)i * v->last_npmax + j];
+      hit[l] = 1;
+      pp += v->h_off[l + 1] - v->h_off[l];
+    }
+  long long vec = 0;
+  for (int l = 0; l < v->nlist; ++l)
+    if (hit[l]) vec += v->h_off[l + 1] - v->h_off[l];
+  if (bytes) *bytes = vec * ((long long)v->d * 4 + 4);
+  if (pairs) *pairs = pp;
+  return TRI_OK;
+}
+
+int tri_merge_topk(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t k_out,
+                   double* out_dists, int64_t* out_ids, void* stream) {
+  if (G < 1 || B < 0 || k_in < 1 || k_out < 1) return fail(TRI_EINVAL, "bad merge shape");
+  if ((long long)G * k_in > 8192) return fail(TRI_EINVAL, "G*k_in=%lld exceeds 8192", (long long)G * k_in);
+  CU(launch_merge_exact(dists, reinterpret_cast<const long long*>(ids), G, B, k_in, k_out, out_dists,
+                        reinterpret_cast<long long*>(out_ids), static_cast<cudaStream_t>(stream)));
+  return TRI_OK;
+}
+
+}  // extern "C"

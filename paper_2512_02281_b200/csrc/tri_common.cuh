@@ -1,0 +1,130 @@
+// Shared device helpers for the Trinity B200 search library (sm_100a).
+//
+// Candidate keys.  Every approximate candidate is a 64-bit key
+//   (order-preserving bits of the fp32 approximate distance) << 32 | position
+// so "smaller key" == "smaller (approx distance, position)".  TRI_KEY_MAX is the
+// empty slot.  Exact results use (fp64 distance, global id) pairs.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define TRI_KEY_MAX 0xFFFFFFFFFFFFFFFFull
+#define TRI_THREADS 256
+
+namespace tri {
+
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__device__ __forceinline__ float ord2f(uint32_t o) {
+  uint32_t b = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+  return __uint_as_float(b);
+}
+
+__device__ __forceinline__ unsigned long long make_key(float d, uint32_t pos) {
+  return ((unsigned long long)f2ord(d) << 32) | (unsigned long long)pos;
+}
+
+__device__ __forceinline__ uint32_t key_pos(unsigned long long k) { return (uint32_t)(k & 0xffffffffull); }
+__device__ __forceinline__ float key_dist(unsigned long long k) { return ord2f((uint32_t)(k >> 32)); }
+
+// Squared L2 distance in float64 between an fp64 query and an fp32 row, in the
+// exact operation order of numpy's einsum("ij,ij->i") on float64 (the
+// reference's rowwise_sq_dists, ann_graph.py:97-105): two lanes, blocks of 8
+// elements whose 2-lane sub-blocks run in reverse order, unfused mul then add,
+// a 2-lane tail, lane0 + lane1.  Intrinsics keep nvcc from contracting to DFMA.
+// Result is bit-identical to the reference.
+__device__ __forceinline__ double exact_sq_dist(const double* __restrict__ q, const float* __restrict__ x, int d) {
+  double l0 = 0.0, l1 = 0.0;
+  int i = 0;
+  for (; i + 8 <= d; i += 8) {
+#pragma unroll
+    for (int sub = 3; sub >= 0; --sub) {
+      double t0 = __dsub_rn(q[i + 2 * sub], (double)x[i + 2 * sub]);
+      double t1 = __dsub_rn(q[i + 2 * sub + 1], (double)x[i + 2 * sub + 1]);
+      l0 = __dadd_rn(__dmul_rn(t0, t0), l0);
+      l1 = __dadd_rn(__dmul_rn(t1, t1), l1);
+    }
+  }
+  for (; i < d; i += 2) {
+    double t0 = __dsub_rn(q[i], (double)x[i]);
+    l0 = __dadd_rn(__dmul_rn(t0, t0), l0);
+    if (i + 1 < d) {
+      double t1 = __dsub_rn(q[i + 1], (double)x[i + 1]);
+      l1 = __dadd_rn(__dmul_rn(t1, t1), l1);
+    }
+  }
+  return __dadd_rn(l0, l1);
+}
+
+// Exact result entry ordered by (dist, id) -- the reference tie rule
+// (ann_graph.py:8-9, lexsort at :136).
+struct Exact {
+  double d;
+  long long id;
+};
+
+__device__ __forceinline__ bool exact_less(const Exact& a, const Exact& b) {
+  return a.d < b.d || (a.d == b.d && a.id < b.id);
+}
+
+__device__ __forceinline__ Exact exact_max() {
+  Exact e;
+  e.d = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  e.id = 0x7fffffffffffffffll;
+  return e;
+}
+
+// ---------------------------------------------------------------------------
+// In-shared-memory bitonic sorts (ascending).  n must be a power of two.
+
+template <typename T, typename Less>
+__device__ __forceinline__ void bitonic_pass(T* a, int n, int k, int j, int t, int nt, Less less) {
+  for (int i = t; i < (n >> 1); i += nt) {
+    int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+    int hi = lo + j;
+    bool up = (lo & k) == 0;
+    T x = a[lo], y = a[hi];
+    bool swap = up ? less(y, x) : less(x, y);
+    if (swap) {
+      a[lo] = y;
+      a[hi] = x;
+    }
+  }
+}
+
+template <typename T, typename Less>
+__device__ void warp_sort(T* a, int n, int lane, Less less) {
+  for (int k = 2; k <= n; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      bitonic_pass(a, n, k, j, lane, 32, less);
+      __syncwarp();
+    }
+}
+
+template <typename T, typename Less>
+__device__ void block_sort(T* a, int n, Less less) {
+  for (int k = 2; k <= n; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      bitonic_pass(a, n, k, j, threadIdx.x, blockDim.x, less);
+      __syncthreads();
+    }
+}
+
+struct KeyLess {
+  __device__ __forceinline__ bool operator()(unsigned long long a, unsigned long long b) const { return a < b; }
+};
+struct ExactLess {
+  __device__ __forceinline__ bool operator()(const Exact& a, const Exact& b) const { return exact_less(a, b); }
+};
+
+__host__ __device__ __forceinline__ int next_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+}  // namespace tri

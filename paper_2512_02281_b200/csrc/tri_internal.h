@@ -1,0 +1,157 @@
+// Internal host/device interface of libtrinity_b200 (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tri {
+
+// One unit of scan work: a contiguous row range of a (list-major) vector
+// matrix scanned against a group of <= gmax queries that share a candidate
+// capacity kp.  Produced on the host for brute force, on the device (the
+// continuous-batch packer) for IVF.
+struct WorkItem {
+  long long row_begin;
+  int row_count;
+  int member_begin;
+  int member_count;
+  int kp;
+  int pad0, pad1;
+};
+
+// A (query, partial-list slot) pair; slot is a key offset into the partial buffer.
+struct Member {
+  int q;
+  int pad;
+  long long slot;
+};
+
+// Per-query plan metadata.
+struct QueryMeta {
+  int k;           // results wanted
+  int kp;          // candidate capacity (power of two >= over-fetch(k))
+  int n_slots;     // partial lists to merge
+  int cls;         // capacity class index (log2(kp) - 5)
+  long long part_off;  // first key of this query's partial lists
+  long long n_total;   // candidates the query scans (all rows / probed-list rows)
+};
+
+constexpr int kNumCls = 7;    // kp in {32 .. 2048}
+constexpr int kMinKp = 32;
+constexpr int kMaxKp = 2048;
+
+struct ScanLaunch {
+  const float* X;
+  long long ldx;
+  const float* xnorm;
+  const float* Q;
+  int qld;
+  const float* qnorm;
+  const WorkItem* items;
+  const int* n_items;
+  int* counter;
+  const Member* members;
+  unsigned long long* part;
+  int dp;
+  int gmax;
+  int cap;      // selection buffer per query (>= 2 * max kp, power of two)
+  int grid;
+};
+
+size_t scan_smem_bytes(int gmax, int qld, int cap);
+int scan_gmax(int qld, int cap, int smem_limit);
+cudaError_t launch_scan(const ScanLaunch& s, cudaStream_t st);
+
+cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,
+                        int* bad, cudaStream_t st);
+cudaError_t launch_norms(const float* X, long long n, int d, long long ldx, float* xnorm,
+                         unsigned long long* xmax_bits, cudaStream_t st);
+
+cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, unsigned long long* merged,
+                         int ld_merged, int B, int kp_max, cudaStream_t st);
+
+struct RerankLaunch {
+  const unsigned long long* merged;
+  int ld_merged;
+  const QueryMeta* meta;
+  const double* q64;
+  int d;
+  const double* qn64;
+  const float* X;
+  long long ldx;
+  const long long* idmap;   // position -> id (nullptr: id = position)
+  long long id_offset;
+  double xmax;              // max row norm (sqrt of squared norm)
+  double cbound;            // relative error constant of the fp32 candidate distance
+  long long* out_ids;
+  double* out_d;
+  int ldo;
+  int* n_flag;
+  int* flag_list;
+  int B;
+  int kp_max;
+};
+cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st);
+
+struct FixupLaunch {
+  const int* n_flag;
+  const int* flag_list;
+  const QueryMeta* meta;
+  const double* q64;
+  int d;
+  const float* X;
+  long long ldx;
+  long long n_rows;             // brute-force mode: rows [0, n_rows)
+  const long long* probes;      // IVF mode: probed list ids (nullptr = brute force)
+  int ld_probes;
+  const int* nprobe;            // per-query probe count (IVF mode)
+  const long long* list_off;    // IVF list offsets (nlist + 1)
+  const long long* idmap;
+  long long id_offset;
+  long long* out_ids;
+  double* out_d;
+  int ldo;
+  int B;
+  int k_max;
+};
+cudaError_t launch_fixup(const FixupLaunch& f, cudaStream_t st);
+
+cudaError_t launch_distance_tasks(const int* owner, const long long* cand, int n_tasks, const double* q64, int d,
+                                  const float* X, long long ldx, long long n_rows, double* out, int* err,
+                                  cudaStream_t st);
+
+cudaError_t launch_merge_exact(const double* dists, const long long* ids, int G, int B, int k_in, int k_out,
+                               double* out_d, long long* out_ids, cudaStream_t st);
+
+// IVF packer ------------------------------------------------------------------
+struct PackLaunch {
+  const long long* probes;
+  int ld_probes;
+  const int* nprobe;
+  QueryMeta* meta;
+  int B;
+  const long long* list_off;
+  const int* list_by_size;   // lists in descending size order
+  int nlist;
+  int* counts;               // nlist * kNumCls
+  int* fill;                 // nlist * kNumCls
+  int* member_base;          // nlist * kNumCls
+  WorkItem* items;
+  int* n_items;
+  Member* members;
+  int gmax;
+};
+cudaError_t launch_pack(const PackLaunch& p, cudaStream_t st);
+
+// k-means / index layout --------------------------------------------------------
+cudaError_t launch_assign(const float* X, long long n, int d, long long ldx, const float* C, int nlist,
+                          long long ldc, const float* cnorm, int* assign, cudaStream_t st);
+cudaError_t launch_counts(const int* assign, long long n, int nlist, int* counts, cudaStream_t st);
+cudaError_t launch_list_members(const int* assign, long long n, int nlist, const long long* offsets,
+                                long long* perm, cudaStream_t st);
+cudaError_t launch_centroid_update(const float* X, long long ldx, int d, const long long* perm,
+                                   const long long* offsets, int nlist, float* C, long long ldc, cudaStream_t st);
+cudaError_t launch_gather_rows(const float* X, long long ldx, const long long* perm, long long n, int dp,
+                               float* out, cudaStream_t st);
+
+}  // namespace tri

@@ -1,0 +1,332 @@
+// IVF-Flat device pieces: the continuous-batch packer (ragged per-query k and
+// nprobe -> list-major work items in one launch) and the k-means / inverted
+// list layout used at index build.
+#include "tri_common.cuh"
+#include "tri_internal.h"
+
+namespace tri {
+
+// ---------------------------------------------------------------------------
+// Packer.  Given each query's probed lists (from the exact coarse step) build
+//   * per (list, capacity-class) member counts,
+//   * work items in descending list-size order (longest-processing-time first
+//     for the persistent scan), one per group of <= gmax queries,
+//   * the members: (query, partial-list slot) pairs.
+// Member order inside a group is atomic-order dependent, which never changes
+// results: a (query, row) distance is computed by the same instruction chain in
+// whichever group position the query lands.
+
+__global__ void pack_hist_kernel(PackLaunch p) {
+  const int q = blockIdx.x;
+  const int np = p.nprobe[q];
+  const int cls = p.meta[q].cls;
+  long long tot = 0;
+  for (int j = threadIdx.x; j < np; j += blockDim.x) {
+    long long l = p.probes[(long long)q * p.ld_probes + j];
+    atomicAdd(&p.counts[l * kNumCls + cls], 1);
+    tot += p.list_off[l + 1] - p.list_off[l];
+  }
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  __shared__ long long part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = tot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[w];
+    p.meta[q].n_total = s;
+  }
+}
+
+__global__ void __launch_bounds__(1024) pack_items_kernel(PackLaunch p) {
+  __shared__ int s_mem[32], s_grp[32];
+  __shared__ int carry_mem, carry_grp;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    carry_mem = 0;
+    carry_grp = 0;
+  }
+  __syncthreads();
+  const int E = p.nlist * kNumCls;
+  for (int base = 0; base < E; base += 1024) {
+    const int e = base + tid;
+    int cnt = 0, ngrp = 0, l = 0, cls = 0;
+    long long lsize = 0;
+    if (e < E) {
+      l = p.list_by_size[e / kNumCls];
+      cls = e % kNumCls;
+      cnt = p.counts[l * kNumCls + cls];
+      lsize = p.list_off[l + 1] - p.list_off[l];
+      ngrp = (cnt > 0 && lsize > 0) ? (cnt + p.gmax - 1) / p.gmax : 0;
+    }
+    // block exclusive scan of (cnt, ngrp)
+    int im = cnt, ig = ngrp;
+    for (int o = 1; o < 32; o <<= 1) {
+      int a = __shfl_up_sync(0xffffffffu, im, o), b = __shfl_up_sync(0xffffffffu, ig, o);
+      if (lane >= o) {
+        im += a;
+        ig += b;
+      }
+    }
+    if (lane == 31) {
+      s_mem[warp] = im;
+      s_grp[warp] = ig;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int vm = s_mem[lane], vg = s_grp[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        int a = __shfl_up_sync(0xffffffffu, vm, o), b = __shfl_up_sync(0xffffffffu, vg, o);
+        if (lane >= o) {
+          vm += a;
+          vg += b;
+        }
+      }
+      s_mem[lane] = vm;
+      s_grp[lane] = vg;
+    }
+    __syncthreads();
+    const int mem_before = carry_mem + (warp ? s_mem[warp - 1] : 0) + im - cnt;
+    const int grp_before = carry_grp + (warp ? s_grp[warp - 1] : 0) + ig - ngrp;
+    if (e < E) {
+      p.member_base[l * kNumCls + cls] = mem_before;
+      for (int g = 0; g < ngrp; ++g) {
+        WorkItem w;
+        w.row_begin = p.list_off[l];
+        w.row_count = (int)lsize;
+        w.member_begin = mem_before + g * p.gmax;
+        w.member_count = min(p.gmax, cnt - g * p.gmax);
+        w.kp = kMinKp << cls;
+        w.pad0 = l;
+        w.pad1 = 0;
+        p.items[grp_before + g] = w;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      carry_mem += s_mem[31];
+      carry_grp += s_grp[31];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *p.n_items = carry_grp;
+}
+
+__global__ void pack_fill_kernel(PackLaunch p) {
+  const int q = blockIdx.x;
+  const int np = p.nprobe[q];
+  const QueryMeta m = p.meta[q];
+  for (int j = threadIdx.x; j < np; j += blockDim.x) {
+    long long l = p.probes[(long long)q * p.ld_probes + j];
+    int slot = atomicAdd(&p.fill[l * kNumCls + m.cls], 1);
+    Member mb;
+    mb.q = q;
+    mb.pad = j;
+    mb.slot = m.part_off + (long long)j * m.kp;
+    p.members[p.member_base[l * kNumCls + m.cls] + slot] = mb;
+  }
+}
+
+cudaError_t launch_pack(const PackLaunch& p, cudaStream_t st) {
+  if (p.B <= 0) return cudaSuccess;
+  size_t cbytes = (size_t)p.nlist * kNumCls * sizeof(int);
+  cudaError_t e = cudaMemsetAsync(p.counts, 0, cbytes, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.fill, 0, cbytes, st);
+  if (e != cudaSuccess) return e;
+  pack_hist_kernel<<<p.B, 64, 0, st>>>(p);
+  pack_items_kernel<<<1, 1024, 0, st>>>(p);
+  pack_fill_kernel<<<p.B, 64, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// k-means assignment: nearest centroid by fp32 dot-form score cn - 2 x.c
+// (the row norm is constant per row).  64x64 register-tiled SGEMM with a
+// running (score, centroid id) argmin; ties go to the smaller id.
+
+constexpr int AB = 64, AK = 16;
+
+__global__ void __launch_bounds__(256) assign_kernel(const float* __restrict__ X, long long n, long long ldx,
+                                                     int dp, const float* __restrict__ C, int nlist, long long ldc,
+                                                     const float* __restrict__ cnorm, int* __restrict__ assign) {
+  __shared__ __align__(16) float As[AK][AB];
+  __shared__ __align__(16) float Bs[AK][AB];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const long long row0 = (long long)blockIdx.x * AB;
+  float best[4];
+  int bid[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    best[i] = __int_as_float(0x7f800000);
+    bid[i] = 0x7fffffff;
+  }
+  const int lr = tid >> 2, lk = (tid & 3) * 4;
+  for (int c0 = 0; c0 < nlist; c0 += AB) {
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int k0 = 0; k0 < dp; k0 += AK) {
+      float4 av = make_float4(0.f, 0.f, 0.f, 0.f), bv = av;
+      if (row0 + lr < n && k0 + lk < dp) av = *reinterpret_cast<const float4*>(X + (row0 + lr) * ldx + k0 + lk);
+      if (c0 + lr < nlist && k0 + lk < dp) bv = *reinterpret_cast<const float4*>(C + (long long)(c0 + lr) * ldc + k0 + lk);
+      __syncthreads();
+      As[lk + 0][lr] = av.x;
+      As[lk + 1][lr] = av.y;
+      As[lk + 2][lr] = av.z;
+      As[lk + 3][lr] = av.w;
+      Bs[lk + 0][lr] = bv.x;
+      Bs[lk + 1][lr] = bv.y;
+      Bs[lk + 2][lr] = bv.z;
+      Bs[lk + 3][lr] = bv.w;
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < AK; ++kk) {
+        float4 a = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+        float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+        float ar[4] = {a.x, a.y, a.z, a.w}, br[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int c = c0 + tx * 4 + j;
+      if (c < nlist) {
+        float cn = cnorm[c];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float s = __fmaf_rn(-2.f, acc[i][j], cn);
+          if (s < best[i] || (s == best[i] && c < bid[i])) {
+            best[i] = s;
+            bid[i] = c;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float s = best[i];
+    int c = bid[i];
+    for (int o = 1; o < 16; o <<= 1) {
+      float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      int c2 = __shfl_xor_sync(0xffffffffu, c, o);
+      if (s2 < s || (s2 == s && c2 < c)) {
+        s = s2;
+        c = c2;
+      }
+    }
+    long long r = row0 + ty * 4 + i;
+    if (tx == 0 && r < n) assign[r] = c;
+  }
+}
+
+cudaError_t launch_assign(const float* X, long long n, int d, long long ldx, const float* C, int nlist,
+                          long long ldc, const float* cnorm, int* assign, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int dp = (d + 3) & ~3;
+  assign_kernel<<<(unsigned)((n + AB - 1) / AB), 256, 0, st>>>(X, n, ldx, dp, C, nlist, ldc, cnorm, assign);
+  return cudaGetLastError();
+}
+
+__global__ void counts_kernel(const int* __restrict__ assign, long long n, int* counts) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(&counts[assign[i]], 1);
+}
+
+cudaError_t launch_counts(const int* assign, long long n, int nlist, int* counts, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)nlist * sizeof(int), st);
+  if (e != cudaSuccess || n <= 0) return e;
+  counts_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(assign, n, counts);
+  return cudaGetLastError();
+}
+
+// One CTA per list: ballot-compact the ids assigned to it, in ascending order.
+__global__ void __launch_bounds__(1024) list_members_kernel(const int* __restrict__ assign, long long n,
+                                                            const long long* __restrict__ offsets,
+                                                            long long* __restrict__ perm) {
+  __shared__ int wsum[32];
+  __shared__ long long s_run;
+  const int l = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_run = offsets[l];
+  __syncthreads();
+  for (long long base = 0; base < n; base += 1024) {
+    long long i = base + threadIdx.x;
+    bool hit = i < n && assign[i] == l;
+    unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) wsum[warp] = __popc(m);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < 32; ++w) {
+      int v = wsum[w];
+      if (w < warp) before += v;
+      total += v;
+    }
+    if (hit) perm[s_run + before + __popc(m & ((1u << lane) - 1))] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) s_run += total;
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_list_members(const int* assign, long long n, int nlist, const long long* offsets,
+                                long long* perm, cudaStream_t st) {
+  if (nlist <= 0) return cudaSuccess;
+  list_members_kernel<<<nlist, 1024, 0, st>>>(assign, n, offsets, perm);
+  return cudaGetLastError();
+}
+
+// Deterministic mean: members summed in ascending id order in float64.
+__global__ void __launch_bounds__(256) centroid_update_kernel(const float* __restrict__ X, long long ldx, int d,
+                                                              const long long* __restrict__ perm,
+                                                              const long long* __restrict__ offsets,
+                                                              float* __restrict__ C, long long ldc) {
+  const int l = blockIdx.x;
+  const long long lo = offsets[l], hi = offsets[l + 1];
+  if (hi <= lo) return;  // empty list keeps its previous centroid
+  const double inv = 1.0 / (double)(hi - lo);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double s = 0.0;
+    long long m = lo;
+    for (; m + 4 <= hi; m += 4) {
+      float a = X[perm[m] * ldx + j], b = X[perm[m + 1] * ldx + j];
+      float c = X[perm[m + 2] * ldx + j], e = X[perm[m + 3] * ldx + j];
+      s += (double)a;
+      s += (double)b;
+      s += (double)c;
+      s += (double)e;
+    }
+    for (; m < hi; ++m) s += (double)X[perm[m] * ldx + j];
+    C[(long long)l * ldc + j] = __double2float_rn(s * inv);
+  }
+}
+
+cudaError_t launch_centroid_update(const float* X, long long ldx, int d, const long long* perm,
+                                   const long long* offsets, int nlist, float* C, long long ldc, cudaStream_t st) {
+  if (nlist <= 0) return cudaSuccess;
+  centroid_update_kernel<<<nlist, 256, 0, st>>>(X, ldx, d, perm, offsets, C, ldc);
+  return cudaGetLastError();
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ X, long long ldx, const long long* __restrict__ perm,
+                                   long long n, int dp, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const float4* src = reinterpret_cast<const float4*>(X + perm[r] * ldx);
+  float4* dst = reinterpret_cast<float4*>(out + r * (long long)dp);
+  for (int j = lane; j < dp / 4; j += 32) dst[j] = src[j];
+}
+
+cudaError_t launch_gather_rows(const float* X, long long ldx, const long long* perm, long long n, int dp,
+                               float* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  gather_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(X, ldx, perm, n, dp, out);
+  return cudaGetLastError();
+}
+
+}  // namespace tri

@@ -1,0 +1,149 @@
+"""Brute-force exact kNN on the GPU vs the reference's golden vectors and the oracle."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import trinity_oracle as orc
+from paper_2512_02281_b200 import _lib
+from paper_2512_02281_b200.ann_graph import (
+    VectorStore,
+    brute_force_knn,
+    brute_force_knn_batch,
+    build_knn_graph,
+    distance,
+    store_sq_dists,
+    validate_graph,
+)
+from paper_2512_02281_b200.workload import gen_matrix
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _reset_options():
+    yield
+    _lib.set_option("force_fixup", 0)
+    _lib.set_option("kp_extra", 0)
+
+
+def test_distance_kats(golden_dir):
+    with open(os.path.join(golden_dir, "distance_kats.json")) as f:
+        cases = json.load(f)
+    for c in cases:
+        assert distance(np.array(c["a"], np.float32), np.array(c["b"], np.float32)) == c["dist"]
+
+
+def test_bruteforce_golden_small_all_k(golden_dir):
+    g = np.load(os.path.join(golden_dir, "bf_small.npz"))
+    store = VectorStore(data=gen_matrix(1000, 8, 11))
+    for k in (10, 1, 37, 1000):
+        ids, d = brute_force_knn_batch(store, g["queries"], k)
+        assert np.array_equal(ids, g[f"ids_k{k}"]), k
+        assert np.array_equal(d, g[f"dists_k{k}"]), k  # bit-exact float64
+
+
+def test_bruteforce_single_query_api(golden_dir):
+    g = np.load(os.path.join(golden_dir, "bf_small.npz"))
+    store = VectorStore(data=gen_matrix(1000, 8, 11))
+    res = brute_force_knn(store, g["queries"][3], 10)
+    assert [n.id for n in res] == g["ids_k10"][3].tolist()
+    assert [n.dist for n in res] == g["dists_k10"][3].tolist()
+
+
+def test_bruteforce_line_store(golden_dir):
+    with open(os.path.join(golden_dir, "bf_line.json")) as f:
+        cases = json.load(f)
+    store = VectorStore(data=np.array([[0.0], [1.0], [2.0]], np.float32))
+    for c in cases:
+        res = brute_force_knn(store, np.array([c["q"]]), c["k"])
+        assert [n.id for n in res] == c["ids"] and [n.dist for n in res] == c["dists"]
+    with pytest.raises(ValueError):
+        brute_force_knn(store, np.array([0.0]), 4)
+    with pytest.raises(ValueError):
+        brute_force_knn(store, np.array([0.0]), 0)
+    with pytest.raises(ValueError):
+        brute_force_knn(store, np.array([0.0, 1.0]), 1)
+
+
+def test_c1_kat_all_queries(golden_dir):
+    """BASELINE config C1 (100K x 128, B=64, k=10): ids and distances bit-exact."""
+    g = np.load(os.path.join(golden_dir, "bf_c1.npz"))
+    store = VectorStore(data=gen_matrix(100_000, 128, 1))
+    qs = gen_matrix(64, 128, 2)
+    ids, d = brute_force_knn_batch(store, qs, 10)
+    assert np.array_equal(ids, g["ids"])
+    assert np.array_equal(d, g["dists"])
+    assert store.device().last_fixups() == 0  # certified without the fallback
+
+
+def test_forced_fixup_path_is_exact(golden_dir):
+    g = np.load(os.path.join(golden_dir, "bf_c1.npz"))
+    store = VectorStore(data=gen_matrix(100_000, 128, 1))
+    qs = gen_matrix(64, 128, 2)
+    _lib.set_option("force_fixup", 1)
+    ids, d = brute_force_knn_batch(store, qs[:8], 10)
+    assert store.device().last_fixups() == 8
+    assert np.array_equal(ids, g["ids"][:8]) and np.array_equal(d, g["dists"][:8])
+
+
+def test_ragged_k_and_capacity_classes():
+    rng = np.random.Generator(np.random.Philox(21))
+    data = rng.standard_normal((20_000, 40)).astype(np.float32)
+    store = VectorStore(data=data)
+    qs = rng.standard_normal((37, 40))
+    ks = np.array([1, 10, 100, 33, 250, 64, 7] * 5 + [500, 1000])
+    ids, d = brute_force_knn_batch(store, qs, ks)
+    for i in range(qs.shape[0]):
+        oi, od = orc.exact_knn(data, qs[i], int(ks[i]))
+        assert np.array_equal(ids[i, : ks[i]], oi), i
+        assert np.array_equal(d[i, : ks[i]], od), i
+
+
+@pytest.mark.parametrize("dim", [1, 3, 5, 16, 17, 100, 768, 1000])
+def test_odd_dimensions(dim):
+    rng = np.random.Generator(np.random.Philox(dim))
+    data = rng.standard_normal((3000, dim)).astype(np.float32)
+    store = VectorStore(data=data)
+    qs = rng.standard_normal((9, dim))
+    ids, d = brute_force_knn_batch(store, qs, 12)
+    for i in range(9):
+        oi, od = orc.exact_knn(data, qs[i], 12)
+        assert np.array_equal(ids[i], oi) and np.array_equal(d[i], od)
+
+
+def test_exact_ties_break_by_id():
+    # many duplicate rows: distances tie exactly, order must follow ids
+    base = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]], np.float32)
+    data = np.tile(base, (400, 1))
+    store = VectorStore(data=data)
+    q = np.array([[0.1, 0.1], [0.5, 0.5]])
+    ids, d = brute_force_knn_batch(store, q, 50)
+    for i in range(2):
+        oi, od = orc.exact_knn(data, q[i], 50)
+        assert np.array_equal(ids[i], oi) and np.array_equal(d[i], od)
+
+
+def test_nonfinite_query_rejected():
+    store = VectorStore(data=np.eye(4, dtype=np.float32))
+    with pytest.raises(ValueError, match="finite"):
+        brute_force_knn(store, np.array([np.nan, 0, 0, 0]), 1)
+
+
+def test_store_sq_dists_and_mixed_batch(golden_dir):
+    g = np.load(os.path.join(golden_dir, "mixed_batch.npz"))
+    store = VectorStore(data=gen_matrix(50, 4, 3))
+    qd = {0: g["q0"], 1: g["q1"]}
+    for o, c, dist in zip(g["owners"], g["cands"], g["dists"]):
+        assert store_sq_dists(store, qd[int(o)], [int(c)])[0] == dist
+
+
+def test_knn_graph_matches_reference(golden_dir):
+    """GPU build_knn_graph == the reference's graph on the acceptance workload."""
+    g = np.load(os.path.join(golden_dir, "engine_c1.npz"))
+    store = VectorStore(data=gen_matrix(5000, 16, 20_240_601))
+    graph = build_knn_graph(store, 16)
+    assert validate_graph(graph, store.count).ok
+    assert np.array_equal(graph.adjacency, g["adjacency"])

@@ -1,0 +1,159 @@
+"""IVF-Flat on the GPU vs the reference-primitive golden vectors and the oracle."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import trinity_oracle as orc
+from paper_2512_02281_b200 import _lib
+from paper_2512_02281_b200.ann_graph import VectorStore
+from paper_2512_02281_b200.ivf import IVFFlatIndex
+from paper_2512_02281_b200.workload import gen_matrix, gen_vectors_chunked
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _reset_options():
+    yield
+    _lib.set_option("force_fixup", 0)
+
+
+@pytest.fixture(scope="module")
+def small(golden_dir):
+    g = np.load(os.path.join(golden_dir, "ivf_small.npz"))
+    data = gen_matrix(20_000, 32, 5)
+    store = VectorStore(data=data)
+    idx = IVFFlatIndex.from_artifact(store, g["centroids"], g["assign"])
+    return g, data, idx
+
+
+def _check_rows(ids, d, g, ks):
+    for i in range(ids.shape[0]):
+        n = int((g["ids"][i] >= 0).sum())
+        k = int(ks[i])
+        m = min(k, n)
+        assert np.array_equal(ids[i, :m], g["ids"][i, :m]), i
+        assert np.array_equal(d[i, :m], g["dists"][i, :m]), i
+        assert (ids[i, m:k] == -1).all()
+
+
+def test_ivf_golden_ragged(small):
+    g, data, idx = small
+    qs = gen_matrix(40, 32, 7)
+    ids, d = idx.search(qs, g["ks"], g["nprobes"])
+    _check_rows(ids, d, g, g["ks"])
+    probes = idx.last_probes(40, 16)
+    for i in range(40):
+        npb = int(g["nprobes"][i])
+        assert probes[i, :npb].tolist() == g["probes"][i, :npb].tolist()
+
+
+def test_ivf_forced_fixup(small):
+    g, data, idx = small
+    qs = gen_matrix(40, 32, 7)
+    _lib.set_option("force_fixup", 1)
+    ids, d = idx.search(qs, g["ks"], g["nprobes"])
+    assert idx.last_fixups() > 0
+    _check_rows(ids, d, g, g["ks"])
+
+
+def test_ivf_export_roundtrip(small):
+    g, data, idx = small
+    cen, asg = idx.export()
+    assert np.array_equal(cen, g["centroids"]) and np.array_equal(asg, g["assign"])
+    sizes = idx.list_sizes()
+    assert np.array_equal(sizes, np.bincount(g["assign"], minlength=64))
+
+
+def test_ivf_single_and_full_probe(small):
+    g, data, idx = small
+    art = orc.IVFArtifact(g["centroids"], g["assign"])
+    qs = gen_matrix(5, 32, 99)
+    for npb in (1, 64):
+        ids, d = idx.search(qs, 10, npb)
+        for i in range(5):
+            oi, od = orc.ivf_search(data, art, qs[i], 10, npb)
+            assert np.array_equal(ids[i], oi) and np.array_equal(d[i], od)
+    # nprobe = nlist is exact brute force
+    bi, bd = orc.exact_knn(data, qs[0], 10)
+    ids, d = idx.search(qs[:1], 10, 64)
+    assert np.array_equal(ids[0], bi) and np.array_equal(d[0], bd)
+
+
+def test_ivf_trained_index_parity_and_balance():
+    data = gen_matrix(30_000, 48, 11)
+    store = VectorStore(data=data)
+    idx = IVFFlatIndex.train(store, nlist=100, iters=5, seed=3)
+    cen, asg = idx.export()
+    sizes = np.bincount(asg, minlength=100)
+    assert sizes.sum() == 30_000 and sizes.max() < 5 * 300
+    # assignment really is nearest-centroid (up to fp32 near-ties)
+    d2 = ((data[:2000, None, :].astype(np.float64) - cen[None].astype(np.float64)) ** 2).sum(-1)
+    agree = (np.argmin(d2, axis=1) == asg[:2000]).mean()
+    assert agree > 0.999
+    art = orc.IVFArtifact(cen, asg)
+    qs = gen_matrix(24, 48, 12)
+    ks = np.array([10, 100, 10] * 8)
+    nps = np.array([8, 32, 4] * 8)
+    ids, d = idx.search(qs, ks, nps)
+    for i in range(24):
+        oi, od = orc.ivf_search(data, art, qs[i], int(ks[i]), int(nps[i]))
+        assert np.array_equal(ids[i, : oi.size], oi) and np.array_equal(d[i, : oi.size], od)
+
+
+def test_ivf_empty_lists_and_tiny_lists():
+    rng = np.random.Generator(np.random.Philox(5))
+    data = rng.standard_normal((300, 8)).astype(np.float32)
+    cen = rng.standard_normal((20, 8)).astype(np.float32)
+    asg = rng.integers(0, 5, size=300).astype(np.int32)  # lists 5..19 empty
+    store = VectorStore(data=data)
+    idx = IVFFlatIndex.from_artifact(store, cen, asg)
+    art = orc.IVFArtifact(cen, asg)
+    qs = rng.standard_normal((10, 8))
+    ids, d = idx.search(qs, 50, 3)
+    for i in range(10):
+        oi, od = orc.ivf_search(data, art, qs[i], 50, 3)
+        n = oi.size
+        assert np.array_equal(ids[i, :n], oi) and np.array_equal(d[i, :n], od)
+        assert (ids[i, n:] == -1).all()
+
+
+def test_ivf_id_offset_shard():
+    rng = np.random.Generator(np.random.Philox(6))
+    data = rng.standard_normal((2000, 16)).astype(np.float32)
+    art = orc.kmeans(data, 16, 3, 1)
+    store = VectorStore(data=data[1000:])
+    idx = IVFFlatIndex.from_artifact(store, art.centroids, art.assign[1000:], id_offset=1000)
+    q = rng.standard_normal((3, 16))
+    ids, d = idx.search(q, 5, 16)
+    for i in range(3):
+        oi, od = orc.exact_knn(data[1000:], q[i], 5)
+        assert np.array_equal(ids[i], oi + 1000) and np.array_equal(d[i], od)
+
+
+@pytest.mark.slow
+def test_c2_scale_parity():
+    """BASELINE C2 shape (1M x 768, nlist 1024, nprobe 32, B 256, k 10), oracle on a subset."""
+    data = gen_vectors_chunked(1_000_000, 768, seed=3)
+    store = VectorStore(data=data)
+    idx = IVFFlatIndex.train(store, nlist=1024, iters=5, seed=4)
+    qs = gen_matrix(256, 768, 4)
+    ids, d = idx.search(qs, 10, 32)
+    assert idx.last_fixups() == 0
+    cen, asg = idx.export()
+    art = orc.IVFArtifact(cen, asg)
+    for i in range(0, 256, 16):
+        oi, od = orc.ivf_search(data, art, qs[i], 10, 32)
+        assert np.array_equal(ids[i], oi) and np.array_equal(d[i], od)
+    # size-independent property: every returned distance is the exact distance of that id
+    sel = ids[:, :10].ravel()
+    q_rep = np.repeat(qs.astype(np.float64), 10, axis=0)
+    diff = q_rep - data[sel].astype(np.float64)
+    ref = np.einsum("ij,ij->i", diff, diff)
+    assert np.array_equal(ref, d[:, :10].ravel())
+    # and rows are sorted by (dist, id)
+    for i in range(256):
+        order = np.lexsort((ids[i], d[i]))
+        assert np.array_equal(order, np.arange(10))
