@@ -1,0 +1,381 @@
+"""Benchmark of the Trinity vector-search pool hot path on B200.
+
+Headline (N=1): BASELINE.json config C2 -- IVF-Flat over 1M x 768 fp32 synthetic
+vectors, nlist=1024 (5 Lloyd iterations), nprobe=32, batch 256, k=10.  A step is
+one batch of 256 queries through the whole device pipeline (exact coarse step,
+device packer, list scan, merge, exact fp64 re-rank, certified fix-up).
+
+N>1 (torchrun, one process per GPU): strong scaling of the same 1M database,
+vector-sharded by id range with the k-means artifact replicated; each rank
+searches its shard and the per-shard top-k lists are all-gathered over NCCL
+and merged on the device by (dist, id).
+
+--impl reference: the CPU oracle (numpy restatement of the reference's
+algorithm, oracle/trinity_oracle.py) on the host cores, same config and metric.
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DB, DIM, NLIST, ITERS, NPROBE, BATCH, K = 1_000_000, 768, 1024, 5, 32, 256, 10
+DB_SEED, Q_SEED, KM_SEED = 3, 4, 4
+METRIC = "search QPS (IVF-Flat 1M x 768, nlist 1024, nprobe 32, k 10)"
+UNIT = "queries/s"
+CONFIG = {
+    "workload": "C2: IVF-Flat 1M x 768 fp32, nlist=1024 (5 Lloyd iters), nprobe=32, batch=256, k=10",
+    "n_db": N_DB, "dim": DIM, "nlist": NLIST, "nprobe": NPROBE, "global_batch": BATCH, "k": K,
+    "db": "gen_vectors_chunked(1_000_000, 768, seed=3): 131072-row Philox chunks seeded [3, i]",
+    "queries": "gen_vectors(256, 768, seed=4) as float64",
+    "l2": "no flush: each batch scans ~3.1 GB of inverted lists (> 126 MB L2); 3 MB of centroids stay L2-resident",
+    "parallelism": "dp1",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=24, help="queries timed for cpu_baseline")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_scan_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML SM-clock / throttle-reason sampler running during the timed region."""
+
+    NAMES = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.NAMES.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_inputs():
+    from paper_2512_02281_b200.workload import gen_matrix, gen_vectors_chunked
+
+    data = gen_vectors_chunked(N_DB, DIM, DB_SEED)
+    queries = gen_matrix(BATCH, DIM, Q_SEED).astype(np.float64)
+    return data, queries
+
+
+def cpu_baseline_qps(data, art, queries, n_sample):
+    from oracle import trinity_oracle as orc
+
+    t0 = time.perf_counter()
+    for i in range(n_sample):
+        orc.ivf_search(data, art, queries[i], K, NPROBE)
+    dt = time.perf_counter() - t0
+    return n_sample / dt, dt
+
+
+# ----------------------------------------------------------------------------
+
+
+def run_reference(args):
+    """CPU oracle arm: numpy restatement of the reference path on all host cores."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from concurrent.futures import ProcessPoolExecutor
+
+    from oracle import trinity_oracle as orc
+
+    data, queries = make_inputs()
+    art = orc.kmeans(data, NLIST, ITERS, KM_SEED)
+    cores = os.cpu_count() or 1
+    per_step = max(cores, 16)
+    global _REF_STATE
+    _REF_STATE = (data, art, queries)
+    with ProcessPoolExecutor(max_workers=cores) as ex:  # fork: workers share the arrays copy-on-write
+        def one_step(s):
+            idx = [(s * per_step + j) % BATCH for j in range(per_step)]
+            list(ex.map(_ref_query, idx, chunksize=1))
+        for s in range(args.warmup):
+            one_step(s)
+        t0 = time.perf_counter()
+        for s in range(args.steps):
+            one_step(s)
+        dt = time.perf_counter() - t0
+    qps = per_step * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": dict(CONFIG, parallelism=f"cpu x{cores}"),
+        "cpu_baseline": {"value": qps, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{per_step} queries per step of the C2 batch, numpy oracle, "
+                                   f"one process per core"},
+        "e2e": {"value": qps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+_REF_STATE = None
+
+
+def _ref_query(i):
+    from oracle import trinity_oracle as orc
+
+    data, art, queries = _REF_STATE
+    return orc.ivf_search(data, art, queries[i], K, NPROBE)
+
+
+# ----------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from oracle import trinity_oracle as orc
+    from paper_2512_02281_b200 import _build
+    from paper_2512_02281_b200.ann_graph import _DeviceStore
+    from paper_2512_02281_b200.ivf import IVFFlatIndex, init_rows, merge_topk_device
+
+    _build.build()
+    data, queries = make_inputs()
+
+    # index: rank 0 trains on the full database, the artifact is broadcast
+    if world == 1:
+        store = _DeviceStore(data, device=local)
+        idx = IVFFlatIndex.train(store, NLIST, ITERS, KM_SEED)
+        cen, asg = idx.export()
+        shard_lo, shard_hi = 0, N_DB
+    else:
+        cen_t = torch.empty((NLIST, DIM), dtype=torch.float32, device="cuda")
+        asg_t = torch.empty((N_DB,), dtype=torch.int32, device="cuda")
+        if rank == 0:
+            full = _DeviceStore(data, device=local)
+            tmp = IVFFlatIndex.train(full, NLIST, ITERS, KM_SEED)
+            c, a = tmp.export()
+            tmp.close()
+            full.close()
+            cen_t.copy_(torch.from_numpy(c))
+            asg_t.copy_(torch.from_numpy(a))
+        dist.broadcast(cen_t, 0)
+        dist.broadcast(asg_t, 0)
+        cen, asg = cen_t.cpu().numpy(), asg_t.cpu().numpy()
+        shard_lo = rank * N_DB // world
+        shard_hi = (rank + 1) * N_DB // world
+        store = _DeviceStore(data[shard_lo:shard_hi], device=local)
+        idx = IVFFlatIndex.from_artifact(store, cen, asg[shard_lo:shard_hi], id_offset=shard_lo)
+
+    q_dev = torch.from_numpy(queries).cuda()
+    ids_dev = torch.empty((BATCH, K), dtype=torch.int64, device="cuda")
+    d_dev = torch.empty((BATCH, K), dtype=torch.float64, device="cuda")
+    if world > 1:
+        g_ids = torch.empty((world, BATCH, K), dtype=torch.int64, device="cuda")
+        g_d = torch.empty((world, BATCH, K), dtype=torch.float64, device="cuda")
+        m_ids = torch.empty((BATCH, K), dtype=torch.int64, device="cuda")
+        m_d = torch.empty((BATCH, K), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        idx.search_device(q_dev, K, NPROBE, ids_dev, d_dev, stream)
+        if world > 1:
+            dist.all_gather_into_tensor(g_ids.view(-1), ids_dev.view(-1))
+            dist.all_gather_into_tensor(g_d.view(-1), d_dev.view(-1))
+            merge_topk_device(g_d, g_ids, K, m_d, m_ids, stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # correctness spot-check against the CPU oracle (untimed)
+    res_ids = (m_ids if world > 1 else ids_dev).cpu().numpy()
+    res_d = (m_d if world > 1 else d_dev).cpu().numpy()
+    art = orc.IVFArtifact(cen, asg)
+    if rank == 0:
+        for i in (0, 97, 255):
+            oi, od = orc.ivf_search(data, art, queries[i], K, NPROBE)
+            if not (np.array_equal(res_ids[i], oi) and np.array_equal(res_d[i], od)):
+                raise SystemExit(f"parity failure on query {i}")
+
+    # timed region: device-resident inputs
+    idx.set_profiling(True)
+    sampler = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    scan_ms, scan_n = idx.scan_time()
+    idx.set_profiling(False)
+    total_ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    qps = BATCH * args.steps / (total_ms / 1e3)
+    scan_bytes, pairs = idx.last_scan_bytes()
+
+    # e2e: public host API, pinned host buffers, copies inside the timed region
+    q_pin = torch.from_numpy(queries).pin_memory()
+    ids_pin = torch.empty((BATCH, K), dtype=torch.int64).pin_memory()
+    d_pin = torch.empty((BATCH, K), dtype=torch.float64).pin_memory()
+    for _ in range(3):
+        idx.search_into(q_pin, K, NPROBE, ids_pin, d_pin)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        idx.search_into(q_pin, K, NPROBE, ids_pin, d_pin)
+        if world > 1:
+            ids_dev.copy_(ids_pin, non_blocking=False)
+            d_dev.copy_(d_pin, non_blocking=False)
+            dist.all_gather_into_tensor(g_ids.view(-1), ids_dev.view(-1))
+            dist.all_gather_into_tensor(g_d.view(-1), d_dev.view(-1))
+            merge_topk_device(g_d, g_ids, K, m_d, m_ids, stream)
+            ids_pin.copy_(m_ids)
+            d_pin.copy_(m_d)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_qps = BATCH * args.steps / e2e_s
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    cpu_qps, cpu_dt = cpu_baseline_qps(data, art, queries, args.cpu_sample)
+    peak, peak_kind = load_peaks()
+    avg_scan_ms = scan_ms / max(scan_n, 1)
+    achieved = scan_bytes / (avg_scan_ms / 1e3) / 1e9
+    kernels_per_step = 12 + (1 if world > 1 else 0)
+    line = {
+        "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 scan + f64 re-rank", "data": "synthetic",
+        "config": dict(CONFIG, parallelism=f"vector-shard x{world}" if world > 1 else "dp1"),
+        "roofline": {
+            "bound": "hbm", "kernel": "tri::scan_kernel (IVF list scan)", "achieved": achieved, "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(),
+            "algorithmic_bytes_per_launch": scan_bytes, "scan_ms_per_launch": avg_scan_ms,
+            "scan_share_of_step": avg_scan_ms / (total_ms / args.steps),
+            "query_vector_pairs_per_launch": pairs,
+        },
+        "cpu_baseline": {"value": cpu_qps, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"first {args.cpu_sample} of the 256 C2 queries through the numpy oracle "
+                                   f"({cpu_dt:.1f} s, 1 core)"},
+        "e2e": {"value": e2e_qps, "unit": UNIT, "h2d_bytes_per_step": BATCH * DIM * 8,
+                "d2h_bytes_per_step": BATCH * K * 16},
+        "gpu_launches": kernels_per_step * args.steps,
+        "clocks": sampler.summary(),
+        "host_cores": os.cpu_count(),
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -185,17 +185,22 @@ def kmeans(data32: np.ndarray, nlist: int, iters: int, seed: int):
     rng = np.random.Generator(np.random.Philox(seed))
     n = data32.shape[0]
     cent = data32[np.sort(rng.choice(n, size=nlist, replace=False))].astype(np.float64)
-    x64 = data32.astype(np.float64)
-    xn = np.einsum("ij,ij->i", x64, x64)
     assign = np.zeros(n, dtype=np.int32)
-    for _ in range(iters + 1):
+    chunk = 1 << 16
+    for it in range(iters + 1):
         cn = np.einsum("ij,ij->i", cent, cent)
-        d = xn[:, None] + cn[None, :] - 2.0 * (x64 @ cent.T)
-        assign = np.argmin(d, axis=1).astype(np.int32)
-        if _ == iters:
+        for s in range(0, n, chunk):  # row norms are constant per row: argmin of cn - 2 x.c
+            x = data32[s:s + chunk].astype(np.float64)
+            assign[s:s + chunk] = np.argmin(cn[None, :] - 2.0 * (x @ cent.T), axis=1)
+        if it == iters:
             break
+        from scipy.sparse import csr_matrix
+
         sums = np.zeros_like(cent)
-        np.add.at(sums, assign, x64)
+        for s in range(0, n, chunk):
+            a = assign[s:s + chunk]
+            onehot = csr_matrix((np.ones(a.size), (a, np.arange(a.size))), shape=(nlist, a.size))
+            sums += onehot @ data32[s:s + chunk].astype(np.float64)
         cnt = np.bincount(assign, minlength=nlist)
         nz = cnt > 0
         cent[nz] = sums[nz] / cnt[nz, None]

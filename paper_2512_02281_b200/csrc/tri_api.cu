@@ -21,6 +21,7 @@ thread_local std::string g_err;
 long long g_force_fixup = 0;
 long long g_kp_extra = 0;
 constexpr int kSmemLimit = 225 * 1024;
+constexpr int kEventPairs = 4096;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -168,10 +169,12 @@ struct tri_ivf {
   int last_B = 0, last_npmax = 0;
   std::vector<int> last_np;
   bool prof = false;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // profiling: a ring of (start, stop) event pairs around the list-scan kernel,
+  // read back lazily so the timed loop never synchronises.
+  std::vector<cudaEvent_t> ev;
+  int ev_used = 0;
   double scan_ms = 0.0;
   int scan_launches = 0;
-  bool pending_event = false;
 };
 
 namespace {
@@ -680,8 +683,6 @@ static int ivf_finish(tri_ivf* v, tri_store* s, const float* Cdev, const int* as
   CU(cudaMemcpyAsync(v->assign, assign_dev, (size_t)v->n * sizeof(int), cudaMemcpyDeviceToDevice, st));
   TRY(store_from_device(Cdev, v->dp, v->nlist, v->d, v->device, &v->cstore));
   CU(cudaStreamCreateWithFlags(&v->own, cudaStreamNonBlocking));
-  CU(cudaEventCreate(&v->ev0));
-  CU(cudaEventCreate(&v->ev1));
   CU(cudaStreamSynchronize(st));
   return TRI_OK;
 }
@@ -793,8 +794,7 @@ int tri_ivf_destroy(tri_ivf* v) {
     release(*b);
   if (v->h_meta.p) cudaFreeHost(v->h_meta.p);
   if (v->cstore) tri_store_destroy(v->cstore);
-  if (v->ev0) cudaEventDestroy(v->ev0);
-  if (v->ev1) cudaEventDestroy(v->ev1);
+  for (cudaEvent_t e : v->ev) cudaEventDestroy(e);
   if (v->own) cudaStreamDestroy(v->own);
   delete v;
   return TRI_OK;
@@ -922,11 +922,19 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   sl.gmax = gmax;
   sl.cap = cap;
   sl.grid = (int)std::min<long long>(sm_count(v->device), members);
-  if (v->prof) CU(cudaEventRecord(v->ev0, st));
+  const bool rec = v->prof && v->ev_used < kEventPairs;
+  if (rec) {
+    while ((int)v->ev.size() < 2 * (v->ev_used + 1)) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      v->ev.push_back(e);
+    }
+    CU(cudaEventRecord(v->ev[2 * v->ev_used], st));
+  }
   CU(launch_scan(sl, st));
-  if (v->prof) {
-    CU(cudaEventRecord(v->ev1, st));
-    v->pending_event = true;
+  if (rec) {
+    CU(cudaEventRecord(v->ev[2 * v->ev_used + 1], st));
+    v->ev_used++;
   }
 
   // 5. merge, exact re-rank, certified fix-up
@@ -1036,21 +1044,21 @@ int tri_ivf_set_profiling(tri_ivf* v, int32_t on) {
   v->prof = on != 0;
   v->scan_ms = 0.0;
   v->scan_launches = 0;
-  v->pending_event = false;
+  v->ev_used = 0;
   return TRI_OK;
 }
 
 int tri_ivf_scan_time(tri_ivf* v, double* total_ms, int32_t* launches) {
   if (!v) return fail(TRI_EINVAL, "index is NULL");
   DeviceGuard g(v->device);
-  if (v->pending_event) {
-    CU(cudaEventSynchronize(v->ev1));
+  for (int i = 0; i < v->ev_used; ++i) {
+    CU(cudaEventSynchronize(v->ev[2 * i + 1]));
     float ms = 0.f;
-    CU(cudaEventElapsedTime(&ms, v->ev0, v->ev1));
+    CU(cudaEventElapsedTime(&ms, v->ev[2 * i], v->ev[2 * i + 1]));
     v->scan_ms += ms;
     v->scan_launches += 1;
-    v->pending_event = false;
   }
+  v->ev_used = 0;
   if (total_ms) *total_ms = v->scan_ms;
   if (launches) *launches = v->scan_launches;
   return TRI_OK;

@@ -124,6 +124,13 @@ class IVFFlatIndex:
                                                   kmax, ids.ctypes.data, dists.ctypes.data, None))
         return ids, dists
 
+    def search_into(self, q_host, k, nprobe, ids_out, dists_out) -> None:
+        """Host-buffer search into caller-owned (ideally pinned) arrays [B, ldo]."""
+        B = int(q_host.shape[0])
+        ks, nps = self._ragged(B, k, nprobe)
+        _lib.check(_lib.gpu().tri_ivf_search(self.handle, _lib.ptr(q_host), B, ks.ctypes.data, nps.ctypes.data,
+                                              int(ids_out.shape[1]), _lib.ptr(ids_out), _lib.ptr(dists_out), None))
+
     def search_device(self, q_dev, k, nprobe, ids_dev, dists_dev, stream=None) -> None:
         """Asynchronous search on device buffers (torch CUDA tensors or raw pointers).
 
