@@ -258,7 +258,9 @@ def run_ours(args):
         g_d = torch.empty((world, BATCH, K), dtype=torch.float64, device="cuda")
         m_ids = torch.empty((BATCH, K), dtype=torch.int64, device="cuda")
         m_d = torch.empty((BATCH, K), dtype=torch.float64, device="cuda")
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # explicit non-default stream: the library launches on it
+    torch.cuda.set_stream(stream)
+    torch.cuda.synchronize()
 
     def step():
         idx.search_device(q_dev, K, NPROBE, ids_dev, d_dev, stream)

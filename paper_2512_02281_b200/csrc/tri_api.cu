@@ -1,4 +1,6 @@
 // C-ABI of libtrinity_b200: handles, host-side planning and launch sequences.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -20,8 +22,11 @@ namespace {
 thread_local std::string g_err;
 long long g_force_fixup = 0;
 long long g_kp_extra = 0;
-constexpr int kSmemLimit = 225 * 1024;
+constexpr int kSmemLimit = 226 * 1024;
 constexpr int kEventPairs = 4096;
+constexpr int kSelCapMin = 512;  // >= one 512-row chunk of appends
+
+int round16(int d) { return (d + 15) & ~15; }
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -88,8 +93,12 @@ int ensure_host(HostBuf& b, size_t bytes) {
   return TRI_OK;
 }
 
-int kp_for(int k) {
-  long long want = (long long)k + std::max<long long>(16, k / 4) + g_kp_extra;
+long long g_scan_kernel = 0;  // 0 auto, 1 SIMT, 2 tensor core
+
+// Candidate capacity: over-fetch so the certified re-rank almost never falls
+// back.  TF32 candidates carry ~2^-9 relative dot error, so they over-fetch 2x.
+int kp_for(int k, bool tc) {
+  long long want = (long long)k + (tc ? std::max<long long>(16, k) : std::max<long long>(16, k / 4)) + g_kp_extra;
   int kp = kMinKp;
   while (kp < want) kp <<= 1;
   return kp;
@@ -107,28 +116,73 @@ int sm_count(int device) {
   return v;
 }
 
-// Relative error constant of the fp32 dot-form candidate distance:
-// |approx - exact| <= c * (|q| + |x|)^2 with c = gamma_d + 6u.
-double bound_const(int d) {
+// Error model of the approximate candidate distance D~ = fl(qn + xn - 2 q.x)
+// against the exact float64 D = |q64 - x|^2:
+//   |D~ - D| <= cdot * 2|q||x| + csum * (|q| + |x|)^2
+// csum = 6u covers query/norm rounding and the two fp32 additions (u = 2^-24);
+// cdot bounds the relative dot-product error: gamma_d for an fp32 FMA chain,
+// 2^-9 (both TF32 inputs truncated to 10 mantissa bits) + accumulation for
+// tcgen05 kind::tf32.
+struct Bound {
+  double cdot, csum;
+};
+Bound bound_for(int d, bool tc) {
   const double u = std::ldexp(1.0, -24);
-  const double gd = d * u / (1.0 - d * u);
-  return gd + 6.0 * u;
+  Bound b;
+  b.csum = 6.0 * u;
+  b.cdot = tc ? std::ldexp(1.0, -9) + std::ldexp(1.0, -19) + 2.0 * d * std::ldexp(1.0, -23) : d * u / (1.0 - d * u);
+  return b;
+}
+
+int sel_cap(int kp_max) { return std::max(kSelCapMin, 2 * kp_max); }
+
+// 2-D TMA descriptors over a row-major fp32 matrix (rows x ldx floats):
+//   SIMT scan : 64-row x 16-float boxes, 64-byte swizzle
+//   TC scan   : 32-row x 32-float boxes, 128-byte swizzle (UMMA K-major SW128)
+int make_tmap(CUtensorMap* map, const float* X, long long rows, int ldx, bool tc) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+    if (!fn || qr != cudaDriverEntryPointSuccess) return fail(TRI_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)ldx, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ldx * sizeof(float)};
+  cuuint32_t box[2] = {tc ? 32u : 16u, tc ? 32u : 64u};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, tc ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TRI_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TRI_OK;
+}
+
+// Scan kernel choice for a row width: the tensor-core scan unless forced off
+// or the queries do not fit its shared-memory layout.
+bool use_tc(int qld, int kp_max_tc) {
+  if (g_scan_kernel == 1) return false;
+  return kp_max_tc <= kMaxKp && qld <= kTcMaxQld &&
+         tc_scan_smem_bytes(qld, std::max(kSelCapMin, 2 * kp_max_tc)) <= (size_t)kSmemLimit;
 }
 
 // Per-search scratch shared by the brute-force and IVF pipelines.
 struct Workspace {
-  DevBuf q64, Q32, qn32, qn64, flags, plan, part, merged, out_ids, out_d;
+  DevBuf q64, Q32, qn32, qn64, flags, plan, part, merged, exact, out_ids, out_d;
   HostBuf h_plan;
   // cached host plan (brute force)
   std::vector<int> plan_k;
   int plan_B = -1;
   long long plan_n = -1;
   int n_items = 0, grid = 0, gmax = 0, cap = 0, kp_max = 0, k_max = 0;
+  long long plan_opts = -1;
+  bool tc = false;
   size_t off_items = 0, off_members = 0, plan_bytes = 0;
   long long part_keys = 0;
   int last_fixups = 0;
   void free_all() {
-    for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &out_ids, &out_d}) release(*b);
+    for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d}) release(*b);
     if (h_plan.p) cudaFreeHost(h_plan.p);
     h_plan.p = nullptr;
   }
@@ -144,6 +198,7 @@ struct tri_store {
   float* X = nullptr;
   float* xnorm = nullptr;
   double xmax = 0.0;
+  CUtensorMap tmap, tmap_tc;
   cudaStream_t own = nullptr;
   Workspace ws;
 };
@@ -160,6 +215,7 @@ struct tri_ivf {
   int* list_by_size = nullptr;
   int* assign = nullptr;  // per original row (store order)
   double xmax = 0.0;
+  CUtensorMap tmap, tmap_tc;
   std::vector<long long> h_off;
   tri_store* cstore = nullptr;  // centroids as a vector store (coarse step)
   cudaStream_t own = nullptr;
@@ -204,8 +260,8 @@ int store_from_device(const float* Xdev, long long ldx, long long n, int d, int 
   s->device = device;
   s->n = n;
   s->d = d;
-  s->dp = (d + 3) & ~3;
-  s->qld = (d + 15) & ~15;
+  s->dp = round16(d);
+  s->qld = s->dp;
   cudaError_t e = cudaMalloc(&s->X, (size_t)n * s->dp * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&s->xnorm, (size_t)n * sizeof(float));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->own, cudaStreamNonBlocking);
@@ -226,6 +282,12 @@ int store_from_device(const float* Xdev, long long ldx, long long n, int d, int 
     return fail(TRI_ECUDA, "store creation failed: %s", cudaGetErrorString(e));
   }
   std::memcpy(&s->xmax, &bits, sizeof(double));
+  int rc = make_tmap(&s->tmap, s->X, n, s->dp, false);
+  if (rc == TRI_OK) rc = make_tmap(&s->tmap_tc, s->X, n, s->dp, true);
+  if (rc != TRI_OK) {
+    tri_store_destroy(s);
+    return rc;
+  }
   *out = s;
   return TRI_OK;
 }
@@ -235,22 +297,44 @@ int store_from_device(const float* Xdev, long long ldx, long long n, int d, int 
 // ranges so that (#ranges x #groups) work items fill the GPU; items are
 // range-major so CTAs running concurrently share rows through L2.
 
+// Kernel + capacities for a batch: tensor-core scan when its layout fits.
+struct ScanChoice {
+  bool tc = false;
+  int kp_max = kMinKp, k_max = 1, cap = 0, gmax = 0;
+};
+
+int choose_scan(int qld, int d, int B, const int* k, std::vector<int>& kp, ScanChoice& ch) {
+  int kp_tc = kMinKp;
+  for (int i = 0; i < B; ++i) kp_tc = std::max(kp_tc, kp_for(k[i], true));
+  ch.tc = use_tc(qld, kp_tc);
+  kp.resize(B);
+  ch.kp_max = kMinKp;
+  ch.k_max = 1;
+  for (int i = 0; i < B; ++i) {
+    kp[i] = kp_for(k[i], ch.tc);
+    ch.kp_max = std::max(ch.kp_max, kp[i]);
+    ch.k_max = std::max(ch.k_max, k[i]);
+  }
+  ch.cap = sel_cap(ch.kp_max);
+  ch.gmax = ch.tc ? kTcGroup : scan_gmax(qld, ch.cap, kSmemLimit);
+  if (ch.gmax < 1) return fail(TRI_EINVAL, "dimension %d too large for the device scan", d);
+  return TRI_OK;
+}
+
+long long plan_opts() { return g_scan_kernel * 100000 + g_kp_extra; }
+
 int plan_bruteforce(tri_store* s, int B, const int* k, cudaStream_t st) {
   Workspace& w = s->ws;
-  if (w.plan_B == B && w.plan_n == s->n && (int)w.plan_k.size() == B &&
+  if (w.plan_B == B && w.plan_n == s->n && w.plan_opts == plan_opts() && (int)w.plan_k.size() == B &&
       std::equal(w.plan_k.begin(), w.plan_k.end(), k))
     return TRI_OK;
-  std::vector<int> kp(B), cls(B);
-  int kp_max = kMinKp, k_max = 1;
-  for (int i = 0; i < B; ++i) {
-    kp[i] = kp_for(k[i]);
-    cls[i] = cls_of(kp[i]);
-    kp_max = std::max(kp_max, kp[i]);
-    k_max = std::max(k_max, k[i]);
-  }
-  const int cap = 2 * kp_max;
-  const int gmax = scan_gmax(s->qld, cap, kSmemLimit);
-  if (gmax < 1) return fail(TRI_EINVAL, "dimension %d too large for the device scan", s->d);
+  std::vector<int> kp, cls(B);
+  ScanChoice ch;
+  TRY(choose_scan(s->qld, s->d, B, k, kp, ch));
+  for (int i = 0; i < B; ++i) cls[i] = cls_of(kp[i]);
+  const int kp_max = ch.kp_max, k_max = ch.k_max, cap = ch.cap, gmax = ch.gmax;
+  // Group size = the smem maximum: every extra group re-reads all rows (from
+  // L2), which costs more than the idle SMs of a short wave.
   // groups: consecutive same-class queries in index order
   std::vector<std::vector<int>> groups;
   for (int c = 0; c < kNumCls; ++c) {
@@ -267,7 +351,7 @@ int plan_bruteforce(tri_store* s, int B, const int* k, cudaStream_t st) {
   }
   const int nsm = sm_count(s->device);
   const long long max_ranges = std::max<long long>(1, (s->n + 511) / 512);
-  long long nr = std::max<long long>(1, (3LL * nsm + (long long)groups.size() - 1) / (long long)groups.size());
+  long long nr = std::max<long long>(1, ((long long)nsm + (long long)groups.size() - 1) / (long long)groups.size());
   nr = std::min(nr, max_ranges);
   long long R = (s->n + nr - 1) / nr;
   R = ((R + 511) / 512) * 512;
@@ -323,6 +407,8 @@ int plan_bruteforce(tri_store* s, int B, const int* k, cudaStream_t st) {
   CU(cudaStreamSynchronize(st));  // h_plan is reused by the next plan
   w.plan_B = B;
   w.plan_n = s->n;
+  w.plan_opts = plan_opts();
+  w.tc = ch.tc;
   w.plan_k.assign(k, k + B);
   w.n_items = (int)n_items;
   w.grid = (int)std::min<long long>(n_items, nsm);
@@ -351,6 +437,7 @@ int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int
   TRY(plan_bruteforce(s, B, k, st));
   TRY(ensure(w.part, (size_t)w.part_keys * sizeof(unsigned long long)));
   TRY(ensure(w.merged, (size_t)B * w.kp_max * sizeof(unsigned long long)));
+  TRY(ensure(w.exact, (size_t)B * w.kp_max * 16));
   TRY(ensure(w.flags, (size_t)(B + 64) * sizeof(int)));
   unsigned char* plan = static_cast<unsigned char*>(w.plan.p);
   const QueryMeta* meta = reinterpret_cast<const QueryMeta*>(plan);
@@ -361,6 +448,8 @@ int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int
   CU(cudaMemsetAsync(n_flag, 0, sizeof(int), st));
 
   ScanLaunch sl;
+  sl.tmap = &s->tmap;
+  sl.tmap_tc = &s->tmap_tc;
   sl.X = s->X;
   sl.ldx = s->dp;
   sl.xnorm = s->xnorm;
@@ -376,11 +465,12 @@ int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int
   sl.gmax = w.gmax;
   sl.cap = w.cap;
   sl.grid = w.grid;
-  CU(launch_scan(sl, st));
+  CU(w.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
   CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
                   st));
   RerankLaunch rr;
   rr.merged = w.merged.as<unsigned long long>();
+  rr.exact = reinterpret_cast<Exact*>(w.exact.p);
   rr.ld_merged = w.kp_max;
   rr.meta = meta;
   rr.q64 = q64dev;
@@ -391,7 +481,9 @@ int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int
   rr.idmap = nullptr;
   rr.id_offset = s->id_offset;
   rr.xmax = s->xmax;
-  rr.cbound = g_force_fixup ? 1e30 : bound_const(s->d);
+  const Bound bd = bound_for(s->d, w.tc);
+  rr.cdot = g_force_fixup ? 1e30 : bd.cdot;
+  rr.csum = bd.csum;
   rr.out_ids = ids;
   rr.out_d = dists;
   rr.ldo = ldo;
@@ -461,6 +553,7 @@ int tri_set_option(const char* name, int64_t value) {
   if (!name) return fail(TRI_EINVAL, "option name is NULL");
   if (!std::strcmp(name, "force_fixup")) g_force_fixup = value;
   else if (!std::strcmp(name, "kp_extra")) g_kp_extra = value;
+  else if (!std::strcmp(name, "scan_kernel")) g_scan_kernel = value;
   else return fail(TRI_EINVAL, "unknown option '%s'", name);
   return TRI_OK;
 }
@@ -621,6 +714,8 @@ static int ivf_layout(tri_ivf* v, const float* X, long long ldx, const long long
   CU(cudaMalloc(&v->xnl, (size_t)n * sizeof(float)));
   CU(cudaMalloc(&v->ids, (size_t)n * sizeof(long long)));
   CU(launch_gather_rows(X, ldx, perm_dev, n, v->dp, v->Xl, st));
+  TRY(make_tmap(&v->tmap, v->Xl, n, v->dp, false));
+  TRY(make_tmap(&v->tmap_tc, v->Xl, n, v->dp, true));
   unsigned long long* xm = nullptr;
   CU(cudaMalloc(&xm, sizeof(unsigned long long)));
   CU(cudaMemsetAsync(xm, 0, sizeof(unsigned long long), st));
@@ -846,16 +941,15 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   TRY(bruteforce_core(v->cstore, w, q, B, nprobe, npmax, v->probes.as<long long>(), v->probe_d.as<double>(), st));
 
   // 2. host-side per-query plan (k, kp, slots) -> device
-  std::vector<int> kp(B);
-  int kp_max = kMinKp, k_max = 1;
+  std::vector<int> kp;
+  ScanChoice ch;
+  TRY(choose_scan(v->qld, v->d, B, k, kp, ch));
+  const int kp_max = ch.kp_max, k_max = ch.k_max;
   long long part_keys = 0, members = 0;
   TRY(ensure_host(v->h_meta, (size_t)B * (sizeof(QueryMeta) + sizeof(int)) + 64));
   QueryMeta* hm = static_cast<QueryMeta*>(v->h_meta.p);
   int* hnp = reinterpret_cast<int*>(hm + B);
   for (int i = 0; i < B; ++i) {
-    kp[i] = kp_for(k[i]);
-    kp_max = std::max(kp_max, kp[i]);
-    k_max = std::max(k_max, k[i]);
     hm[i].k = k[i];
     hm[i].kp = kp[i];
     hm[i].n_slots = nprobe[i];
@@ -866,15 +960,16 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
     part_keys += (long long)nprobe[i] * kp[i];
     members += nprobe[i];
   }
-  const int cap = 2 * kp_max;
-  const int gmax = scan_gmax(v->qld, cap, kSmemLimit);
-  if (gmax < 1) return fail(TRI_EINVAL, "dimension %d too large for the device scan", v->d);
+  const int cap = ch.cap, gmax = ch.gmax;
+  int cls_mask = 0;
+  for (int i = 0; i < B; ++i) cls_mask |= 1 << hm[i].cls;
   TRY(ensure(v->meta, (size_t)B * (sizeof(QueryMeta) + sizeof(int)) + 64));
   CU(cudaMemcpyAsync(v->meta.p, v->h_meta.p, (size_t)B * (sizeof(QueryMeta) + sizeof(int)), cudaMemcpyHostToDevice, st));
   QueryMeta* dmeta = v->meta.as<QueryMeta>();
   int* dnp = reinterpret_cast<int*>(dmeta + B);
   TRY(ensure(w.part, (size_t)part_keys * sizeof(unsigned long long)));
   TRY(ensure(w.merged, (size_t)B * kp_max * sizeof(unsigned long long)));
+  TRY(ensure(w.exact, (size_t)B * kp_max * 16));
   CU(cudaMemsetAsync(w.part.p, 0xff, (size_t)part_keys * sizeof(unsigned long long), st));
   size_t cbytes = (size_t)v->nlist * kNumCls * sizeof(int);
   TRY(ensure(v->counts, cbytes));
@@ -903,10 +998,13 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   pk.n_items = ctr;
   pk.members = v->members.as<Member>();
   pk.gmax = gmax;
+  pk.cls_mask = cls_mask;
   CU(launch_pack(pk, st));
 
   // 4. list scan (persistent, one CTA per SM)
   ScanLaunch sl;
+  sl.tmap = &v->tmap;
+  sl.tmap_tc = &v->tmap_tc;
   sl.X = v->Xl;
   sl.ldx = v->dp;
   sl.xnorm = v->xnl;
@@ -931,7 +1029,7 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
     }
     CU(cudaEventRecord(v->ev[2 * v->ev_used], st));
   }
-  CU(launch_scan(sl, st));
+  CU(ch.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
   if (rec) {
     CU(cudaEventRecord(v->ev[2 * v->ev_used + 1], st));
     v->ev_used++;
@@ -944,6 +1042,7 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   CU(cudaMemsetAsync(n_flag, 0, sizeof(int), st));
   RerankLaunch rr;
   rr.merged = w.merged.as<unsigned long long>();
+  rr.exact = reinterpret_cast<Exact*>(w.exact.p);
   rr.ld_merged = kp_max;
   rr.meta = dmeta;
   rr.q64 = q;
@@ -954,7 +1053,9 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   rr.idmap = v->ids;
   rr.id_offset = 0;
   rr.xmax = v->xmax;
-  rr.cbound = g_force_fixup ? 1e30 : bound_const(v->d);
+  const Bound bd = bound_for(v->d, ch.tc);
+  rr.cdot = g_force_fixup ? 1e30 : bd.cdot;
+  rr.csum = bd.csum;
   rr.out_ids = reinterpret_cast<long long*>(ids);
   rr.out_d = dists;
   rr.ldo = ldo;

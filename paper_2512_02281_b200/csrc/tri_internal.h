@@ -41,6 +41,8 @@ constexpr int kMinKp = 32;
 constexpr int kMaxKp = 2048;
 
 struct ScanLaunch {
+  const void* tmap;     // CUtensorMap over X: 64-row x 16-float boxes, 64B swizzle (SIMT scan)
+  const void* tmap_tc;  // CUtensorMap over X: 32-row x 32-float boxes, 128B swizzle (tensor-core scan)
   const float* X;
   long long ldx;
   const float* xnorm;
@@ -62,6 +64,12 @@ size_t scan_smem_bytes(int gmax, int qld, int cap);
 int scan_gmax(int qld, int cap, int smem_limit);
 cudaError_t launch_scan(const ScanLaunch& s, cudaStream_t st);
 
+// tensor-core scan (tri_tcscan.cu): fixed groups of 16 queries, qld <= kTcMaxQld
+constexpr int kTcMaxQld = 1024;
+constexpr int kTcGroup = 16;
+size_t tc_scan_smem_bytes(int qld, int cap);
+cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st);
+
 cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,
                         int* bad, cudaStream_t st);
 cudaError_t launch_norms(const float* X, long long n, int d, long long ldx, float* xnorm,
@@ -70,8 +78,11 @@ cudaError_t launch_norms(const float* X, long long n, int d, long long ldx, floa
 cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, unsigned long long* merged,
                          int ld_merged, int B, int kp_max, cudaStream_t st);
 
+struct Exact;
+
 struct RerankLaunch {
   const unsigned long long* merged;
+  Exact* exact;             // B x ld_merged scratch
   int ld_merged;
   const QueryMeta* meta;
   const double* q64;
@@ -82,7 +93,8 @@ struct RerankLaunch {
   const long long* idmap;   // position -> id (nullptr: id = position)
   long long id_offset;
   double xmax;              // max row norm (sqrt of squared norm)
-  double cbound;            // relative error constant of the fp32 candidate distance
+  double cdot;              // |approx - exact| <= cdot*2|q||x| + csum*(|q|+|x|)^2
+  double csum;
   long long* out_ids;
   double* out_d;
   int ldo;
@@ -133,6 +145,7 @@ struct PackLaunch {
   const long long* list_off;
   const int* list_by_size;   // lists in descending size order
   int nlist;
+  int cls_mask;              // capacity classes present in the batch
   int* counts;               // nlist * kNumCls
   int* fill;                 // nlist * kNumCls
   int* member_base;          // nlist * kNumCls

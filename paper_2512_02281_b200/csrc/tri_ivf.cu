@@ -46,14 +46,17 @@ __global__ void __launch_bounds__(1024) pack_items_kernel(PackLaunch p) {
     carry_grp = 0;
   }
   __syncthreads();
-  const int E = p.nlist * kNumCls;
+  int pc[kNumCls], npc = 0;  // capacity classes present in this batch
+  for (int c = 0; c < kNumCls; ++c)
+    if (p.cls_mask & (1 << c)) pc[npc++] = c;
+  const int E = p.nlist * npc;
   for (int base = 0; base < E; base += 1024) {
     const int e = base + tid;
     int cnt = 0, ngrp = 0, l = 0, cls = 0;
     long long lsize = 0;
     if (e < E) {
-      l = p.list_by_size[e / kNumCls];
-      cls = e % kNumCls;
+      l = p.list_by_size[e / npc];
+      cls = pc[e % npc];
       cnt = p.counts[l * kNumCls + cls];
       lsize = p.list_off[l + 1] - p.list_off[l];
       ngrp = (cnt > 0 && lsize > 0) ? (cnt + p.gmax - 1) / p.gmax : 0;

@@ -1,22 +1,13 @@
-// Candidate generation, merge, exact re-rank and certified fix-up kernels.
-//
-// Pipeline for one batch of queries (brute force, IVF coarse step and IVF
-// list scan all share it):
-//   prep      fp64 queries -> fp32 rows + norms
-//   scan      persistent CTAs take WorkItems (row range x query group); each
-//             thread owns 2 rows per 512-row pass, rows stream HBM -> smem via
-//             a 3-stage cp.async pipeline (16-float slabs, XOR swizzle), queries
-//             sit in smem and are read as broadcasts; fp32 dot-form distances
-//             feed a per-query threshold-filtered selection buffer in smem
-//             (warp bitonic compaction).  The distance matrix never reaches HBM:
-//             only a top-kp list per (query, work item) is written.
+// Per-query kernels around the list scan (tri_listscan.cu):
+//   prep      fp64 queries -> fp32 rows (zero padded) + norms
 //   merge     per query: top-kp over its partial lists
-//   rerank    per query: fp64 distances in the reference's exact summation
-//             order, sort by (dist, id), certify (see below)
+//   exact     one thread pair per (query, candidate): fp64 distance in the
+//             reference's exact summation order (the two numpy lanes are two
+//             threads), then per query: sort by (dist, id) and certify
 //   fixup     per uncertified query: exact fp64 scan of its whole candidate set
 //
 // Certification: every dropped candidate has approx distance >= T (the kp-th
-// kept one) and |approx - exact| <= E = cbound*(|q|+max|x|)^2, so if the k-th
+// kept one) and |approx - exact| <= E = cdot*2|q|max|x| + csum*(|q|+max|x|)^2, so if the k-th
 // exact distance + E < T no dropped vector can enter the exact top-k.
 #include "tri_common.cuh"
 #include "tri_internal.h"
@@ -24,248 +15,6 @@
 namespace tri {
 
 constexpr int kThreads = 256;
-constexpr int kRowsPerThread = 2;
-constexpr int kChunk = kThreads * kRowsPerThread;  // rows per pass
-constexpr int kSlabW = 16;                          // floats per slab row
-constexpr int kStages = 3;
-constexpr int kSlabFloats = kChunk * kSlabW;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-size_t scan_smem_bytes(int gmax, int qld, int cap) {
-  return (size_t)gmax * qld * sizeof(float) + (size_t)kStages * kSlabFloats * sizeof(float) +
-         (size_t)gmax * cap * sizeof(unsigned long long);
-}
-
-int scan_gmax(int qld, int cap, int smem_limit) {
-  for (int g = 16; g >= 1; g >>= 1)
-    if (scan_smem_bytes(g, qld, cap) <= (size_t)smem_limit) return g;
-  return 0;
-}
-
-// Stage one 512-row x 16-float slab of X into shared memory (zero-filled
-// outside the valid rows / columns).  Row r, 16-byte chunk c lands at float4
-// index r*4 + (c ^ ((r >> 1) & 3)), which makes the row-per-thread LDS.128
-// reads below bank-conflict free.
-__device__ __forceinline__ void load_slab(float* slab, const float* __restrict__ X, long long ldx,
-                                          long long row0, int rows, int col0, int dp) {
-  const uint32_t base = smem_u32(slab);
-#pragma unroll
-  for (int j = 0; j < (kChunk * 4) / kThreads; ++j) {
-    int i = threadIdx.x + j * kThreads;
-    int r = i >> 2, c = i & 3;
-    int col = col0 + c * 4;
-    bool ok = (r < rows) && (col < dp);
-    const float* src = ok ? X + (row0 + r) * ldx + col : X;
-    uint32_t dst = base + (uint32_t)((r * 4 + (c ^ ((r >> 1) & 3))) * 16);
-    cp_async16(dst, src, ok ? 16 : 0);
-  }
-}
-
-struct ScanShared {
-  int cnt[16];
-  unsigned long long thr[16];
-  float qn[16];
-  int item;
-};
-
-template <int GT>
-__device__ void scan_item(const ScanLaunch& a, const WorkItem& w, float* Qs, float* slabs,
-                          unsigned long long* sel, ScanShared& sh) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gc = w.member_count;
-  const int kp = w.kp;
-  const int cap = a.cap;
-  const int qld = a.qld;
-
-  // Stage the group's queries (zero rows past gc) and reset selection state.
-  {
-    const float4* Q4 = reinterpret_cast<const float4*>(a.Q);
-    float4* Qs4 = reinterpret_cast<float4*>(Qs);
-    const int q4 = qld >> 2;
-    for (int i = tid; i < GT * q4; i += kThreads) {
-      int g = i / q4, c = i - g * q4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (g < gc) v = Q4[(long long)a.members[w.member_begin + g].q * q4 + c];
-      Qs4[i] = v;
-    }
-    if (tid < GT) {
-      sh.cnt[tid] = 0;
-      sh.thr[tid] = TRI_KEY_MAX;
-      sh.qn[tid] = tid < gc ? a.qnorm[a.members[w.member_begin + tid].q] : 0.f;
-    }
-  }
-  __syncthreads();
-
-  const int nslab = qld / kSlabW;
-  const float4* Qs4 = reinterpret_cast<const float4*>(Qs);
-  const int q4 = qld >> 2;
-  const int r0 = tid, r1 = tid + kThreads;
-  const int sw = (tid >> 1) & 3;  // same for r0 and r1
-
-  for (int c0 = 0; c0 < w.row_count; c0 += kChunk) {
-    const int rows = min(kChunk, w.row_count - c0);
-    const long long row0 = w.row_begin + c0;
-    float acc0[GT], acc1[GT];
-#pragma unroll
-    for (int g = 0; g < GT; ++g) acc0[g] = acc1[g] = 0.f;
-
-#pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
-      if (s < nslab) load_slab(slabs + s * kSlabFloats, a.X, a.ldx, row0, rows, s * kSlabW, a.dp);
-      cp_async_commit();
-    }
-    for (int s = 0; s < nslab; ++s) {
-      int sn = s + kStages - 1;
-      if (sn < nslab) load_slab(slabs + (sn % kStages) * kSlabFloats, a.X, a.ldx, row0, rows, sn * kSlabW, a.dp);
-      cp_async_commit();
-      cp_async_wait<kStages - 1>();
-      __syncthreads();
-      const float4* sl = reinterpret_cast<const float4*>(slabs + (s % kStages) * kSlabFloats);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float4 x0 = sl[r0 * 4 + (c ^ sw)];
-        float4 x1 = sl[r1 * 4 + (c ^ sw)];
-#pragma unroll
-        for (int g = 0; g < GT; ++g) {
-          float4 qv = Qs4[g * q4 + s * 4 + c];
-          acc0[g] = fmaf(x0.x, qv.x, acc0[g]);
-          acc0[g] = fmaf(x0.y, qv.y, acc0[g]);
-          acc0[g] = fmaf(x0.z, qv.z, acc0[g]);
-          acc0[g] = fmaf(x0.w, qv.w, acc0[g]);
-          acc1[g] = fmaf(x1.x, qv.x, acc1[g]);
-          acc1[g] = fmaf(x1.y, qv.y, acc1[g]);
-          acc1[g] = fmaf(x1.z, qv.z, acc1[g]);
-          acc1[g] = fmaf(x1.w, qv.w, acc1[g]);
-        }
-      }
-      __syncthreads();
-    }
-
-    // Approximate distances -> threshold-filtered append.
-    const bool v0 = r0 < rows, v1 = r1 < rows;
-    const float xn0 = v0 ? a.xnorm[row0 + r0] : 0.f;
-    const float xn1 = v1 ? a.xnorm[row0 + r1] : 0.f;
-    const uint32_t p0 = (uint32_t)(row0 + r0), p1 = (uint32_t)(row0 + r1);
-    uint32_t pend = 0;
-#pragma unroll
-    for (int g = 0; g < GT; ++g) {
-      if (g < gc) {
-        const float qn = sh.qn[g];
-        const unsigned long long thr = sh.thr[g];
-        if (v0) {
-          unsigned long long key = make_key(__fmaf_rn(-2.f, acc0[g], __fadd_rn(qn, xn0)), p0);
-          if (key < thr) {
-            int p = atomicAdd(&sh.cnt[g], 1);
-            if (p < cap) sel[g * cap + p] = key; else pend |= 1u << (2 * g);
-          }
-        }
-        if (v1) {
-          unsigned long long key = make_key(__fmaf_rn(-2.f, acc1[g], __fadd_rn(qn, xn1)), p1);
-          if (key < thr) {
-            int p = atomicAdd(&sh.cnt[g], 1);
-            if (p < cap) sel[g * cap + p] = key; else pend |= 1u << (2 * g + 1);
-          }
-        }
-      }
-    }
-    while (true) {
-      __syncthreads();
-      for (int g = warp; g < gc; g += kThreads / 32) {
-        int n = sh.cnt[g];
-        if (n > kp) {
-          int m = min(n, cap);
-          int p2 = next_pow2(m);
-          unsigned long long* s = sel + g * cap;
-          for (int i = m + lane; i < p2; i += 32) s[i] = TRI_KEY_MAX;
-          __syncwarp();
-          warp_sort(s, p2, lane, KeyLess());
-          if (lane == 0) {
-            sh.cnt[g] = kp;
-            sh.thr[g] = s[kp - 1];
-          }
-          __syncwarp();
-        }
-      }
-      if (!__syncthreads_or(pend != 0)) break;
-      uint32_t still = 0;
-#pragma unroll
-      for (int g = 0; g < GT; ++g) {
-        if (pend & (1u << (2 * g))) {
-          unsigned long long key = make_key(__fmaf_rn(-2.f, acc0[g], __fadd_rn(sh.qn[g], xn0)), p0);
-          if (key < sh.thr[g]) {
-            int p = atomicAdd(&sh.cnt[g], 1);
-            if (p < cap) sel[g * cap + p] = key; else still |= 1u << (2 * g);
-          }
-        }
-        if (pend & (1u << (2 * g + 1))) {
-          unsigned long long key = make_key(__fmaf_rn(-2.f, acc1[g], __fadd_rn(sh.qn[g], xn1)), p1);
-          if (key < sh.thr[g]) {
-            int p = atomicAdd(&sh.cnt[g], 1);
-            if (p < cap) sel[g * cap + p] = key; else still |= 1u << (2 * g + 1);
-          }
-        }
-      }
-      pend = still;
-    }
-  }
-
-  // Final per-query sort and write-out of the top-kp partial list.
-  for (int g = warp; g < gc; g += kThreads / 32) {
-    int n = sh.cnt[g];
-    int p2 = next_pow2(n > 0 ? n : 1);
-    unsigned long long* s = sel + g * cap;
-    for (int i = n + lane; i < p2; i += 32) s[i] = TRI_KEY_MAX;
-    __syncwarp();
-    warp_sort(s, p2, lane, KeyLess());
-    unsigned long long* out = a.part + a.members[w.member_begin + g].slot;
-    for (int i = lane; i < kp; i += 32) out[i] = i < n ? s[i] : TRI_KEY_MAX;
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kThreads, 1) scan_kernel(ScanLaunch a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ ScanShared sh;
-  float* Qs = reinterpret_cast<float*>(smem_raw);
-  float* slabs = Qs + (size_t)a.gmax * a.qld;
-  unsigned long long* sel = reinterpret_cast<unsigned long long*>(slabs + (size_t)kStages * kSlabFloats);
-  const int n_items = *a.n_items;
-  while (true) {
-    if (threadIdx.x == 0) sh.item = atomicAdd(a.counter, 1);
-    __syncthreads();
-    const int it = sh.item;
-    __syncthreads();
-    if (it >= n_items) break;
-    const WorkItem w = a.items[it];
-    if (w.row_count <= 0) continue;
-    const int gc = w.member_count;
-    if (gc <= 1) scan_item<1>(a, w, Qs, slabs, sel, sh);
-    else if (gc <= 2) scan_item<2>(a, w, Qs, slabs, sel, sh);
-    else if (gc <= 4) scan_item<4>(a, w, Qs, slabs, sel, sh);
-    else if (gc <= 8) scan_item<8>(a, w, Qs, slabs, sel, sh);
-    else scan_item<16>(a, w, Qs, slabs, sel, sh);
-  }
-}
-
-cudaError_t launch_scan(const ScanLaunch& s, cudaStream_t st) {
-  size_t smem = scan_smem_bytes(s.gmax, s.qld, s.cap);
-  cudaError_t e = cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  scan_kernel<<<s.grid, kThreads, smem, st>>>(s);
-  return cudaGetLastError();
-}
 
 // ---------------------------------------------------------------------------
 // Query preparation and row norms.
@@ -406,37 +155,104 @@ cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, 
 
 // ---------------------------------------------------------------------------
 // Exact fp64 re-rank + certification.
+//
+// exact_pairs_kernel: one CTA per (query, 32 candidates); thread pair
+// (2c, 2c+1) computes candidate c, thread 2c+l running numpy lane l (elements
+// 8b + 2*sub + l, sub = 3..0, then the 2-lane tail), so the value is
+// bit-identical to exact_sq_dist / the reference.  Candidate rows and the
+// fp64 query are staged through shared memory in 256-float slabs with
+// cp.async (all loads in flight at once); slabs are 8-aligned so numpy's
+// 8-element blocks never straddle one.
 
-__global__ void __launch_bounds__(kThreads) rerank_kernel(RerankLaunch r) {
+constexpr int kPairCands = 32;
+constexpr int kPairSlab = 256;
+constexpr int kPairStride = kPairSlab + 4;  // 2-way worst bank conflict, 16B aligned rows
+
+__global__ void __launch_bounds__(2 * kPairCands) exact_pairs_kernel(RerankLaunch r) {
+  __shared__ __align__(16) float xs[kPairCands * kPairStride];
+  __shared__ __align__(16) double qs[kPairSlab];
+  __shared__ long long pos_s[kPairCands];
+  const int groups = r.ld_merged / kPairCands;
+  const int q = blockIdx.x / groups;
+  const int c = (blockIdx.x - q * groups) * kPairCands + (threadIdx.x >> 1);
+  const int ln = threadIdx.x & 1;
+  const int kp = r.meta[q].kp;
+  if ((c & ~(kPairCands - 1)) >= kp) return;  // whole CTA beyond this query's capacity
+  const long long p = (long long)q * r.ld_merged + c;
+  const unsigned long long key = r.merged[p];
+  const bool active = key != TRI_KEY_MAX;
+  const long long pos = active ? (long long)key_pos(key) : -1;
+  if (ln == 0) pos_s[threadIdx.x >> 1] = pos;
+  __syncthreads();
+  const int d = r.d;
+  const double* qg = r.q64 + (long long)q * d;
+  double acc = 0.0;
+  for (int s0 = 0; s0 < d; s0 += kPairSlab) {
+    const int w = min(kPairSlab, d - s0);
+    const int w4 = (w + 3) >> 2;  // stored rows are zero padded to a multiple of 16
+    const uint32_t xbase = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
+    for (int i = threadIdx.x; i < kPairCands * w4; i += blockDim.x) {
+      const int row = i / w4, ch = i - row * w4;
+      const long long rp = pos_s[row];
+      const float* src = rp >= 0 ? r.X + rp * r.ldx + s0 + ch * 4 : r.X;
+      const uint32_t dst = xbase + (uint32_t)((row * kPairStride + ch * 4) * 4);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(rp >= 0 ? 16 : 0));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    for (int j = threadIdx.x; j < w; j += blockDim.x) qs[j] = qg[s0 + j];
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    if (active) {
+      const float* xr = xs + (threadIdx.x >> 1) * kPairStride;
+      int i = 0;
+      for (; i < w && s0 + i + 8 <= d; i += 8) {
+#pragma unroll
+        for (int sub = 3; sub >= 0; --sub) {
+          const int e = i + 2 * sub + ln;
+          const double df = __dsub_rn(qs[e], (double)xr[e]);
+          acc = __dadd_rn(__dmul_rn(df, df), acc);
+        }
+      }
+      for (; i < w; i += 2) {  // numpy's 2-lane tail (last slab only)
+        const int e = i + ln;
+        if (s0 + e < d) {
+          const double df = __dsub_rn(qs[e], (double)xr[e]);
+          acc = __dadd_rn(__dmul_rn(df, df), acc);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const double other = __shfl_xor_sync(0xffffffffu, acc, 1);
+  if (ln == 0 && c < kp) {
+    Exact e = exact_max();
+    if (active) {
+      e.d = __dadd_rn(acc, other);
+      e.id = (r.idmap ? r.idmap[pos] : pos) + r.id_offset;
+    }
+    r.exact[p] = e;
+  }
+}
+
+__global__ void __launch_bounds__(128) finalize_kernel(RerankLaunch r) {
   extern __shared__ Exact ebuf[];
   const int q = blockIdx.x;
   const QueryMeta m = r.meta[q];
   const int kp = m.kp;
-  const unsigned long long* mk = r.merged + (long long)q * r.ld_merged;
-  const double* qv = r.q64 + (long long)q * r.d;
-  for (int i = threadIdx.x; i < kp; i += kThreads) {
-    unsigned long long key = mk[i];
-    Exact e = exact_max();
-    if (key != TRI_KEY_MAX) {
-      long long pos = key_pos(key);
-      e.d = exact_sq_dist(qv, r.X + pos * r.ldx, r.d);
-      e.id = (r.idmap ? r.idmap[pos] : pos) + r.id_offset;
-    }
-    ebuf[i] = e;
-  }
+  for (int i = threadIdx.x; i < kp; i += blockDim.x) ebuf[i] = r.exact[(long long)q * r.ld_merged + i];
   __syncthreads();
   block_sort(ebuf, kp, ExactLess());
   if (threadIdx.x == 0) {
     bool cert = true;
     if (m.n_total > kp) {
-      const double T = (double)key_dist(mk[kp - 1]);
+      const double T = (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]);
       const double s = r.qn64[q] + r.xmax;
-      const double E = r.cbound * s * s * 1.001 + 1e-30;
+      const double E = (r.cdot * 2.0 * r.qn64[q] * r.xmax + r.csum * s * s) * 1.001 + 1e-30;
       cert = ebuf[m.k - 1].d + E < T;
     }
     if (!cert) r.flag_list[atomicAdd(r.n_flag, 1)] = q;
   }
-  for (int j = threadIdx.x; j < m.k; j += kThreads) {
+  for (int j = threadIdx.x; j < m.k; j += blockDim.x) {
     const Exact e = ebuf[j];
     const bool ok = e.id != 0x7fffffffffffffffll;
     r.out_ids[(long long)q * r.ldo + j] = ok ? e.id : -1;
@@ -446,10 +262,13 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankLaunch r) {
 
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
   if (r.B <= 0) return cudaSuccess;
-  size_t smem = (size_t)r.kp_max * sizeof(Exact);
-  cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  exact_pairs_kernel<<<(unsigned)(r.B * (r.ld_merged / kPairCands)), 2 * kPairCands, 0, st>>>(r);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  rerank_kernel<<<r.B, kThreads, smem, st>>>(r);
+  size_t smem = (size_t)r.kp_max * sizeof(Exact);
+  e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  finalize_kernel<<<r.B, 128, smem, st>>>(r);
   return cudaGetLastError();
 }
 

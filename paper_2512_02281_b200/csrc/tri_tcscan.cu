@@ -1,0 +1,357 @@
+// Tensor-core list scan (sm_100a): tcgen05.mma kind::tf32, TMEM accumulators,
+// TMA-fed shared-memory ring.  Same work items / partial-list contract as the
+// SIMT scan in tri_listscan.cu, which remains the path for qld > kTcMaxQld.
+//
+// Roles (one persistent CTA per SM, 192 threads):
+//   warp 0  producer : claims work items, publishes descriptors, streams each
+//                      item's rows with 2-D TMA (32-row x 32-float boxes,
+//                      128B swizzle = the UMMA K-major SW128 canonical layout)
+//                      into a kStages-deep ring of 128-row x 32-float slabs.
+//   warp 1  MMA      : allocates 32 TMEM columns (two 128x16 fp32
+//                      accumulators); one elected lane issues 4 MMAs
+//                      (M=128 rows, N=16 queries, K=8) per slab,
+//                      tcgen05.commit frees the slab / publishes a chunk.
+//   warps 2-5 epilogue: stage the group's queries into smem in the same SW128
+//                      K-major layout, then per 128-row chunk: tcgen05.ld their
+//                      TMEM lane quadrant (thread = row), form the fp32
+//                      dot-form distance qn + xn - 2 q.x and run the
+//                      threshold-filtered per-query top-kp selection.
+// Distances are approximate (TF32 inputs); the certified fp64 re-rank
+// (tri_select.cu) makes the final result exact.
+#include <cuda.h>
+
+#include "tri_common.cuh"
+#include "tri_internal.h"
+
+namespace tri {
+
+constexpr int kTcThreads = 192;
+constexpr int kTcRows = 128;                    // MMA M = rows per chunk
+constexpr int kTcN = 16;                        // MMA N = queries per group
+constexpr int kTcSlabF = 32;                    // floats per row per slab (128 B)
+constexpr int kTcSlabBytes = kTcRows * kTcSlabF * 4;  // 16 KB
+constexpr int kTcBoxRows = 32;
+constexpr int kTcStages = 6;
+constexpr int kTcQTile = kTcN * kTcSlabF * 4;   // 2 KB of queries per slab
+constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
+                              ((uint32_t)(kTcRows >> 4) << 24);  // F32 accum, TF32 A/B, K-major, N=16, M=128
+
+__device__ __forceinline__ uint32_t tsu32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void tmb_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(tsu32(b)), "r"(c));
+}
+__device__ __forceinline__ void tmb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tsu32(b)) : "memory");
+}
+__device__ __forceinline__ void tmb_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tsu32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tmb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n TWAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TWAIT_%=;\n}\n" ::"r"(tsu32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void ttma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(tsu32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(tsu32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(tsu32(bar))
+               : "memory");
+}
+
+struct TcSmem {
+  uint64_t full[kTcStages], empty[kTcStages];
+  uint64_t wfull[2], wempty[2];
+  uint64_t qfull;
+  uint64_t tfull[2], tempty[2];
+  WorkItem witem[2];
+  int wend[2];
+  uint32_t tmem_base;
+  int cnt[kTcN];
+  unsigned long long thr[kTcN];
+  float qn[kTcN];
+};
+
+size_t tc_scan_smem_bytes(int qld, int cap) {
+  const int nslab = (qld + kTcSlabF - 1) / kTcSlabF;
+  return 1024 + (size_t)kTcStages * kTcSlabBytes + (size_t)nslab * kTcQTile + (size_t)kTcN * cap * 8;
+}
+
+// ---------------------------------------------------------------------------
+
+__device__ void tc_producer(const ScanLaunch& a, const CUtensorMap* map, TcSmem& sh, unsigned char* ring) {
+  const int n_items = *a.n_items;
+  const int nslab = (a.qld + kTcSlabF - 1) / kTcSlabF;
+  int wslot = 0, wphase = 0, stage = 0, sphase = 0;
+  for (;;) {
+    const int it = atomicAdd(a.counter, 1);
+    tmb_wait(&sh.wempty[wslot], wphase ^ 1);
+    if (it >= n_items) {
+      sh.wend[wslot] = 1;
+      tmb_arrive(&sh.wfull[wslot]);
+      return;
+    }
+    const WorkItem w = a.items[it];
+    sh.witem[wslot] = w;
+    sh.wend[wslot] = 0;
+    tmb_arrive(&sh.wfull[wslot]);
+    if (++wslot == 2) {
+      wslot = 0;
+      wphase ^= 1;
+    }
+    const int nchunk = (w.row_count + kTcRows - 1) / kTcRows;
+    for (int c = 0; c < nchunk; ++c) {
+      const int rows = min(kTcRows, w.row_count - c * kTcRows);
+      const int nbox = (rows + kTcBoxRows - 1) / kTcBoxRows;
+      const int row0 = (int)(w.row_begin + (long long)c * kTcRows);
+      for (int s = 0; s < nslab; ++s) {
+        tmb_wait(&sh.empty[stage], sphase ^ 1);
+        unsigned char* dst = ring + (size_t)stage * kTcSlabBytes;
+        tmb_expect(&sh.full[stage], (uint32_t)nbox * kTcBoxRows * kTcSlabF * 4u);
+        for (int b = 0; b < nbox; ++b)
+          ttma_2d(dst + b * kTcBoxRows * kTcSlabF * 4, map, s * kTcSlabF, row0 + b * kTcBoxRows, &sh.full[stage]);
+        if (++stage == kTcStages) {
+          stage = 0;
+          sphase ^= 1;
+        }
+      }
+    }
+  }
+}
+
+__device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, unsigned char* qs) {
+  const int lane = threadIdx.x & 31;
+  const int nslab = (a.qld + kTcSlabF - 1) / kTcSlabF;
+  int wslot = 0, wphase = 0, stage = 0, sphase = 0, qphase = 0, acc = 0, aphase = 0;
+  const uint32_t tmem = sh.tmem_base;
+  const uint32_t ring_s = tsu32(ring), qs_s = tsu32(qs);
+  for (;;) {
+    tmb_wait(&sh.wfull[wslot], wphase);
+    const int end = sh.wend[wslot];
+    const WorkItem w = sh.witem[wslot];
+    __syncwarp();
+    if (lane == 0) tmb_arrive(&sh.wempty[wslot]);
+    if (++wslot == 2) {
+      wslot = 0;
+      wphase ^= 1;
+    }
+    if (end) return;
+    tmb_wait(&sh.qfull, qphase);
+    qphase ^= 1;
+    const int nchunk = (w.row_count + kTcRows - 1) / kTcRows;
+    for (int c = 0; c < nchunk; ++c) {
+      tmb_wait(&sh.tempty[acc], aphase ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t d_tmem = tmem + (uint32_t)(acc * kTcN);
+      for (int s = 0; s < nslab; ++s) {
+        tmb_wait(&sh.full[stage], sphase);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (lane == 0) {
+          const uint32_t a0 = ring_s + (uint32_t)stage * kTcSlabBytes;
+          const uint32_t b0 = qs_s + (uint32_t)s * kTcQTile;
+#pragma unroll
+          for (int k = 0; k < kTcSlabF / 8; ++k)
+            umma_tf32(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), (s | k) != 0);
+          umma_commit(&sh.empty[stage]);  // slab reusable once these MMAs retire
+          if (s == nslab - 1) umma_commit(&sh.tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == kTcStages) {
+          stage = 0;
+          sphase ^= 1;
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+}
+
+// Epilogue: 4 warps, thread e (0..127) <-> TMEM lane e <-> chunk row e.
+__device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, unsigned long long* sel) {
+  const int e = threadIdx.x - 64;              // 0..127
+  const int lane = threadIdx.x & 31;
+  const int ew = e >> 5;                       // epilogue warp 0..3
+  const int quad = (threadIdx.x >> 5) & 3;     // TMEM lane quadrant this warp may access
+  const int row_in_chunk = quad * 32 + lane;   // == TMEM lane
+  const int nslab = (a.qld + kTcSlabF - 1) / kTcSlabF;
+  const int cap = a.cap;
+  int wslot = 0, wphase = 0, acc = 0, aphase = 0;
+  const uint32_t tmem = sh.tmem_base;
+  for (;;) {
+    tmb_wait(&sh.wfull[wslot], wphase);
+    const int end = sh.wend[wslot];
+    const WorkItem w = sh.witem[wslot];
+    __syncwarp();
+    if (lane == 0) tmb_arrive(&sh.wempty[wslot]);
+    if (++wslot == 2) {
+      wslot = 0;
+      wphase ^= 1;
+    }
+    if (end) return;
+    const int gc = w.member_count, kp = w.kp;
+    // Stage queries: slab s, query g, 16B chunk c -> qs + s*2KB + g*128 + ((c ^ (g&7)) << 4)
+    {
+      const float4* Q4 = reinterpret_cast<const float4*>(a.Q);
+      const int q4 = a.qld >> 2;
+      const int total = nslab * kTcN * 8;
+      for (int i = e; i < total; i += 128) {
+        const int c = i & 7, g = (i >> 3) & (kTcN - 1), s = i >> 7;
+        const int col4 = s * 8 + c;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (g < gc && col4 < q4) v = Q4[(long long)a.members[w.member_begin + g].q * q4 + col4];
+        *reinterpret_cast<float4*>(qs + s * kTcQTile + g * 128 + ((c ^ (g & 7)) << 4)) = v;
+      }
+      if (e < kTcN) {
+        sh.cnt[e] = 0;
+        sh.thr[e] = TRI_KEY_MAX;
+        sh.qn[e] = e < gc ? a.qnorm[a.members[w.member_begin + e].q] : 0.f;
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core reads
+      epi_sync();
+      if (e == 0) tmb_arrive(&sh.qfull);
+    }
+    const int nchunk = (w.row_count + kTcRows - 1) / kTcRows;
+    for (int c = 0; c < nchunk; ++c) {
+      const int rows = min(kTcRows, w.row_count - c * kTcRows);
+      const long long row = w.row_begin + (long long)c * kTcRows + row_in_chunk;
+      const bool valid = row_in_chunk < rows;
+      const float xn = valid ? a.xnorm[row] : 0.f;
+      tmb_wait(&sh.tfull[acc], aphase);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      uint32_t v[kTcN];
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kTcN);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tmb_arrive(&sh.tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+      if (valid) {
+        const uint32_t pos = (uint32_t)row;
+#pragma unroll
+        for (int g = 0; g < kTcN; ++g) {
+          if (g < gc) {
+            const float dot = __uint_as_float(v[g]);
+            const unsigned long long key = make_key(__fmaf_rn(-2.f, dot, __fadd_rn(sh.qn[g], xn)), pos);
+            if (key < sh.thr[g]) sel[g * cap + atomicAdd(&sh.cnt[g], 1)] = key;  // cap - kp >= 128: no overflow
+          }
+        }
+      }
+      epi_sync();
+      for (int g = ew; g < gc; g += 4) {
+        const int n = sh.cnt[g];
+        if (n > kp) {
+          const int p2 = next_pow2(n);
+          unsigned long long* s = sel + g * cap;
+          for (int i = n + lane; i < p2; i += 32) s[i] = TRI_KEY_MAX;
+          __syncwarp();
+          warp_sort(s, p2, lane, KeyLess());
+          if (lane == 0) {
+            sh.cnt[g] = kp;
+            sh.thr[g] = s[kp - 1];
+          }
+          __syncwarp();
+        }
+      }
+      epi_sync();
+    }
+    for (int g = ew; g < gc; g += 4) {
+      const int n = sh.cnt[g];
+      const int p2 = next_pow2(n > 0 ? n : 1);
+      unsigned long long* s = sel + g * cap;
+      for (int i = n + lane; i < p2; i += 32) s[i] = TRI_KEY_MAX;
+      __syncwarp();
+      warp_sort(s, p2, lane, KeyLess());
+      unsigned long long* out = a.part + a.members[w.member_begin + g].slot;
+      for (int i = lane; i < kp; i += 32) out[i] = i < n ? s[i] : TRI_KEY_MAX;
+    }
+    epi_sync();  // selection buffers and qs free for the next item
+  }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_constant__ CUtensorMap map, ScanLaunch a) {
+  extern __shared__ __align__(1024) unsigned char tsmem_raw[];
+  __shared__ TcSmem sh;
+  unsigned char* base = tsmem_raw + ((1024u - (tsu32(tsmem_raw) & 1023u)) & 1023u);
+  unsigned char* ring = base;
+  unsigned char* qs = ring + (size_t)kTcStages * kTcSlabBytes;
+  const int nslab = (a.qld + kTcSlabF - 1) / kTcSlabF;
+  unsigned long long* sel = reinterpret_cast<unsigned long long*>(qs + (size_t)nslab * kTcQTile);
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      tmb_init(&sh.full[s], 1);
+      tmb_init(&sh.empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tmb_init(&sh.wfull[s], 1);
+      tmb_init(&sh.wempty[s], 5);  // MMA warp + 4 epilogue warps
+      tmb_init(&sh.tfull[s], 1);
+      tmb_init(&sh.tempty[s], 4);
+    }
+    tmb_init(&sh.qfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(tsu32(&sh.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == 0) {
+    if ((threadIdx.x & 31) == 0) tc_producer(a, &map, sh, ring);
+  } else if (warp == 1) {
+    tc_mma(a, sh, ring, qs);
+  } else {
+    tc_epilogue(a, sh, qs, sel);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(sh.tmem_base));
+  }
+}
+
+cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st) {
+  const size_t smem = tc_scan_smem_bytes(s.qld, s.cap);
+  cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  scan_tc_kernel<<<s.grid, kTcThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(s.tmap_tc), s);
+  return cudaGetLastError();
+}
+
+}  // namespace tri

@@ -22,9 +22,12 @@ from paper_2512_02281_b200.workload import gen_matrix
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def _reset_options():
-    yield
+@pytest.fixture(params=["tc", "simt"], autouse=True)
+def scan_kernel(request):
+    """Run every test on both candidate-generation kernels (tcgen05 TF32 and SIMT fp32)."""
+    _lib.set_option("scan_kernel", 0 if request.param == "tc" else 1)
+    yield request.param
+    _lib.set_option("scan_kernel", 0)
     _lib.set_option("force_fixup", 0)
     _lib.set_option("kp_extra", 0)
 
