@@ -50,7 +50,9 @@ const char* tri_last_error(void);
 int tri_version(void);
 int tri_device_count(int32_t* count);
 /* Debug/test knobs: "force_fixup" (1 = treat every query as uncertified),
- * "kp_extra" (extra over-fetch added to k). */
+ * "kp_extra" (extra over-fetch added to k), "scan_kernel" (0 auto,
+ * 1 fp32 SIMT scan, 2 tensor-core scan when it fits), "scan_debug" (timing
+ * experiments only: results are invalid while set). */
 int tri_set_option(const char* name, int64_t value);
 
 /* Vector store: replaces ann_graph.VectorStore (ann_graph.py:21-48).
@@ -107,9 +109,14 @@ int tri_ivf_last_probes(tri_ivf* v, int64_t* probes, int32_t ld);
 /* Queries of the last search that needed the exact fix-up (host int). */
 int tri_ivf_last_fixups(tri_ivf* v, int32_t* n);
 int tri_store_last_fixups(tri_store* s, int32_t* n);
-/* Profiling: when enabled, CUDA events bracket the list-scan kernel. */
+/* Profiling: when enabled, CUDA events bracket every pipeline stage of each
+ * search (read back lazily, no synchronisation inside a timed loop).
+ * scan_time: accumulated list-scan kernel time and number of searches;
+ * stage_times: ms[6] = coarse step, packer, list scan, merge, exact re-rank,
+ * certified fix-up. */
 int tri_ivf_set_profiling(tri_ivf* v, int32_t on);
 int tri_ivf_scan_time(tri_ivf* v, double* total_ms, int32_t* launches);
+int tri_ivf_stage_times(tri_ivf* v, double* ms, int32_t* searches);
 /* Algorithmic bytes of the last search's list scan: every probed list read
  * once (d*4 + 4 bytes per vector).  Also returns the number of scanned
  * (query, vector) pairs. */

@@ -52,6 +52,7 @@ _SIGS = {
     "tri_store_last_fixups": [_vp, _i32p],
     "tri_ivf_set_profiling": [_vp, _i32],
     "tri_ivf_scan_time": [_vp, _f64p, _i32p],
+    "tri_ivf_stage_times": [_vp, _vp, _i32p],
     "tri_ivf_last_scan_bytes": [_vp, _i64p, _i64p],
     "tri_merge_topk": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp],
 }

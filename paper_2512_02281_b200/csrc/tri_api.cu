@@ -23,7 +23,8 @@ thread_local std::string g_err;
 long long g_force_fixup = 0;
 long long g_kp_extra = 0;
 constexpr int kSmemLimit = 226 * 1024;
-constexpr int kEventPairs = 4096;
+constexpr int kProfSearches = 2048;  // profiled searches kept before read-back
+constexpr int kStagesProf = 6;       // coarse, pack, scan, merge, rerank, fixup
 constexpr int kSelCapMin = 512;  // >= one 512-row chunk of appends
 
 int round16(int d) { return (d + 15) & ~15; }
@@ -94,6 +95,7 @@ int ensure_host(HostBuf& b, size_t bytes) {
 }
 
 long long g_scan_kernel = 0;  // 0 auto, 1 SIMT, 2 tensor core
+long long g_scan_debug = 0;   // timing experiments only (results invalid when set)
 
 // Candidate capacity: over-fetch so the certified re-rank almost never falls
 // back.  TF32 candidates carry ~2^-9 relative dot error, so they over-fetch 2x.
@@ -163,8 +165,7 @@ int make_tmap(CUtensorMap* map, const float* X, long long rows, int ldx, bool tc
 // or the queries do not fit its shared-memory layout.
 bool use_tc(int qld, int kp_max_tc) {
   if (g_scan_kernel == 1) return false;
-  return kp_max_tc <= kMaxKp && qld <= kTcMaxQld &&
-         tc_scan_smem_bytes(qld, std::max(kSelCapMin, 2 * kp_max_tc)) <= (size_t)kSmemLimit;
+  return kp_max_tc <= kTcMaxKp && qld <= kTcMaxQld && tc_scan_smem_bytes(qld) <= (size_t)kSmemLimit;
 }
 
 // Per-search scratch shared by the brute-force and IVF pipelines.
@@ -192,6 +193,7 @@ struct Workspace {
 
 struct tri_store {
   int device = 0;
+  int prefer_simt = 0;  // 1: fp32 SIMT scan (tight certification bound; IVF coarse step)
   long long n = 0;
   int d = 0, dp = 0, qld = 0;
   long long id_offset = 0;
@@ -228,9 +230,9 @@ struct tri_ivf {
   // profiling: a ring of (start, stop) event pairs around the list-scan kernel,
   // read back lazily so the timed loop never synchronises.
   std::vector<cudaEvent_t> ev;
-  int ev_used = 0;
-  double scan_ms = 0.0;
-  int scan_launches = 0;
+  int ev_used = 0;  // profiled searches with pending events (7 events each)
+  double stage_ms[kStagesProf] = {0, 0, 0, 0, 0, 0};
+  int prof_n = 0;
 };
 
 namespace {
@@ -303,10 +305,10 @@ struct ScanChoice {
   int kp_max = kMinKp, k_max = 1, cap = 0, gmax = 0;
 };
 
-int choose_scan(int qld, int d, int B, const int* k, std::vector<int>& kp, ScanChoice& ch) {
+int choose_scan(int qld, int d, int B, const int* k, std::vector<int>& kp, ScanChoice& ch, bool prefer_simt) {
   int kp_tc = kMinKp;
   for (int i = 0; i < B; ++i) kp_tc = std::max(kp_tc, kp_for(k[i], true));
-  ch.tc = use_tc(qld, kp_tc);
+  ch.tc = !prefer_simt && use_tc(qld, kp_tc);
   kp.resize(B);
   ch.kp_max = kMinKp;
   ch.k_max = 1;
@@ -330,11 +332,26 @@ int plan_bruteforce(tri_store* s, int B, const int* k, cudaStream_t st) {
     return TRI_OK;
   std::vector<int> kp, cls(B);
   ScanChoice ch;
-  TRY(choose_scan(s->qld, s->d, B, k, kp, ch));
+  TRY(choose_scan(s->qld, s->d, B, k, kp, ch, s->prefer_simt != 0));
   for (int i = 0; i < B; ++i) cls[i] = cls_of(kp[i]);
-  const int kp_max = ch.kp_max, k_max = ch.k_max, cap = ch.cap, gmax = ch.gmax;
-  // Group size = the smem maximum: every extra group re-reads all rows (from
-  // L2), which costs more than the idle SMs of a short wave.
+  const int kp_max = ch.kp_max, k_max = ch.k_max, cap = ch.cap;
+  const int nsm = sm_count(s->device);
+  const long long max_ranges = std::max<long long>(1, (s->n + 511) / 512);
+  // Group size: as large as shared memory allows (each extra group re-reads
+  // the rows from L2), except that the SIMT scan's per-thread FFMA work grows
+  // with the group -- small stores (the IVF coarse step) shrink groups until
+  // the items cover every SM.
+  int gmax = ch.gmax;
+  if (!ch.tc) {
+    auto n_groups = [&](int g) {
+      std::vector<int> per(kNumCls, 0);
+      for (int i = 0; i < B; ++i) per[cls[i]]++;
+      long long t = 0;
+      for (int c = 0; c < kNumCls; ++c) t += (per[c] + g - 1) / g;
+      return t;
+    };
+    while (gmax > 4 && n_groups(gmax) * max_ranges < nsm) gmax >>= 1;
+  }
   // groups: consecutive same-class queries in index order
   std::vector<std::vector<int>> groups;
   for (int c = 0; c < kNumCls; ++c) {
@@ -349,8 +366,6 @@ int plan_bruteforce(tri_store* s, int B, const int* k, cudaStream_t st) {
       }
     if (!cur.empty()) groups.push_back(cur);
   }
-  const int nsm = sm_count(s->device);
-  const long long max_ranges = std::max<long long>(1, (s->n + 511) / 512);
   long long nr = std::max<long long>(1, ((long long)nsm + (long long)groups.size() - 1) / (long long)groups.size());
   nr = std::min(nr, max_ranges);
   long long R = (s->n + nr - 1) / nr;
@@ -465,6 +480,7 @@ int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int
   sl.gmax = w.gmax;
   sl.cap = w.cap;
   sl.grid = w.grid;
+  sl.dbg = 0;
   CU(w.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
   CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
                   st));
@@ -554,6 +570,7 @@ int tri_set_option(const char* name, int64_t value) {
   if (!std::strcmp(name, "force_fixup")) g_force_fixup = value;
   else if (!std::strcmp(name, "kp_extra")) g_kp_extra = value;
   else if (!std::strcmp(name, "scan_kernel")) g_scan_kernel = value;
+  else if (!std::strcmp(name, "scan_debug")) g_scan_debug = value;
   else return fail(TRI_EINVAL, "unknown option '%s'", name);
   return TRI_OK;
 }
@@ -777,6 +794,10 @@ static int ivf_finish(tri_ivf* v, tri_store* s, const float* Cdev, const int* as
   CU(cudaMalloc(&v->assign, (size_t)v->n * sizeof(int)));
   CU(cudaMemcpyAsync(v->assign, assign_dev, (size_t)v->n * sizeof(int), cudaMemcpyDeviceToDevice, st));
   TRY(store_from_device(Cdev, v->dp, v->nlist, v->d, v->device, &v->cstore));
+  // Coarse step on the fp32 SIMT scan: centroid distances sit close together and
+  // singleton lists give centroids data-point norms, so the TF32 bound would
+  // rarely certify (measured: 251/256 fix-ups); fp32 certifies every query.
+  v->cstore->prefer_simt = 1;
   CU(cudaStreamCreateWithFlags(&v->own, cudaStreamNonBlocking));
   CU(cudaStreamSynchronize(st));
   return TRI_OK;
@@ -933,7 +954,19 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   Workspace& w = v->ws;
   const int npmax = *std::max_element(nprobe, nprobe + B);
   TRY(ensure_query_bufs(w, B, v->d, v->qld));
+  const bool rec = v->prof && v->ev_used < kProfSearches;
+  auto mark = [&](int j) -> int {
+    if (!rec) return TRI_OK;
+    while ((int)v->ev.size() < 7 * (v->ev_used + 1)) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      v->ev.push_back(e);
+    }
+    CU(cudaEventRecord(v->ev[7 * v->ev_used + j], st));
+    return TRI_OK;
+  };
   TRY(prep_queries(w, q, B, v->d, v->qld, st));
+  TRY(mark(0));
 
   // 1. coarse step: exact top-nprobe centroids per query
   TRY(ensure(v->probes, (size_t)B * npmax * sizeof(long long)));
@@ -943,7 +976,7 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   // 2. host-side per-query plan (k, kp, slots) -> device
   std::vector<int> kp;
   ScanChoice ch;
-  TRY(choose_scan(v->qld, v->d, B, k, kp, ch));
+  TRY(choose_scan(v->qld, v->d, B, k, kp, ch, false));
   const int kp_max = ch.kp_max, k_max = ch.k_max;
   long long part_keys = 0, members = 0;
   TRY(ensure_host(v->h_meta, (size_t)B * (sizeof(QueryMeta) + sizeof(int)) + 64));
@@ -981,6 +1014,7 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   int* ctr = v->counters.as<int>();
   CU(cudaMemsetAsync(ctr, 0, 4 * sizeof(int), st));
 
+  TRY(mark(1));
   // 3. device packer
   PackLaunch pk;
   pk.probes = v->probes.as<long long>();
@@ -1020,23 +1054,14 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   sl.gmax = gmax;
   sl.cap = cap;
   sl.grid = (int)std::min<long long>(sm_count(v->device), members);
-  const bool rec = v->prof && v->ev_used < kEventPairs;
-  if (rec) {
-    while ((int)v->ev.size() < 2 * (v->ev_used + 1)) {
-      cudaEvent_t e;
-      CU(cudaEventCreate(&e));
-      v->ev.push_back(e);
-    }
-    CU(cudaEventRecord(v->ev[2 * v->ev_used], st));
-  }
+  sl.dbg = (int)g_scan_debug;
+  TRY(mark(2));
   CU(ch.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
-  if (rec) {
-    CU(cudaEventRecord(v->ev[2 * v->ev_used + 1], st));
-    v->ev_used++;
-  }
+  TRY(mark(3));
 
   // 5. merge, exact re-rank, certified fix-up
   CU(launch_merge(w.part.as<unsigned long long>(), dmeta, w.merged.as<unsigned long long>(), kp_max, B, kp_max, st));
+  TRY(mark(4));
   int* n_flag = w.flags.as<int>();
   int* flag_list = n_flag + 64;
   CU(cudaMemsetAsync(n_flag, 0, sizeof(int), st));
@@ -1064,6 +1089,7 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   rr.B = B;
   rr.kp_max = kp_max;
   CU(launch_rerank(rr, st));
+  TRY(mark(5));
   FixupLaunch fx;
   fx.n_flag = n_flag;
   fx.flag_list = flag_list;
@@ -1085,6 +1111,8 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   fx.B = B;
   fx.k_max = k_max;
   CU(launch_fixup(fx, st));
+  TRY(mark(6));
+  if (rec) v->ev_used++;
   v->last_B = B;
   v->last_npmax = npmax;
   v->last_np.assign(nprobe, nprobe + B);
@@ -1143,25 +1171,40 @@ int tri_ivf_last_fixups(tri_ivf* v, int32_t* n) {
 int tri_ivf_set_profiling(tri_ivf* v, int32_t on) {
   if (!v) return fail(TRI_EINVAL, "index is NULL");
   v->prof = on != 0;
-  v->scan_ms = 0.0;
-  v->scan_launches = 0;
+  for (double& x : v->stage_ms) x = 0.0;
+  v->prof_n = 0;
+  v->ev_used = 0;
+  return TRI_OK;
+}
+
+static int ivf_collect(tri_ivf* v) {
+  DeviceGuard g(v->device);
+  for (int i = 0; i < v->ev_used; ++i) {
+    CU(cudaEventSynchronize(v->ev[7 * i + 6]));
+    for (int j = 0; j < kStagesProf; ++j) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, v->ev[7 * i + j], v->ev[7 * i + j + 1]));
+      v->stage_ms[j] += ms;
+    }
+    v->prof_n += 1;
+  }
   v->ev_used = 0;
   return TRI_OK;
 }
 
 int tri_ivf_scan_time(tri_ivf* v, double* total_ms, int32_t* launches) {
   if (!v) return fail(TRI_EINVAL, "index is NULL");
-  DeviceGuard g(v->device);
-  for (int i = 0; i < v->ev_used; ++i) {
-    CU(cudaEventSynchronize(v->ev[2 * i + 1]));
-    float ms = 0.f;
-    CU(cudaEventElapsedTime(&ms, v->ev[2 * i], v->ev[2 * i + 1]));
-    v->scan_ms += ms;
-    v->scan_launches += 1;
-  }
-  v->ev_used = 0;
-  if (total_ms) *total_ms = v->scan_ms;
-  if (launches) *launches = v->scan_launches;
+  TRY(ivf_collect(v));
+  if (total_ms) *total_ms = v->stage_ms[2];
+  if (launches) *launches = v->prof_n;
+  return TRI_OK;
+}
+
+int tri_ivf_stage_times(tri_ivf* v, double* ms, int32_t* searches) {
+  if (!v || !ms) return fail(TRI_EINVAL, "NULL argument");
+  TRY(ivf_collect(v));
+  for (int j = 0; j < kStagesProf; ++j) ms[j] = v->stage_ms[j];
+  if (searches) *searches = v->prof_n;
   return TRI_OK;
 }
 

@@ -58,6 +58,7 @@ struct ScanLaunch {
   int gmax;
   int cap;      // selection buffer per query (>= 2 * max kp, power of two)
   int grid;
+  int dbg;      // experiment switches (0 in production): 1 skip selection, 2 skip MMA
 };
 
 size_t scan_smem_bytes(int gmax, int qld, int cap);
@@ -67,7 +68,8 @@ cudaError_t launch_scan(const ScanLaunch& s, cudaStream_t st);
 // tensor-core scan (tri_tcscan.cu): fixed groups of 16 queries, qld <= kTcMaxQld
 constexpr int kTcMaxQld = 1024;
 constexpr int kTcGroup = 16;
-size_t tc_scan_smem_bytes(int qld, int cap);
+constexpr int kTcMaxKp = 256;  // register-resident top-kp lists in the epilogue
+size_t tc_scan_smem_bytes(int qld);
 cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st);
 
 cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,

@@ -7,8 +7,8 @@
 //                      item's rows with 2-D TMA (32-row x 32-float boxes,
 //                      128B swizzle = the UMMA K-major SW128 canonical layout)
 //                      into a kStages-deep ring of 128-row x 32-float slabs.
-//   warp 1  MMA      : allocates 32 TMEM columns (two 128x16 fp32
-//                      accumulators); one elected lane issues 4 MMAs
+//   warp 1  MMA      : allocates 64 TMEM columns (a ring of four 128x16
+//                      fp32 accumulators); one elected lane issues 4 MMAs
 //                      (M=128 rows, N=16 queries, K=8) per slab,
 //                      tcgen05.commit frees the slab / publishes a chunk.
 //   warps 2-5 epilogue: stage the group's queries into smem in the same SW128
@@ -31,7 +31,8 @@ constexpr int kTcN = 16;                        // MMA N = queries per group
 constexpr int kTcSlabF = 32;                    // floats per row per slab (128 B)
 constexpr int kTcSlabBytes = kTcRows * kTcSlabF * 4;  // 16 KB
 constexpr int kTcBoxRows = 32;
-constexpr int kTcStages = 6;
+constexpr int kTcStages = 9;
+constexpr int kTcAcc = 4;                       // TMEM accumulator ring (x16 columns)
 constexpr int kTcQTile = kTcN * kTcSlabF * 4;   // 2 KB of queries per slab
 constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
                               ((uint32_t)(kTcRows >> 4) << 24);  // F32 accum, TF32 A/B, K-major, N=16, M=128
@@ -85,7 +86,7 @@ struct TcSmem {
   uint64_t full[kTcStages], empty[kTcStages];
   uint64_t wfull[2], wempty[2];
   uint64_t qfull;
-  uint64_t tfull[2], tempty[2];
+  uint64_t tfull[kTcAcc], tempty[kTcAcc];
   WorkItem witem[2];
   int wend[2];
   uint32_t tmem_base;
@@ -94,9 +95,9 @@ struct TcSmem {
   float qn[kTcN];
 };
 
-size_t tc_scan_smem_bytes(int qld, int cap) {
+size_t tc_scan_smem_bytes(int qld) {
   const int nslab = (qld + kTcSlabF - 1) / kTcSlabF;
-  return 1024 + (size_t)kTcStages * kTcSlabBytes + (size_t)nslab * kTcQTile + (size_t)kTcN * cap * 8;
+  return 1024 + (size_t)kTcStages * kTcSlabBytes + (size_t)nslab * kTcQTile + (size_t)kTcN * kTcRows * 8;
 }
 
 // ---------------------------------------------------------------------------
@@ -171,9 +172,11 @@ __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, uns
         if (lane == 0) {
           const uint32_t a0 = ring_s + (uint32_t)stage * kTcSlabBytes;
           const uint32_t b0 = qs_s + (uint32_t)s * kTcQTile;
+          if (!(a.dbg & 2)) {
 #pragma unroll
-          for (int k = 0; k < kTcSlabF / 8; ++k)
-            umma_tf32(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), (s | k) != 0);
+            for (int k = 0; k < kTcSlabF / 8; ++k)
+              umma_tf32(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), (s | k) != 0);
+          }
           umma_commit(&sh.empty[stage]);  // slab reusable once these MMAs retire
           if (s == nslab - 1) umma_commit(&sh.tfull[acc]);
         }
@@ -183,7 +186,7 @@ __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, uns
           sphase ^= 1;
         }
       }
-      if (++acc == 2) {
+      if (++acc == kTcAcc) {
         acc = 0;
         aphase ^= 1;
       }
@@ -191,17 +194,144 @@ __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, uns
   }
 }
 
+// ---------------------------------------------------------------------------
+// Epilogue selection: every epilogue warp owns 4 of the group's queries
+// (g = ew, ew+4, ew+8, ew+12) and keeps each one's running top-kp list sorted
+// in registers (element j*32 + lane in v[j], kp = 32*KL).  Per 128-row chunk,
+// all 128 threads append the candidates that beat the query's threshold to a
+// small per-query smem buffer; the owner warp then folds them in 32 at a time:
+// register bitonic sort of the 32 (shuffles), then the bitonic split against
+// the list's last 32 and a bitonic merge back to sorted order.  No smem sorts,
+// two named barriers per chunk.
+
+__device__ __forceinline__ unsigned long long kmin(unsigned long long x, unsigned long long y) { return x < y ? x : y; }
+__device__ __forceinline__ unsigned long long kmax(unsigned long long x, unsigned long long y) { return x < y ? y : x; }
+
+__device__ __forceinline__ unsigned long long warp_sort32(unsigned long long x, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, j);
+      x = (((lane & k) == 0) == ((lane & j) == 0)) ? kmin(x, y) : kmax(x, y);
+    }
+  return x;
+}
+
+// v (sorted, 32*KL keys) <- smallest 32*KL of v U {x (sorted, one per lane)}, sorted.
+template <int KL>
+__device__ __forceinline__ void list_merge32(unsigned long long (&v)[KL], unsigned long long x, int lane) {
+  v[KL - 1] = kmin(v[KL - 1], __shfl_sync(0xffffffffu, x, 31 - lane));  // bitonic split vs the reversed batch
+#pragma unroll
+  for (int dj = KL / 2; dj >= 1; dj >>= 1)
+#pragma unroll
+    for (int j = 0; j < KL; ++j)
+      if ((j & dj) == 0) {
+        const unsigned long long lo = kmin(v[j], v[j + dj]), hi = kmax(v[j], v[j + dj]);
+        v[j] = lo;
+        v[j + dj] = hi;
+      }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1)
+#pragma unroll
+    for (int j = 0; j < KL; ++j) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, v[j], d);
+      v[j] = (lane & d) ? kmax(v[j], y) : kmin(v[j], y);
+    }
+}
+
+// One work item; returns the updated accumulator ring state (acc | aphase << 8).
+template <int KL>
+__device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& w, TcSmem& sh,
+                                           unsigned long long* sel, int ring) {
+  int acc = ring & 0xff, aphase = ring >> 8;
+  const int e = threadIdx.x - 64, lane = threadIdx.x & 31, ew = e >> 5;
+  const int quad = (threadIdx.x >> 5) & 3;
+  const int row_in_chunk = quad * 32 + lane;  // == TMEM lane
+  const int gc = w.member_count;
+  const uint32_t tmem = sh.tmem_base;
+  unsigned long long L[4][KL];
+#pragma unroll
+  for (int qi = 0; qi < 4; ++qi)
+#pragma unroll
+    for (int j = 0; j < KL; ++j) L[qi][j] = TRI_KEY_MAX;
+  const int nchunk = (w.row_count + kTcRows - 1) / kTcRows;
+  float xn_next = row_in_chunk < w.row_count ? a.xnorm[w.row_begin + row_in_chunk] : 0.f;
+  for (int c = 0; c < nchunk; ++c) {
+    const int rows = min(kTcRows, w.row_count - c * kTcRows);
+    const long long row = w.row_begin + (long long)c * kTcRows + row_in_chunk;
+    const bool valid = row_in_chunk < rows;
+    const float xn = xn_next;  // loaded one chunk ahead (HBM latency off the critical path)
+    if ((c + 1) * kTcRows + row_in_chunk < w.row_count) xn_next = a.xnorm[row + kTcRows];
+    tmb_wait(&sh.tfull[acc], aphase);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    uint32_t v[kTcN];
+    const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kTcN);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) tmb_arrive(&sh.tempty[acc]);
+    if (++acc == kTcAcc) {
+      acc = 0;
+      aphase ^= 1;
+    }
+    if (a.dbg & 1) continue;
+    if (valid) {
+      const uint32_t pos = (uint32_t)row;
+#pragma unroll
+      for (int g = 0; g < kTcN; ++g) {
+        if (g < gc) {
+          const float dot = __uint_as_float(v[g]);
+          const unsigned long long key = make_key(__fmaf_rn(-2.f, dot, __fadd_rn(sh.qn[g], xn)), pos);
+          if (key < sh.thr[g]) sel[g * kTcRows + atomicAdd(&sh.cnt[g], 1)] = key;  // <= 128 per chunk
+        }
+      }
+    }
+    epi_sync();
+#pragma unroll
+    for (int qi = 0; qi < 4; ++qi) {
+      const int g = ew + 4 * qi;
+      if (g < gc) {
+        const int n = sh.cnt[g];
+        for (int b = 0; b < n; b += 32) {
+          unsigned long long x = b + lane < n ? sel[g * kTcRows + b + lane] : TRI_KEY_MAX;
+          x = warp_sort32(x, lane);
+          list_merge32<KL>(L[qi], x, lane);
+        }
+        if (n > 0) {
+          const unsigned long long t = __shfl_sync(0xffffffffu, L[qi][KL - 1], 31);
+          if (lane == 0) {
+            sh.cnt[g] = 0;
+            sh.thr[g] = t;
+          }
+        }
+      }
+    }
+    epi_sync();
+  }
+#pragma unroll
+  for (int qi = 0; qi < 4; ++qi) {
+    const int g = ew + 4 * qi;
+    if (g < gc) {
+      unsigned long long* out = a.part + a.members[w.member_begin + g].slot;
+#pragma unroll
+      for (int j = 0; j < KL; ++j) out[j * 32 + lane] = L[qi][j];
+    }
+  }
+  return acc | (aphase << 8);
+}
+
 // Epilogue: 4 warps, thread e (0..127) <-> TMEM lane e <-> chunk row e.
 __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, unsigned long long* sel) {
-  const int e = threadIdx.x - 64;              // 0..127
+  const int e = threadIdx.x - 64;  // 0..127
   const int lane = threadIdx.x & 31;
-  const int ew = e >> 5;                       // epilogue warp 0..3
-  const int quad = (threadIdx.x >> 5) & 3;     // TMEM lane quadrant this warp may access
-  const int row_in_chunk = quad * 32 + lane;   // == TMEM lane
   const int nslab = (a.qld + kTcSlabF - 1) / kTcSlabF;
-  const int cap = a.cap;
-  int wslot = 0, wphase = 0, acc = 0, aphase = 0;
-  const uint32_t tmem = sh.tmem_base;
+  int wslot = 0, wphase = 0, ring = 0;
   for (;;) {
     tmb_wait(&sh.wfull[wslot], wphase);
     const int end = sh.wend[wslot];
@@ -213,7 +343,7 @@ __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, 
       wphase ^= 1;
     }
     if (end) return;
-    const int gc = w.member_count, kp = w.kp;
+    const int gc = w.member_count;
     // Stage queries: slab s, query g, 16B chunk c -> qs + s*2KB + g*128 + ((c ^ (g&7)) << 4)
     {
       const float4* Q4 = reinterpret_cast<const float4*>(a.Q);
@@ -235,69 +365,13 @@ __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, 
       epi_sync();
       if (e == 0) tmb_arrive(&sh.qfull);
     }
-    const int nchunk = (w.row_count + kTcRows - 1) / kTcRows;
-    for (int c = 0; c < nchunk; ++c) {
-      const int rows = min(kTcRows, w.row_count - c * kTcRows);
-      const long long row = w.row_begin + (long long)c * kTcRows + row_in_chunk;
-      const bool valid = row_in_chunk < rows;
-      const float xn = valid ? a.xnorm[row] : 0.f;
-      tmb_wait(&sh.tfull[acc], aphase);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      uint32_t v[kTcN];
-      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kTcN);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) tmb_arrive(&sh.tempty[acc]);
-      if (++acc == 2) {
-        acc = 0;
-        aphase ^= 1;
-      }
-      if (valid) {
-        const uint32_t pos = (uint32_t)row;
-#pragma unroll
-        for (int g = 0; g < kTcN; ++g) {
-          if (g < gc) {
-            const float dot = __uint_as_float(v[g]);
-            const unsigned long long key = make_key(__fmaf_rn(-2.f, dot, __fadd_rn(sh.qn[g], xn)), pos);
-            if (key < sh.thr[g]) sel[g * cap + atomicAdd(&sh.cnt[g], 1)] = key;  // cap - kp >= 128: no overflow
-          }
-        }
-      }
-      epi_sync();
-      for (int g = ew; g < gc; g += 4) {
-        const int n = sh.cnt[g];
-        if (n > kp) {
-          const int p2 = next_pow2(n);
-          unsigned long long* s = sel + g * cap;
-          for (int i = n + lane; i < p2; i += 32) s[i] = TRI_KEY_MAX;
-          __syncwarp();
-          warp_sort(s, p2, lane, KeyLess());
-          if (lane == 0) {
-            sh.cnt[g] = kp;
-            sh.thr[g] = s[kp - 1];
-          }
-          __syncwarp();
-        }
-      }
-      epi_sync();
+    switch (w.kp) {
+      case 32: ring = tc_epi_item<1>(a, w, sh, sel, ring); break;
+      case 64: ring = tc_epi_item<2>(a, w, sh, sel, ring); break;
+      case 128: ring = tc_epi_item<4>(a, w, sh, sel, ring); break;
+      default: ring = tc_epi_item<8>(a, w, sh, sel, ring); break;  // 256 (host caps tc kp at kTcMaxKp)
     }
-    for (int g = ew; g < gc; g += 4) {
-      const int n = sh.cnt[g];
-      const int p2 = next_pow2(n > 0 ? n : 1);
-      unsigned long long* s = sel + g * cap;
-      for (int i = n + lane; i < p2; i += 32) s[i] = TRI_KEY_MAX;
-      __syncwarp();
-      warp_sort(s, p2, lane, KeyLess());
-      unsigned long long* out = a.part + a.members[w.member_begin + g].slot;
-      for (int i = lane; i < kp; i += 32) out[i] = i < n ? s[i] : TRI_KEY_MAX;
-    }
-    epi_sync();  // selection buffers and qs free for the next item
+    epi_sync();  // qs and the append buffers are free for the next item
   }
 }
 
@@ -318,6 +392,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
     for (int s = 0; s < 2; ++s) {
       tmb_init(&sh.wfull[s], 1);
       tmb_init(&sh.wempty[s], 5);  // MMA warp + 4 epilogue warps
+    }
+    for (int s = 0; s < kTcAcc; ++s) {
       tmb_init(&sh.tfull[s], 1);
       tmb_init(&sh.tempty[s], 4);
     }
@@ -325,7 +401,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(tsu32(&sh.tmem_base)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n" ::"r"(tsu32(&sh.tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -342,12 +418,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(sh.tmem_base));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(sh.tmem_base));
   }
 }
 
 cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st) {
-  const size_t smem = tc_scan_smem_bytes(s.qld, s.cap);
+  const size_t smem = tc_scan_smem_bytes(s.qld);
   cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   scan_tc_kernel<<<s.grid, kTcThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(s.tmap_tc), s);

@@ -165,6 +165,15 @@ class IVFFlatIndex:
         _lib.check(_lib.gpu().tri_ivf_scan_time(self.handle, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    STAGES = ("coarse", "pack", "scan", "merge", "rerank", "fixup")
+
+    def stage_times(self):
+        """Accumulated per-stage device ms over profiled searches: (dict, n_searches)."""
+        ms = np.zeros(6, dtype=np.float64)
+        n = C.c_int32(0)
+        _lib.check(_lib.gpu().tri_ivf_stage_times(self.handle, ms.ctypes.data, C.byref(n)))
+        return dict(zip(self.STAGES, ms.tolist())), n.value
+
     def last_scan_bytes(self):
         b = C.c_int64(0)
         p = C.c_int64(0)
