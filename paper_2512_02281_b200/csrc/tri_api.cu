@@ -96,6 +96,7 @@ int ensure_host(HostBuf& b, size_t bytes) {
 
 long long g_scan_kernel = 0;  // 0 auto, 1 SIMT, 2 tensor core
 long long g_scan_debug = 0;   // timing experiments only (results invalid when set)
+long long g_dense_off = 0;    // 1: never use the dense small-store brute force
 
 // Candidate capacity: over-fetch so the certified re-rank almost never falls
 // back.  TF32 candidates carry ~2^-9 relative dot error, so they over-fetch 2x.
@@ -179,11 +180,13 @@ struct Workspace {
   int n_items = 0, grid = 0, gmax = 0, cap = 0, kp_max = 0, k_max = 0;
   long long plan_opts = -1;
   bool tc = false;
+  bool dense = false;
+  DevBuf dmat;
   size_t off_items = 0, off_members = 0, plan_bytes = 0;
   long long part_keys = 0;
   int last_fixups = 0;
   void free_all() {
-    for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d}) release(*b);
+    for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat}) release(*b);
     if (h_plan.p) cudaFreeHost(h_plan.p);
     h_plan.p = nullptr;
   }
@@ -323,13 +326,49 @@ int choose_scan(int qld, int d, int B, const int* k, std::vector<int>& kp, ScanC
   return TRI_OK;
 }
 
-long long plan_opts() { return g_scan_kernel * 100000 + g_kp_extra; }
+long long plan_opts() { return g_dense_off * 10000000 + g_scan_kernel * 100000 + g_kp_extra; }
 
 int plan_bruteforce(tri_store* s, int B, const int* k, cudaStream_t st) {
   Workspace& w = s->ws;
   if (w.plan_B == B && w.plan_n == s->n && w.plan_opts == plan_opts() && (int)w.plan_k.size() == B &&
       std::equal(w.plan_k.begin(), w.plan_k.end(), k))
     return TRI_OK;
+  // Dense path for small stores: the whole B x n distance matrix is cheap.
+  {
+    int kpd = kMinKp, kmx = 1;
+    for (int i = 0; i < B; ++i) {
+      kpd = std::max(kpd, kp_for(k[i], false));
+      kmx = std::max(kmx, k[i]);
+    }
+    if (!g_dense_off && s->n <= kDenseMaxN && kpd <= kDenseMaxKp) {
+      const size_t bytes = (((size_t)B * sizeof(QueryMeta) + 255) & ~(size_t)255) + 256;
+      TRY(ensure_host(w.h_plan, bytes));
+      TRY(ensure(w.plan, bytes));
+      QueryMeta* hm = static_cast<QueryMeta*>(w.h_plan.p);
+      for (int i = 0; i < B; ++i) {
+        hm[i].k = k[i];
+        hm[i].kp = kp_for(k[i], false);
+        hm[i].n_slots = 1;
+        hm[i].cls = cls_of(hm[i].kp);
+        hm[i].part_off = 0;
+        hm[i].n_total = s->n;
+      }
+      CU(cudaMemcpyAsync(w.plan.p, hm, bytes, cudaMemcpyHostToDevice, st));
+      CU(cudaStreamSynchronize(st));
+      w.plan_bytes = bytes;
+      w.plan_B = B;
+      w.plan_n = s->n;
+      w.plan_opts = plan_opts();
+      w.plan_k.assign(k, k + B);
+      w.dense = true;
+      w.tc = false;
+      w.kp_max = kpd;
+      w.k_max = kmx;
+      w.part_keys = 0;
+      return TRI_OK;
+    }
+  }
+  w.dense = false;
   std::vector<int> kp, cls(B);
   ScanChoice ch;
   TRY(choose_scan(s->qld, s->d, B, k, kp, ch, s->prefer_simt != 0));
@@ -444,12 +483,32 @@ int ensure_query_bufs(Workspace& w, int B, int d, int qld) {
   return TRI_OK;
 }
 
+int finish_bruteforce(tri_store* s, const double* q64dev, const Workspace& qw, const QueryMeta* meta, int B, int ldo,
+                      long long* ids, double* dists, bool tc, cudaStream_t st);
+
+// Dense small-store brute force: distance matrix + warp select -> merged.
+int dense_core(tri_store* s, const Workspace& qw, const double* q64dev, int B, int ldo, long long* ids,
+               double* dists, cudaStream_t st) {
+  Workspace& w = s->ws;
+  const long long ldd = (s->n + 3) & ~3LL;
+  TRY(ensure(w.dmat, (size_t)kDenseSlices * B * ldd * sizeof(float)));
+  TRY(ensure(w.merged, (size_t)B * w.kp_max * sizeof(unsigned long long)));
+  TRY(ensure(w.exact, (size_t)B * w.kp_max * 16));
+  TRY(ensure(w.flags, (size_t)(B + 64) * sizeof(int)));
+  const QueryMeta* meta = static_cast<const QueryMeta*>(w.plan.p);
+  CU(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
+  CU(launch_dense(qw.Q32.as<float>(), s->qld, qw.qn32.as<float>(), B, s->X, s->dp, s->xnorm, s->n, s->dp,
+                  w.dmat.as<float>(), ldd, meta, w.merged.as<unsigned long long>(), w.kp_max, w.kp_max, st));
+  return finish_bruteforce(s, q64dev, qw, meta, B, ldo, ids, dists, false, st);
+}
+
 // Run the brute-force pipeline on prepared queries (Q32/qn32/qn64 in `qw`,
 // fp64 queries at q64dev).  Results to device ids/dists with row stride ldo.
 int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int B, const int* k, int ldo,
                     long long* ids, double* dists, cudaStream_t st) {
   Workspace& w = s->ws;
   TRY(plan_bruteforce(s, B, k, st));
+  if (w.dense) return dense_core(s, qw, q64dev, B, ldo, ids, dists, st);
   TRY(ensure(w.part, (size_t)w.part_keys * sizeof(unsigned long long)));
   TRY(ensure(w.merged, (size_t)B * w.kp_max * sizeof(unsigned long long)));
   TRY(ensure(w.exact, (size_t)B * w.kp_max * 16));
@@ -484,6 +543,15 @@ int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int
   CU(w.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
   CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
                   st));
+  return finish_bruteforce(s, q64dev, qw, meta, B, ldo, ids, dists, w.tc, st);
+}
+
+// Exact re-rank + certification + fix-up shared by the scan and dense paths.
+int finish_bruteforce(tri_store* s, const double* q64dev, const Workspace& qw, const QueryMeta* meta, int B, int ldo,
+                      long long* ids, double* dists, bool tc, cudaStream_t st) {
+  Workspace& w = s->ws;
+  int* n_flag = w.flags.as<int>();
+  int* flag_list = n_flag + 64;
   RerankLaunch rr;
   rr.merged = w.merged.as<unsigned long long>();
   rr.exact = reinterpret_cast<Exact*>(w.exact.p);
@@ -497,7 +565,7 @@ int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int
   rr.idmap = nullptr;
   rr.id_offset = s->id_offset;
   rr.xmax = s->xmax;
-  const Bound bd = bound_for(s->d, w.tc);
+  const Bound bd = bound_for(s->d, tc);
   rr.cdot = g_force_fixup ? 1e30 : bd.cdot;
   rr.csum = bd.csum;
   rr.out_ids = ids;
@@ -571,6 +639,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "kp_extra")) g_kp_extra = value;
   else if (!std::strcmp(name, "scan_kernel")) g_scan_kernel = value;
   else if (!std::strcmp(name, "scan_debug")) g_scan_debug = value;
+  else if (!std::strcmp(name, "dense_off")) g_dense_off = value;
   else return fail(TRI_EINVAL, "unknown option '%s'", name);
   return TRI_OK;
 }

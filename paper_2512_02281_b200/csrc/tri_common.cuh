@@ -121,6 +121,64 @@ struct ExactLess {
   __device__ __forceinline__ bool operator()(const Exact& a, const Exact& b) const { return exact_less(a, b); }
 };
 
+// ---------------------------------------------------------------------------
+// Warp-register bitonic networks.  A sorted list of 32*KL keys lives in a warp
+// as v[j] on lane l = element j*32 + l.
+
+__device__ __forceinline__ unsigned long long kmin(unsigned long long x, unsigned long long y) { return x < y ? x : y; }
+__device__ __forceinline__ unsigned long long kmax(unsigned long long x, unsigned long long y) { return x < y ? y : x; }
+
+// Sort 32 keys (one per lane) ascending.
+__device__ __forceinline__ unsigned long long warp_sort32(unsigned long long x, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, j);
+      x = (((lane & k) == 0) == ((lane & j) == 0)) ? kmin(x, y) : kmax(x, y);
+    }
+  return x;
+}
+
+// Sort a bitonic register list ascending (all compare-exchanges ascending).
+template <int KL>
+__device__ __forceinline__ void bitonic_merge_regs(unsigned long long (&v)[KL], int lane) {
+#pragma unroll
+  for (int dj = KL / 2; dj >= 1; dj >>= 1)
+#pragma unroll
+    for (int j = 0; j < KL; ++j)
+      if ((j & dj) == 0) {
+        const unsigned long long lo = kmin(v[j], v[j + dj]), hi = kmax(v[j], v[j + dj]);
+        v[j] = lo;
+        v[j + dj] = hi;
+      }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1)
+#pragma unroll
+    for (int j = 0; j < KL; ++j) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, v[j], d);
+      v[j] = (lane & d) ? kmax(v[j], y) : kmin(v[j], y);
+    }
+}
+
+// v (sorted, 32*KL keys) <- smallest 32*KL of v U {x (sorted, one per lane)}, sorted:
+// bitonic split of v's last 32 against the reversed batch, then a bitonic merge.
+template <int KL>
+__device__ __forceinline__ void list_merge32(unsigned long long (&v)[KL], unsigned long long x, int lane) {
+  v[KL - 1] = kmin(v[KL - 1], __shfl_sync(0xffffffffu, x, 31 - lane));
+  bitonic_merge_regs<KL>(v, lane);
+}
+
+// v (sorted) <- smallest 32*KL of v U p where p is a sorted list of the same
+// size given REVERSED (p_rev[j] on lane l = p[KP-1 - (j*32+l)]).
+template <int KL>
+__device__ __forceinline__ void list_merge_rev(unsigned long long (&v)[KL], const unsigned long long (&p_rev)[KL],
+                                               int lane) {
+#pragma unroll
+  for (int j = 0; j < KL; ++j) v[j] = kmin(v[j], p_rev[j]);
+  bitonic_merge_regs<KL>(v, lane);
+}
+
 __host__ __device__ __forceinline__ int next_pow2(int v) {
   int p = 1;
   while (p < v) p <<= 1;

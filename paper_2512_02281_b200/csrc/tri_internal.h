@@ -77,6 +77,15 @@ cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, fl
 cudaError_t launch_norms(const float* X, long long n, int d, long long ldx, float* xnorm,
                          unsigned long long* xmax_bits, cudaStream_t st);
 
+// dense small-store brute force (tri_dense.cu): distances to D (B x ldd fp32),
+// then per-query top-kp (kp <= kDenseMaxKp) straight into `merged`.
+constexpr long long kDenseMaxN = 4096;
+constexpr int kDenseMaxKp = 256;
+constexpr int kDenseSlices = 2;  // split-K slices of the distance GEMM (D holds kDenseSlices x B x ldd partials)
+cudaError_t launch_dense(const float* Q, int qld, const float* qn, int B, const float* X, long long ldx,
+                         const float* xn, long long n, int dp, float* D, long long ldd, const QueryMeta* meta,
+                         unsigned long long* merged, int ld_merged, int kp_max, cudaStream_t st);
+
 cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, unsigned long long* merged,
                          int ld_merged, int B, int kp_max, cudaStream_t st);
 

@@ -9,6 +9,8 @@
 // Certification: every dropped candidate has approx distance >= T (the kp-th
 // kept one) and |approx - exact| <= E = cdot*2|q|max|x| + csum*(|q|+max|x|)^2, so if the k-th
 // exact distance + E < T no dropped vector can enter the exact top-k.
+#include <algorithm>
+
 #include "tri_common.cuh"
 #include "tri_internal.h"
 
@@ -142,9 +144,88 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(const unsigned long lon
   for (int i = threadIdx.x; i < kp; i += kThreads) merged[(long long)q * ld_merged + i] = i < n ? buf[i] : TRI_KEY_MAX;
 }
 
+// Warp-tree merge (kp <= 256): 8 warps per query; warp w folds slots
+// w, w+8, ... into a register list (each partial list is sorted, so one bitonic
+// split + merge per slot; a slot whose best key cannot beat the list is
+// skipped), then the 8 lists are merged pairwise through shared memory.
+constexpr int kMergeWarps = 8;
+
+template <int KL>
+__device__ __forceinline__ void merge_tree(const unsigned long long* __restrict__ src, int n_slots,
+                                           unsigned long long* __restrict__ dst, unsigned long long* sm) {
+  constexpr int KP = 32 * KL;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long L[KL];
+#pragma unroll
+  for (int j = 0; j < KL; ++j) L[j] = TRI_KEY_MAX;
+  unsigned long long thr = TRI_KEY_MAX;
+  for (int s0 = warp; s0 < n_slots; s0 += 2 * kMergeWarps) {
+    // two slots in flight per warp: both loads issue before either merge
+    unsigned long long P0[KL], P1[KL];
+    const int s1 = s0 + kMergeWarps;
+    const unsigned long long* a0 = src + (long long)s0 * KP;
+    const unsigned long long* a1 = src + (long long)s1 * KP;
+#pragma unroll
+    for (int j = 0; j < KL; ++j) {
+      P0[j] = a0[(KL - 1 - j) * 32 + (31 - lane)];
+      P1[j] = s1 < n_slots ? a1[(KL - 1 - j) * 32 + (31 - lane)] : TRI_KEY_MAX;
+    }
+    if (__shfl_sync(0xffffffffu, P0[KL - 1], 31) < thr) {  // P0[KL-1] on lane 31 = the slot's best key
+      list_merge_rev<KL>(L, P0, lane);
+      thr = __shfl_sync(0xffffffffu, L[KL - 1], 31);
+    }
+    if (__shfl_sync(0xffffffffu, P1[KL - 1], 31) < thr) {
+      list_merge_rev<KL>(L, P1, lane);
+      thr = __shfl_sync(0xffffffffu, L[KL - 1], 31);
+    }
+  }
+  for (int stride = 1; stride < kMergeWarps; stride <<= 1) {
+    if ((warp & (2 * stride - 1)) == stride) {
+#pragma unroll
+      for (int j = 0; j < KL; ++j) sm[warp * KP + j * 32 + lane] = L[j];
+    }
+    __syncthreads();
+    if ((warp & (2 * stride - 1)) == 0) {
+      unsigned long long R[KL];
+#pragma unroll
+      for (int j = 0; j < KL; ++j) R[j] = sm[(warp + stride) * KP + (KL - 1 - j) * 32 + (31 - lane)];
+      list_merge_rev<KL>(L, R, lane);
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+#pragma unroll
+    for (int j = 0; j < KL; ++j) dst[j * 32 + lane] = L[j];
+  }
+}
+
+__global__ void __launch_bounds__(32 * kMergeWarps) merge_tree_kernel(const unsigned long long* __restrict__ part,
+                                                                      const QueryMeta* __restrict__ meta,
+                                                                      unsigned long long* __restrict__ merged,
+                                                                      int ld_merged) {
+  extern __shared__ unsigned long long msm[];
+  const int q = blockIdx.x;
+  const QueryMeta m = meta[q];
+  const unsigned long long* src = part + m.part_off;
+  unsigned long long* dst = merged + (long long)q * ld_merged;
+  switch (m.kp) {
+    case 32: merge_tree<1>(src, m.n_slots, dst, msm); break;
+    case 64: merge_tree<2>(src, m.n_slots, dst, msm); break;
+    case 128: merge_tree<4>(src, m.n_slots, dst, msm); break;
+    default: merge_tree<8>(src, m.n_slots, dst, msm); break;
+  }
+}
+
 cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, unsigned long long* merged,
                          int ld_merged, int B, int kp_max, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
+  if (kp_max <= 256) {
+    const size_t smem = (size_t)kMergeWarps * kp_max * sizeof(unsigned long long);
+    cudaError_t e = cudaFuncSetAttribute(merge_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    merge_tree_kernel<<<B, 32 * kMergeWarps, smem, st>>>(part, meta, merged, ld_merged);
+    return cudaGetLastError();
+  }
   int buf_n = next_pow2(kp_max + kThreads * 4);
   size_t smem = (size_t)buf_n * sizeof(unsigned long long);
   cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -156,54 +237,72 @@ cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, 
 // ---------------------------------------------------------------------------
 // Exact fp64 re-rank + certification.
 //
-// exact_pairs_kernel: one CTA per (query, 32 candidates); thread pair
-// (2c, 2c+1) computes candidate c, thread 2c+l running numpy lane l (elements
-// 8b + 2*sub + l, sub = 3..0, then the 2-lane tail), so the value is
-// bit-identical to exact_sq_dist / the reference.  Candidate rows and the
-// fp64 query are staged through shared memory in 256-float slabs with
-// cp.async (all loads in flight at once); slabs are 8-aligned so numpy's
-// 8-element blocks never straddle one.
+// exact_pairs_kernel: one warp-sized CTA per (query, 16 candidates); thread
+// pair (2c, 2c+1) computes candidate c, thread 2c+l running numpy lane l
+// (elements 8b + 2*sub + l, sub = 3..0, then the 2-lane tail), so the value is
+// bit-identical to exact_sq_dist / the reference.  The candidate rows arrive
+// in shared memory by 1-D bulk copies (one per row per <= 1024-float slab,
+// one mbarrier); slabs are 8-aligned so numpy's 8-element blocks never
+// straddle one.
 
-constexpr int kPairCands = 32;
-constexpr int kPairSlab = 256;
-constexpr int kPairStride = kPairSlab + 4;  // 2-way worst bank conflict, 16B aligned rows
+constexpr int kPairCands = 16;
+constexpr int kPairSlab = 1024;  // floats
 
-__global__ void __launch_bounds__(2 * kPairCands) exact_pairs_kernel(RerankLaunch r) {
-  __shared__ __align__(16) float xs[kPairCands * kPairStride];
-  __shared__ __align__(16) double qs[kPairSlab];
+__device__ __forceinline__ uint32_t sel_su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__global__ void __launch_bounds__(2 * kPairCands) exact_pairs_kernel(RerankLaunch r, int row_stride) {
+  extern __shared__ __align__(16) unsigned char pair_smem[];
+  __shared__ __align__(8) uint64_t bar;
   __shared__ long long pos_s[kPairCands];
+  double* qs = reinterpret_cast<double*>(pair_smem);
+  const int slab_max = min(kPairSlab, (r.d + 15) & ~15);
+  float* xs = reinterpret_cast<float*>(qs + slab_max);
   const int groups = r.ld_merged / kPairCands;
   const int q = blockIdx.x / groups;
   const int c = (blockIdx.x - q * groups) * kPairCands + (threadIdx.x >> 1);
-  const int ln = threadIdx.x & 1;
+  const int ln = threadIdx.x & 1, lane = threadIdx.x;
   const int kp = r.meta[q].kp;
   if ((c & ~(kPairCands - 1)) >= kp) return;  // whole CTA beyond this query's capacity
   const long long p = (long long)q * r.ld_merged + c;
   const unsigned long long key = r.merged[p];
   const bool active = key != TRI_KEY_MAX;
   const long long pos = active ? (long long)key_pos(key) : -1;
-  if (ln == 0) pos_s[threadIdx.x >> 1] = pos;
-  __syncthreads();
+  if (ln == 0) pos_s[lane >> 1] = pos;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sel_su32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
   const int d = r.d;
   const double* qg = r.q64 + (long long)q * d;
   double acc = 0.0;
+  uint32_t phase = 0;
   for (int s0 = 0; s0 < d; s0 += kPairSlab) {
     const int w = min(kPairSlab, d - s0);
-    const int w4 = (w + 3) >> 2;  // stored rows are zero padded to a multiple of 16
-    const uint32_t xbase = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
-    for (int i = threadIdx.x; i < kPairCands * w4; i += blockDim.x) {
-      const int row = i / w4, ch = i - row * w4;
-      const long long rp = pos_s[row];
-      const float* src = rp >= 0 ? r.X + rp * r.ldx + s0 + ch * 4 : r.X;
-      const uint32_t dst = xbase + (uint32_t)((row * kPairStride + ch * 4) * 4);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(rp >= 0 ? 16 : 0));
+    const int w16 = (w + 15) & ~15;  // stored rows are zero padded to a multiple of 16
+    if (lane == 0) {
+      int nrow = 0;
+      for (int i = 0; i < kPairCands; ++i) nrow += pos_s[i] >= 0;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sel_su32(&bar)),
+                   "r"((uint32_t)(nrow * w16 * 4))
+                   : "memory");
+      for (int i = 0; i < kPairCands; ++i)
+        if (pos_s[i] >= 0)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                           sel_su32(xs + i * row_stride)),
+                       "l"(r.X + pos_s[i] * r.ldx + s0), "r"((uint32_t)(w16 * 4)), "r"(sel_su32(&bar))
+                       : "memory");
     }
-    asm volatile("cp.async.commit_group;\n" ::);
-    for (int j = threadIdx.x; j < w; j += blockDim.x) qs[j] = qg[s0 + j];
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncthreads();
+    for (int j = lane; j < w; j += 32) qs[j] = qg[s0 + j];
+    __syncwarp();
+    asm volatile(
+        "{\n .reg .pred P;\n PWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra PWAIT_%=;\n}\n" ::"r"(
+            sel_su32(&bar)),
+        "r"(phase)
+        : "memory");
+    phase ^= 1;
     if (active) {
-      const float* xr = xs + (threadIdx.x >> 1) * kPairStride;
+      const float* xr = xs + (lane >> 1) * row_stride;
       int i = 0;
       for (; i < w && s0 + i + 8 <= d; i += 8) {
 #pragma unroll
@@ -221,7 +320,7 @@ __global__ void __launch_bounds__(2 * kPairCands) exact_pairs_kernel(RerankLaunc
         }
       }
     }
-    __syncthreads();
+    __syncwarp();
   }
   const double other = __shfl_xor_sync(0xffffffffu, acc, 1);
   if (ln == 0 && c < kp) {
@@ -231,6 +330,99 @@ __global__ void __launch_bounds__(2 * kPairCands) exact_pairs_kernel(RerankLaunc
       e.id = (r.idmap ? r.idmap[pos] : pos) + r.id_offset;
     }
     r.exact[p] = e;
+  }
+}
+
+// finalize: one warp per query sorts its kp exact (dist, id) entries in
+// registers (bitonic network over element j*32 + lane), certifies, writes k.
+__device__ __forceinline__ bool ex_less(double ad, long long ai, double bd, long long bi) {
+  return ad < bd || (ad == bd && ai < bi);
+}
+
+template <int KL>
+__device__ __forceinline__ void finalize_query(const RerankLaunch& r, int q, int lane) {
+  constexpr int KP = 32 * KL;
+  const QueryMeta m = r.meta[q];
+  double d[KL];
+  long long id[KL];
+#pragma unroll
+  for (int j = 0; j < KL; ++j) {
+    const Exact e = r.exact[(long long)q * r.ld_merged + j * 32 + lane];
+    d[j] = e.d;
+    id[j] = e.id;
+  }
+#pragma unroll
+  for (int k = 2; k <= KP; k <<= 1)
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      if (jj >= 32) {
+        const int dj = jj >> 5;
+#pragma unroll
+        for (int j = 0; j < KL; ++j)
+          if ((j & dj) == 0) {
+            const int e = j * 32 + lane;
+            const bool up = (e & k) == 0;
+            const bool sw = up ? ex_less(d[j + dj], id[j + dj], d[j], id[j]) : ex_less(d[j], id[j], d[j + dj], id[j + dj]);
+            if (sw) {
+              const double td = d[j];
+              const long long ti = id[j];
+              d[j] = d[j + dj];
+              id[j] = id[j + dj];
+              d[j + dj] = td;
+              id[j + dj] = ti;
+            }
+          }
+      } else {
+#pragma unroll
+        for (int j = 0; j < KL; ++j) {
+          const double od = __shfl_xor_sync(0xffffffffu, d[j], jj);
+          const long long oi = __shfl_xor_sync(0xffffffffu, id[j], jj);
+          const int e = j * 32 + lane;
+          const bool keep_min = ((e & k) == 0) == ((lane & jj) == 0);
+          const bool other_less = ex_less(od, oi, d[j], id[j]);
+          if (keep_min == other_less) {
+            d[j] = od;
+            id[j] = oi;
+          }
+        }
+      }
+    }
+  // certification: every dropped candidate has approx distance >= T
+  bool cert = true;
+  if (m.n_total > m.kp) {
+    const int kk = m.k - 1;
+    double dk = 0.0;
+#pragma unroll
+    for (int j = 0; j < KL; ++j) {
+      const double t = __shfl_sync(0xffffffffu, d[j], kk & 31);
+      if (j == (kk >> 5)) dk = t;
+    }
+    const double T = (double)key_dist(r.merged[(long long)q * r.ld_merged + m.kp - 1]);
+    const double s = r.qn64[q] + r.xmax;
+    const double E = (r.cdot * 2.0 * r.qn64[q] * r.xmax + r.csum * s * s) * 1.001 + 1e-30;
+    cert = dk + E < T;
+  }
+  if (!cert && lane == 0) r.flag_list[atomicAdd(r.n_flag, 1)] = q;
+#pragma unroll
+  for (int j = 0; j < KL; ++j) {
+    const int e = j * 32 + lane;
+    if (e < m.k) {
+      const bool ok = id[j] != 0x7fffffffffffffffll;
+      r.out_ids[(long long)q * r.ldo + e] = ok ? id[j] : -1;
+      r.out_d[(long long)q * r.ldo + e] = d[j];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) finalize_warp_kernel(RerankLaunch r) {
+  const int q = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (q >= r.B) return;
+  const int lane = threadIdx.x & 31;
+  switch (r.meta[q].kp) {
+    case 32: finalize_query<1>(r, q, lane); break;
+    case 64: finalize_query<2>(r, q, lane); break;
+    case 128: finalize_query<4>(r, q, lane); break;
+    default: finalize_query<8>(r, q, lane); break;
   }
 }
 
@@ -260,15 +452,209 @@ __global__ void __launch_bounds__(128) finalize_kernel(RerankLaunch r) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused exact re-rank (kp <= 256): one CTA per query, 2*kp_max threads.
+// The fp64 query is staged in shared memory once; thread pair (2c, 2c+1) runs
+// numpy's two lanes for candidate c reading the row straight from L2/HBM in
+// 4-block (32-float) groups, double-buffered in registers; warp 0 then sorts
+// the kp (dist, id) pairs in registers, certifies and writes the top k.
+
+// Fused exact re-rank (kp <= 256): one CTA per query, 2*kp_max threads.
+// The fp64 query is staged in shared memory once; thread pair (2c, 2c+1) runs
+// numpy's two lanes for candidate c, reading the row straight from L2/HBM in
+// 4-block (32-float) groups with the next group's 8 float4 loads in flight.
+// fp32 -> fp64 is done with integer bit moves for normal numbers (F2F sits on
+// a slow conversion pipe; the value is identical since the conversion is
+// exact).  The (dist, id) order comes from parallel rank counting (O(kp^2)
+// compares, no serial sorting network); rank k-1 feeds the certification.
+
+// One 1-D bulk copy per candidate row per slab, issued by the candidate's own
+// pair-leader thread (all rows in flight at once, no per-16B address math).
+__device__ __forceinline__ void rf_issue(float* buf, uint64_t* bar, int S, int c, long long pos, const float* X,
+                                         long long ldx, int s0, int dpad, int nvalid, bool leader) {
+  const int w = min(S, dpad - s0);
+  if (threadIdx.x == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"((uint32_t)(nvalid * w * 4))
+                 : "memory");
+  if (leader && pos >= 0)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(buf + c * (S + 4)))),
+                 "l"(X + pos * ldx + s0), "r"((uint32_t)(w * 4)),
+                 "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+
+// Exact fp32 -> fp64 without the F2F pipe for normal numbers and zeros
+// (branch-free); *sub is set when x is subnormal (caller falls back to F2F).
+__device__ __forceinline__ double f2d_bits(float x, bool& sub) {
+  const uint32_t u = __float_as_uint(x);
+  const uint32_t e = (u >> 23) & 0xffu;
+  const uint32_t nz = e ? 0xffffffffu : 0u;
+  sub = sub || (e == 0 && (u & 0x7fffffu));
+  return __hiloint2double((int)((u & 0x80000000u) | ((((e + 896u) << 20) | ((u >> 3) & 0xfffffu)) & nz)),
+                          (int)((u << 29) & nz));
+}
+
+__global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S) {
+  extern __shared__ __align__(16) unsigned char rf_smem[];
+  __shared__ double s_dk;
+  __shared__ __align__(8) uint64_t bars[2];
+  const int q = blockIdx.x;
+  const QueryMeta m = r.meta[q];
+  const int d = r.d, kpm = r.kp_max, kp = m.kp;
+  const int dpad = (d + 15) & ~15;
+  double* qs = reinterpret_cast<double*>(rf_smem);       // dpad
+  double* exd = qs + dpad;                               // kp_max
+  long long* exi = reinterpret_cast<long long*>(exd + kpm);
+  float* ring = reinterpret_cast<float*>(exi + kpm);     // 2 x kp_max x (S + 4)
+  const int tid = threadIdx.x, nthr = blockDim.x, c = tid >> 1, ln = tid & 1;
+  unsigned long long key = TRI_KEY_MAX;
+  if (c < kp) key = r.merged[(long long)q * r.ld_merged + c];
+  const bool active = key != TRI_KEY_MAX;
+  const long long pos = active ? (long long)key_pos(key) : -1;
+  const bool leader = ln == 0 && c < kp;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bars[0]))));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bars[1]))));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  const double* qg = r.q64 + (long long)q * d;
+  for (int j = tid; j < dpad; j += nthr) qs[j] = j < d ? qg[j] : 0.0;
+  const int nvalid = __syncthreads_count(leader && active);
+  const int nslab = (dpad + S - 1) / S;
+  const int buf_floats = kpm * (S + 4);
+  rf_issue(ring, &bars[0], S, c, pos, r.X, r.ldx, 0, dpad, nvalid, leader);
+  double acc = 0.0;
+  const int nfull = d >> 3;  // numpy's full 8-element blocks (global count)
+  for (int s = 0; s < nslab; ++s) {
+    if (s + 1 < nslab)
+      rf_issue(ring + ((s + 1) & 1) * buf_floats, &bars[(s + 1) & 1], S, c, pos, r.X, r.ldx, (s + 1) * S, dpad, nvalid,
+               leader);
+    asm volatile(
+        "{\n .reg .pred P;\n RFW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra RFW_%=;\n}\n" ::"r"(
+            static_cast<uint32_t>(__cvta_generic_to_shared(&bars[s & 1]))),
+        "r"((uint32_t)((s >> 1) & 1))
+        : "memory");
+    const int s0 = s * S;
+    if (active) {
+      const float* xr = ring + (s & 1) * buf_floats + c * (S + 4);
+      const double* qb = qs + s0;
+      const int bend = min(S >> 3, nfull - (s0 >> 3));  // full blocks inside this slab
+      int b = 0;
+      for (; b + 4 <= bend; b += 4) {
+        // 16 independent squared differences first, then the 16-step chain
+        double t2[16];
+        bool sub = false;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const float4 lo = *reinterpret_cast<const float4*>(xr + 8 * (b + bb));
+          const float4 hi = *reinterpret_cast<const float4*>(xr + 8 * (b + bb) + 4);
+          const float xs[4] = {ln ? hi.w : hi.z, ln ? hi.y : hi.x, ln ? lo.w : lo.z, ln ? lo.y : lo.x};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {  // sub = 3 - t -> element 2*(3-t) + ln
+            const double df = __dsub_rn(qb[8 * (b + bb) + 2 * (3 - t) + ln], f2d_bits(xs[t], sub));
+            t2[bb * 4 + t] = __dmul_rn(df, df);
+          }
+        }
+        if (__builtin_expect(__any_sync(__activemask(), sub), 0)) {
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int e = 8 * (b + bb) + 2 * (3 - t) + ln;
+              const double df = __dsub_rn(qb[e], (double)xr[e]);
+              t2[bb * 4 + t] = __dmul_rn(df, df);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 16; ++t) acc = __dadd_rn(t2[t], acc);
+      }
+      for (; b < bend; ++b) {
+#pragma unroll
+        for (int sub = 3; sub >= 0; --sub) {
+          const int e = 8 * b + 2 * sub + ln;
+          const double df = __dsub_rn(qb[e], (double)xr[e]);
+          acc = __dadd_rn(__dmul_rn(df, df), acc);
+        }
+      }
+      if (s0 + 8 * bend >= 8 * nfull) {  // numpy's 2-lane tail lives in this slab
+        for (int i = 8 * nfull - s0; i < min(S, d - s0); i += 2) {
+          const int e = i + ln;
+          if (s0 + e < d) {
+            const double df = __dsub_rn(qb[e], (double)xr[e]);
+            acc = __dadd_rn(__dmul_rn(df, df), acc);
+          }
+        }
+      }
+    }
+    __syncthreads();  // buffer (s & 1) is refilled by the next iteration's stage
+  }
+  const double other = __shfl_xor_sync(0xffffffffu, acc, 1);
+  if (ln == 0 && c < kpm) {
+    exd[c] = active ? __dadd_rn(acc, other) : __longlong_as_double(0x7ff0000000000000ll);
+    exi[c] = active ? (r.idmap ? r.idmap[pos] : pos) + r.id_offset : 0x7fffffffffffffffll;
+  }
+  __syncthreads();
+  if (tid < kp) {
+    const double md = exd[tid];
+    const long long mi = exi[tid];
+    int rank = 0;
+    for (int j = 0; j < kp; ++j) {  // (dist, id) order; slot index breaks ties between empty slots
+      const double dj = exd[j];
+      const long long ij = exi[j];
+      rank += ex_less(dj, ij, md, mi) || (dj == md && ij == mi && j < tid);
+    }
+    if (rank < m.k) {
+      const bool ok = mi != 0x7fffffffffffffffll;
+      r.out_ids[(long long)q * r.ldo + rank] = ok ? mi : -1;
+      r.out_d[(long long)q * r.ldo + rank] = md;
+    }
+    if (rank == m.k - 1) s_dk = md;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    bool cert = true;
+    if (m.n_total > kp) {
+      const double T = (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]);
+      const double sq = r.qn64[q] + r.xmax;
+      const double E = (r.cdot * 2.0 * r.qn64[q] * r.xmax + r.csum * sq * sq) * 1.001 + 1e-30;
+      cert = s_dk + E < T;
+    }
+    if (!cert) r.flag_list[atomicAdd(r.n_flag, 1)] = q;
+  }
+}
+
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
   if (r.B <= 0) return cudaSuccess;
-  exact_pairs_kernel<<<(unsigned)(r.B * (r.ld_merged / kPairCands)), 2 * kPairCands, 0, st>>>(r);
-  cudaError_t e = cudaGetLastError();
+  // slab width: 2 buffers x kp x (S+4) floats <= ~72 KB (several CTAs per SM)
+  const int S = std::max(32, std::min(256, 8192 / r.kp_max));
+  const size_t rf_smem = (size_t)((r.d + 15) & ~15) * sizeof(double) + (size_t)r.kp_max * 16 +
+                         (size_t)2 * r.kp_max * (S + 4) * sizeof(float);
+  if (r.kp_max <= 256 && rf_smem <= 200 * 1024) {
+    const size_t smem = rf_smem;
+    cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    rerank_fused_kernel<<<r.B, 2 * r.kp_max, smem, st>>>(r, S);
+    return cudaGetLastError();
+  }
+  const int slab = std::min(kPairSlab, (r.d + 15) & ~15);
+  const int row_stride = slab + 4;  // floats; 16B-aligned rows, 2-way worst bank conflict
+  const size_t smem = (size_t)slab * sizeof(double) + (size_t)kPairCands * row_stride * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(exact_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  size_t smem = (size_t)r.kp_max * sizeof(Exact);
-  e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  exact_pairs_kernel<<<(unsigned)(r.B * (r.ld_merged / kPairCands)), 2 * kPairCands, smem, st>>>(r, row_stride);
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  finalize_kernel<<<r.B, 128, smem, st>>>(r);
+  if (r.kp_max <= 256) {
+    finalize_warp_kernel<<<(r.B + 3) / 4, 128, 0, st>>>(r);
+    return cudaGetLastError();
+  }
+  const size_t fsm = (size_t)r.kp_max * sizeof(Exact);
+  e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+  if (e != cudaSuccess) return e;
+  finalize_kernel<<<r.B, 128, fsm, st>>>(r);
   return cudaGetLastError();
 }
 

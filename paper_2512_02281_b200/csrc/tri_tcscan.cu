@@ -204,42 +204,6 @@ __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, uns
 // the list's last 32 and a bitonic merge back to sorted order.  No smem sorts,
 // two named barriers per chunk.
 
-__device__ __forceinline__ unsigned long long kmin(unsigned long long x, unsigned long long y) { return x < y ? x : y; }
-__device__ __forceinline__ unsigned long long kmax(unsigned long long x, unsigned long long y) { return x < y ? y : x; }
-
-__device__ __forceinline__ unsigned long long warp_sort32(unsigned long long x, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, j);
-      x = (((lane & k) == 0) == ((lane & j) == 0)) ? kmin(x, y) : kmax(x, y);
-    }
-  return x;
-}
-
-// v (sorted, 32*KL keys) <- smallest 32*KL of v U {x (sorted, one per lane)}, sorted.
-template <int KL>
-__device__ __forceinline__ void list_merge32(unsigned long long (&v)[KL], unsigned long long x, int lane) {
-  v[KL - 1] = kmin(v[KL - 1], __shfl_sync(0xffffffffu, x, 31 - lane));  // bitonic split vs the reversed batch
-#pragma unroll
-  for (int dj = KL / 2; dj >= 1; dj >>= 1)
-#pragma unroll
-    for (int j = 0; j < KL; ++j)
-      if ((j & dj) == 0) {
-        const unsigned long long lo = kmin(v[j], v[j + dj]), hi = kmax(v[j], v[j + dj]);
-        v[j] = lo;
-        v[j + dj] = hi;
-      }
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1)
-#pragma unroll
-    for (int j = 0; j < KL; ++j) {
-      const unsigned long long y = __shfl_xor_sync(0xffffffffu, v[j], d);
-      v[j] = (lane & d) ? kmax(v[j], y) : kmin(v[j], y);
-    }
-}
-
 // One work item; returns the updated accumulator ring state (acc | aphase << 8).
 template <int KL>
 __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& w, TcSmem& sh,

@@ -14,12 +14,15 @@ from paper_2512_02281_b200.workload import gen_matrix, gen_vectors_chunked
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["tc", "simt"], autouse=True)
+@pytest.fixture(params=["auto", "simt", "nodense"], autouse=True)
 def scan_kernel(request):
-    """Run every test on both candidate-generation kernels (tcgen05 TF32 and SIMT fp32)."""
-    _lib.set_option("scan_kernel", 0 if request.param == "tc" else 1)
+    """Run every test on each candidate-generation path: auto (dense small-store
+    brute force + tcgen05 TF32 scan), fp32 SIMT scan only, and scan-only (no dense)."""
+    _lib.set_option("scan_kernel", 1 if request.param == "simt" else 0)
+    _lib.set_option("dense_off", 1 if request.param != "auto" else 0)
     yield request.param
     _lib.set_option("scan_kernel", 0)
+    _lib.set_option("dense_off", 0)
     _lib.set_option("force_fixup", 0)
 
 

@@ -10,6 +10,9 @@ from paper_2512_02281_b200 import _lib  # noqa: E402
 from paper_2512_02281_b200.ann_graph import _DeviceStore  # noqa: E402
 
 SHAPES = [(1024, 768, 256, 32), (4096, 768, 256, 32), (100_000, 128, 64, 10), (100_000, 128, 1024, 10)]
+if len(sys.argv) > 1:
+    SHAPES = [SHAPES[int(i)] for i in sys.argv[1].split(",")]
+KERNELS = (1, 2) if len(sys.argv) <= 2 else tuple(int(x) for x in sys.argv[2].split(","))
 lib = _lib.gpu()
 for n, d, B, k in SHAPES:
     rng = np.random.Generator(np.random.Philox(n + d))
@@ -20,7 +23,7 @@ for n, d, B, k in SHAPES:
     dd = torch.empty((B, k), dtype=torch.float64, device="cuda")
     ks = np.full(B, k, np.int32)
     s = torch.cuda.Stream()
-    for kern in (1, 2):
+    for kern in KERNELS:
         _lib.set_option("scan_kernel", kern)
         def run():
             _lib.check(lib.tri_knn_bruteforce_dev(st.handle, q.data_ptr(), B, ks.ctypes.data, k, ids.data_ptr(),
