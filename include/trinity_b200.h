@@ -50,9 +50,11 @@ const char* tri_last_error(void);
 int tri_version(void);
 int tri_device_count(int32_t* count);
 /* Debug/test knobs: "force_fixup" (1 = treat every query as uncertified),
- * "kp_extra" (extra over-fetch added to k), "scan_kernel" (0 auto,
- * 1 fp32 SIMT scan, 2 tensor-core scan when it fits), "scan_debug" (timing
- * experiments only: results are invalid while set). */
+ * "kp_extra" (extra over-fetch added to k), "scan_kernel" (0 auto: IVF
+ * lists on the fp16 tensor-core scan, stores on TF32 when it fits; 1 fp32
+ * SIMT scan; 2 TF32 tensor-core scan, no fp16), "dense_off" (1 = no dense
+ * small-store path), "scan_debug" (timing experiments only: results are
+ * invalid while set). */
 int tri_set_option(const char* name, int64_t value);
 
 /* Vector store: replaces ann_graph.VectorStore (ann_graph.py:21-48).

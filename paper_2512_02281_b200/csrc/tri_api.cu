@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -94,7 +95,7 @@ int ensure_host(HostBuf& b, size_t bytes) {
   return TRI_OK;
 }
 
-long long g_scan_kernel = 0;  // 0 auto, 1 SIMT, 2 tensor core
+long long g_scan_kernel = 0;  // 0 auto (IVF: fp16 tensor core), 1 fp32 SIMT, 2 TF32 tensor core
 long long g_scan_debug = 0;   // timing experiments only (results invalid when set)
 long long g_dense_off = 0;    // 1: never use the dense small-store brute force
 
@@ -129,11 +130,29 @@ int sm_count(int device) {
 struct Bound {
   double cdot, csum;
 };
-Bound bound_for(int d, bool tc) {
+// Scan arithmetic -> certification constants:
+//   kSimt  fp32 FFMA dot of fp32(q) and x                       cdot = gamma_d
+//   kTf32  tensor-core TF32 (operands truncated to 10 bits)     cdot = 2^-9 + ...
+//   kF16   tensor-core f16 on power-of-two scaled RN fp16 copies of fp32(q)
+//          and x: conversion 2^-11 each (+2^-24 for q -> fp32), subnormal floor
+//          2^-25 of a 2^14-scaled element on each side (<= 2^-38 sqrt(d)),
+//          accumulation as for TF32; csum gains 2^-80 for an fp32 subnormal
+//          product after the exact 1/(s_q s_x) rescale.
+enum ScanMode { kSimt = 0, kTf32 = 1, kF16 = 2 };
+Bound bound_for(int d, int mode) {
   const double u = std::ldexp(1.0, -24);
   Bound b;
   b.csum = 6.0 * u;
-  b.cdot = tc ? std::ldexp(1.0, -9) + std::ldexp(1.0, -19) + 2.0 * d * std::ldexp(1.0, -23) : d * u / (1.0 - d * u);
+  const double acc = 2.0 * d * std::ldexp(1.0, -23);
+  if (mode == kTf32) {
+    b.cdot = std::ldexp(1.0, -9) + std::ldexp(1.0, -19) + acc;
+  } else if (mode == kF16) {
+    const double u16 = std::ldexp(1.0, -11);
+    b.cdot = 2 * u16 + u + 3 * u16 * u16 + acc * (1.0 + 4 * u16) + std::ldexp(1.0, -37) * std::sqrt((double)d);
+    b.csum += std::ldexp(1.0, -80);
+  } else {
+    b.cdot = d * u / (1.0 - d * u);
+  }
   return b;
 }
 
@@ -142,7 +161,7 @@ int sel_cap(int kp_max) { return std::max(kSelCapMin, 2 * kp_max); }
 // 2-D TMA descriptors over a row-major fp32 matrix (rows x ldx floats):
 //   SIMT scan : 64-row x 16-float boxes, 64-byte swizzle
 //   TC scan   : 32-row x 32-float boxes, 128-byte swizzle (UMMA K-major SW128)
-int make_tmap(CUtensorMap* map, const float* X, long long rows, int ldx, bool tc) {
+int make_tmap(CUtensorMap* map, const void* X, long long rows, int ldx, bool tc, bool f16 = false) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult qr;
@@ -151,11 +170,13 @@ int make_tmap(CUtensorMap* map, const float* X, long long rows, int ldx, bool tc
     if (!fn || qr != cudaDriverEntryPointSuccess) return fail(TRI_ECUDA, "cuTensorMapEncodeTiled unavailable");
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
+  const size_t esz = f16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)ldx, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ldx * sizeof(float)};
-  cuuint32_t box[2] = {tc ? 32u : 16u, tc ? 32u : 64u};
+  cuuint64_t strides[1] = {(cuuint64_t)ldx * esz};
+  cuuint32_t box[2] = {tc ? (cuuint32_t)(128 / esz) : 16u, tc ? 32u : 64u};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
+  CUresult r = encode(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                      const_cast<void*>(X), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, tc ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TRI_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -166,13 +187,25 @@ int make_tmap(CUtensorMap* map, const float* X, long long rows, int ldx, bool tc
 // or the queries do not fit its shared-memory layout.
 bool use_tc(int qld, int kp_max_tc) {
   if (g_scan_kernel == 1) return false;
-  return kp_max_tc <= kTcMaxKp && qld <= kTcMaxQld && tc_scan_smem_bytes(qld) <= (size_t)kSmemLimit;
+  return kp_max_tc <= kTcMaxKp && qld <= kTcMaxQld && tc_scan_smem_bytes(qld * 4) <= (size_t)kSmemLimit;
 }
 
-// Per-search scratch shared by the brute-force and IVF pipelines.
+// Per-search scratch shared by the brute-force and IVF pipelines.  One
+// Workspace per stream ("lane", see Lanes): searches issued on different
+// streams never share scratch, so they can overlap on the device.
 struct Workspace {
+  static constexpr int kStaging = 4;  // pinned host staging ring depth
   DevBuf q64, Q32, qn32, qn64, flags, plan, part, merged, exact, out_ids, out_d;
+  // IVF per-search buffers
+  DevBuf probes, probe_d, counts, fill, mbase, items, members, counters, meta;
+  DevBuf Qh, qinv;  // fp16 scan: scaled fp16 queries + 1/(s_q s_x)
   HostBuf h_plan;
+  HostBuf h_stage[kStaging];
+  cudaEvent_t staged[kStaging] = {nullptr, nullptr, nullptr, nullptr};
+  bool staged_live[kStaging] = {false, false, false, false};
+  int stage_i = 0;
+  cudaEvent_t done = nullptr;  // recorded after the last search issued on this lane
+  bool done_live = false;
   // cached host plan (brute force)
   std::vector<int> plan_k;
   int plan_B = -1;
@@ -185,12 +218,83 @@ struct Workspace {
   size_t off_items = 0, off_members = 0, plan_bytes = 0;
   long long part_keys = 0;
   int last_fixups = 0;
+  int last_B = 0, last_npmax = 0, last_f16 = 0;
+  std::vector<int> last_np;
   void free_all() {
-    for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat}) release(*b);
+    for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat,
+                      &probes, &probe_d, &counts, &fill, &mbase, &items, &members, &counters, &meta, &Qh, &qinv})
+      release(*b);
     if (h_plan.p) cudaFreeHost(h_plan.p);
     h_plan.p = nullptr;
+    for (int i = 0; i < kStaging; ++i) {
+      if (h_stage[i].p) cudaFreeHost(h_stage[i].p);
+      h_stage[i].p = nullptr;
+      if (staged[i]) cudaEventDestroy(staged[i]);
+      staged[i] = nullptr;
+    }
+    if (done) cudaEventDestroy(done);
+    done = nullptr;
   }
 };
+
+// Pinned host staging for an async upload: returns a slot of the lane's ring
+// whose previous upload has completed (host waits only if the device is
+// kStaging uploads behind).  Call staged_upload() after filling it.
+int stage_host(Workspace& w, size_t bytes, int* slot, void** ptr) {
+  const int i = w.stage_i;
+  w.stage_i = (w.stage_i + 1) % Workspace::kStaging;
+  if (w.staged_live[i]) CU(cudaEventSynchronize(w.staged[i]));
+  w.staged_live[i] = false;
+  TRY(ensure_host(w.h_stage[i], bytes));
+  *slot = i;
+  *ptr = w.h_stage[i].p;
+  return TRI_OK;
+}
+
+int staged_upload(Workspace& w, int slot, void* dst, size_t bytes, cudaStream_t st) {
+  CU(cudaMemcpyAsync(dst, w.h_stage[slot].p, bytes, cudaMemcpyHostToDevice, st));
+  if (!w.staged[slot]) CU(cudaEventCreateWithFlags(&w.staged[slot], cudaEventDisableTiming));
+  CU(cudaEventRecord(w.staged[slot], st));
+  w.staged_live[slot] = true;
+  return TRI_OK;
+}
+
+// Stream -> Workspace map.  A new stream takes a free lane; with all lanes
+// taken the least recently assigned one is recycled after its last search
+// (its `done` event) has completed.
+struct Lanes {
+  static constexpr int kMax = 4;
+  Workspace w[kMax];
+  cudaStream_t st[kMax] = {nullptr, nullptr, nullptr, nullptr};
+  int used = 0, next_victim = 0, last = 0;
+  int get(cudaStream_t s, Workspace** out) {
+    for (int i = 0; i < used; ++i)
+      if (st[i] == s) {
+        last = i;
+        *out = &w[i];
+        return TRI_OK;
+      }
+    int i = used < kMax ? used++ : next_victim;
+    if (i == next_victim && used == kMax) next_victim = (next_victim + 1) % kMax;
+    if (w[i].done_live) CU(cudaEventSynchronize(w[i].done));
+    w[i].done_live = false;
+    st[i] = s;
+    last = i;
+    *out = &w[i];
+    return TRI_OK;
+  }
+  Workspace& recent() { return w[last]; }
+  void free_all() {
+    for (auto& x : w) x.free_all();
+  }
+};
+
+int lane_done(Workspace& w, cudaStream_t st) {
+  if (!w.done) CU(cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming));
+  CU(cudaEventRecord(w.done, st));
+  w.done_live = true;
+  return TRI_OK;
+}
 
 }  // namespace
 
@@ -205,7 +309,8 @@ struct tri_store {
   double xmax = 0.0;
   CUtensorMap tmap, tmap_tc;
   cudaStream_t own = nullptr;
-  Workspace ws;
+  Lanes lanes;
+  std::mutex mu;  // enqueue is serialised per handle; waits happen outside it
 };
 
 struct tri_ivf {
@@ -221,14 +326,16 @@ struct tri_ivf {
   int* assign = nullptr;  // per original row (store order)
   double xmax = 0.0;
   CUtensorMap tmap, tmap_tc;
+  // fp16 copy of the lists for candidate generation (null: TF32 / SIMT scans)
+  void* Xh = nullptr;
+  int dph = 0;       // row stride in halves (multiple of 64)
+  float sx = 1.f;    // power-of-two scale of the fp16 copy
+  CUtensorMap tmap_h;
   std::vector<long long> h_off;
   tri_store* cstore = nullptr;  // centroids as a vector store (coarse step)
   cudaStream_t own = nullptr;
-  Workspace ws;
-  DevBuf probes, probe_d, counts, fill, mbase, items, members, counters, meta;
-  HostBuf h_meta;
-  int last_B = 0, last_npmax = 0;
-  std::vector<int> last_np;
+  Lanes lanes;
+  std::mutex mu;  // enqueue is serialised per handle; waits happen outside it
   bool prof = false;
   // profiling: a ring of (start, stop) event pairs around the list-scan kernel,
   // read back lazily so the timed loop never synchronises.
@@ -328,8 +435,7 @@ int choose_scan(int qld, int d, int B, const int* k, std::vector<int>& kp, ScanC
 
 long long plan_opts() { return g_dense_off * 10000000 + g_scan_kernel * 100000 + g_kp_extra; }
 
-int plan_bruteforce(tri_store* s, int B, const int* k, cudaStream_t st) {
-  Workspace& w = s->ws;
+int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_t st) {
   if (w.plan_B == B && w.plan_n == s->n && w.plan_opts == plan_opts() && (int)w.plan_k.size() == B &&
       std::equal(w.plan_k.begin(), w.plan_k.end(), k))
     return TRI_OK;
@@ -483,13 +589,12 @@ int ensure_query_bufs(Workspace& w, int B, int d, int qld) {
   return TRI_OK;
 }
 
-int finish_bruteforce(tri_store* s, const double* q64dev, const Workspace& qw, const QueryMeta* meta, int B, int ldo,
-                      long long* ids, double* dists, bool tc, cudaStream_t st);
+int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Workspace& qw, const QueryMeta* meta,
+                      int B, int ldo, long long* ids, double* dists, bool tc, cudaStream_t st);
 
 // Dense small-store brute force: distance matrix + warp select -> merged.
-int dense_core(tri_store* s, const Workspace& qw, const double* q64dev, int B, int ldo, long long* ids,
+int dense_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q64dev, int B, int ldo, long long* ids,
                double* dists, cudaStream_t st) {
-  Workspace& w = s->ws;
   const long long ldd = (s->n + 3) & ~3LL;
   TRY(ensure(w.dmat, (size_t)kDenseSlices * B * ldd * sizeof(float)));
   TRY(ensure(w.merged, (size_t)B * w.kp_max * sizeof(unsigned long long)));
@@ -499,16 +604,15 @@ int dense_core(tri_store* s, const Workspace& qw, const double* q64dev, int B, i
   CU(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
   CU(launch_dense(qw.Q32.as<float>(), s->qld, qw.qn32.as<float>(), B, s->X, s->dp, s->xnorm, s->n, s->dp,
                   w.dmat.as<float>(), ldd, meta, w.merged.as<unsigned long long>(), w.kp_max, w.kp_max, st));
-  return finish_bruteforce(s, q64dev, qw, meta, B, ldo, ids, dists, false, st);
+  return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, false, st);
 }
 
 // Run the brute-force pipeline on prepared queries (Q32/qn32/qn64 in `qw`,
 // fp64 queries at q64dev).  Results to device ids/dists with row stride ldo.
-int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int B, const int* k, int ldo,
-                    long long* ids, double* dists, cudaStream_t st) {
-  Workspace& w = s->ws;
-  TRY(plan_bruteforce(s, B, k, st));
-  if (w.dense) return dense_core(s, qw, q64dev, B, ldo, ids, dists, st);
+int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q64dev, int B, const int* k,
+                    int ldo, long long* ids, double* dists, cudaStream_t st) {
+  TRY(plan_bruteforce(s, w, B, k, st));
+  if (w.dense) return dense_core(s, w, qw, q64dev, B, ldo, ids, dists, st);
   TRY(ensure(w.part, (size_t)w.part_keys * sizeof(unsigned long long)));
   TRY(ensure(w.merged, (size_t)B * w.kp_max * sizeof(unsigned long long)));
   TRY(ensure(w.exact, (size_t)B * w.kp_max * 16));
@@ -521,7 +625,7 @@ int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int
   CU(cudaMemsetAsync(ctr + 1, 0, sizeof(int), st));
   CU(cudaMemsetAsync(n_flag, 0, sizeof(int), st));
 
-  ScanLaunch sl;
+  ScanLaunch sl{};
   sl.tmap = &s->tmap;
   sl.tmap_tc = &s->tmap_tc;
   sl.X = s->X;
@@ -543,16 +647,15 @@ int bruteforce_core(tri_store* s, const Workspace& qw, const double* q64dev, int
   CU(w.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
   CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
                   st));
-  return finish_bruteforce(s, q64dev, qw, meta, B, ldo, ids, dists, w.tc, st);
+  return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, w.tc, st);
 }
 
 // Exact re-rank + certification + fix-up shared by the scan and dense paths.
-int finish_bruteforce(tri_store* s, const double* q64dev, const Workspace& qw, const QueryMeta* meta, int B, int ldo,
-                      long long* ids, double* dists, bool tc, cudaStream_t st) {
-  Workspace& w = s->ws;
+int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Workspace& qw, const QueryMeta* meta,
+                      int B, int ldo, long long* ids, double* dists, bool tc, cudaStream_t st) {
   int* n_flag = w.flags.as<int>();
   int* flag_list = n_flag + 64;
-  RerankLaunch rr;
+  RerankLaunch rr{};
   rr.merged = w.merged.as<unsigned long long>();
   rr.exact = reinterpret_cast<Exact*>(w.exact.p);
   rr.ld_merged = w.kp_max;
@@ -565,7 +668,7 @@ int finish_bruteforce(tri_store* s, const double* q64dev, const Workspace& qw, c
   rr.idmap = nullptr;
   rr.id_offset = s->id_offset;
   rr.xmax = s->xmax;
-  const Bound bd = bound_for(s->d, tc);
+  const Bound bd = bound_for(s->d, tc ? kTf32 : kSimt);
   rr.cdot = g_force_fixup ? 1e30 : bd.cdot;
   rr.csum = bd.csum;
   rr.out_ids = ids;
@@ -670,7 +773,7 @@ int tri_store_destroy(tri_store* s) {
   if (s->own) cudaStreamSynchronize(s->own);
   if (s->X) cudaFree(s->X);
   if (s->xnorm) cudaFree(s->xnorm);
-  s->ws.free_all();
+  s->lanes.free_all();
   if (s->own) cudaStreamDestroy(s->own);
   delete s;
   return TRI_OK;
@@ -698,11 +801,15 @@ int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32
   TRY(validate_k(k, B, s->n, "k"));
   int km = *std::max_element(k, k + B);
   if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
+  std::lock_guard<std::mutex> lk(s->mu);
   DeviceGuard g(s->device);
   cudaStream_t st = pick(stream, s->own);
-  TRY(ensure_query_bufs(s->ws, B, s->d, s->qld));
-  TRY(prep_queries(s->ws, q, B, s->d, s->qld, st));
-  return bruteforce_core(s, s->ws, q, B, k, ldo, reinterpret_cast<long long*>(ids), dists, st);
+  Workspace* w = nullptr;
+  TRY(s->lanes.get(st, &w));
+  TRY(ensure_query_bufs(*w, B, s->d, s->qld));
+  TRY(prep_queries(*w, q, B, s->d, s->qld, st));
+  TRY(bruteforce_core(s, *w, *w, q, B, k, ldo, reinterpret_cast<long long*>(ids), dists, st));
+  return lane_done(*w, st);
 }
 
 int tri_knn_bruteforce(tri_store* s, const double* q, int32_t B, const int32_t* k, int32_t ldo, int64_t* ids,
@@ -714,15 +821,18 @@ int tri_knn_bruteforce(tri_store* s, const double* q, int32_t B, const int32_t* 
   int km = *std::max_element(k, k + B);
   if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
   TRY(check_queries(q, (long long)B * s->d));
+  std::lock_guard<std::mutex> lk(s->mu);
   DeviceGuard g(s->device);
   cudaStream_t st = pick(stream, s->own);
-  Workspace& w = s->ws;
+  Workspace* wp = nullptr;
+  TRY(s->lanes.get(st, &wp));
+  Workspace& w = *wp;
   TRY(ensure_query_bufs(w, B, s->d, s->qld));
   TRY(ensure(w.out_ids, (size_t)B * ldo * sizeof(long long)));
   TRY(ensure(w.out_d, (size_t)B * ldo * sizeof(double)));
   CU(cudaMemcpyAsync(w.q64.p, q, (size_t)B * s->d * sizeof(double), cudaMemcpyHostToDevice, st));
   TRY(prep_queries(w, w.q64.as<double>(), B, s->d, s->qld, st));
-  TRY(bruteforce_core(s, w, w.q64.as<double>(), B, k, ldo, w.out_ids.as<long long>(), w.out_d.as<double>(), st));
+  TRY(bruteforce_core(s, w, w, w.q64.as<double>(), B, k, ldo, w.out_ids.as<long long>(), w.out_d.as<double>(), st));
   CU(cudaMemcpyAsync(ids, w.out_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(dists, w.out_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(&w.last_fixups, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -734,9 +844,10 @@ int tri_store_last_fixups(tri_store* s, int32_t* n) {
   if (!s || !n) return fail(TRI_EINVAL, "NULL argument");
   DeviceGuard g(s->device);
   int v = 0;
-  if (s->ws.flags.p) {
-    CU(cudaStreamSynchronize(s->own));
-    CU(cudaMemcpy(&v, s->ws.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
+  Workspace& w = s->lanes.recent();
+  if (w.flags.p) {
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(&v, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
   }
   *n = v;
   return TRI_OK;
@@ -757,6 +868,7 @@ int tri_distance_tasks(tri_store* s, const int32_t* owner, const int64_t* cand, 
   if (n_tasks == 0) return TRI_OK;
   for (int i = 0; i < n_tasks; ++i)
     if (owner[i] < 0 || owner[i] >= n_queries) return fail(TRI_EINVAL, "task %d owner %d out of range", i, owner[i]);
+  std::lock_guard<std::mutex> lk(s->mu);
   DeviceGuard g(s->device);
   cudaStream_t st = pick(stream, s->own);
   auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
@@ -764,15 +876,17 @@ int tri_distance_tasks(tri_store* s, const int32_t* owner, const int64_t* cand, 
   const size_t o_c = al(qb), o_o = o_c + al((size_t)n_tasks * sizeof(long long));
   const size_t o_out = o_o + al((size_t)n_tasks * sizeof(int));
   const size_t total = o_out + al((size_t)n_tasks * sizeof(double));
-  DevBuf& buf = s->ws.merged;  // reuse a scratch buffer
+  Workspace* w = nullptr;
+  TRY(s->lanes.get(st, &w));
+  DevBuf& buf = w->merged;  // reuse a scratch buffer
   TRY(ensure(buf, total));
   unsigned char* base = buf.as<unsigned char>();
   double* dq = reinterpret_cast<double*>(base);
   long long* dc = reinterpret_cast<long long*>(base + o_c);
   int* dow = reinterpret_cast<int*>(base + o_o);
   double* dout = reinterpret_cast<double*>(base + o_out);
-  TRY(ensure(s->ws.flags, 64 * sizeof(int)));
-  int* derr = s->ws.flags.as<int>() + 1;
+  TRY(ensure(w->flags, 64 * sizeof(int)));
+  int* derr = w->flags.as<int>() + 1;
   CU(cudaMemcpyAsync(dq, queries, qb, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(dc, cand, (size_t)n_tasks * sizeof(long long), cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(dow, owner, (size_t)n_tasks * sizeof(int), cudaMemcpyHostToDevice, st));
@@ -794,6 +908,30 @@ int tri_distance_tasks(tri_store* s, const int32_t* owner, const int64_t* cand, 
 // ---------------------------------------------------------------------------
 // IVF
 
+// fp16 copy of the list-major rows for the tensor-core scan, scaled by
+// sx = 2^(14 - ilogb(max|x|)).  Skipped (TF32 scan) when the data's largest
+// magnitude is outside [2^-30, 2^30] or the rows are too wide for the TC scan.
+static int ivf_half_copy(tri_ivf* v, cudaStream_t st) {
+  if (v->n < 1 || v->qld > kTcMaxQld) return TRI_OK;
+  unsigned int* mb = nullptr;
+  CU(cudaMalloc(&mb, sizeof(unsigned int)));
+  CU(cudaMemsetAsync(mb, 0, sizeof(unsigned int), st));
+  CU(launch_absmax(v->Xl, v->n, v->d, v->dp, mb, st));
+  unsigned int bits = 0;
+  CU(cudaMemcpyAsync(&bits, mb, sizeof(bits), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  cudaFree(mb);
+  float m;
+  std::memcpy(&m, &bits, sizeof(m));
+  if (!(m >= std::ldexp(1.0f, -30) && m <= std::ldexp(1.0f, 30))) return TRI_OK;
+  v->sx = std::ldexp(1.0f, 14 - std::ilogb(m));
+  v->dph = (v->d + 63) & ~63;
+  CU(cudaMalloc(&v->Xh, (size_t)v->n * v->dph * 2));
+  CU(launch_to_half(v->Xl, v->n, v->d, v->dp, v->sx, v->Xh, v->dph, st));
+  TRY(make_tmap(&v->tmap_h, v->Xh, v->n, v->dph, true, true));
+  return TRI_OK;
+}
+
 static int ivf_layout(tri_ivf* v, const float* X, long long ldx, const long long* perm_dev, cudaStream_t st) {
   const long long n = v->n;
   CU(cudaMalloc(&v->Xl, (size_t)n * v->dp * sizeof(float)));
@@ -812,6 +950,7 @@ static int ivf_layout(tri_ivf* v, const float* X, long long ldx, const long long
   CU(cudaStreamSynchronize(st));
   cudaFree(xm);
   std::memcpy(&v->xmax, &bits, sizeof(double));
+  TRY(ivf_half_copy(v, st));
   // list order by descending size (ties: smaller list id first)
   std::vector<int> order(v->nlist);
   std::iota(order.begin(), order.end(), 0);
@@ -971,13 +1110,9 @@ int tri_ivf_destroy(tri_ivf* v) {
   DeviceGuard g(v->device);
   if (v->own) cudaStreamSynchronize(v->own);
   for (void* p : {(void*)v->Xl, (void*)v->xnl, (void*)v->ids, (void*)v->list_off, (void*)v->list_by_size,
-                  (void*)v->assign})
+                  (void*)v->assign, v->Xh})
     if (p) cudaFree(p);
-  v->ws.free_all();
-  for (DevBuf* b : {&v->probes, &v->probe_d, &v->counts, &v->fill, &v->mbase, &v->items, &v->members, &v->counters,
-                    &v->meta})
-    release(*b);
-  if (v->h_meta.p) cudaFreeHost(v->h_meta.p);
+  v->lanes.free_all();
   if (v->cstore) tri_store_destroy(v->cstore);
   for (cudaEvent_t e : v->ev) cudaEventDestroy(e);
   if (v->own) cudaStreamDestroy(v->own);
@@ -1009,8 +1144,8 @@ int tri_ivf_list_sizes(tri_ivf* v, int64_t* sizes) {
   return TRI_OK;
 }
 
-int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe,
-                       int32_t ldo, int64_t* ids, double* dists, void* stream) {
+static int ivf_search_enqueue(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe,
+                              int32_t ldo, int64_t* ids, double* dists, void* stream) {
   if (!v) return fail(TRI_EINVAL, "index is NULL");
   if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
   if (B == 0) return TRI_OK;
@@ -1020,7 +1155,11 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
   DeviceGuard g(v->device);
   cudaStream_t st = pick(stream, v->own);
-  Workspace& w = v->ws;
+  Workspace* wp = nullptr;
+  Workspace* cw = nullptr;
+  TRY(v->lanes.get(st, &wp));
+  TRY(v->cstore->lanes.get(st, &cw));
+  Workspace& w = *wp;
   const int npmax = *std::max_element(nprobe, nprobe + B);
   TRY(ensure_query_bufs(w, B, v->d, v->qld));
   const bool rec = v->prof && v->ev_used < kProfSearches;
@@ -1038,18 +1177,29 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   TRY(mark(0));
 
   // 1. coarse step: exact top-nprobe centroids per query
-  TRY(ensure(v->probes, (size_t)B * npmax * sizeof(long long)));
-  TRY(ensure(v->probe_d, (size_t)B * npmax * sizeof(double)));
-  TRY(bruteforce_core(v->cstore, w, q, B, nprobe, npmax, v->probes.as<long long>(), v->probe_d.as<double>(), st));
+  TRY(ensure(w.probes, (size_t)B * npmax * sizeof(long long)));
+  TRY(ensure(w.probe_d, (size_t)B * npmax * sizeof(double)));
+  TRY(bruteforce_core(v->cstore, *cw, w, q, B, nprobe, npmax, w.probes.as<long long>(), w.probe_d.as<double>(),
+                      st));
 
   // 2. host-side per-query plan (k, kp, slots) -> device
   std::vector<int> kp;
   ScanChoice ch;
   TRY(choose_scan(v->qld, v->d, B, k, kp, ch, false));
   const int kp_max = ch.kp_max, k_max = ch.k_max;
+  // fp16 tensor-core scan when the index holds the fp16 copy (scan_kernel 2 forces TF32)
+  const bool f16 = ch.tc && v->Xh && g_scan_kernel != 2;
+  if (f16) {
+    TRY(ensure(w.Qh, (size_t)B * v->dph * 2));
+    TRY(ensure(w.qinv, (size_t)B * sizeof(float)));
+    CU(launch_prep_half(w.Q32.as<float>(), B, v->qld, v->d, v->sx, w.Qh.p, v->dph, w.qinv.as<float>(), st));
+  }
   long long part_keys = 0, members = 0;
-  TRY(ensure_host(v->h_meta, (size_t)B * (sizeof(QueryMeta) + sizeof(int)) + 64));
-  QueryMeta* hm = static_cast<QueryMeta*>(v->h_meta.p);
+  const size_t meta_bytes = (size_t)B * (sizeof(QueryMeta) + sizeof(int));
+  int slot = 0;
+  void* hbuf = nullptr;
+  TRY(stage_host(w, meta_bytes + 64, &slot, &hbuf));
+  QueryMeta* hm = static_cast<QueryMeta*>(hbuf);
   int* hnp = reinterpret_cast<int*>(hm + B);
   for (int i = 0; i < B; ++i) {
     hm[i].k = k[i];
@@ -1065,28 +1215,28 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   const int cap = ch.cap, gmax = ch.gmax;
   int cls_mask = 0;
   for (int i = 0; i < B; ++i) cls_mask |= 1 << hm[i].cls;
-  TRY(ensure(v->meta, (size_t)B * (sizeof(QueryMeta) + sizeof(int)) + 64));
-  CU(cudaMemcpyAsync(v->meta.p, v->h_meta.p, (size_t)B * (sizeof(QueryMeta) + sizeof(int)), cudaMemcpyHostToDevice, st));
-  QueryMeta* dmeta = v->meta.as<QueryMeta>();
+  TRY(ensure(w.meta, meta_bytes + 64));
+  TRY(staged_upload(w, slot, w.meta.p, meta_bytes, st));
+  QueryMeta* dmeta = w.meta.as<QueryMeta>();
   int* dnp = reinterpret_cast<int*>(dmeta + B);
   TRY(ensure(w.part, (size_t)part_keys * sizeof(unsigned long long)));
   TRY(ensure(w.merged, (size_t)B * kp_max * sizeof(unsigned long long)));
   TRY(ensure(w.exact, (size_t)B * kp_max * 16));
   CU(cudaMemsetAsync(w.part.p, 0xff, (size_t)part_keys * sizeof(unsigned long long), st));
   size_t cbytes = (size_t)v->nlist * kNumCls * sizeof(int);
-  TRY(ensure(v->counts, cbytes));
-  TRY(ensure(v->fill, cbytes));
-  TRY(ensure(v->mbase, cbytes));
-  TRY(ensure(v->items, (size_t)members * sizeof(WorkItem)));
-  TRY(ensure(v->members, (size_t)members * sizeof(Member)));
-  TRY(ensure(v->counters, 64 * sizeof(int)));
-  int* ctr = v->counters.as<int>();
+  TRY(ensure(w.counts, cbytes));
+  TRY(ensure(w.fill, cbytes));
+  TRY(ensure(w.mbase, cbytes));
+  TRY(ensure(w.items, (size_t)members * sizeof(WorkItem)));
+  TRY(ensure(w.members, (size_t)members * sizeof(Member)));
+  TRY(ensure(w.counters, 64 * sizeof(int)));
+  int* ctr = w.counters.as<int>();
   CU(cudaMemsetAsync(ctr, 0, 4 * sizeof(int), st));
 
   TRY(mark(1));
   // 3. device packer
   PackLaunch pk;
-  pk.probes = v->probes.as<long long>();
+  pk.probes = w.probes.as<long long>();
   pk.ld_probes = npmax;
   pk.nprobe = dnp;
   pk.meta = dmeta;
@@ -1094,30 +1244,34 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   pk.list_off = v->list_off;
   pk.list_by_size = v->list_by_size;
   pk.nlist = v->nlist;
-  pk.counts = v->counts.as<int>();
-  pk.fill = v->fill.as<int>();
-  pk.member_base = v->mbase.as<int>();
-  pk.items = v->items.as<WorkItem>();
+  pk.counts = w.counts.as<int>();
+  pk.fill = w.fill.as<int>();
+  pk.member_base = w.mbase.as<int>();
+  pk.items = w.items.as<WorkItem>();
   pk.n_items = ctr;
-  pk.members = v->members.as<Member>();
+  pk.members = w.members.as<Member>();
   pk.gmax = gmax;
   pk.cls_mask = cls_mask;
   CU(launch_pack(pk, st));
 
   // 4. list scan (persistent, one CTA per SM)
-  ScanLaunch sl;
+  ScanLaunch sl{};
   sl.tmap = &v->tmap;
-  sl.tmap_tc = &v->tmap_tc;
+  sl.tmap_tc = f16 ? &v->tmap_h : &v->tmap_tc;
+  sl.f16 = f16 ? 1 : 0;
+  sl.Qh = f16 ? w.Qh.p : nullptr;
+  sl.qldh = v->dph;
+  sl.qinv = f16 ? w.qinv.as<float>() : nullptr;
   sl.X = v->Xl;
   sl.ldx = v->dp;
   sl.xnorm = v->xnl;
   sl.Q = w.Q32.as<float>();
   sl.qld = v->qld;
   sl.qnorm = w.qn32.as<float>();
-  sl.items = v->items.as<WorkItem>();
+  sl.items = w.items.as<WorkItem>();
   sl.n_items = ctr;
   sl.counter = ctr + 1;
-  sl.members = v->members.as<Member>();
+  sl.members = w.members.as<Member>();
   sl.part = w.part.as<unsigned long long>();
   sl.dp = v->dp;
   sl.gmax = gmax;
@@ -1134,7 +1288,7 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   int* n_flag = w.flags.as<int>();
   int* flag_list = n_flag + 64;
   CU(cudaMemsetAsync(n_flag, 0, sizeof(int), st));
-  RerankLaunch rr;
+  RerankLaunch rr{};
   rr.merged = w.merged.as<unsigned long long>();
   rr.exact = reinterpret_cast<Exact*>(w.exact.p);
   rr.ld_merged = kp_max;
@@ -1147,7 +1301,8 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   rr.idmap = v->ids;
   rr.id_offset = 0;
   rr.xmax = v->xmax;
-  const Bound bd = bound_for(v->d, ch.tc);
+  const Bound bd = bound_for(v->d, f16 ? kF16 : ch.tc ? kTf32 : kSimt);
+  rr.qinv = f16 ? w.qinv.as<float>() : nullptr;
   rr.cdot = g_force_fixup ? 1e30 : bd.cdot;
   rr.csum = bd.csum;
   rr.out_ids = reinterpret_cast<long long*>(ids);
@@ -1168,7 +1323,7 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   fx.X = v->Xl;
   fx.ldx = v->dp;
   fx.n_rows = v->n;
-  fx.probes = v->probes.as<long long>();
+  fx.probes = w.probes.as<long long>();
   fx.ld_probes = npmax;
   fx.nprobe = dnp;
   fx.list_off = v->list_off;
@@ -1182,10 +1337,19 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   CU(launch_fixup(fx, st));
   TRY(mark(6));
   if (rec) v->ev_used++;
-  v->last_B = B;
-  v->last_npmax = npmax;
-  v->last_np.assign(nprobe, nprobe + B);
-  return TRI_OK;
+  w.last_B = B;
+  w.last_npmax = npmax;
+  w.last_f16 = f16 ? 1 : 0;
+  w.last_np.assign(nprobe, nprobe + B);
+  TRY(lane_done(*cw, st));
+  return lane_done(w, st);
+}
+
+int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe,
+                       int32_t ldo, int64_t* ids, double* dists, void* stream) {
+  if (!v) return fail(TRI_EINVAL, "index is NULL");
+  std::lock_guard<std::mutex> lk(v->mu);
+  return ivf_search_enqueue(v, q, B, k, nprobe, ldo, ids, dists, stream);
 }
 
 int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe, int32_t ldo,
@@ -1196,33 +1360,39 @@ int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, con
   TRY(check_queries(q, (long long)B * v->d));
   DeviceGuard g(v->device);
   cudaStream_t st = pick(stream, v->own);
-  Workspace& w = v->ws;
-  int km = 0;
-  for (int i = 0; i < B; ++i) km = std::max(km, k[i]);
-  if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
-  TRY(ensure(w.q64, (size_t)B * v->d * sizeof(double)));
-  TRY(ensure(w.out_ids, (size_t)B * ldo * sizeof(long long)));
-  TRY(ensure(w.out_d, (size_t)B * ldo * sizeof(double)));
-  CU(cudaMemcpyAsync(w.q64.p, q, (size_t)B * v->d * sizeof(double), cudaMemcpyHostToDevice, st));
-  TRY(tri_ivf_search_dev(v, w.q64.as<double>(), B, k, nprobe, ldo, reinterpret_cast<int64_t*>(w.out_ids.p),
-                         w.out_d.as<double>(), st));
-  CU(cudaMemcpyAsync(ids, w.out_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
-  CU(cudaMemcpyAsync(dists, w.out_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+  {
+    std::lock_guard<std::mutex> lk(v->mu);
+    Workspace* wp = nullptr;
+    TRY(v->lanes.get(st, &wp));
+    Workspace& w = *wp;
+    int km = 0;
+    for (int i = 0; i < B; ++i) km = std::max(km, k[i]);
+    if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
+    TRY(ensure(w.q64, (size_t)B * v->d * sizeof(double)));
+    TRY(ensure(w.out_ids, (size_t)B * ldo * sizeof(long long)));
+    TRY(ensure(w.out_d, (size_t)B * ldo * sizeof(double)));
+    CU(cudaMemcpyAsync(w.q64.p, q, (size_t)B * v->d * sizeof(double), cudaMemcpyHostToDevice, st));
+    TRY(ivf_search_enqueue(v, w.q64.as<double>(), B, k, nprobe, ldo, reinterpret_cast<int64_t*>(w.out_ids.p),
+                           w.out_d.as<double>(), st));
+    CU(cudaMemcpyAsync(ids, w.out_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(dists, w.out_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
   CU(cudaStreamSynchronize(st));
   return TRI_OK;
 }
 
 int tri_ivf_last_probes(tri_ivf* v, int64_t* probes, int32_t ld) {
   if (!v || !probes) return fail(TRI_EINVAL, "NULL argument");
-  if (ld < v->last_npmax) return fail(TRI_EINVAL, "ld=%d < nprobe max %d", ld, v->last_npmax);
+  const Workspace& w = v->lanes.recent();
+  if (ld < w.last_npmax) return fail(TRI_EINVAL, "ld=%d < nprobe max %d", ld, w.last_npmax);
   DeviceGuard g(v->device);
   CU(cudaDeviceSynchronize());
-  std::vector<long long> h((size_t)v->last_B * v->last_npmax);
+  std::vector<long long> h((size_t)w.last_B * w.last_npmax);
   if (!h.empty())
-    CU(cudaMemcpy(h.data(), v->probes.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
-  for (int i = 0; i < v->last_B; ++i)
+    CU(cudaMemcpy(h.data(), w.probes.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < w.last_B; ++i)
     for (int j = 0; j < ld; ++j)
-      probes[(long long)i * ld + j] = j < v->last_np[i] ? h[(size_t)i * v->last_npmax + j] : -1;
+      probes[(long long)i * ld + j] = j < w.last_np[i] ? h[(size_t)i * w.last_npmax + j] : -1;
   return TRI_OK;
 }
 
@@ -1231,8 +1401,12 @@ int tri_ivf_last_fixups(tri_ivf* v, int32_t* n) {
   DeviceGuard g(v->device);
   CU(cudaDeviceSynchronize());
   int a = 0, b = 0;
-  if (v->ws.flags.p) CU(cudaMemcpy(&a, v->ws.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
-  if (v->cstore && v->cstore->ws.flags.p) CU(cudaMemcpy(&b, v->cstore->ws.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
+  const Workspace& w = v->lanes.recent();
+  if (w.flags.p) CU(cudaMemcpy(&a, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (v->cstore) {
+    const Workspace& c = v->cstore->lanes.recent();
+    if (c.flags.p) CU(cudaMemcpy(&b, c.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
+  }
   *n = a + b;
   return TRI_OK;
 }
@@ -1279,20 +1453,21 @@ int tri_ivf_stage_times(tri_ivf* v, double* ms, int32_t* searches) {
 
 int tri_ivf_last_scan_bytes(tri_ivf* v, int64_t* bytes, int64_t* pairs) {
   if (!v) return fail(TRI_EINVAL, "index is NULL");
-  std::vector<int64_t> pr((size_t)v->last_B * std::max(1, v->last_npmax));
-  TRY(tri_ivf_last_probes(v, pr.data(), std::max(1, v->last_npmax)));
+  const Workspace& w = v->lanes.recent();
+  std::vector<int64_t> pr((size_t)w.last_B * std::max(1, w.last_npmax));
+  TRY(tri_ivf_last_probes(v, pr.data(), std::max(1, w.last_npmax)));
   std::vector<char> hit(v->nlist, 0);
   long long pp = 0;
-  for (int i = 0; i < v->last_B; ++i)
-    for (int j = 0; j < v->last_np[i]; ++j) {
-      long long l = pr[(size_t)i * v->last_npmax + j];
+  for (int i = 0; i < w.last_B; ++i)
+    for (int j = 0; j < w.last_np[i]; ++j) {
+      long long l = pr[(size_t)i * w.last_npmax + j];
       hit[l] = 1;
       pp += v->h_off[l + 1] - v->h_off[l];
     }
   long long vec = 0;
   for (int l = 0; l < v->nlist; ++l)
     if (hit[l]) vec += v->h_off[l + 1] - v->h_off[l];
-  if (bytes) *bytes = vec * ((long long)v->d * 4 + 4);
+  if (bytes) *bytes = vec * ((long long)v->d * (w.last_f16 ? 2 : 4) + 4);  // row (fp16 / fp32) + its norm
   if (pairs) *pairs = pp;
   return TRI_OK;
 }

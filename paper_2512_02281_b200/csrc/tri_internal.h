@@ -59,6 +59,12 @@ struct ScanLaunch {
   int cap;      // selection buffer per query (>= 2 * max kp, power of two)
   int grid;
   int dbg;      // experiment switches (0 in production): 1 skip selection, 2 skip MMA
+  // fp16 tensor-core scan (f16 != 0): tmap_tc maps the fp16 copy of X, queries
+  // come from Qh (row stride qldh halves) and dots are scaled by qinv[query].
+  int f16;
+  const void* Qh;
+  int qldh;
+  const float* qinv;
 };
 
 size_t scan_smem_bytes(int gmax, int qld, int cap);
@@ -69,11 +75,16 @@ cudaError_t launch_scan(const ScanLaunch& s, cudaStream_t st);
 constexpr int kTcMaxQld = 1024;
 constexpr int kTcGroup = 16;
 constexpr int kTcMaxKp = 256;  // register-resident top-kp lists in the epilogue
-size_t tc_scan_smem_bytes(int qld);
+size_t tc_scan_smem_bytes(int row_bytes);  // row_bytes: query row width in bytes (qld*4 or qldh*2)
 cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st);
 
 cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,
                         int* bad, cudaStream_t st);
+cudaError_t launch_absmax(const float* X, long long n, int d, long long ldx, unsigned int* bits, cudaStream_t st);
+cudaError_t launch_to_half(const float* X, long long n, int d, long long ldx, float sx, void* Xh, int ldh,
+                           cudaStream_t st);
+cudaError_t launch_prep_half(const float* Q32, int B, int qld, int d, float sx, void* Qh, int ldh, float* qinv,
+                             cudaStream_t st);
 cudaError_t launch_norms(const float* X, long long n, int d, long long ldx, float* xnorm,
                          unsigned long long* xmax_bits, cudaStream_t st);
 
@@ -113,6 +124,7 @@ struct RerankLaunch {
   int* flag_list;
   int B;
   int kp_max;
+  const float* qinv;        // fp16 scan: qinv[q] < 0 marks a query the scan could not scale (never certified)
 };
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st);
 

@@ -9,6 +9,8 @@
 // Certification: every dropped candidate has approx distance >= T (the kp-th
 // kept one) and |approx - exact| <= E = cdot*2|q|max|x| + csum*(|q|+max|x|)^2, so if the k-th
 // exact distance + E < T no dropped vector can enter the exact top-k.
+#include <cuda_fp16.h>
+
 #include <algorithm>
 
 #include "tri_common.cuh"
@@ -87,6 +89,97 @@ cudaError_t launch_norms(const float* X, long long n, int d, long long ldx, floa
   long long blocks = (n + 7) / 8;
   norms_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, n, d, ldx, xnorm, xmax_bits);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// fp16 candidate-generation copies.  Both sides are
+// scaled by powers of two so the largest magnitude lands in [2^14, 2^15):
+// scaling is exact, fp16 cannot overflow, and the subnormal floor is 2^-38 of
+// the largest element.  The scan multiplies the accumulator by
+// qinv = 1 / (s_q * s_x), also exact.
+
+__global__ void absmax_kernel(const float* __restrict__ X, long long n, int d, long long ldx,
+                              unsigned int* __restrict__ bits) {
+  float m = 0.f;
+  const long long total = n * (long long)d;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / d;
+    m = fmaxf(m, fabsf(X[r * ldx + (i - r * d)]));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(bits, __float_as_uint(m));  // m >= 0: bit order = value order
+}
+
+cudaError_t launch_absmax(const float* X, long long n, int d, long long ldx, unsigned int* bits, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  absmax_kernel<<<4 * 148, 256, 0, st>>>(X, n, d, ldx, bits);
+  return cudaGetLastError();
+}
+
+// Xh[r, j] = fp16(X[r, j] * sx) for j < d, 0 for d <= j < ldh.
+__global__ void to_half_kernel(const float* __restrict__ X, long long n, int d, long long ldx, float sx,
+                               __half* __restrict__ Xh, int ldh) {
+  const long long total = n * (long long)ldh;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / ldh;
+    const int j = (int)(i - r * ldh);
+    Xh[i] = __float2half_rn(j < d ? X[r * ldx + j] * sx : 0.f);
+  }
+}
+
+cudaError_t launch_to_half(const float* X, long long n, int d, long long ldx, float sx, void* Xh, int ldh,
+                           cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  to_half_kernel<<<8 * 148, 256, 0, st>>>(X, n, d, ldx, sx, static_cast<__half*>(Xh), ldh);
+  return cudaGetLastError();
+}
+
+// Per query: s_q = 2^(14 - ilogb(max|Q32|)), Qh = fp16(Q32 * s_q) (zero padded
+// to ldh), qinv = 1 / (s_q * sx).  Queries whose largest element is outside
+// [2^-60, 2^60] get qinv = -1 and a zero row: the re-rank never certifies
+// them, so the exact fix-up answers them.  All-zero queries are exact (s_q = 1).
+__global__ void prep_half_kernel(const float* __restrict__ Q32, int qld, int d, float sx, __half* __restrict__ Qh,
+                                 int ldh, float* __restrict__ qinv) {
+  const int q = blockIdx.x;
+  const float* row = Q32 + (long long)q * qld;
+  float m = 0.f;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) m = fmaxf(m, fabsf(row[j]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+  bool bad = false;
+  float sq = 1.f;
+  if (m > 0.f) {
+    const int e = ilogbf(m);
+    bad = e < -60 || e > 60;
+    sq = bad ? 0.f : ldexpf(1.f, 14 - e);
+  }
+  for (int j = threadIdx.x; j < ldh; j += blockDim.x)
+    Qh[(long long)q * ldh + j] = __float2half_rn(j < d ? row[j] * sq : 0.f);
+  if (threadIdx.x == 0) qinv[q] = bad ? -1.f : 1.f / (sq * sx);
+}
+
+cudaError_t launch_prep_half(const float* Q32, int B, int qld, int d, float sx, void* Qh, int ldh, float* qinv,
+                             cudaStream_t st) {
+  if (B <= 0) return cudaSuccess;
+  prep_half_kernel<<<B, 128, 0, st>>>(Q32, qld, d, sx, static_cast<__half*>(Qh), ldh, qinv);
+  return cudaGetLastError();
+}
+
+// Certification test (k-th exact distance dk, kp-th kept approx distance T).
+// A non-finite T (overflowed approx distances) or an unscalable fp16 query
+// is never certified.
+__device__ __forceinline__ bool certified(const RerankLaunch& r, int q, double dk, double T) {
+  if (!(T < INFINITY)) return false;
+  if (r.qinv && r.qinv[q] < 0.f) return false;
+  const double s = r.qn64[q] + r.xmax;
+  const double E = (r.cdot * 2.0 * r.qn64[q] * r.xmax + r.csum * s * s) * 1.001 + 1e-30;
+  return dk + E < T;
 }
 
 // ---------------------------------------------------------------------------
@@ -397,10 +490,7 @@ __device__ __forceinline__ void finalize_query(const RerankLaunch& r, int q, int
       const double t = __shfl_sync(0xffffffffu, d[j], kk & 31);
       if (j == (kk >> 5)) dk = t;
     }
-    const double T = (double)key_dist(r.merged[(long long)q * r.ld_merged + m.kp - 1]);
-    const double s = r.qn64[q] + r.xmax;
-    const double E = (r.cdot * 2.0 * r.qn64[q] * r.xmax + r.csum * s * s) * 1.001 + 1e-30;
-    cert = dk + E < T;
+    cert = certified(r, q, dk, (double)key_dist(r.merged[(long long)q * r.ld_merged + m.kp - 1]));
   }
   if (!cert && lane == 0) r.flag_list[atomicAdd(r.n_flag, 1)] = q;
 #pragma unroll
@@ -437,10 +527,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(RerankLaunch r) {
   if (threadIdx.x == 0) {
     bool cert = true;
     if (m.n_total > kp) {
-      const double T = (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]);
-      const double s = r.qn64[q] + r.xmax;
-      const double E = (r.cdot * 2.0 * r.qn64[q] * r.xmax + r.csum * s * s) * 1.001 + 1e-30;
-      cert = ebuf[m.k - 1].d + E < T;
+      cert = certified(r, q, ebuf[m.k - 1].d, (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]));
     }
     if (!cert) r.flag_list[atomicAdd(r.n_flag, 1)] = q;
   }
@@ -617,10 +704,7 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
   if (tid == 0) {
     bool cert = true;
     if (m.n_total > kp) {
-      const double T = (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]);
-      const double sq = r.qn64[q] + r.xmax;
-      const double E = (r.cdot * 2.0 * r.qn64[q] * r.xmax + r.csum * sq * sq) * 1.001 + 1e-30;
-      cert = s_dk + E < T;
+      cert = certified(r, q, s_dk, (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]));
     }
     if (!cert) r.flag_list[atomicAdd(r.n_flag, 1)] = q;
   }

@@ -1,22 +1,24 @@
-// Tensor-core list scan (sm_100a): tcgen05.mma kind::tf32, TMEM accumulators,
+// Tensor-core list scan (sm_100a): tcgen05.mma kind::f16 (fp16 copy of the
+// lists) or kind::tf32 (fp32 lists), TMEM accumulators,
 // TMA-fed shared-memory ring.  Same work items / partial-list contract as the
 // SIMT scan in tri_listscan.cu, which remains the path for qld > kTcMaxQld.
 //
 // Roles (one persistent CTA per SM, 192 threads):
 //   warp 0  producer : claims work items, publishes descriptors, streams each
-//                      item's rows with 2-D TMA (32-row x 32-float boxes,
+//                      item's rows with 2-D TMA (32-row x 128-byte boxes,
 //                      128B swizzle = the UMMA K-major SW128 canonical layout)
-//                      into a kStages-deep ring of 128-row x 32-float slabs.
+//                      into a kStages-deep ring of 128-row x 128-byte slabs
+//                      (64 halves or 32 floats of every row).
 //   warp 1  MMA      : allocates 64 TMEM columns (a ring of four 128x16
 //                      fp32 accumulators); one elected lane issues 4 MMAs
-//                      (M=128 rows, N=16 queries, K=8) per slab,
+//                      (M=128 rows, N=16 queries, K=16 f16 / K=8 tf32) per slab,
 //                      tcgen05.commit frees the slab / publishes a chunk.
 //   warps 2-5 epilogue: stage the group's queries into smem in the same SW128
 //                      K-major layout, then per 128-row chunk: tcgen05.ld their
 //                      TMEM lane quadrant (thread = row), form the fp32
 //                      dot-form distance qn + xn - 2 q.x and run the
 //                      threshold-filtered per-query top-kp selection.
-// Distances are approximate (TF32 inputs); the certified fp64 re-rank
+// Distances are approximate (fp16 / TF32 inputs); the certified fp64 re-rank
 // (tri_select.cu) makes the final result exact.
 #include <cuda.h>
 
@@ -28,14 +30,20 @@ namespace tri {
 constexpr int kTcThreads = 192;
 constexpr int kTcRows = 128;                    // MMA M = rows per chunk
 constexpr int kTcN = 16;                        // MMA N = queries per group
-constexpr int kTcSlabF = 32;                    // floats per row per slab (128 B)
-constexpr int kTcSlabBytes = kTcRows * kTcSlabF * 4;  // 16 KB
+constexpr int kTcRowB = 128;                    // bytes per row per slab (one SW128 row)
+constexpr int kTcSlabBytes = kTcRows * kTcRowB;  // 16 KB
 constexpr int kTcBoxRows = 32;
 constexpr int kTcStages = 9;
 constexpr int kTcAcc = 4;                       // TMEM accumulator ring (x16 columns)
-constexpr int kTcQTile = kTcN * kTcSlabF * 4;   // 2 KB of queries per slab
-constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
-                              ((uint32_t)(kTcRows >> 4) << 24);  // F32 accum, TF32 A/B, K-major, N=16, M=128
+constexpr int kTcQTile = kTcN * kTcRowB;        // 2 KB of queries per slab
+// Instruction descriptors: F32 accumulator, K-major A/B, N=16, M=128; A/B
+// format TF32 (2) for kind::tf32, F16 (0) for kind::f16.
+constexpr uint32_t kTcIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
+                                  ((uint32_t)(kTcRows >> 4) << 24);
+constexpr uint32_t kTcIdescF16 = (1u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+template <bool H>
+__host__ __device__ constexpr int slab_elems() { return H ? 64 : 32; }
+__host__ __device__ inline int tc_nslab(int row_bytes) { return (row_bytes + kTcRowB - 1) / kTcRowB; }
 
 __device__ __forceinline__ uint32_t tsu32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -71,11 +79,19 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
-__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "r"(accumulate));
+template <bool H>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  if (H) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(kTcIdescF16), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(kTcIdescTf32), "r"(accumulate));
+  }
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(tsu32(bar))
@@ -93,18 +109,23 @@ struct TcSmem {
   int cnt[kTcN];
   unsigned long long thr[kTcN];
   float qn[kTcN];
+  float qinv[kTcN];
 };
 
-size_t tc_scan_smem_bytes(int qld) {
-  const int nslab = (qld + kTcSlabF - 1) / kTcSlabF;
-  return 1024 + (size_t)kTcStages * kTcSlabBytes + (size_t)nslab * kTcQTile + (size_t)kTcN * kTcRows * 8;
+size_t tc_scan_smem_bytes(int row_bytes) {
+  return 1024 + (size_t)kTcStages * kTcSlabBytes + (size_t)tc_nslab(row_bytes) * kTcQTile +
+         (size_t)kTcN * kTcRows * 8;
 }
+
+template <bool H>
+__device__ __forceinline__ int row_bytes_of(const ScanLaunch& a) { return H ? a.qldh * 2 : a.qld * 4; }
 
 // ---------------------------------------------------------------------------
 
+template <bool H>
 __device__ void tc_producer(const ScanLaunch& a, const CUtensorMap* map, TcSmem& sh, unsigned char* ring) {
   const int n_items = *a.n_items;
-  const int nslab = (a.qld + kTcSlabF - 1) / kTcSlabF;
+  const int nslab = tc_nslab(row_bytes_of<H>(a));
   int wslot = 0, wphase = 0, stage = 0, sphase = 0;
   for (;;) {
     const int it = atomicAdd(a.counter, 1);
@@ -130,9 +151,9 @@ __device__ void tc_producer(const ScanLaunch& a, const CUtensorMap* map, TcSmem&
       for (int s = 0; s < nslab; ++s) {
         tmb_wait(&sh.empty[stage], sphase ^ 1);
         unsigned char* dst = ring + (size_t)stage * kTcSlabBytes;
-        tmb_expect(&sh.full[stage], (uint32_t)nbox * kTcBoxRows * kTcSlabF * 4u);
+        tmb_expect(&sh.full[stage], (uint32_t)nbox * kTcBoxRows * kTcRowB);
         for (int b = 0; b < nbox; ++b)
-          ttma_2d(dst + b * kTcBoxRows * kTcSlabF * 4, map, s * kTcSlabF, row0 + b * kTcBoxRows, &sh.full[stage]);
+          ttma_2d(dst + b * kTcBoxRows * kTcRowB, map, s * slab_elems<H>(), row0 + b * kTcBoxRows, &sh.full[stage]);
         if (++stage == kTcStages) {
           stage = 0;
           sphase ^= 1;
@@ -142,9 +163,10 @@ __device__ void tc_producer(const ScanLaunch& a, const CUtensorMap* map, TcSmem&
   }
 }
 
+template <bool H>
 __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, unsigned char* qs) {
   const int lane = threadIdx.x & 31;
-  const int nslab = (a.qld + kTcSlabF - 1) / kTcSlabF;
+  const int nslab = tc_nslab(row_bytes_of<H>(a));
   int wslot = 0, wphase = 0, stage = 0, sphase = 0, qphase = 0, acc = 0, aphase = 0;
   const uint32_t tmem = sh.tmem_base;
   const uint32_t ring_s = tsu32(ring), qs_s = tsu32(qs);
@@ -174,8 +196,8 @@ __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, uns
           const uint32_t b0 = qs_s + (uint32_t)s * kTcQTile;
           if (!(a.dbg & 2)) {
 #pragma unroll
-            for (int k = 0; k < kTcSlabF / 8; ++k)
-              umma_tf32(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), (s | k) != 0);
+            for (int k = 0; k < kTcRowB / 32; ++k)  // 32 B of K per MMA (16 halves / 8 floats)
+              umma<H>(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), (s | k) != 0);
           }
           umma_commit(&sh.empty[stage]);  // slab reusable once these MMAs retire
           if (s == nslab - 1) umma_commit(&sh.tfull[acc]);
@@ -205,7 +227,7 @@ __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, uns
 // two named barriers per chunk.
 
 // One work item; returns the updated accumulator ring state (acc | aphase << 8).
-template <int KL>
+template <bool H, int KL>
 __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& w, TcSmem& sh,
                                            unsigned long long* sel, int ring) {
   int acc = ring & 0xff, aphase = ring >> 8;
@@ -250,7 +272,7 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
 #pragma unroll
       for (int g = 0; g < kTcN; ++g) {
         if (g < gc) {
-          const float dot = __uint_as_float(v[g]);
+          const float dot = H ? __uint_as_float(v[g]) * sh.qinv[g] : __uint_as_float(v[g]);
           const unsigned long long key = make_key(__fmaf_rn(-2.f, dot, __fadd_rn(sh.qn[g], xn)), pos);
           if (key < sh.thr[g]) sel[g * kTcRows + atomicAdd(&sh.cnt[g], 1)] = key;  // <= 128 per chunk
         }
@@ -291,10 +313,12 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
 }
 
 // Epilogue: 4 warps, thread e (0..127) <-> TMEM lane e <-> chunk row e.
+template <bool H>
 __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, unsigned long long* sel) {
   const int e = threadIdx.x - 64;  // 0..127
   const int lane = threadIdx.x & 31;
-  const int nslab = (a.qld + kTcSlabF - 1) / kTcSlabF;
+  const int row_bytes = row_bytes_of<H>(a);
+  const int nslab = tc_nslab(row_bytes);
   int wslot = 0, wphase = 0, ring = 0;
   for (;;) {
     tmb_wait(&sh.wfull[wslot], wphase);
@@ -310,42 +334,45 @@ __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, 
     const int gc = w.member_count;
     // Stage queries: slab s, query g, 16B chunk c -> qs + s*2KB + g*128 + ((c ^ (g&7)) << 4)
     {
-      const float4* Q4 = reinterpret_cast<const float4*>(a.Q);
-      const int q4 = a.qld >> 2;
+      const uint4* Q4 = reinterpret_cast<const uint4*>(H ? a.Qh : static_cast<const void*>(a.Q));
+      const int q4 = row_bytes >> 4;
       const int total = nslab * kTcN * 8;
       for (int i = e; i < total; i += 128) {
         const int c = i & 7, g = (i >> 3) & (kTcN - 1), s = i >> 7;
         const int col4 = s * 8 + c;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if (g < gc && col4 < q4) v = Q4[(long long)a.members[w.member_begin + g].q * q4 + col4];
-        *reinterpret_cast<float4*>(qs + s * kTcQTile + g * 128 + ((c ^ (g & 7)) << 4)) = v;
+        *reinterpret_cast<uint4*>(qs + s * kTcQTile + g * 128 + ((c ^ (g & 7)) << 4)) = v;
       }
       if (e < kTcN) {
+        const int q = e < gc ? a.members[w.member_begin + e].q : -1;
         sh.cnt[e] = 0;
         sh.thr[e] = TRI_KEY_MAX;
-        sh.qn[e] = e < gc ? a.qnorm[a.members[w.member_begin + e].q] : 0.f;
+        sh.qn[e] = q >= 0 ? a.qnorm[q] : 0.f;
+        sh.qinv[e] = (H && q >= 0) ? a.qinv[q] : 0.f;
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core reads
       epi_sync();
       if (e == 0) tmb_arrive(&sh.qfull);
     }
     switch (w.kp) {
-      case 32: ring = tc_epi_item<1>(a, w, sh, sel, ring); break;
-      case 64: ring = tc_epi_item<2>(a, w, sh, sel, ring); break;
-      case 128: ring = tc_epi_item<4>(a, w, sh, sel, ring); break;
-      default: ring = tc_epi_item<8>(a, w, sh, sel, ring); break;  // 256 (host caps tc kp at kTcMaxKp)
+      case 32: ring = tc_epi_item<H, 1>(a, w, sh, sel, ring); break;
+      case 64: ring = tc_epi_item<H, 2>(a, w, sh, sel, ring); break;
+      case 128: ring = tc_epi_item<H, 4>(a, w, sh, sel, ring); break;
+      default: ring = tc_epi_item<H, 8>(a, w, sh, sel, ring); break;  // 256 (host caps tc kp at kTcMaxKp)
     }
     epi_sync();  // qs and the append buffers are free for the next item
   }
 }
 
+template <bool H>
 __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_constant__ CUtensorMap map, ScanLaunch a) {
   extern __shared__ __align__(1024) unsigned char tsmem_raw[];
   __shared__ TcSmem sh;
   unsigned char* base = tsmem_raw + ((1024u - (tsu32(tsmem_raw) & 1023u)) & 1023u);
   unsigned char* ring = base;
   unsigned char* qs = ring + (size_t)kTcStages * kTcSlabBytes;
-  const int nslab = (a.qld + kTcSlabF - 1) / kTcSlabF;
+  const int nslab = tc_nslab(row_bytes_of<H>(a));
   unsigned long long* sel = reinterpret_cast<unsigned long long*>(qs + (size_t)nslab * kTcQTile);
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -372,11 +399,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   if (warp == 0) {
-    if ((threadIdx.x & 31) == 0) tc_producer(a, &map, sh, ring);
+    if ((threadIdx.x & 31) == 0) tc_producer<H>(a, &map, sh, ring);
   } else if (warp == 1) {
-    tc_mma(a, sh, ring, qs);
+    tc_mma<H>(a, sh, ring, qs);
   } else {
-    tc_epilogue(a, sh, qs, sel);
+    tc_epilogue<H>(a, sh, qs, sel);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -386,12 +413,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
   }
 }
 
-cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st) {
-  const size_t smem = tc_scan_smem_bytes(s.qld);
-  cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <bool H>
+cudaError_t launch_tc(const ScanLaunch& s, cudaStream_t st) {
+  const size_t smem = tc_scan_smem_bytes(H ? s.qldh * 2 : s.qld * 4);
+  cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  scan_tc_kernel<<<s.grid, kTcThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(s.tmap_tc), s);
+  scan_tc_kernel<H><<<s.grid, kTcThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(s.tmap_tc), s);
   return cudaGetLastError();
+}
+
+cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st) {
+  return s.f16 ? launch_tc<true>(s, st) : launch_tc<false>(s, st);
 }
 
 }  // namespace tri

@@ -25,6 +25,29 @@ from . import _lib
 from .ann_graph import VectorStore, _DeviceStore
 
 
+def _stream_ptr(stream):
+    """torch.cuda.Stream / raw cudaStream_t int / None (the handle's own stream)."""
+    if stream is None:
+        return None
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _check_buf(name, a, dtype: str, cols=None, rows=None) -> None:
+    """Raw-buffer APIs read memory directly: reject wrong dtype / layout loudly."""
+    dt = str(a.dtype).replace("torch.", "")
+    if dt != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {dt}")
+    if a.ndim != 2:
+        raise ValueError(f"{name} must be 2-D, got shape {tuple(a.shape)}")
+    contig = a.is_contiguous() if hasattr(a, "is_contiguous") else a.flags["C_CONTIGUOUS"]
+    if not contig:
+        raise ValueError(f"{name} must be C-contiguous")
+    if cols is not None and int(a.shape[1]) != cols:
+        raise ValueError(f"{name} has {int(a.shape[1])} columns, expected {cols}")
+    if rows is not None and int(a.shape[0]) < rows:
+        raise ValueError(f"{name} has {int(a.shape[0])} rows, expected >= {rows}")
+
+
 def init_rows(n: int, nlist: int, seed: int) -> np.ndarray:
     """Seeded k-means initial rows (same rule as the oracle's CPU k-means)."""
     rng = np.random.Generator(np.random.Philox(seed))
@@ -124,12 +147,20 @@ class IVFFlatIndex:
                                                   kmax, ids.ctypes.data, dists.ctypes.data, None))
         return ids, dists
 
-    def search_into(self, q_host, k, nprobe, ids_out, dists_out) -> None:
-        """Host-buffer search into caller-owned (ideally pinned) arrays [B, ldo]."""
+    def search_into(self, q_host, k, nprobe, ids_out, dists_out, stream=None) -> None:
+        """Host-buffer search into caller-owned (ideally pinned) arrays [B, ldo].
+
+        Blocking.  Calls on different ``stream``s use separate library
+        workspaces, so host threads driving one stream each overlap on the GPU.
+        """
         B = int(q_host.shape[0])
+        _check_buf("queries", q_host, "float64", cols=self.dim)
+        _check_buf("ids_out", ids_out, "int64", rows=B)
+        _check_buf("dists_out", dists_out, "float64", cols=int(ids_out.shape[1]), rows=B)
         ks, nps = self._ragged(B, k, nprobe)
         _lib.check(_lib.gpu().tri_ivf_search(self.handle, _lib.ptr(q_host), B, ks.ctypes.data, nps.ctypes.data,
-                                              int(ids_out.shape[1]), _lib.ptr(ids_out), _lib.ptr(dists_out), None))
+                                              int(ids_out.shape[1]), _lib.ptr(ids_out), _lib.ptr(dists_out),
+                                              _stream_ptr(stream)))
 
     def search_device(self, q_dev, k, nprobe, ids_dev, dists_dev, stream=None) -> None:
         """Asynchronous search on device buffers (torch CUDA tensors or raw pointers).
@@ -137,13 +168,13 @@ class IVFFlatIndex:
         q_dev: float64 [B, d]; ids_dev int64 / dists_dev float64 [B, ldo].
         """
         B = int(q_dev.shape[0])
+        _check_buf("queries", q_dev, "float64", cols=self.dim)
+        _check_buf("ids", ids_dev, "int64", rows=B)
+        _check_buf("dists", dists_dev, "float64", cols=int(ids_dev.shape[1]), rows=B)
         ks, nps = self._ragged(B, k, nprobe)
         ldo = int(ids_dev.shape[1])
-        st = None
-        if stream is not None:
-            st = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         _lib.check(_lib.gpu().tri_ivf_search_dev(self.handle, _lib.ptr(q_dev), B, ks.ctypes.data, nps.ctypes.data,
-                                                  ldo, _lib.ptr(ids_dev), _lib.ptr(dists_dev), st))
+                                                  ldo, _lib.ptr(ids_dev), _lib.ptr(dists_dev), _stream_ptr(stream)))
 
     # -- introspection --------------------------------------------------------
     def last_probes(self, B: int, ld: int) -> np.ndarray:

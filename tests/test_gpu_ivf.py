@@ -14,11 +14,12 @@ from paper_2512_02281_b200.workload import gen_matrix, gen_vectors_chunked
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["auto", "simt", "nodense"], autouse=True)
+@pytest.fixture(params=["auto", "simt", "tf32", "nodense"], autouse=True)
 def scan_kernel(request):
     """Run every test on each candidate-generation path: auto (dense small-store
-    brute force + tcgen05 TF32 scan), fp32 SIMT scan only, and scan-only (no dense)."""
-    _lib.set_option("scan_kernel", 1 if request.param == "simt" else 0)
+    brute force + tcgen05 fp16 list scan), fp32 SIMT scan only, the TF32
+    tensor-core scan, and scan-only (no dense)."""
+    _lib.set_option("scan_kernel", {"simt": 1, "tf32": 2}.get(request.param, 0))
     _lib.set_option("dense_off", 1 if request.param != "auto" else 0)
     yield request.param
     _lib.set_option("scan_kernel", 0)
@@ -163,3 +164,67 @@ def test_c2_scale_parity():
     for i in range(256):
         order = np.lexsort((ids[i], d[i]))
         assert np.array_equal(order, np.arange(10))
+
+
+def test_ivf_concurrent_lanes(small):
+    """Batches in flight on several streams (one library workspace per stream)
+    and host threads driving one stream each give the single-stream results."""
+    import threading
+
+    import torch
+
+    g, data, idx = small
+    g = {key: g[key] for key in g.files}  # NpzFile reads lazily and is not thread-safe
+    qs = gen_matrix(40, 32, 7).astype(np.float64)  # device / host-buffer APIs take float64 queries
+    ks, nps = g["ks"], g["nprobes"]
+    streams = [torch.cuda.Stream() for _ in range(5)]  # > the 4 lanes: forces lane recycling
+    q_dev = torch.from_numpy(qs).cuda()
+    outs = [(torch.empty((40, 100), dtype=torch.int64, device="cuda"),
+             torch.empty((40, 100), dtype=torch.float64, device="cuda")) for _ in streams]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for st, (oi, od) in zip(streams, outs):
+            idx.search_device(q_dev, ks, nps, oi, od, st)
+    torch.cuda.synchronize()
+    for oi, od in outs:
+        _check_rows(oi.cpu().numpy(), od.cpu().numpy(), g, ks)
+
+    errs = []
+
+    def worker(j):
+        try:
+            ids = np.empty((40, 100), np.int64)
+            d = np.empty((40, 100), np.float64)
+            for _ in range(4):
+                idx.search_into(qs, ks, nps, ids, d, stream=streams[j])
+                _check_rows(ids, d, g, ks)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    ths = [threading.Thread(target=worker, args=(j,)) for j in range(3)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errs, errs
+
+
+@pytest.mark.parametrize("scale", [2.0 ** 25, 2.0 ** -25, 1.0])
+def test_ivf_scaled_data_and_extreme_queries(scale):
+    """fp16 candidate copy is power-of-two scaled: large / tiny data stay exact;
+    queries the fp16 scan cannot scale (max element > 2^60), overflowing
+    approximate distances and all-zero queries are answered exactly too."""
+    base = gen_matrix(6000, 40, 61)
+    data = (base.astype(np.float64) * scale).astype(np.float32)
+    art = orc.kmeans(data, 24, 3, 6)
+    idx = IVFFlatIndex.from_artifact(VectorStore(data=data), art.centroids, art.assign)
+    qs = gen_matrix(12, 40, 62).astype(np.float64) * scale
+    qs[3] *= 2.0 ** 70
+    qs[5] = 0.0
+    qs[7] *= 2.0 ** -80
+    k, npb = 9, 5
+    ids, d = idx.search(qs, k, npb)
+    for i, q in enumerate(qs):
+        oi, od = orc.ivf_search(data, art, q, k, npb)
+        assert np.array_equal(ids[i, : oi.size], oi), i
+        assert np.array_equal(d[i, : od.size], od), i
