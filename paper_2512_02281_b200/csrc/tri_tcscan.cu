@@ -3,7 +3,7 @@
 // TMA-fed shared-memory ring.  Same work items / partial-list contract as the
 // SIMT scan in tri_listscan.cu, which remains the path for qld > kTcMaxQld.
 //
-// Roles (one persistent CTA per SM, 192 threads):
+// Roles (one persistent CTA per SM, 320 threads):
 //   warp 0  producer : claims work items, publishes descriptors, streams each
 //                      item's rows with 2-D TMA (32-row x 128-byte boxes,
 //                      128B swizzle = the UMMA K-major SW128 canonical layout)
@@ -13,7 +13,7 @@
 //                      fp32 accumulators); one elected lane issues 4 MMAs
 //                      (M=128 rows, N=16 queries, K=16 f16 / K=8 tf32) per slab,
 //                      tcgen05.commit frees the slab / publishes a chunk.
-//   warps 2-5 epilogue: stage the group's queries into smem in the same SW128
+//   warps 2-9 epilogue: stage the group's queries into smem in the same SW128
 //                      K-major layout, then per 128-row chunk: tcgen05.ld their
 //                      TMEM lane quadrant (thread = row), form the fp32
 //                      dot-form distance qn + xn - 2 q.x and run the
@@ -27,7 +27,7 @@
 
 namespace tri {
 
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 320;  // producer warp, MMA warp, 8 epilogue warps
 constexpr int kTcRows = 128;                    // MMA M = rows per chunk
 constexpr int kTcN = 16;                        // MMA N = queries per group
 constexpr int kTcRowB = 128;                    // bytes per row per slab (one SW128 row)
@@ -71,7 +71,7 @@ __device__ __forceinline__ void ttma_2d(void* dst, const CUtensorMap* map, int c
       "l"(map), "r"(c0), "r"(c1), "r"(tsu32(bar))
       : "memory");
 }
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); }
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 2, 256;\n" ::: "memory"); }
 
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -106,7 +106,7 @@ struct TcSmem {
   WorkItem witem[2];
   int wend[2];
   uint32_t tmem_base;
-  int cnt[kTcN];
+  int cnt[2][kTcN];
   unsigned long long thr[kTcN];
   float qn[kTcN];
   float qinv[kTcN];
@@ -114,7 +114,7 @@ struct TcSmem {
 
 size_t tc_scan_smem_bytes(int row_bytes) {
   return 1024 + (size_t)kTcStages * kTcSlabBytes + (size_t)tc_nslab(row_bytes) * kTcQTile +
-         (size_t)kTcN * kTcRows * 8;
+         (size_t)2 * kTcN * kTcRows * 8;  // ring + query tile + double-buffered append lists
 }
 
 template <bool H>
@@ -217,33 +217,38 @@ __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, uns
 }
 
 // ---------------------------------------------------------------------------
-// Epilogue selection: every epilogue warp owns 4 of the group's queries
-// (g = ew, ew+4, ew+8, ew+12) and keeps each one's running top-kp list sorted
-// in registers (element j*32 + lane in v[j], kp = 32*KL).  Per 128-row chunk,
-// all 128 threads append the candidates that beat the query's threshold to a
-// small per-query smem buffer; the owner warp then folds them in 32 at a time:
-// register bitonic sort of the 32 (shuffles), then the bitonic split against
-// the list's last 32 and a bitonic merge back to sorted order.  No smem sorts,
-// two named barriers per chunk.
+// Epilogue selection (8 warps).  Warp w reads TMEM lane quadrant w % 4 (=
+// chunk rows 32*(w%4) ..) and column half h = ew / 4 (queries 8h .. 8h+7).
+// Every query g of the group has one owner warp (ew = g % 8) that keeps its
+// running top-kp list sorted in registers (element j*32 + lane in v[j],
+// kp = 32*KL).  Per 128-row chunk, all 256 threads append the candidates that
+// beat the query's threshold to its smem buffer (double-buffered by chunk
+// parity); after ONE named barrier each owner folds its buffer in 32 at a
+// time: register bitonic sort (shuffles), bitonic split against the list's
+// last 32, bitonic merge.  Thresholds are published by the owner and read
+// (possibly one chunk stale, which only admits more candidates) by appenders.
+constexpr int kEpiWarps = 8;
 
-// One work item; returns the updated accumulator ring state (acc | aphase << 8).
 template <bool H, int KL>
 __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& w, TcSmem& sh,
                                            unsigned long long* sel, int ring) {
   int acc = ring & 0xff, aphase = ring >> 8;
   const int e = threadIdx.x - 64, lane = threadIdx.x & 31, ew = e >> 5;
   const int quad = (threadIdx.x >> 5) & 3;
+  const int half = ew >> 2;
   const int row_in_chunk = quad * 32 + lane;  // == TMEM lane
   const int gc = w.member_count;
   const uint32_t tmem = sh.tmem_base;
-  unsigned long long L[4][KL];
+  unsigned long long L[2][KL];
 #pragma unroll
-  for (int qi = 0; qi < 4; ++qi)
+  for (int qi = 0; qi < 2; ++qi)
 #pragma unroll
     for (int j = 0; j < KL; ++j) L[qi][j] = TRI_KEY_MAX;
   const int nchunk = (w.row_count + kTcRows - 1) / kTcRows;
   float xn_next = row_in_chunk < w.row_count ? a.xnorm[w.row_begin + row_in_chunk] : 0.f;
+  volatile unsigned long long* thr = sh.thr;
   for (int c = 0; c < nchunk; ++c) {
+    const int buf = c & 1;
     const int rows = min(kTcRows, w.row_count - c * kTcRows);
     const long long row = w.row_begin + (long long)c * kTcRows + row_in_chunk;
     const bool valid = row_in_chunk < rows;
@@ -251,13 +256,11 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
     if ((c + 1) * kTcRows + row_in_chunk < w.row_count) xn_next = a.xnorm[row + kTcRows];
     tmb_wait(&sh.tfull[acc], aphase);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    uint32_t v[kTcN];
-    const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kTcN);
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
+    uint32_t v[8];
+    const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kTcN + half * 8);
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncwarp();
@@ -269,40 +272,41 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
     if (a.dbg & 1) continue;
     if (valid) {
       const uint32_t pos = (uint32_t)row;
+      unsigned long long* sb = sel + (size_t)buf * kTcN * kTcRows;
 #pragma unroll
-      for (int g = 0; g < kTcN; ++g) {
+      for (int j = 0; j < 8; ++j) {
+        const int g = half * 8 + j;
         if (g < gc) {
-          const float dot = H ? __uint_as_float(v[g]) * sh.qinv[g] : __uint_as_float(v[g]);
+          const float dot = H ? __uint_as_float(v[j]) * sh.qinv[g] : __uint_as_float(v[j]);
           const unsigned long long key = make_key(__fmaf_rn(-2.f, dot, __fadd_rn(sh.qn[g], xn)), pos);
-          if (key < sh.thr[g]) sel[g * kTcRows + atomicAdd(&sh.cnt[g], 1)] = key;  // <= 128 per chunk
+          if (key < thr[g]) sb[g * kTcRows + atomicAdd(&sh.cnt[buf][g], 1)] = key;  // <= 128 per chunk
         }
       }
     }
     epi_sync();
 #pragma unroll
-    for (int qi = 0; qi < 4; ++qi) {
-      const int g = ew + 4 * qi;
+    for (int qi = 0; qi < 2; ++qi) {
+      const int g = ew + kEpiWarps * qi;
       if (g < gc) {
-        const int n = sh.cnt[g];
+        const int n = sh.cnt[buf][g];
+        const unsigned long long* sb = sel + (size_t)buf * kTcN * kTcRows + g * kTcRows;
         for (int b = 0; b < n; b += 32) {
-          unsigned long long x = b + lane < n ? sel[g * kTcRows + b + lane] : TRI_KEY_MAX;
+          unsigned long long x = b + lane < n ? sb[b + lane] : TRI_KEY_MAX;
           x = warp_sort32(x, lane);
           list_merge32<KL>(L[qi], x, lane);
         }
         if (n > 0) {
           const unsigned long long t = __shfl_sync(0xffffffffu, L[qi][KL - 1], 31);
-          if (lane == 0) {
-            sh.cnt[g] = 0;
-            sh.thr[g] = t;
-          }
+          if (lane == 0) thr[g] = t;
         }
+        __syncwarp();
+        if (lane == 0) sh.cnt[buf][g] = 0;
       }
     }
-    epi_sync();
   }
 #pragma unroll
-  for (int qi = 0; qi < 4; ++qi) {
-    const int g = ew + 4 * qi;
+  for (int qi = 0; qi < 2; ++qi) {
+    const int g = ew + kEpiWarps * qi;
     if (g < gc) {
       unsigned long long* out = a.part + a.members[w.member_begin + g].slot;
 #pragma unroll
@@ -312,10 +316,10 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
   return acc | (aphase << 8);
 }
 
-// Epilogue: 4 warps, thread e (0..127) <-> TMEM lane e <-> chunk row e.
+// Epilogue: 8 warps (256 threads); see tc_epi_item for the TMEM mapping.
 template <bool H>
 __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, unsigned long long* sel) {
-  const int e = threadIdx.x - 64;  // 0..127
+  const int e = threadIdx.x - 64;  // 0..255
   const int lane = threadIdx.x & 31;
   const int row_bytes = row_bytes_of<H>(a);
   const int nslab = tc_nslab(row_bytes);
@@ -337,7 +341,7 @@ __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, 
       const uint4* Q4 = reinterpret_cast<const uint4*>(H ? a.Qh : static_cast<const void*>(a.Q));
       const int q4 = row_bytes >> 4;
       const int total = nslab * kTcN * 8;
-      for (int i = e; i < total; i += 128) {
+      for (int i = e; i < total; i += 32 * kEpiWarps) {
         const int c = i & 7, g = (i >> 3) & (kTcN - 1), s = i >> 7;
         const int col4 = s * 8 + c;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
@@ -346,7 +350,8 @@ __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, 
       }
       if (e < kTcN) {
         const int q = e < gc ? a.members[w.member_begin + e].q : -1;
-        sh.cnt[e] = 0;
+        sh.cnt[0][e] = 0;
+        sh.cnt[1][e] = 0;
         sh.thr[e] = TRI_KEY_MAX;
         sh.qn[e] = q >= 0 ? a.qnorm[q] : 0.f;
         sh.qinv[e] = (H && q >= 0) ? a.qinv[q] : 0.f;
@@ -361,7 +366,7 @@ __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, 
       case 128: ring = tc_epi_item<H, 4>(a, w, sh, sel, ring); break;
       default: ring = tc_epi_item<H, 8>(a, w, sh, sel, ring); break;  // 256 (host caps tc kp at kTcMaxKp)
     }
-    epi_sync();  // qs and the append buffers are free for the next item
+    epi_sync();  // qs, counters and the append buffers are free for the next item
   }
 }
 
@@ -382,11 +387,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
     }
     for (int s = 0; s < 2; ++s) {
       tmb_init(&sh.wfull[s], 1);
-      tmb_init(&sh.wempty[s], 5);  // MMA warp + 4 epilogue warps
+      tmb_init(&sh.wempty[s], 9);  // MMA warp + 8 epilogue warps
     }
     for (int s = 0; s < kTcAcc; ++s) {
       tmb_init(&sh.tfull[s], 1);
-      tmb_init(&sh.tempty[s], 4);
+      tmb_init(&sh.tempty[s], 8);
     }
     tmb_init(&sh.qfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
