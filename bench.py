@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=24, help="queries timed for cpu_baseline")
+    ap.add_argument("--tc-stages", type=int, default=0, help="tensor-core scan ring depth cap (0 = deepest)")
+    ap.add_argument("--scan-reserve", type=int, default=0, help="SMs the list scan leaves to other lanes")
     ap.add_argument("--lanes", type=int, default=2,
                     help="independent batches in flight (one CUDA stream + library workspace each)")
     return ap.parse_args()
@@ -225,6 +227,10 @@ def run_ours(args):
     from paper_2512_02281_b200.ivf import IVFFlatIndex, init_rows, merge_topk_device
 
     _build.build()
+    from paper_2512_02281_b200 import _lib
+
+    _lib.set_option("tc_stages", args.tc_stages)
+    _lib.set_option("scan_reserve", args.scan_reserve)
     data, queries = make_inputs()
 
     # index: rank 0 trains on the full database, the artifact is broadcast

@@ -53,7 +53,9 @@ int tri_device_count(int32_t* count);
  * "kp_extra" (extra over-fetch added to k), "scan_kernel" (0 auto: IVF
  * lists on the fp16 tensor-core scan, stores on TF32 when it fits; 1 fp32
  * SIMT scan; 2 TF32 tensor-core scan, no fp16), "dense_off" (1 = no dense
- * small-store path), "scan_debug" (timing experiments only: results are
+ * small-store path), "tc_stages" (cap on the tensor-core scan ring depth,
+ * 0 = deepest that fits), "scan_reserve" (SMs the IVF list scan leaves free
+ * for batches on other streams), "scan_debug" (timing experiments only: results are
  * invalid while set). */
 int tri_set_option(const char* name, int64_t value);
 

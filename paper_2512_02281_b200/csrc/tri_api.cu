@@ -95,6 +95,9 @@ int ensure_host(HostBuf& b, size_t bytes) {
   return TRI_OK;
 }
 
+long long g_box_rows = 128;     // rows per TMA box of the tensor-core scan maps (fixed at index creation)
+long long g_scan_reserve = 0;  // SMs the IVF list scan leaves to other streams
+long long g_tc_stages = 0;   // tensor-core scan ring depth cap (0 = as deep as shared memory allows)
 long long g_scan_kernel = 0;  // 0 auto (IVF: fp16 tensor core), 1 fp32 SIMT, 2 TF32 tensor core
 long long g_scan_debug = 0;   // timing experiments only (results invalid when set)
 long long g_dense_off = 0;    // 1: never use the dense small-store brute force
@@ -161,7 +164,7 @@ int sel_cap(int kp_max) { return std::max(kSelCapMin, 2 * kp_max); }
 // 2-D TMA descriptors over a row-major fp32 matrix (rows x ldx floats):
 //   SIMT scan : 64-row x 16-float boxes, 64-byte swizzle
 //   TC scan   : 32-row x 32-float boxes, 128-byte swizzle (UMMA K-major SW128)
-int make_tmap(CUtensorMap* map, const void* X, long long rows, int ldx, bool tc, bool f16 = false) {
+int make_tmap(CUtensorMap* map, const void* X, long long rows, int ldx, bool tc, bool f16 = false, int box_rows = 32) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult qr;
@@ -173,7 +176,7 @@ int make_tmap(CUtensorMap* map, const void* X, long long rows, int ldx, bool tc,
   const size_t esz = f16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)ldx, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ldx * esz};
-  cuuint32_t box[2] = {tc ? (cuuint32_t)(128 / esz) : 16u, tc ? 32u : 64u};
+  cuuint32_t box[2] = {tc ? (cuuint32_t)(128 / esz) : 16u, tc ? (cuuint32_t)box_rows : 64u};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                       const_cast<void*>(X), dims, strides, box, estr,
@@ -307,7 +310,8 @@ struct tri_store {
   float* X = nullptr;
   float* xnorm = nullptr;
   double xmax = 0.0;
-  CUtensorMap tmap, tmap_tc;
+  CUtensorMap tmap, tmap_tc, tmap_tc_tail;
+  int box_rows = 32;
   cudaStream_t own = nullptr;
   Lanes lanes;
   std::mutex mu;  // enqueue is serialised per handle; waits happen outside it
@@ -325,12 +329,13 @@ struct tri_ivf {
   int* list_by_size = nullptr;
   int* assign = nullptr;  // per original row (store order)
   double xmax = 0.0;
-  CUtensorMap tmap, tmap_tc;
+  CUtensorMap tmap, tmap_tc, tmap_tc_tail;
+  int box_rows = 32;
   // fp16 copy of the lists for candidate generation (null: TF32 / SIMT scans)
   void* Xh = nullptr;
   int dph = 0;       // row stride in halves (multiple of 64)
   float sx = 1.f;    // power-of-two scale of the fp16 copy
-  CUtensorMap tmap_h;
+  CUtensorMap tmap_h, tmap_h_tail;
   std::vector<long long> h_off;
   tri_store* cstore = nullptr;  // centroids as a vector store (coarse step)
   cudaStream_t own = nullptr;
@@ -395,7 +400,9 @@ int store_from_device(const float* Xdev, long long ldx, long long n, int d, int 
   }
   std::memcpy(&s->xmax, &bits, sizeof(double));
   int rc = make_tmap(&s->tmap, s->X, n, s->dp, false);
-  if (rc == TRI_OK) rc = make_tmap(&s->tmap_tc, s->X, n, s->dp, true);
+  if (rc == TRI_OK) rc = make_tmap(&s->tmap_tc, s->X, n, s->dp, true, false, (int)g_box_rows);
+  if (rc == TRI_OK) rc = make_tmap(&s->tmap_tc_tail, s->X, n, s->dp, true, false, 32);
+  s->box_rows = (int)g_box_rows;
   if (rc != TRI_OK) {
     tri_store_destroy(s);
     return rc;
@@ -628,6 +635,7 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   ScanLaunch sl{};
   sl.tmap = &s->tmap;
   sl.tmap_tc = &s->tmap_tc;
+  sl.tmap_tc_tail = &s->tmap_tc_tail;
   sl.X = s->X;
   sl.ldx = s->dp;
   sl.xnorm = s->xnorm;
@@ -644,6 +652,8 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   sl.cap = w.cap;
   sl.grid = w.grid;
   sl.dbg = 0;
+  sl.stages = tc_scan_stages(s->qld * 4, kSmemLimit, (int)g_tc_stages);
+  sl.box_rows = s->box_rows;
   CU(w.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
   CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
                   st));
@@ -743,6 +753,12 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "scan_kernel")) g_scan_kernel = value;
   else if (!std::strcmp(name, "scan_debug")) g_scan_debug = value;
   else if (!std::strcmp(name, "dense_off")) g_dense_off = value;
+  else if (!std::strcmp(name, "tc_stages")) g_tc_stages = value;
+  else if (!std::strcmp(name, "scan_reserve")) g_scan_reserve = value;
+  else if (!std::strcmp(name, "tc_box_rows")) {
+    if (value != 32 && value != 64 && value != 128) return fail(TRI_EINVAL, "tc_box_rows must be 32, 64 or 128");
+    g_box_rows = value;
+  }
   else return fail(TRI_EINVAL, "unknown option '%s'", name);
   return TRI_OK;
 }
@@ -928,7 +944,8 @@ static int ivf_half_copy(tri_ivf* v, cudaStream_t st) {
   v->dph = (v->d + 63) & ~63;
   CU(cudaMalloc(&v->Xh, (size_t)v->n * v->dph * 2));
   CU(launch_to_half(v->Xl, v->n, v->d, v->dp, v->sx, v->Xh, v->dph, st));
-  TRY(make_tmap(&v->tmap_h, v->Xh, v->n, v->dph, true, true));
+  TRY(make_tmap(&v->tmap_h, v->Xh, v->n, v->dph, true, true, v->box_rows));
+  TRY(make_tmap(&v->tmap_h_tail, v->Xh, v->n, v->dph, true, true, 32));
   return TRI_OK;
 }
 
@@ -939,7 +956,9 @@ static int ivf_layout(tri_ivf* v, const float* X, long long ldx, const long long
   CU(cudaMalloc(&v->ids, (size_t)n * sizeof(long long)));
   CU(launch_gather_rows(X, ldx, perm_dev, n, v->dp, v->Xl, st));
   TRY(make_tmap(&v->tmap, v->Xl, n, v->dp, false));
-  TRY(make_tmap(&v->tmap_tc, v->Xl, n, v->dp, true));
+  TRY(make_tmap(&v->tmap_tc, v->Xl, n, v->dp, true, false, (int)g_box_rows));
+  TRY(make_tmap(&v->tmap_tc_tail, v->Xl, n, v->dp, true, false, 32));
+  v->box_rows = (int)g_box_rows;
   unsigned long long* xm = nullptr;
   CU(cudaMalloc(&xm, sizeof(unsigned long long)));
   CU(cudaMemsetAsync(xm, 0, sizeof(unsigned long long), st));
@@ -1258,6 +1277,7 @@ static int ivf_search_enqueue(tri_ivf* v, const double* q, int32_t B, const int3
   ScanLaunch sl{};
   sl.tmap = &v->tmap;
   sl.tmap_tc = f16 ? &v->tmap_h : &v->tmap_tc;
+  sl.tmap_tc_tail = f16 ? &v->tmap_h_tail : &v->tmap_tc_tail;
   sl.f16 = f16 ? 1 : 0;
   sl.Qh = f16 ? w.Qh.p : nullptr;
   sl.qldh = v->dph;
@@ -1276,8 +1296,12 @@ static int ivf_search_enqueue(tri_ivf* v, const double* q, int32_t B, const int3
   sl.dp = v->dp;
   sl.gmax = gmax;
   sl.cap = cap;
-  sl.grid = (int)std::min<long long>(sm_count(v->device), members);
+  // persistent scan: one CTA per SM, minus `scan_reserve` SMs left free for
+  // batches in flight on other streams (the scan is HBM-bound, they are not)
+  sl.grid = (int)std::max<long long>(1, std::min<long long>(sm_count(v->device) - g_scan_reserve, members));
   sl.dbg = (int)g_scan_debug;
+  sl.stages = tc_scan_stages(f16 ? v->dph * 2 : v->qld * 4, kSmemLimit, (int)g_tc_stages);
+  sl.box_rows = v->box_rows;
   TRY(mark(2));
   CU(ch.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
   TRY(mark(3));

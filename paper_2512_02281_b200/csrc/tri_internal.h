@@ -42,7 +42,8 @@ constexpr int kMaxKp = 2048;
 
 struct ScanLaunch {
   const void* tmap;     // CUtensorMap over X: 64-row x 16-float boxes, 64B swizzle (SIMT scan)
-  const void* tmap_tc;  // CUtensorMap over X: 32-row x 32-float boxes, 128B swizzle (tensor-core scan)
+  const void* tmap_tc;  // CUtensorMap over X (fp32 or the fp16 copy): box_rows x 128-byte boxes, 128B swizzle
+  const void* tmap_tc_tail;  // same tensor, 32-row boxes (partial last chunk of a work item)
   const float* X;
   long long ldx;
   const float* xnorm;
@@ -62,6 +63,8 @@ struct ScanLaunch {
   // fp16 tensor-core scan (f16 != 0): tmap_tc maps the fp16 copy of X, queries
   // come from Qh (row stride qldh halves) and dots are scaled by qinv[query].
   int f16;
+  int stages;   // tensor-core scan: shared-memory ring depth (tc_scan_stages)
+  int box_rows; // tensor-core scan: rows per TMA box of tmap_tc (32, 64 or 128; full chunks)
   const void* Qh;
   int qldh;
   const float* qinv;
@@ -75,7 +78,9 @@ cudaError_t launch_scan(const ScanLaunch& s, cudaStream_t st);
 constexpr int kTcMaxQld = 1024;
 constexpr int kTcGroup = 16;
 constexpr int kTcMaxKp = 256;  // register-resident top-kp lists in the epilogue
-size_t tc_scan_smem_bytes(int row_bytes);  // row_bytes: query row width in bytes (qld*4 or qldh*2)
+constexpr int kTcMinStages = 4;
+size_t tc_scan_smem_bytes(int row_bytes);  // minimum (kTcMinStages ring); row_bytes = qld*4 or qldh*2
+int tc_scan_stages(int row_bytes, int smem_limit, int want);  // deepest ring that fits (want > 0 caps it)
 cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st);
 
 cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,

@@ -3,37 +3,41 @@
 // TMA-fed shared-memory ring.  Same work items / partial-list contract as the
 // SIMT scan in tri_listscan.cu, which remains the path for qld > kTcMaxQld.
 //
-// Roles (one persistent CTA per SM, 320 threads):
-//   warp 0  producer : claims work items, publishes descriptors, streams each
-//                      item's rows with 2-D TMA (32-row x 128-byte boxes,
-//                      128B swizzle = the UMMA K-major SW128 canonical layout)
-//                      into a kStages-deep ring of 128-row x 128-byte slabs
-//                      (64 halves or 32 floats of every row).
+// Roles (one persistent CTA per SM, 352 threads):
+//   warp 0  producer : claims work items and publishes each one ahead of
+//                      streaming it, then TMA-loads the item's rows (32-row x
+//                      128-byte boxes, 128B swizzle = the UMMA K-major SW128
+//                      canonical layout) into a ring of 128-row x 128-byte
+//                      slabs (64 halves or 32 floats of every row).
+//   warp 10 queries  : stages the next item's (<= 16) query rows into the
+//                      free one of two query tiles (same SW128 layout).
 //   warp 1  MMA      : allocates 64 TMEM columns (a ring of four 128x16
 //                      fp32 accumulators); one elected lane issues 4 MMAs
 //                      (M=128 rows, N=16 queries, K=16 f16 / K=8 tf32) per slab,
-//                      tcgen05.commit frees the slab / publishes a chunk.
-//   warps 2-9 epilogue: stage the group's queries into smem in the same SW128
-//                      K-major layout, then per 128-row chunk: tcgen05.ld their
-//                      TMEM lane quadrant (thread = row), form the fp32
+//                      tcgen05.commit frees the slab / the query tile and
+//                      publishes a chunk.
+//   warps 2-9 epilogue: per 128-row chunk, tcgen05.ld their TMEM lane quadrant
+//                      (thread = row) x column half (8 queries), form the fp32
 //                      dot-form distance qn + xn - 2 q.x and run the
 //                      threshold-filtered per-query top-kp selection.
 // Distances are approximate (fp16 / TF32 inputs); the certified fp64 re-rank
 // (tri_select.cu) makes the final result exact.
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "tri_common.cuh"
 #include "tri_internal.h"
 
 namespace tri {
 
-constexpr int kTcThreads = 320;  // producer warp, MMA warp, 8 epilogue warps
+constexpr int kTcThreads = 352;  // producer warp, MMA warp, 8 epilogue warps, query-staging warp
+constexpr int kWSlots = 4;        // work-item ring (the producer publishes one item ahead)
 constexpr int kTcRows = 128;                    // MMA M = rows per chunk
 constexpr int kTcN = 16;                        // MMA N = queries per group
 constexpr int kTcRowB = 128;                    // bytes per row per slab (one SW128 row)
 constexpr int kTcSlabBytes = kTcRows * kTcRowB;  // 16 KB
-constexpr int kTcBoxRows = 32;
-constexpr int kTcStages = 9;
+constexpr int kTcMaxStages = 12;  // ring depth: as many 16 KB slabs as shared memory allows (ScanLaunch::stages)
 constexpr int kTcAcc = 4;                       // TMEM accumulator ring (x16 columns)
 constexpr int kTcQTile = kTcN * kTcRowB;        // 2 KB of queries per slab
 // Instruction descriptors: F32 accumulator, K-major A/B, N=16, M=128; A/B
@@ -99,12 +103,12 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 }
 
 struct TcSmem {
-  uint64_t full[kTcStages], empty[kTcStages];
-  uint64_t wfull[2], wempty[2];
-  uint64_t qfull;
+  uint64_t full[kTcMaxStages], empty[kTcMaxStages];
+  uint64_t wfull[kWSlots], wempty[kWSlots];
+  uint64_t qfull[2], qempty[2];
   uint64_t tfull[kTcAcc], tempty[kTcAcc];
-  WorkItem witem[2];
-  int wend[2];
+  WorkItem witem[kWSlots];
+  int wend[kWSlots];
   uint32_t tmem_base;
   int cnt[2][kTcN];
   unsigned long long thr[kTcN];
@@ -112,77 +116,152 @@ struct TcSmem {
   float qinv[kTcN];
 };
 
-size_t tc_scan_smem_bytes(int row_bytes) {
-  return 1024 + (size_t)kTcStages * kTcSlabBytes + (size_t)tc_nslab(row_bytes) * kTcQTile +
-         (size_t)2 * kTcN * kTcRows * 8;  // ring + query tile + double-buffered append lists
+// alignment pad + two query tiles + double-buffered append lists
+static size_t tc_fixed_smem(int row_bytes) {
+  return 1024 + (size_t)2 * tc_nslab(row_bytes) * kTcQTile + (size_t)2 * kTcN * kTcRows * 8;
+}
+
+size_t tc_scan_smem_bytes(int row_bytes) { return tc_fixed_smem(row_bytes) + (size_t)kTcMinStages * kTcSlabBytes; }
+
+int tc_scan_stages(int row_bytes, int smem_limit, int want) {
+  int n = (int)(((long long)smem_limit - (long long)tc_fixed_smem(row_bytes)) / kTcSlabBytes);
+  if (want > 0) n = std::min(n, want);
+  return std::max(std::min(n, kTcMaxStages), 0);
 }
 
 template <bool H>
 __device__ __forceinline__ int row_bytes_of(const ScanLaunch& a) { return H ? a.qldh * 2 : a.qld * 4; }
 
+// Consumer side of the work-item ring (every consumer warp sees every item, in order).
+struct ItemRing {
+  int slot = 0, phase = 0;
+};
+__device__ __forceinline__ bool next_item(TcSmem& sh, ItemRing& r, WorkItem& w, int lane) {
+  tmb_wait(&sh.wfull[r.slot], r.phase);
+  const int end = sh.wend[r.slot];
+  w = sh.witem[r.slot];
+  __syncwarp();
+  if (lane == 0) tmb_arrive(&sh.wempty[r.slot]);
+  if (++r.slot == kWSlots) {
+    r.slot = 0;
+    r.phase ^= 1;
+  }
+  return !end;
+}
+
 // ---------------------------------------------------------------------------
 
+// Producer (one thread): claims work items, publishes each one ring slot
+// AHEAD of streaming it (so the query-staging warp prepares item i+1 while
+// item i streams), then TMA-loads the item's rows slab by slab.
 template <bool H>
-__device__ void tc_producer(const ScanLaunch& a, const CUtensorMap* map, TcSmem& sh, unsigned char* ring) {
+__device__ void tc_producer(const ScanLaunch& a, const CUtensorMap* map, const CUtensorMap* tail, TcSmem& sh,
+                            unsigned char* ring) {
   const int n_items = *a.n_items;
   const int nslab = tc_nslab(row_bytes_of<H>(a));
   int wslot = 0, wphase = 0, stage = 0, sphase = 0;
-  for (;;) {
-    const int it = atomicAdd(a.counter, 1);
+  auto publish = [&](int it) -> bool {
     tmb_wait(&sh.wempty[wslot], wphase ^ 1);
-    if (it >= n_items) {
-      sh.wend[wslot] = 1;
-      tmb_arrive(&sh.wfull[wslot]);
-      return;
-    }
-    const WorkItem w = a.items[it];
-    sh.witem[wslot] = w;
-    sh.wend[wslot] = 0;
+    const bool ok = it < n_items;
+    if (ok) sh.witem[wslot] = a.items[it];
+    sh.wend[wslot] = ok ? 0 : 1;
     tmb_arrive(&sh.wfull[wslot]);
-    if (++wslot == 2) {
+    if (++wslot == kWSlots) {
       wslot = 0;
       wphase ^= 1;
     }
+    return ok;
+  };
+  int cur = atomicAdd(a.counter, 1);
+  if (!publish(cur)) return;
+  for (;;) {
+    const WorkItem w = a.items[cur];
+    const int nxt = atomicAdd(a.counter, 1);
+    const bool more = publish(nxt);
     const int nchunk = (w.row_count + kTcRows - 1) / kTcRows;
     for (int c = 0; c < nchunk; ++c) {
       const int rows = min(kTcRows, w.row_count - c * kTcRows);
-      const int nbox = (rows + kTcBoxRows - 1) / kTcBoxRows;
+      // full chunks: box_rows-row boxes (few TMA ops: the per-SM TMA issue rate
+      // bounds the stream otherwise); a partial last chunk: 32-row boxes
+      // (over-reads at most 31 rows of the next list)
+      const bool full = rows == kTcRows;
+      const CUtensorMap* m = full ? map : tail;
+      const int br = full ? a.box_rows : 32;
+      const int nbox = (rows + br - 1) / br;
       const int row0 = (int)(w.row_begin + (long long)c * kTcRows);
       for (int s = 0; s < nslab; ++s) {
         tmb_wait(&sh.empty[stage], sphase ^ 1);
         unsigned char* dst = ring + (size_t)stage * kTcSlabBytes;
-        tmb_expect(&sh.full[stage], (uint32_t)nbox * kTcBoxRows * kTcRowB);
+        tmb_expect(&sh.full[stage], (uint32_t)(nbox * br * kTcRowB));
         for (int b = 0; b < nbox; ++b)
-          ttma_2d(dst + b * kTcBoxRows * kTcRowB, map, s * slab_elems<H>(), row0 + b * kTcBoxRows, &sh.full[stage]);
-        if (++stage == kTcStages) {
+          ttma_2d(dst + b * br * kTcRowB, m, s * slab_elems<H>(), row0 + b * br, &sh.full[stage]);
+        if (++stage == a.stages) {
           stage = 0;
           sphase ^= 1;
         }
       }
     }
+    if (!more) return;
+    cur = nxt;
+  }
+}
+
+// Query-staging warp: copies the next item's (up to 16) query rows into the
+// free query tile in the UMMA SW128 K-major layout -- slab s, query g, 16-byte
+// chunk c at s*2KB + g*128 + ((c ^ (g&7)) << 4) -- then hands it to the MMA warp.
+template <bool H>
+__device__ void tc_qstage(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, int qtile_bytes) {
+  const int lane = threadIdx.x & 31;
+  const int row_bytes = row_bytes_of<H>(a);
+  const int nslab = tc_nslab(row_bytes);
+  const uint4* Q4 = reinterpret_cast<const uint4*>(H ? a.Qh : static_cast<const void*>(a.Q));
+  const int q4 = row_bytes >> 4;
+  const int total = nslab * kTcN * 8;
+  ItemRing r;
+  WorkItem w;
+  for (int j = 0; next_item(sh, r, w, lane); ++j) {
+    const int qb = j & 1;
+    tmb_wait(&sh.qempty[qb], ((j >> 1) & 1) ^ 1);
+    unsigned char* dst = qs + qb * qtile_bytes;
+    const int gc = w.member_count;
+    const int myq = lane < gc ? a.members[w.member_begin + lane].q : 0;
+    for (int i0 = 0; i0 < total; i0 += 32 * 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * 32 + lane;
+        const int c = i & 7, g = (i >> 3) & (kTcN - 1), sl = i >> 7;
+        const int col4 = sl * 8 + c;
+        const int qq = __shfl_sync(0xffffffffu, myq, g);
+        v[u] = make_uint4(0u, 0u, 0u, 0u);
+        if (i < total && g < gc && col4 < q4) v[u] = Q4[(long long)qq * q4 + col4];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * 32 + lane;
+        const int c = i & 7, g = (i >> 3) & (kTcN - 1), sl = i >> 7;
+        if (i < total) *reinterpret_cast<uint4*>(dst + sl * kTcQTile + g * 128 + ((c ^ (g & 7)) << 4)) = v[u];
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core reads
+    __syncwarp();
+    if (lane == 0) tmb_arrive(&sh.qfull[qb]);
   }
 }
 
 template <bool H>
-__device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, unsigned char* qs) {
+__device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, unsigned char* qs, int qtile_bytes) {
   const int lane = threadIdx.x & 31;
   const int nslab = tc_nslab(row_bytes_of<H>(a));
-  int wslot = 0, wphase = 0, stage = 0, sphase = 0, qphase = 0, acc = 0, aphase = 0;
+  int stage = 0, sphase = 0, acc = 0, aphase = 0;
   const uint32_t tmem = sh.tmem_base;
-  const uint32_t ring_s = tsu32(ring), qs_s = tsu32(qs);
-  for (;;) {
-    tmb_wait(&sh.wfull[wslot], wphase);
-    const int end = sh.wend[wslot];
-    const WorkItem w = sh.witem[wslot];
-    __syncwarp();
-    if (lane == 0) tmb_arrive(&sh.wempty[wslot]);
-    if (++wslot == 2) {
-      wslot = 0;
-      wphase ^= 1;
-    }
-    if (end) return;
-    tmb_wait(&sh.qfull, qphase);
-    qphase ^= 1;
+  const uint32_t ring_s = tsu32(ring);
+  ItemRing r;
+  WorkItem w;
+  for (int j = 0; next_item(sh, r, w, lane); ++j) {
+    const int qb = j & 1;
+    tmb_wait(&sh.qfull[qb], (j >> 1) & 1);
+    const uint32_t qs_s = tsu32(qs + qb * qtile_bytes);
     const int nchunk = (w.row_count + kTcRows - 1) / kTcRows;
     for (int c = 0; c < nchunk; ++c) {
       tmb_wait(&sh.tempty[acc], aphase ^ 1);
@@ -200,10 +279,13 @@ __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, uns
               umma<H>(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), (s | k) != 0);
           }
           umma_commit(&sh.empty[stage]);  // slab reusable once these MMAs retire
-          if (s == nslab - 1) umma_commit(&sh.tfull[acc]);
+          if (s == nslab - 1) {
+            umma_commit(&sh.tfull[acc]);
+            if (c == nchunk - 1) umma_commit(&sh.qempty[qb]);  // query tile reusable
+          }
         }
         __syncwarp();
-        if (++stage == kTcStages) {
+        if (++stage == a.stages) {
           stage = 0;
           sphase ^= 1;
         }
@@ -318,82 +400,61 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
 
 // Epilogue: 8 warps (256 threads); see tc_epi_item for the TMEM mapping.
 template <bool H>
-__device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, unsigned long long* sel) {
+__device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned long long* sel) {
   const int e = threadIdx.x - 64;  // 0..255
   const int lane = threadIdx.x & 31;
-  const int row_bytes = row_bytes_of<H>(a);
-  const int nslab = tc_nslab(row_bytes);
-  int wslot = 0, wphase = 0, ring = 0;
-  for (;;) {
-    tmb_wait(&sh.wfull[wslot], wphase);
-    const int end = sh.wend[wslot];
-    const WorkItem w = sh.witem[wslot];
-    __syncwarp();
-    if (lane == 0) tmb_arrive(&sh.wempty[wslot]);
-    if (++wslot == 2) {
-      wslot = 0;
-      wphase ^= 1;
-    }
-    if (end) return;
+  int ring = 0;
+  ItemRing r;
+  WorkItem w;
+  while (next_item(sh, r, w, lane)) {
     const int gc = w.member_count;
-    // Stage queries: slab s, query g, 16B chunk c -> qs + s*2KB + g*128 + ((c ^ (g&7)) << 4)
-    {
-      const uint4* Q4 = reinterpret_cast<const uint4*>(H ? a.Qh : static_cast<const void*>(a.Q));
-      const int q4 = row_bytes >> 4;
-      const int total = nslab * kTcN * 8;
-      for (int i = e; i < total; i += 32 * kEpiWarps) {
-        const int c = i & 7, g = (i >> 3) & (kTcN - 1), s = i >> 7;
-        const int col4 = s * 8 + c;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (g < gc && col4 < q4) v = Q4[(long long)a.members[w.member_begin + g].q * q4 + col4];
-        *reinterpret_cast<uint4*>(qs + s * kTcQTile + g * 128 + ((c ^ (g & 7)) << 4)) = v;
-      }
-      if (e < kTcN) {
-        const int q = e < gc ? a.members[w.member_begin + e].q : -1;
-        sh.cnt[0][e] = 0;
-        sh.cnt[1][e] = 0;
-        sh.thr[e] = TRI_KEY_MAX;
-        sh.qn[e] = q >= 0 ? a.qnorm[q] : 0.f;
-        sh.qinv[e] = (H && q >= 0) ? a.qinv[q] : 0.f;
-      }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core reads
-      epi_sync();
-      if (e == 0) tmb_arrive(&sh.qfull);
+    if (e < kTcN) {
+      const int q = e < gc ? a.members[w.member_begin + e].q : -1;
+      sh.cnt[0][e] = 0;
+      sh.cnt[1][e] = 0;
+      sh.thr[e] = TRI_KEY_MAX;
+      sh.qn[e] = q >= 0 ? a.qnorm[q] : 0.f;
+      sh.qinv[e] = (H && q >= 0) ? a.qinv[q] : 0.f;
     }
+    epi_sync();
     switch (w.kp) {
       case 32: ring = tc_epi_item<H, 1>(a, w, sh, sel, ring); break;
       case 64: ring = tc_epi_item<H, 2>(a, w, sh, sel, ring); break;
       case 128: ring = tc_epi_item<H, 4>(a, w, sh, sel, ring); break;
       default: ring = tc_epi_item<H, 8>(a, w, sh, sel, ring); break;  // 256 (host caps tc kp at kTcMaxKp)
     }
-    epi_sync();  // qs, counters and the append buffers are free for the next item
+    epi_sync();  // counters and append buffers are free for the next item
   }
 }
 
 template <bool H>
-__global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_constant__ CUtensorMap map, ScanLaunch a) {
+__global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_constant__ CUtensorMap map,
+                                                                const __grid_constant__ CUtensorMap tail, ScanLaunch a) {
   extern __shared__ __align__(1024) unsigned char tsmem_raw[];
   __shared__ TcSmem sh;
   unsigned char* base = tsmem_raw + ((1024u - (tsu32(tsmem_raw) & 1023u)) & 1023u);
   unsigned char* ring = base;
-  unsigned char* qs = ring + (size_t)kTcStages * kTcSlabBytes;
-  const int nslab = tc_nslab(row_bytes_of<H>(a));
-  unsigned long long* sel = reinterpret_cast<unsigned long long*>(qs + (size_t)nslab * kTcQTile);
+  unsigned char* qs = ring + (size_t)a.stages * kTcSlabBytes;
+  const int qtile_bytes = tc_nslab(row_bytes_of<H>(a)) * kTcQTile;
+  unsigned long long* sel = reinterpret_cast<unsigned long long*>(qs + 2 * (size_t)qtile_bytes);
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTcStages; ++s) {
+    for (int s = 0; s < a.stages; ++s) {
       tmb_init(&sh.full[s], 1);
       tmb_init(&sh.empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kWSlots; ++s) {
       tmb_init(&sh.wfull[s], 1);
-      tmb_init(&sh.wempty[s], 9);  // MMA warp + 8 epilogue warps
+      tmb_init(&sh.wempty[s], 10);  // MMA warp + 8 epilogue warps + query-staging warp
+    }
+    for (int s = 0; s < 2; ++s) {
+      tmb_init(&sh.qfull[s], 1);
+      tmb_init(&sh.qempty[s], 1);
     }
     for (int s = 0; s < kTcAcc; ++s) {
       tmb_init(&sh.tfull[s], 1);
       tmb_init(&sh.tempty[s], 8);
     }
-    tmb_init(&sh.qfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -404,11 +465,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   if (warp == 0) {
-    if ((threadIdx.x & 31) == 0) tc_producer<H>(a, &map, sh, ring);
+    if ((threadIdx.x & 31) == 0) tc_producer<H>(a, &map, &tail, sh, ring);
   } else if (warp == 1) {
-    tc_mma<H>(a, sh, ring, qs);
+    tc_mma<H>(a, sh, ring, qs, qtile_bytes);
+  } else if (warp == 10) {
+    tc_qstage<H>(a, sh, qs, qtile_bytes);
   } else {
-    tc_epilogue<H>(a, sh, qs, sel);
+    tc_epilogue<H>(a, sh, sel);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -420,10 +483,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
 
 template <bool H>
 cudaError_t launch_tc(const ScanLaunch& s, cudaStream_t st) {
-  const size_t smem = tc_scan_smem_bytes(H ? s.qldh * 2 : s.qld * 4);
+  if (s.stages < kTcMinStages || s.stages > kTcMaxStages) return cudaErrorInvalidValue;
+  const size_t smem = tc_fixed_smem(H ? s.qldh * 2 : s.qld * 4) + (size_t)s.stages * kTcSlabBytes;
   cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  scan_tc_kernel<H><<<s.grid, kTcThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(s.tmap_tc), s);
+  scan_tc_kernel<H><<<s.grid, kTcThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(s.tmap_tc),
+                                                      *reinterpret_cast<const CUtensorMap*>(s.tmap_tc_tail), s);
   return cudaGetLastError();
 }
 

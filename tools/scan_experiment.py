@@ -26,16 +26,23 @@ ap.add_argument("--k", type=int, default=10)
 ap.add_argument("--B", type=int, default=256)
 ap.add_argument("--modes", default="0,1,2,3")
 ap.add_argument("--kernels", default="0,1")
+ap.add_argument("--stages", default="0", help="tensor-core ring depth caps to try (0 = deepest)")
+ap.add_argument("--reserve", default="0", help="SMs left out of the scan grid")
+ap.add_argument("--box-rows", type=int, default=128)
 args = ap.parse_args()
 
 data = gen_vectors_chunked(args.n, args.d, 3)
 qs = gen_matrix(args.B, args.d, 4).astype(np.float64)
+_lib.set_option("tc_box_rows", args.box_rows)
 store = _DeviceStore(data)
 t = time.time()
 idx = IVFFlatIndex.train(store, args.nlist, 5, 4)
 print(f"train {time.time() - t:.2f}s", flush=True)
-for kern in [int(x) for x in args.kernels.split(",")]:
+for kern, stg, rsv in [(int(x), int(y), int(z)) for x in args.kernels.split(",") for y in args.stages.split(",")
+                       for z in args.reserve.split(",")]:
     _lib.set_option("scan_kernel", kern)
+    _lib.set_option("tc_stages", stg)
+    _lib.set_option("scan_reserve", rsv)
     for mode in [int(x) for x in args.modes.split(",")]:
         _lib.set_option("scan_debug", mode)
         for _ in range(3):
@@ -49,7 +56,7 @@ for kern in [int(x) for x in args.kernels.split(",")]:
         ms = st["scan"]
         idx.set_profiling(False)
         b, pairs = idx.last_scan_bytes()
-        print(f"kernel={kern} mode={mode} scan {ms / n:.3f} ms ({b / (ms / n) / 1e6:.0f} GB/s)  "
+        print(f"kernel={kern} stages={stg} reserve={rsv} mode={mode} scan {ms / n:.3f} ms ({b / (ms / n) / 1e6:.0f} GB/s)  "
               f"call {wall * 1e3:.3f} ms  fixups={idx.last_fixups()}  stages(us)="
               + " ".join(f"{k}={v / n * 1e3:.0f}" for k, v in st.items()), flush=True)
 _lib.set_option("scan_debug", 0)
