@@ -329,6 +329,7 @@ def run_ours(args):
         total_ms = float(t.item())
     qps = BATCH * args.steps / (total_ms / 1e3)
     scan_bytes, pairs = idx.last_scan_bytes()
+    scan_kind = idx.last_scan_kind()
 
     # e2e: public host API, pinned host buffers, copies inside the timed region
     # (one host thread per lane, each a blocking search_into on its own stream)
@@ -384,10 +385,10 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 scan + f64 re-rank", "data": "synthetic",
+        "dtype": f"{scan_kind} candidate scan (certified bound) + f64 exact re-rank", "data": "synthetic",
         "config": dict(CONFIG, parallelism=f"vector-shard x{world}" if world > 1 else "dp1", lanes=L),
         "roofline": {
-            "bound": "hbm", "kernel": "tri::scan_kernel (IVF list scan)", "achieved": achieved, "peak": peak,
+            "bound": "hbm", "kernel": f"tri::scan_tc_kernel ({scan_kind} tcgen05 IVF list scan)", "achieved": achieved, "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(),
             "algorithmic_bytes_per_launch": scan_bytes, "scan_ms_per_launch": avg_scan_ms,
             "scan_share_of_step": avg_scan_ms / (total_ms / args.steps),

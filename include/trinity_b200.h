@@ -126,6 +126,10 @@ int tri_ivf_stage_times(tri_ivf* v, double* ms, int32_t* searches);
  * (query, vector) pairs. */
 int tri_ivf_last_scan_bytes(tri_ivf* v, int64_t* bytes, int64_t* pairs);
 
+/* Arithmetic of the last search's list scan: 2 = fp16 tensor-core
+ * candidates (certified), 1 = fp32/TF32 candidates, 0 = no search yet. */
+int tri_ivf_last_scan_kind(tri_ivf* v, int32_t* kind);
+
 /* Exact merge of G per-shard result lists (device buffers, G x B x k_in,
  * id -1 = empty) into the global top-k_out by (dist, id). */
 int tri_merge_topk(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t k_out,

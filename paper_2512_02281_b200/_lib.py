@@ -54,6 +54,7 @@ _SIGS = {
     "tri_ivf_scan_time": [_vp, _f64p, _i32p],
     "tri_ivf_stage_times": [_vp, _vp, _i32p],
     "tri_ivf_last_scan_bytes": [_vp, _i64p, _i64p],
+    "tri_ivf_last_scan_kind": [_vp, _i32p],
     "tri_merge_topk": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp],
 }
 _RESTYPE = {"tri_last_error": C.c_char_p}

@@ -1496,6 +1496,13 @@ int tri_ivf_last_scan_bytes(tri_ivf* v, int64_t* bytes, int64_t* pairs) {
   return TRI_OK;
 }
 
+int tri_ivf_last_scan_kind(tri_ivf* v, int32_t* kind) {
+  if (!v || !kind) return fail(TRI_EINVAL, "null handle");
+  const Workspace& w = v->lanes.recent();
+  *kind = w.last_f16 ? 2 : (v->lanes.used ? 1 : 0);
+  return TRI_OK;
+}
+
 int tri_merge_topk(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t k_out,
                    double* out_dists, int64_t* out_ids, void* stream) {
   if (G < 1 || B < 0 || k_in < 1 || k_out < 1) return fail(TRI_EINVAL, "bad merge shape");

@@ -211,6 +211,12 @@ class IVFFlatIndex:
         _lib.check(_lib.gpu().tri_ivf_last_scan_bytes(self.handle, C.byref(b), C.byref(p)))
         return b.value, p.value
 
+    def last_scan_kind(self) -> str:
+        """"f16" (fp16 tensor-core candidates), "f32" (fp32 / TF32 candidates) or "none"."""
+        k = C.c_int32(0)
+        _lib.check(_lib.gpu().tri_ivf_last_scan_kind(self.handle, C.byref(k)))
+        return {2: "f16", 1: "f32"}.get(k.value, "none")
+
 
 def merge_topk_device(dists, ids, k_out: int, out_dists, out_ids, stream=None) -> None:
     """Exact (dist, id) merge of per-shard lists on the device (tensors [G, B, k_in])."""
