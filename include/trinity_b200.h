@@ -130,6 +130,35 @@ int tri_ivf_last_scan_bytes(tri_ivf* v, int64_t* bytes, int64_t* pairs);
  * candidates (certified), 1 = fp32/TF32 candidates, 0 = no search yet. */
 int tri_ivf_last_scan_kind(tri_ivf* v, int32_t* kind);
 
+/* Device-resident continuous-batching graph search: replaces
+ * engine.ContinuousBatchEngine (engine.py:312-422).  adjacency: n x degree
+ * uint32 (NeighborGraph, ann_graph.py:51-70); the config mirrors EngineConfig
+ * (engine.py:39-66; m <= 256, p * degree <= 512).  Requests are seeded,
+ * extended, merged and finalized on the device with the reference's exact
+ * float64 distances; results and batch accounting are bit-identical. */
+typedef struct tri_engine tri_engine;
+int tri_engine_create(tri_store* s, const uint32_t* adjacency, int32_t degree, int32_t m, int32_t p,
+                      int32_t entry_count, int32_t batch_capacity, int32_t stop_streak, int32_t max_extends,
+                      tri_engine** out);
+int tri_engine_destroy(tri_engine* e);
+/* ContinuousBatchEngine.submit (engine.py:337-345): q is one float64 row of
+ * the store's dimension; queued until the next step admits it. */
+int tri_engine_submit(tri_engine* e, const double* q, int32_t k, int64_t* rid);
+/* active_count / pending_admissions (engine.py:347-353). */
+int tri_engine_counts(tri_engine* e, int32_t* active, int32_t* pending);
+/* Up to max_steps steps (engine.py:369-411); step 0 admits the pending
+ * requests.  until_idle != 0 stops after the first step that leaves no
+ * active request (run_to_completion, engine.py:413-422).  Per-step outputs
+ * (arrays of max_steps, may be NULL): total emissions (batch accounting:
+ * ceil(E / batch_capacity) batches), admissions, retirements. */
+int tri_engine_run(tri_engine* e, int32_t max_steps, int32_t until_idle, int32_t* steps_done,
+                   int64_t* emissions, int32_t* admitted, int32_t* retired);
+/* Drain up to cap retired results (retirement order: step, then request id):
+ * request id, extends, k, step index of the run, and k ids / float64
+ * distances per row (row stride ld). */
+int tri_engine_retired(tri_engine* e, int32_t cap, int32_t ld, int32_t* n, int64_t* rids, int32_t* extends,
+                       int32_t* ks, int32_t* steps, int64_t* ids, double* dists);
+
 /* Exact merge of G per-shard result lists (device buffers, G x B x k_in,
  * id -1 = empty) into the global top-k_out by (dist, id). */
 int tri_merge_topk(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t k_out,

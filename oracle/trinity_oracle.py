@@ -17,6 +17,9 @@ BASELINE.json (citations are ``path:line`` under the read-only reference
   same (dist, id) tie semantics.
 * ``merge_shards``        <- (dist, id) lexicographic merge, the tie rule of
   ann_graph.py:8-9 applied to per-shard lists.
+* ``engine_run``          <- ``engine.ContinuousBatchEngine`` driven by a
+  submit/step schedule (engine.py:136-422): seed, parents, expand, task-array
+  accounting, distances, merge, early stop, finalize.
 
 Parity pin: ``tests/golden/`` holds vectors produced by importing the reference
 itself (``tests/golden/make_golden.py``); ``tests/test_oracle_golden.py`` checks
@@ -218,3 +221,73 @@ def merge_shards(parts, k: int):
     keep = ids >= 0
     ids, dists = ids[keep], dists[keep]
     return _lex_topk(dists, ids, min(k, ids.size))
+
+
+# ----------------------------------------------------------------------------
+# continuous-batching graph engine
+
+
+def engine_run(data32: np.ndarray, adjacency: np.ndarray, queries, ks, admit_step, m: int = 64, p: int = 2,
+               entry_count: int = 8, batch_capacity: int = 512, stop_streak: int = 1, max_extends: int = 256):
+    """Restatement of the reference engine's state machine (engine.py:136-422).
+
+    Query i is submitted just before step ``admit_step[i]`` (a non-decreasing
+    schedule); steps continue until no request is active, as
+    ``step()`` x waves followed by ``run_to_completion()``.  Returns
+    (ids list, dists list, extends array, batch_real_counts, n_steps).
+    """
+    n = data32.shape[0]
+    queries = np.asarray(queries, dtype=np.float64)
+    nq = queries.shape[0]
+    entries = list(dict.fromkeys(i * n // entry_count for i in range(entry_count)))  # engine.py:136-143
+    states = {}
+    out_ids, out_d = [None] * nq, [None] * nq
+    extends = np.zeros(nq, dtype=np.int64)
+    batch_real_counts = []
+    nxt = 0
+    step = 0
+    while nxt < nq or states:
+        while nxt < nq and admit_step[nxt] <= step:  # seed at submit, admitted at step start
+            q = queries[nxt]
+            dd = sq_dists(q, data32[entries].astype(np.float64))
+            top = sorted(((float(d), v, False) for v, d in zip(entries, dd)))
+            states[nxt] = {"q": q, "top": [list(t) for t in top], "vis": set(entries), "ext": 0, "streak": 0}
+            nxt += 1
+        total = 0
+        emitted = {}
+        for rid in sorted(states):  # engine.py:379-385
+            st = states[rid]
+            parents = [e for e in st["top"] if not e[2]][:p]  # engine.py:176-184
+            em = []
+            for e in parents:  # engine.py:187-205
+                for nid in adjacency[e[1]]:
+                    nid = int(nid)
+                    if nid not in st["vis"]:
+                        st["vis"].add(nid)
+                        em.append(nid)
+                e[2] = True
+            emitted[rid] = em
+            total += len(em)
+        for s0 in range(0, total, batch_capacity):  # build_task_array accounting, engine.py:208-226
+            batch_real_counts.append(min(batch_capacity, total - s0))
+        for rid in sorted(states):
+            st = states[rid]
+            em = emitted[rid]
+            changed = False
+            if em:  # scatter_merge, engine.py:259-275
+                dd = sq_dists(st["q"], data32[em].astype(np.float64))
+                before = [e[1] for e in st["top"]]
+                pool = st["top"] + [[float(d), c, False] for c, d in zip(em, dd)]
+                pool.sort(key=lambda e: (e[0], e[1]))
+                st["top"] = pool[:m]
+                changed = [e[1] for e in st["top"]] != before
+            st["ext"] += 1
+            st["streak"] = 0 if changed else st["streak"] + 1  # engine.py:278-290
+            if (st["streak"] >= stop_streak or all(e[2] for e in st["top"]) or st["ext"] >= max_extends):
+                k = int(ks[rid])
+                out_ids[rid] = np.array([e[1] for e in st["top"][:k]], dtype=np.int64)
+                out_d[rid] = np.array([e[0] for e in st["top"][:k]], dtype=np.float64)
+                extends[rid] = st["ext"]
+                del states[rid]
+        step += 1
+    return out_ids, out_d, extends, batch_real_counts, step

@@ -55,6 +55,12 @@ _SIGS = {
     "tri_ivf_stage_times": [_vp, _vp, _i32p],
     "tri_ivf_last_scan_bytes": [_vp, _i64p, _i64p],
     "tri_ivf_last_scan_kind": [_vp, _i32p],
+    "tri_engine_create": [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, C.POINTER(_vp)],
+    "tri_engine_destroy": [_vp],
+    "tri_engine_submit": [_vp, _vp, _i32, _i64p],
+    "tri_engine_counts": [_vp, _i32p, _i32p],
+    "tri_engine_run": [_vp, _i32, _i32, _i32p, _vp, _vp, _vp],
+    "tri_engine_retired": [_vp, _i32, _i32, _i32p, _vp, _vp, _vp, _vp, _vp, _vp],
     "tri_merge_topk": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp],
 }
 _RESTYPE = {"tri_last_error": C.c_char_p}

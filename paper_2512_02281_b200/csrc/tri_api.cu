@@ -729,6 +729,28 @@ int prep_queries(Workspace& w, const double* q64dev, int B, int d, int qld, cuda
 }  // namespace
 
 // ===========================================================================
+namespace tri {
+int store_view(const tri_store* s, StoreView* v) {
+  if (!s || !v) return fail(TRI_EINVAL, "store is NULL");
+  v->X = s->X;
+  v->ldx = s->dp;
+  v->n = s->n;
+  v->d = s->d;
+  v->device = s->device;
+  return TRI_OK;
+}
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+}  // namespace tri
+
 extern "C" {
 
 const char* tri_last_error(void) { return g_err.c_str(); }

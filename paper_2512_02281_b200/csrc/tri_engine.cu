@@ -1,0 +1,686 @@
+// Device-resident continuous-batching graph search (the reference's
+// engine.ContinuousBatchEngine, pkg/src/trinity/engine.py:312-422).
+//
+// Every request lives in a device SLOT: its float64 query, its top-M list
+// (fp64 distance, id, expanded flag) sorted by (dist, id), its visited bitmap
+// over the store, and its counters (extends, no-change streak).  One launch of
+// `engine_step_kernel` advances EVERY active request through exactly one
+// extend -- one CTA per slot:
+//
+//   seed (admitted this step; engine.py:146-173)  ->  select parents
+//   (engine.py:176-184)  ->  expand with test-and-set on the visited bitmap
+//   (engine.py:187-205)  ->  exact distances of the emitted candidates in the
+//   reference's float64 operation order (rowwise_sq_dists, ann_graph.py:97-105;
+//   bit-identical)  ->  merge into top-M by (dist, id) (engine.py:259-275)  ->
+//   early stop / finalize (engine.py:278-302).
+//
+// The reference's fixed-shape task array (build_task_array, engine.py:208-226)
+// exists only to give its simulated GPU a static launch shape; its observable
+// effect is the batch accounting, which depends only on the step's total
+// emission count E: ceil(E / C) batches, the last one padded.  The kernel
+// counts E per step and the host derives the identical EngineStats.  Results
+// do not depend on how tasks are packed (a distance is independent of its
+// batch, ann_graph.py:98-103).
+//
+// Steps run back to back on the device without host synchronisation; the host
+// reads per-step counters (emissions, retirements, active count) once per
+// chunk of steps, so run_to_completion costs one launch per extend.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "../../include/trinity_b200.h"
+#include "tri_common.cuh"
+#include "tri_internal.h"
+
+namespace tri {
+namespace {
+
+constexpr int kEngThreads = 128;
+constexpr int kEngMaxM = 256;     // top-M capacity per request
+constexpr int kEngMaxEmit = 512;  // p * degree per extend
+constexpr int kStats = 4;         // per-step counters: emissions, retired, active after, error
+constexpr int kMaxChunk = 64;     // steps launched between host read-backs
+
+enum SlotStatus : int { kFree = 0, kSeed = 1, kActive = 2 };
+enum EngErr : int { kErrNone = 0, kErrRange = 1, kErrK = 2 };
+
+struct EngineLaunch {
+  const float* X;
+  long long ldx;
+  long long n;
+  int d;
+  const unsigned* adj;
+  int D;
+  int m, p, E, stop_streak, max_extends;
+  int* status;
+  const double* q64;
+  const int* kq;
+  const long long* rid;
+  int* ext;
+  int* streak;
+  int* cnt;
+  double* topd;
+  int* topi;
+  unsigned char* tope;
+  unsigned* vis;
+  long long vw;
+  int* stats;  // this step's kStats counters
+  int step;
+  // retirements (host drains after each chunk)
+  int* res_n;
+  long long* res_rid;
+  int* res_ext;
+  int* res_k;
+  int* res_step;
+  int* res_slot;
+  int* res_ids;
+  double* res_d;
+};
+
+__device__ __forceinline__ bool lt(double da, int ia, double db, int ib) {
+  return da < db || (da == db && ia < ib);
+}
+
+__global__ void __launch_bounds__(kEngThreads) engine_step_kernel(EngineLaunch L) {
+  const int s = blockIdx.x;
+  const int st = L.status[s];
+  if (st != kSeed && st != kActive) return;
+  const int tid = threadIdx.x;
+
+  // combined list: [0, cnt) the current top-M, [cnt, cnt + ne) this extend's emissions
+  __shared__ double cd[kEngMaxM + kEngMaxEmit];
+  __shared__ int ci[kEngMaxM + kEngMaxEmit];
+  __shared__ unsigned char ce[kEngMaxM + kEngMaxEmit];
+  __shared__ double od[kEngMaxM];
+  __shared__ int oi[kEngMaxM];
+  __shared__ unsigned char oe[kEngMaxM];
+  __shared__ int parents[kEngMaxEmit];
+  __shared__ int s_cnt, s_ne, s_np, s_err;
+
+  const double* q = L.q64 + (long long)s * L.d;
+  unsigned* vis = L.vis + (long long)s * L.vw;
+  const int m = L.m;
+
+  if (tid == 0) {
+    s_err = kErrNone;
+    s_ne = 0;
+  }
+  if (st == kSeed) {
+    // strided entry points floor(i*n/E), deduplicated (engine.py:136-143); the
+    // sequence is non-decreasing, so duplicates are adjacent
+    if (tid == 0) {
+      int c = 0;
+      long long last = -1;
+      for (int i = 0; i < L.E; ++i) {
+        long long v = (long long)i * L.n / L.E;
+        if (v != last) {
+          ci[kEngMaxM + c++] = (int)v;
+          last = v;
+        }
+      }
+      s_ne = c;
+    }
+    __syncthreads();
+    const int c = s_ne;
+    for (int i = tid; i < c; i += kEngThreads) {
+      const int v = ci[kEngMaxM + i];
+      cd[kEngMaxM + i] = exact_sq_dist(q, L.X + (long long)v * L.ldx, L.d);
+      atomicOr(&vis[v >> 5], 1u << (v & 31));
+    }
+    __syncthreads();
+    // rank placement of the entries (ids unique) -> sorted top list
+    for (int i = tid; i < c; i += kEngThreads) {
+      const double di = cd[kEngMaxM + i];
+      const int ii = ci[kEngMaxM + i];
+      int r = 0;
+      for (int j = 0; j < c; ++j) r += lt(cd[kEngMaxM + j], ci[kEngMaxM + j], di, ii);
+      od[r] = di;
+      oi[r] = ii;
+    }
+    __syncthreads();
+    for (int i = tid; i < c; i += kEngThreads) {
+      cd[i] = od[i];
+      ci[i] = oi[i];
+      ce[i] = 0;
+    }
+    if (tid == 0) {
+      s_cnt = c;
+      s_ne = 0;
+    }
+    __syncthreads();
+  } else {
+    const int c = L.cnt[s];
+    const long long base = (long long)s * m;
+    for (int i = tid; i < c; i += kEngThreads) {
+      cd[i] = L.topd[base + i];
+      ci[i] = L.topi[base + i];
+      ce[i] = L.tope[base + i];
+    }
+    if (tid == 0) s_cnt = c;
+    __syncthreads();
+  }
+  const int cnt = s_cnt;
+
+  // select parents: the first <= p unexpanded entries, best first (engine.py:176-184)
+  if (tid == 0) {
+    int np = 0;
+    for (int r = 0; r < cnt && np < L.p; ++r)
+      if (!ce[r]) parents[np++] = r;
+    s_np = np;
+  }
+  __syncthreads();
+  const int np = s_np;
+
+  // expand: neighbours of each parent, test-and-set on the visited bitmap so an
+  // id shared by two parents is emitted once (engine.py:187-205)
+  for (int t = tid; t < np * L.D; t += kEngThreads) {
+    const int pi = t / L.D;
+    const unsigned nid = L.adj[(long long)ci[parents[pi]] * L.D + (t - pi * L.D)];
+    if ((long long)nid >= L.n) {
+      s_err = kErrRange;
+      continue;
+    }
+    const unsigned bit = 1u << (nid & 31);
+    if (!(atomicOr(&vis[nid >> 5], bit) & bit)) {
+      const int e = atomicAdd(&s_ne, 1);
+      ci[cnt + e] = (int)nid;
+      ce[cnt + e] = 0;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < np; i += kEngThreads) ce[parents[i]] = 1;
+  const int ne = s_ne;
+
+  // exact float64 distances of the emissions, reference operation order
+  for (int i = tid; i < ne; i += kEngThreads)
+    cd[cnt + i] = exact_sq_dist(q, L.X + (long long)ci[cnt + i] * L.ldx, L.d);
+  __syncthreads();
+
+  // merge into top-M by (dist, id): rank placement over the combined list
+  const int nc = cnt + ne;
+  const int newcnt = nc < m ? nc : m;
+  for (int i = tid; i < nc; i += kEngThreads) {
+    const double di = cd[i];
+    const int ii = ci[i];
+    int r = 0;
+    for (int j = 0; j < nc; ++j) r += lt(cd[j], ci[j], di, ii);
+    if (r < m) {
+      od[r] = di;
+      oi[r] = ii;
+      oe[r] = ce[i];
+    }
+  }
+  __syncthreads();
+  // changed = the ordered id list differs (engine.py:259-275; no results -> unchanged)
+  int diff = 0, unexp = 0;
+  for (int r = tid; r < newcnt; r += kEngThreads) {
+    diff |= (r >= cnt) || (oi[r] != ci[r]);
+    unexp |= !oe[r];
+  }
+  const int any_diff = __syncthreads_or(diff);
+  const bool all_expanded = !__syncthreads_or(unexp);
+  const bool changed = (ne > 0) && (any_diff || newcnt != cnt);
+
+  if (tid == 0) {
+    if (ne) atomicAdd(&L.stats[0], ne);
+    if (s_err) atomicMax(&L.stats[3], s_err);
+  }
+  const int extends = (st == kSeed ? 0 : L.ext[s]) + 1;
+  const int streak = changed ? 0 : (st == kSeed ? 0 : L.streak[s]) + 1;
+  const bool converged = streak >= L.stop_streak || all_expanded || extends >= L.max_extends;
+  const int k = L.kq[s];
+  if (converged) {
+    // finalize (engine.py:293-302): first k entries
+    __shared__ int slot;
+    if (tid == 0) {
+      if (k > newcnt) {
+        atomicMax(&L.stats[3], kErrK);
+        slot = -1;
+      } else {
+        slot = atomicAdd(L.res_n, 1);
+        L.res_rid[slot] = L.rid[s];
+        L.res_ext[slot] = extends;
+        L.res_k[slot] = k;
+        L.res_step[slot] = L.step;
+        L.res_slot[slot] = s;
+        atomicAdd(&L.stats[1], 1);
+      }
+      // the slot is free on the device now; the host reuses it only after it
+      // has read this retirement record
+      L.status[s] = kFree;
+    }
+    __syncthreads();
+    if (slot >= 0)
+      for (int r = tid; r < k; r += kEngThreads) {
+        L.res_ids[(long long)slot * m + r] = oi[r];
+        L.res_d[(long long)slot * m + r] = od[r];
+      }
+    return;
+  }
+  const long long base = (long long)s * m;
+  for (int r = tid; r < newcnt; r += kEngThreads) {
+    L.topd[base + r] = od[r];
+    L.topi[base + r] = oi[r];
+    L.tope[base + r] = oe[r];
+  }
+  if (tid == 0) {
+    L.cnt[s] = newcnt;
+    L.ext[s] = extends;
+    L.streak[s] = streak;
+    L.status[s] = kActive;
+    atomicAdd(&L.stats[2], 1);
+  }
+}
+
+// Admission: copy the staged queries into their slots, reset counters and the
+// visited bitmap (the reference's seed happens at submit; here it is the first
+// thing the slot's next step does -- same values, engine.py:146-173).
+__global__ void engine_admit_kernel(const int* __restrict__ slots, const long long* __restrict__ rids,
+                                    const int* __restrict__ ks, const double* __restrict__ q, int d, int* status,
+                                    double* q64, int* kq, long long* rid, unsigned* vis, long long vw) {
+  const int a = blockIdx.x;
+  const int s = slots[a];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) q64[(long long)s * d + i] = q[(long long)a * d + i];
+  unsigned* v = vis + (long long)s * vw;
+  for (long long i = threadIdx.x; i < vw; i += blockDim.x) v[i] = 0u;
+  if (threadIdx.x == 0) {
+    kq[s] = ks[a];
+    rid[s] = rids[a];
+    status[s] = kSeed;
+  }
+}
+
+template <typename T>
+cudaError_t grow(T*& p, size_t old_elems, size_t new_elems, cudaStream_t st) {
+  T* np = nullptr;
+  cudaError_t e = cudaMalloc(&np, new_elems * sizeof(T));
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(np, 0, new_elems * sizeof(T), st);
+  if (e == cudaSuccess && p && old_elems) e = cudaMemcpyAsync(np, p, old_elems * sizeof(T), cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) {
+    cudaFree(np);
+    return e;
+  }
+  if (p) {
+    cudaStreamSynchronize(st);
+    cudaFree(p);
+  }
+  p = np;
+  return cudaSuccess;
+}
+
+}  // namespace
+}  // namespace tri
+
+using namespace tri;
+
+struct tri_engine {
+  StoreView sv{};
+  int D = 0, m = 0, p = 0, E = 0, C = 0, S = 0, maxext = 0;
+  unsigned* adj = nullptr;
+  long long vw = 0;
+  cudaStream_t st = nullptr;
+  // slots
+  int cap = 0, hw = 0;
+  int *status = nullptr, *kq = nullptr, *ext = nullptr, *streak = nullptr, *cnt = nullptr;
+  long long* rid = nullptr;
+  double *q64 = nullptr, *topd = nullptr;
+  int* topi = nullptr;
+  unsigned char* tope = nullptr;
+  unsigned* vis = nullptr;
+  // retirements
+  int* res_n = nullptr;
+  long long* res_rid = nullptr;
+  int *res_ext = nullptr, *res_k = nullptr, *res_step = nullptr, *res_slot = nullptr, *res_ids = nullptr;
+  double* res_d = nullptr;
+  int* stats = nullptr;  // kMaxChunk x kStats
+  // admission staging
+  int* a_slot = nullptr;
+  long long* a_rid = nullptr;
+  int* a_k = nullptr;
+  double* a_q = nullptr;
+  int a_cap = 0;
+  // host state
+  std::vector<int> free_slots;
+  std::vector<long long> p_rid;
+  std::vector<int> p_k;
+  std::vector<double> p_q;
+  long long next_rid = 0;
+  int n_active = 0;
+  struct Done {
+    long long rid;
+    int ext, k, step;
+    std::vector<int> ids;
+    std::vector<double> d;
+  };
+  std::vector<Done> retired;
+  // pinned read-back
+  int* h_stats = nullptr;
+};
+
+namespace {
+
+#define ECU(expr)                                                                                     \
+  do {                                                                                                \
+    cudaError_t _e = (expr);                                                                          \
+    if (_e != cudaSuccess) return set_error(TRI_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+struct Guard {
+  int prev = -1;
+  explicit Guard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~Guard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int grow_slots(tri_engine* e, int need) {
+  if (need <= e->cap) return TRI_OK;
+  int nc = std::max(need, std::max(64, 2 * e->cap));
+  const size_t oc = e->cap, ncz = nc, m = e->m, d = e->sv.d;
+  cudaStream_t st = e->st;
+  ECU(grow(e->status, oc, ncz, st));
+  ECU(grow(e->kq, oc, ncz, st));
+  ECU(grow(e->ext, oc, ncz, st));
+  ECU(grow(e->streak, oc, ncz, st));
+  ECU(grow(e->cnt, oc, ncz, st));
+  ECU(grow(e->rid, oc, ncz, st));
+  ECU(grow(e->q64, oc * d, ncz * d, st));
+  ECU(grow(e->topd, oc * m, ncz * m, st));
+  ECU(grow(e->topi, oc * m, ncz * m, st));
+  ECU(grow(e->tope, oc * m, ncz * m, st));
+  ECU(grow(e->vis, oc * e->vw, ncz * e->vw, st));
+  // retirement buffers: at most one retirement per slot between read-backs
+  ECU(grow(e->res_rid, 0, ncz, st));
+  ECU(grow(e->res_ext, 0, ncz, st));
+  ECU(grow(e->res_k, 0, ncz, st));
+  ECU(grow(e->res_step, 0, ncz, st));
+  ECU(grow(e->res_slot, 0, ncz, st));
+  ECU(grow(e->res_ids, 0, ncz * m, st));
+  ECU(grow(e->res_d, 0, ncz * m, st));
+  for (int s = nc - 1; s >= e->cap; --s) e->free_slots.push_back(s);
+  e->cap = nc;
+  return TRI_OK;
+}
+
+// Admit every pending request into a free slot (engine.py:371-375).
+int admit(tri_engine* e, int* admitted) {
+  const int na = (int)e->p_rid.size();
+  *admitted = na;
+  if (!na) return TRI_OK;
+  if ((int)e->free_slots.size() < na) {
+    int rc = grow_slots(e, e->cap + na - (int)e->free_slots.size());
+    if (rc) return rc;
+  }
+  if (na > e->a_cap) {
+    int c = std::max(na, 2 * e->a_cap);
+    ECU(grow(e->a_slot, 0, c, e->st));
+    ECU(grow(e->a_rid, 0, c, e->st));
+    ECU(grow(e->a_k, 0, c, e->st));
+    ECU(grow(e->a_q, 0, (size_t)c * e->sv.d, e->st));
+    e->a_cap = c;
+  }
+  std::vector<int> slots(na);
+  for (int i = 0; i < na; ++i) {
+    slots[i] = e->free_slots.back();
+    e->free_slots.pop_back();
+    e->hw = std::max(e->hw, slots[i] + 1);
+  }
+  ECU(cudaMemcpyAsync(e->a_slot, slots.data(), na * sizeof(int), cudaMemcpyHostToDevice, e->st));
+  ECU(cudaMemcpyAsync(e->a_rid, e->p_rid.data(), na * sizeof(long long), cudaMemcpyHostToDevice, e->st));
+  ECU(cudaMemcpyAsync(e->a_k, e->p_k.data(), na * sizeof(int), cudaMemcpyHostToDevice, e->st));
+  ECU(cudaMemcpyAsync(e->a_q, e->p_q.data(), e->p_q.size() * sizeof(double), cudaMemcpyHostToDevice, e->st));
+  engine_admit_kernel<<<na, 256, 0, e->st>>>(e->a_slot, e->a_rid, e->a_k, e->a_q, e->sv.d, e->status, e->q64,
+                                             e->kq, e->rid, e->vis, e->vw);
+  ECU(cudaGetLastError());
+  // the host vectors must outlive the async copies
+  ECU(cudaStreamSynchronize(e->st));
+  e->p_rid.clear();
+  e->p_k.clear();
+  e->p_q.clear();
+  e->n_active += na;
+  return TRI_OK;
+}
+
+EngineLaunch launch_of(tri_engine* e) {
+  EngineLaunch L;
+  L.X = e->sv.X;
+  L.ldx = e->sv.ldx;
+  L.n = e->sv.n;
+  L.d = e->sv.d;
+  L.adj = e->adj;
+  L.D = e->D;
+  L.m = e->m;
+  L.p = e->p;
+  L.E = e->E;
+  L.stop_streak = e->S;
+  L.max_extends = e->maxext;
+  L.status = e->status;
+  L.q64 = e->q64;
+  L.kq = e->kq;
+  L.rid = e->rid;
+  L.ext = e->ext;
+  L.streak = e->streak;
+  L.cnt = e->cnt;
+  L.topd = e->topd;
+  L.topi = e->topi;
+  L.tope = e->tope;
+  L.vis = e->vis;
+  L.vw = e->vw;
+  L.res_n = e->res_n;
+  L.res_rid = e->res_rid;
+  L.res_ext = e->res_ext;
+  L.res_k = e->res_k;
+  L.res_step = e->res_step;
+  L.res_slot = e->res_slot;
+  L.res_ids = e->res_ids;
+  L.res_d = e->res_d;
+  return L;
+}
+
+// Read back this chunk's retirements and return their slots to the free list.
+int collect(tri_engine* e) {
+  int n = 0;
+  ECU(cudaMemcpyAsync(&n, e->res_n, sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaStreamSynchronize(e->st));
+  if (!n) return TRI_OK;
+  const int m = e->m;
+  std::vector<long long> rid(n);
+  std::vector<int> ext(n), k(n), step(n), slot(n), ids((size_t)n * m);
+  std::vector<double> d((size_t)n * m);
+  ECU(cudaMemcpyAsync(rid.data(), e->res_rid, n * sizeof(long long), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(ext.data(), e->res_ext, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(k.data(), e->res_k, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(step.data(), e->res_step, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(slot.data(), e->res_slot, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(ids.data(), e->res_ids, ids.size() * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(d.data(), e->res_d, d.size() * sizeof(double), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemsetAsync(e->res_n, 0, sizeof(int), e->st));
+  ECU(cudaStreamSynchronize(e->st));
+  for (int s : slot) e->free_slots.push_back(s);
+  e->n_active -= n;
+  // reuse the lowest slots first so the step grid stays compact
+  std::sort(e->free_slots.begin(), e->free_slots.end(), std::greater<int>());
+  if (e->n_active == 0) e->hw = 0;
+  // retirements in step order, ascending request id within a step (engine.py:398-411)
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(),
+            [&](int a, int b) { return step[a] != step[b] ? step[a] < step[b] : rid[a] < rid[b]; });
+  for (int i : order) {
+    tri_engine::Done r;
+    r.rid = rid[i];
+    r.ext = ext[i];
+    r.k = k[i];
+    r.step = step[i];
+    r.ids.assign(ids.begin() + (size_t)i * m, ids.begin() + (size_t)i * m + k[i]);
+    r.d.assign(d.begin() + (size_t)i * m, d.begin() + (size_t)i * m + k[i]);
+    e->retired.push_back(std::move(r));
+  }
+  return TRI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tri_engine_create(tri_store* s, const uint32_t* adjacency, int32_t degree, int32_t m, int32_t p,
+                      int32_t entry_count, int32_t batch_capacity, int32_t stop_streak, int32_t max_extends,
+                      tri_engine** out) {
+  if (!out) return set_error(TRI_EINVAL, "out is NULL");
+  StoreView sv;
+  int rc = store_view(s, &sv);
+  if (rc) return rc;
+  if (degree < 1) return set_error(TRI_EINVAL, "degree must be >= 1, got %d", degree);
+  if (!(1 <= p && p <= m)) return set_error(TRI_EINVAL, "p must be in [1, m=%d], got %d", m, p);
+  if (!(1 <= entry_count && entry_count <= m))
+    return set_error(TRI_EINVAL, "entry_count must be in [1, m=%d], got %d", m, entry_count);
+  if (batch_capacity < 1) return set_error(TRI_EINVAL, "batch_capacity must be >= 1, got %d", batch_capacity);
+  if (stop_streak < 1) return set_error(TRI_EINVAL, "stop_streak must be >= 1, got %d", stop_streak);
+  if (max_extends < 1) return set_error(TRI_EINVAL, "max_extends must be >= 1, got %d", max_extends);
+  if (m > kEngMaxM) return set_error(TRI_EINVAL, "the device engine supports m <= %d, got %d", kEngMaxM, m);
+  if ((long long)p * degree > kEngMaxEmit)
+    return set_error(TRI_EINVAL, "the device engine supports p * degree <= %d, got %lld", kEngMaxEmit,
+                     (long long)p * degree);
+  Guard g(sv.device);
+  tri_engine* e = new tri_engine();
+  e->sv = sv;
+  e->D = degree;
+  e->m = m;
+  e->p = p;
+  e->E = entry_count;
+  e->C = batch_capacity;
+  e->S = stop_streak;
+  e->maxext = max_extends;
+  e->vw = (sv.n + 31) / 32;
+  auto bail = [&](int code) {
+    tri_engine_destroy(e);
+    return code;
+  };
+  if (cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(set_error(TRI_ECUDA, "stream creation failed"));
+  const size_t adj_bytes = (size_t)sv.n * degree * sizeof(unsigned);
+  if (cudaMalloc(&e->adj, adj_bytes) != cudaSuccess ||
+      cudaMemcpy(e->adj, adjacency, adj_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMalloc(&e->res_n, sizeof(int)) != cudaSuccess || cudaMemset(e->res_n, 0, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&e->stats, kMaxChunk * kStats * sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&e->h_stats, kMaxChunk * kStats * sizeof(int)) != cudaSuccess)
+    return bail(set_error(TRI_ECUDA, "engine allocation failed"));
+  rc = grow_slots(e, 64);
+  if (rc) return bail(rc);
+  *out = e;
+  return TRI_OK;
+}
+
+int tri_engine_destroy(tri_engine* e) {
+  if (!e) return TRI_OK;
+  Guard g(e->sv.device);
+  if (e->st) cudaStreamSynchronize(e->st);
+  void* bufs[] = {e->adj, e->status, e->kq, e->ext, e->streak, e->cnt, e->rid, e->q64, e->topd, e->topi,
+                  e->tope, e->vis, e->res_n, e->res_rid, e->res_ext, e->res_k, e->res_step, e->res_slot, e->res_ids,
+                  e->res_d, e->stats, e->a_slot, e->a_rid, e->a_k, e->a_q};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (e->h_stats) cudaFreeHost(e->h_stats);
+  if (e->st) cudaStreamDestroy(e->st);
+  delete e;
+  return TRI_OK;
+}
+
+int tri_engine_submit(tri_engine* e, const double* q, int32_t k, int64_t* rid) {
+  if (!e || !q) return set_error(TRI_EINVAL, "null argument");
+  for (int i = 0; i < e->sv.d; ++i)
+    if (!std::isfinite(q[i])) return set_error(TRI_EINVAL, "query must be finite");
+  if (!(1 <= k && k <= e->m)) return set_error(TRI_EINVAL, "k must be in [1, m=%d], got %d", e->m, k);
+  const long long r = e->next_rid++;
+  e->p_rid.push_back(r);
+  e->p_k.push_back(k);
+  e->p_q.insert(e->p_q.end(), q, q + e->sv.d);
+  if (rid) *rid = r;
+  return TRI_OK;
+}
+
+int tri_engine_counts(tri_engine* e, int32_t* active, int32_t* pending) {
+  if (!e) return set_error(TRI_EINVAL, "engine is NULL");
+  if (active) *active = e->n_active;
+  if (pending) *pending = (int32_t)e->p_rid.size();
+  return TRI_OK;
+}
+
+int tri_engine_run(tri_engine* e, int32_t max_steps, int32_t until_idle, int32_t* steps_done,
+                   int64_t* emissions, int32_t* admitted, int32_t* retired) {
+  if (!e) return set_error(TRI_EINVAL, "engine is NULL");
+  if (max_steps < 0) return set_error(TRI_EINVAL, "max_steps must be >= 0");
+  Guard g(e->sv.device);
+  int done = 0;
+  if (steps_done) *steps_done = 0;
+  if (until_idle && e->n_active == 0 && e->p_rid.empty()) return TRI_OK;
+  int chunk = 4;
+  while (done < max_steps) {
+    int adm = 0;
+    if (done == 0) {
+      int rc = admit(e, &adm);
+      if (rc) return rc;
+    }
+    const int n = std::min({chunk, kMaxChunk, max_steps - done});
+    ECU(cudaMemsetAsync(e->stats, 0, n * kStats * sizeof(int), e->st));
+    EngineLaunch L = launch_of(e);
+    for (int i = 0; i < n; ++i) {
+      L.stats = e->stats + i * kStats;
+      L.step = done + i;
+      if (e->hw > 0) engine_step_kernel<<<e->hw, kEngThreads, 0, e->st>>>(L);
+    }
+    ECU(cudaGetLastError());
+    ECU(cudaMemcpyAsync(e->h_stats, e->stats, n * kStats * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+    int rc = collect(e);  // synchronises
+    if (rc) return rc;
+    int used = n;
+    for (int i = 0; i < n; ++i) {
+      const int* sti = e->h_stats + i * kStats;
+      if (sti[3] == kErrRange)
+        return set_error(TRI_EINTERNAL, "candidate id out of range [0, %lld) (engine.py:249-250)", e->sv.n);
+      if (sti[3] == kErrK) return set_error(TRI_EINVAL, "k exceeds top-M length (engine.py:299-300)");
+      if (emissions) emissions[done + i] = sti[0];
+      if (retired) retired[done + i] = sti[1];
+      if (admitted) admitted[done + i] = (done + i == 0) ? adm : 0;
+      if (until_idle && sti[2] == 0) {
+        used = i + 1;
+        break;
+      }
+    }
+    done += used;
+    if (until_idle && e->h_stats[(used - 1) * kStats + 2] == 0) break;
+    chunk = std::min(kMaxChunk, chunk * 2);
+  }
+  if (steps_done) *steps_done = done;
+  return TRI_OK;
+}
+
+int tri_engine_retired(tri_engine* e, int32_t cap, int32_t ld, int32_t* n, int64_t* rids, int32_t* extends,
+                       int32_t* ks, int32_t* steps, int64_t* ids, double* dists) {
+  if (!e || !n) return set_error(TRI_EINVAL, "null argument");
+  const int cnt = std::min<int>(cap, (int)e->retired.size());
+  for (int i = 0; i < cnt; ++i) {
+    const auto& r = e->retired[i];
+    if (rids) rids[i] = r.rid;
+    if (extends) extends[i] = r.ext;
+    if (ks) ks[i] = r.k;
+    if (steps) steps[i] = r.step;
+    for (int j = 0; j < r.k && j < ld; ++j) {
+      if (ids) ids[(size_t)i * ld + j] = r.ids[j];
+      if (dists) dists[(size_t)i * ld + j] = r.d[j];
+    }
+  }
+  e->retired.erase(e->retired.begin(), e->retired.begin() + cnt);
+  *n = cnt;
+  return TRI_OK;
+}
+
+}  // extern "C"

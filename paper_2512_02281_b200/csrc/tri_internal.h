@@ -195,4 +195,20 @@ cudaError_t launch_centroid_update(const float* X, long long ldx, int d, const l
 cudaError_t launch_gather_rows(const float* X, long long ldx, const long long* perm, long long n, int dp,
                                float* out, cudaStream_t st);
 
+// Engine support (tri_engine.cu): a read-only view of a store's device rows and
+// the library's per-thread error slot.
+struct StoreView {
+  const float* X;
+  long long ldx;
+  long long n;
+  int d;
+  int device;
+};
+
+}  // namespace tri
+
+struct tri_store;
+namespace tri {
+int store_view(const tri_store* s, StoreView* v);
+int set_error(int code, const char* fmt, ...);
 }  // namespace tri

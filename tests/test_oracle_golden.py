@@ -133,3 +133,20 @@ def test_gen_trace_matches_reference(golden_dir):
     assert np.array_equal([r.output_len for r in tr], g["output"])
     assert np.array_equal(np.concatenate([r.queries for r in tr]), g["queries"])
     assert [r.queries.shape[0] for r in tr] == g["counts"].tolist()
+
+
+def test_engine_oracle_matches_reference_run(golden_dir):
+    """The engine restatement reproduces the reference's acceptance run
+    (test_acceptance.py:47-81; pkg/test_output.txt:16: 144 batches, 62736 tasks)."""
+    from paper_2512_02281_b200.workload import gen_matrix
+
+    g = np.load(os.path.join(golden_dir, "engine_c1.npz"))
+    data = gen_matrix(5000, 16, 20_240_601)
+    queries = gen_matrix(200, 16, 20_240_602)
+    ids, d, ext, brc, _ = orc.engine_run(data, g["adjacency"], queries, np.full(200, 10),
+                                         np.repeat(np.arange(10), 20))
+    assert all(np.array_equal(ids[i], g["ids"][i]) for i in range(200))
+    assert all(np.array_equal(d[i], g["dists"][i]) for i in range(200))
+    assert np.array_equal(ext, g["extends"])
+    assert brc == g["batch_real_counts"].tolist()
+    assert len(brc) == 144 and sum(brc) == 62736
