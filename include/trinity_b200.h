@@ -144,6 +144,10 @@ int tri_engine_destroy(tri_engine* e);
 /* ContinuousBatchEngine.submit (engine.py:337-345): q is one float64 row of
  * the store's dimension; queued until the next step admits it. */
 int tri_engine_submit(tri_engine* e, const double* q, int32_t k, int64_t* rid);
+/* Batched submit (B rows, per-request k); same validation, all or nothing. */
+int tri_engine_submit_batch(tri_engine* e, const double* q, int32_t B, const int32_t* k, int64_t* rids);
+/* Accumulated device time of the step launches (CUDA events) and steps run. */
+int tri_engine_device_time(tri_engine* e, double* ms, int64_t* steps);
 /* active_count / pending_admissions (engine.py:347-353). */
 int tri_engine_counts(tri_engine* e, int32_t* active, int32_t* pending);
 /* Up to max_steps steps (engine.py:369-411); step 0 admits the pending

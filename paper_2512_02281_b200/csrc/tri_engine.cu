@@ -360,6 +360,10 @@ struct tri_engine {
   std::vector<Done> retired;
   // pinned read-back
   int* h_stats = nullptr;
+  // device time of the step launches (CUDA events around each chunk)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double dev_ms = 0.0;
+  long long dev_steps = 0;
 };
 
 namespace {
@@ -571,7 +575,8 @@ int tri_engine_create(tri_store* s, const uint32_t* adjacency, int32_t degree, i
       cudaMemcpy(e->adj, adjacency, adj_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMalloc(&e->res_n, sizeof(int)) != cudaSuccess || cudaMemset(e->res_n, 0, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&e->stats, kMaxChunk * kStats * sizeof(int)) != cudaSuccess ||
-      cudaMallocHost(&e->h_stats, kMaxChunk * kStats * sizeof(int)) != cudaSuccess)
+      cudaMallocHost(&e->h_stats, kMaxChunk * kStats * sizeof(int)) != cudaSuccess ||
+      cudaEventCreate(&e->ev0) != cudaSuccess || cudaEventCreate(&e->ev1) != cudaSuccess)
     return bail(set_error(TRI_ECUDA, "engine allocation failed"));
   rc = grow_slots(e, 64);
   if (rc) return bail(rc);
@@ -589,6 +594,8 @@ int tri_engine_destroy(tri_engine* e) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (e->h_stats) cudaFreeHost(e->h_stats);
+  if (e->ev0) cudaEventDestroy(e->ev0);
+  if (e->ev1) cudaEventDestroy(e->ev1);
   if (e->st) cudaStreamDestroy(e->st);
   delete e;
   return TRI_OK;
@@ -604,6 +611,30 @@ int tri_engine_submit(tri_engine* e, const double* q, int32_t k, int64_t* rid) {
   e->p_k.push_back(k);
   e->p_q.insert(e->p_q.end(), q, q + e->sv.d);
   if (rid) *rid = r;
+  return TRI_OK;
+}
+
+int tri_engine_submit_batch(tri_engine* e, const double* q, int32_t B, const int32_t* k, int64_t* rids) {
+  if (!e || (B > 0 && (!q || !k))) return set_error(TRI_EINVAL, "null argument");
+  const long long n = (long long)B * e->sv.d;
+  for (long long i = 0; i < n; ++i)
+    if (!std::isfinite(q[i])) return set_error(TRI_EINVAL, "query must be finite");
+  for (int i = 0; i < B; ++i)
+    if (!(1 <= k[i] && k[i] <= e->m)) return set_error(TRI_EINVAL, "k must be in [1, m=%d], got %d", e->m, k[i]);
+  for (int i = 0; i < B; ++i) {
+    const long long r = e->next_rid++;
+    e->p_rid.push_back(r);
+    e->p_k.push_back(k[i]);
+    if (rids) rids[i] = r;
+  }
+  e->p_q.insert(e->p_q.end(), q, q + n);
+  return TRI_OK;
+}
+
+int tri_engine_device_time(tri_engine* e, double* ms, int64_t* steps) {
+  if (!e) return set_error(TRI_EINVAL, "engine is NULL");
+  if (ms) *ms = e->dev_ms;
+  if (steps) *steps = e->dev_steps;
   return TRI_OK;
 }
 
@@ -632,15 +663,19 @@ int tri_engine_run(tri_engine* e, int32_t max_steps, int32_t until_idle, int32_t
     const int n = std::min({chunk, kMaxChunk, max_steps - done});
     ECU(cudaMemsetAsync(e->stats, 0, n * kStats * sizeof(int), e->st));
     EngineLaunch L = launch_of(e);
+    ECU(cudaEventRecord(e->ev0, e->st));
     for (int i = 0; i < n; ++i) {
       L.stats = e->stats + i * kStats;
       L.step = done + i;
       if (e->hw > 0) engine_step_kernel<<<e->hw, kEngThreads, 0, e->st>>>(L);
     }
     ECU(cudaGetLastError());
+    ECU(cudaEventRecord(e->ev1, e->st));
     ECU(cudaMemcpyAsync(e->h_stats, e->stats, n * kStats * sizeof(int), cudaMemcpyDeviceToHost, e->st));
     int rc = collect(e);  // synchronises
     if (rc) return rc;
+    float ms = 0.f;
+    ECU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
     int used = n;
     for (int i = 0; i < n; ++i) {
       const int* sti = e->h_stats + i * kStats;
@@ -656,6 +691,8 @@ int tri_engine_run(tri_engine* e, int32_t max_steps, int32_t until_idle, int32_t
       }
     }
     done += used;
+    e->dev_ms += ms * used / n;  // steps past idle are empty launches
+    e->dev_steps += used;
     if (until_idle && e->h_stats[(used - 1) * kStats + 2] == 0) break;
     chunk = std::min(kMaxChunk, chunk * 2);
   }

@@ -1,0 +1,117 @@
+"""Graph-engine benchmark: the reference's ``trinity bench-engine`` batch mode
+(cli.py:245-300) on the device-resident ContinuousBatchEngine.
+
+Workload: store ``gen_vectors(n, d, seed=1)``, exact kNN graph of degree 16
+(device build), ``nq`` queries ``gen_vectors(nq, d, seed=2)``, k=10, default
+EngineConfig (m=64, p=2, entry_count=8, C=512).  All queries are submitted,
+then ``run_to_completion`` -- the public API a user calls; the timed region
+includes query upload, every extend on the device and result read-back.
+
+Parity: results are compared with the CPU engine oracle (oracle.engine_run,
+pinned to the reference's acceptance run) on the first ``check`` queries.
+
+CPU baseline: the oracle engine over a bounded sample of the same queries
+(the reference engine is the same pure-Python state machine).
+
+usage: python tools/bench_engine.py [--n 100000] [--d 128] [--nq 4096] [--reps 5]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def run(n=100_000, d=128, nq=4096, reps=5, check=64, cpu_sample=32, degree=16):
+    from oracle import trinity_oracle as orc
+    from paper_2512_02281_b200.ann_graph import VectorStore, build_knn_graph
+    from paper_2512_02281_b200.engine import ContinuousBatchEngine, EngineConfig
+    from paper_2512_02281_b200.workload import gen_matrix
+
+    data = gen_matrix(n, d, 1)
+    queries = gen_matrix(nq, d, 2).astype(np.float64)
+    store = VectorStore(data=data)
+    t0 = time.perf_counter()
+    graph = build_knn_graph(store, degree)
+    t_graph = time.perf_counter() - t0
+    cfg = EngineConfig()
+
+    def one(batched):
+        eng = ContinuousBatchEngine(store, graph, cfg)
+        t0 = time.perf_counter()
+        if batched:
+            rids = eng.submit_many(queries, 10)
+        else:
+            rids = [eng.submit(q, k=10) for q in queries]
+        steps = eng.run_to_completion()
+        if batched:
+            out = eng.result_arrays(rids)
+            res = None
+        else:
+            res = [eng.result(r) for r in rids]
+        dt = time.perf_counter() - t0
+        dev_ms, dev_steps = eng.device_time()
+        eng.close()
+        return dt, steps, res, eng.stats, dev_ms
+
+    one(False)  # warm-up
+    times, devs, btimes = [], [], []
+    for _ in range(reps):
+        dt, steps, res, st, dev_ms = one(False)
+        times.append(dt)
+        devs.append(dev_ms)
+        btimes.append(one(True)[0])
+    dt = float(np.median(times))
+    bdt = float(np.median(btimes))
+    dev = float(np.median(devs)) / 1e3
+
+    ids, dd, ext, _, _ = orc.engine_run(data, graph.adjacency, queries[:check], np.full(check, 10),
+                                        np.zeros(check, np.int64))
+    # the oracle runs the first `check` queries alone; trajectories are per
+    # request, so each must match the batched device run exactly
+    ok = all([x.id for x in res[i].neighbors] == ids[i].tolist() and
+             [x.dist for x in res[i].neighbors] == dd[i].tolist() and res[i].extends == int(ext[i])
+             for i in range(check))
+
+    t0 = time.perf_counter()
+    orc.engine_run(data, graph.adjacency, queries[:cpu_sample], np.full(cpu_sample, 10), np.zeros(cpu_sample, np.int64))
+    cpu_dt = time.perf_counter() - t0
+
+    return {
+        "workload": f"graph engine (bench-engine batch mode): {n} x {d} fp32, degree-{degree} exact kNN graph, "
+                    f"{nq} queries k=10, EngineConfig defaults (m=64, p=2, E=8, C=512)",
+        "qps": nq / dev, "unit": "queries/s", "device_ms": dev * 1e3, "steps": steps,
+        "us_per_step": dev * 1e6 / max(steps, 1),
+        "e2e_qps": nq / dt, "e2e_note": "submit() per query + run_to_completion() + result() objects",
+        "e2e_batched_qps": nq / bdt, "e2e_batched_note": "submit_many() + run_to_completion() + result_arrays()",
+        "distance_evals": st.real_tasks, "batches": st.batches_launched,
+        "distance_evals_per_s": st.real_tasks / dev,
+        "parity": f"{'ok' if ok else 'MISMATCH'}: first {check} results == CPU engine oracle (ids, f64 dists, extends)",
+        "graph_build_s": t_graph,
+        "cpu_baseline": {"value": cpu_sample / cpu_dt, "unit": "queries/s", "cores": 1, "kind": "port",
+                         "sample": f"oracle engine over the first {cpu_sample} queries ({cpu_dt:.1f} s)"},
+        "timed": "qps: device time of the step launches (CUDA events); e2e: wall clock of the public API, "
+                 "host query upload and result read-back included; medians of reps",
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=100_000)
+    ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--nq", type=int, default=4096)
+    ap.add_argument("--reps", type=int, default=5)
+    a = ap.parse_args()
+    print(json.dumps(run(a.n, a.d, a.nq, a.reps)))
+
+
+if __name__ == "__main__":
+    main()
