@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=24, help="queries timed for cpu_baseline")
     ap.add_argument("--tc-stages", type=int, default=0, help="tensor-core scan ring depth cap (0 = deepest)")
     ap.add_argument("--scan-reserve", type=int, default=0, help="SMs the list scan leaves to other lanes")
-    ap.add_argument("--lanes", type=int, default=2,
+    ap.add_argument("--lanes", type=int, default=3,
                     help="independent batches in flight (one CUDA stream + library workspace each)")
     return ap.parse_args()
 

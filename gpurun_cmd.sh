@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_engine.py tests/test_gpu_engine_device.py -x -q --timeout 600 -p no:randomly > gpurun_out/eng_tests.log 2>&1; echo tests=$?; tail -3 gpurun_out/eng_tests.log
-timeout 600 python tools/bench_engine.py > gpurun_out/eng1.json 2>gpurun_out/eng1.err; echo e1=$?; cat gpurun_out/eng1.json; tail -3 gpurun_out/eng1.err
-timeout 600 python tools/bench_engine.py --n 20000 --d 768 --nq 1024 > gpurun_out/eng2.json 2>gpurun_out/eng2.err; echo e2=$?; cat gpurun_out/eng2.json; tail -3 gpurun_out/eng2.err
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:engine_step --launch-skip 20 -c 1 -o gpurun_out/eng_full -f python tools/bench_engine.py --reps 1 > gpurun_out/ncu_eng.log 2>&1; echo ncu=$?
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 600 -p no:randomly > gpurun_out/gpu_tests.log 2>&1; echo tests=$?; tail -3 gpurun_out/gpu_tests.log
+for cfg in "2 0" "3 0" "3 16" "3 24" "4 24" "4 32"; do set -- $cfg
+timeout 600 python bench.py --lanes $1 --scan-reserve $2 --steps 300 --cpu-sample 1 > gpurun_out/b_$1_$2.json 2>/dev/null; python -c "
+import json;d=json.load(open('gpurun_out/b_$1_$2.json'));r=d['roofline'];print('lanes=$1 reserve=$2', round(d['value']), round(d['e2e']['value']), round(d['ms_per_step'],4), round(r['frac'],3), round(r['scan_ms_per_launch'],4))"; done

@@ -62,8 +62,14 @@ struct DevBuf {
   }
 };
 
+// Bumped whenever a device scratch buffer moves or a cached plan is rewritten:
+// captured CUDA graphs bake in pointers and plan contents, so any bump retires them.
+long long g_epoch = 0;
+long long g_graphs = 1;  // capture repeated search shapes into CUDA graphs (option "graphs")
+
 int ensure(DevBuf& b, size_t bytes) {
   if (bytes <= b.cap && b.p) return TRI_OK;
+  ++g_epoch;
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
   b.cap = 0;
@@ -223,7 +229,45 @@ struct Workspace {
   int last_fixups = 0;
   int last_B = 0, last_npmax = 0, last_f16 = 0;
   std::vector<int> last_np;
+  // CUDA-graph capture of repeated search shapes (see graph_run)
+  bool capturing = false;
+  HostBuf* cap_host = nullptr;  // graph-owned pinned staging used while capturing
+  cudaEvent_t* cap_ph = nullptr;  // profiling placeholders recorded as graph event nodes
+  struct Graph {
+    int mode = 0, B = 0, ldo = 0;
+    std::vector<int> k, np;
+    const void *q = nullptr, *ids = nullptr, *dists = nullptr;
+    bool prof = false;
+    long long opts = 0, epoch = -1;
+    int state = 0;  // 1 seen once (next call captures), 2 graph ready, 3 capture failed (stay eager)
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    HostBuf host;
+    cudaEvent_t ph[7] = {};
+    cudaGraphNode_t evnode[7] = {};
+    unsigned long long used = 0;
+    int last_B = 0, last_npmax = 0, last_f16 = 0;
+    std::vector<int> last_np;
+    void destroy() {
+      if (exec) cudaGraphExecDestroy(exec);
+      exec = nullptr;
+      if (graph) cudaGraphDestroy(graph);
+      graph = nullptr;
+      if (host.p) cudaFreeHost(host.p);
+      host.p = nullptr;
+      host.cap = 0;
+      for (auto& e : ph)
+        if (e) {
+          cudaEventDestroy(e);
+          e = nullptr;
+        }
+    }
+  };
+  std::vector<Graph> graphs;
+  unsigned long long graph_clock = 0;
   void free_all() {
+    for (auto& g : graphs) g.destroy();
+    graphs.clear();
     for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat,
                       &probes, &probe_d, &counts, &fill, &mbase, &items, &members, &counters, &meta, &Qh, &qinv})
       release(*b);
@@ -244,6 +288,12 @@ struct Workspace {
 // whose previous upload has completed (host waits only if the device is
 // kStaging uploads behind).  Call staged_upload() after filling it.
 int stage_host(Workspace& w, size_t bytes, int* slot, void** ptr) {
+  if (w.capturing) {  // the graph replays this upload: it gets its own buffer
+    if (!w.cap_host || w.cap_host->cap < bytes) return fail(TRI_EINTERNAL, "graph staging buffer too small");
+    *slot = -1;
+    *ptr = w.cap_host->p;
+    return TRI_OK;
+  }
   const int i = w.stage_i;
   w.stage_i = (w.stage_i + 1) % Workspace::kStaging;
   if (w.staged_live[i]) CU(cudaEventSynchronize(w.staged[i]));
@@ -255,6 +305,10 @@ int stage_host(Workspace& w, size_t bytes, int* slot, void** ptr) {
 }
 
 int staged_upload(Workspace& w, int slot, void* dst, size_t bytes, cudaStream_t st) {
+  if (slot < 0) {
+    CU(cudaMemcpyAsync(dst, w.cap_host->p, bytes, cudaMemcpyHostToDevice, st));
+    return TRI_OK;
+  }
   CU(cudaMemcpyAsync(dst, w.h_stage[slot].p, bytes, cudaMemcpyHostToDevice, st));
   if (!w.staged[slot]) CU(cudaEventCreateWithFlags(&w.staged[slot], cudaEventDisableTiming));
   CU(cudaEventRecord(w.staged[slot], st));
@@ -293,6 +347,7 @@ struct Lanes {
 };
 
 int lane_done(Workspace& w, cudaStream_t st) {
+  if (w.capturing) return TRI_OK;  // recorded after the graph launch instead
   if (!w.done) CU(cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming));
   CU(cudaEventRecord(w.done, st));
   w.done_live = true;
@@ -446,6 +501,8 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
   if (w.plan_B == B && w.plan_n == s->n && w.plan_opts == plan_opts() && (int)w.plan_k.size() == B &&
       std::equal(w.plan_k.begin(), w.plan_k.end(), k))
     return TRI_OK;
+  if (w.capturing) return fail(TRI_EINTERNAL, "re-plan during graph capture");
+  ++g_epoch;  // graphs captured against the old plan read its device copy
   // Dense path for small stores: the whole B x n distance matrix is cheap.
   {
     int kpd = kMinKp, kmx = 1;
@@ -777,6 +834,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "dense_off")) g_dense_off = value;
   else if (!std::strcmp(name, "tc_stages")) g_tc_stages = value;
   else if (!std::strcmp(name, "scan_reserve")) g_scan_reserve = value;
+  else if (!std::strcmp(name, "graphs")) g_graphs = value;
   else if (!std::strcmp(name, "tc_box_rows")) {
     if (value != 32 && value != 64 && value != 128) return fail(TRI_EINVAL, "tc_box_rows must be 32, 64 or 128");
     g_box_rows = value;
@@ -1185,8 +1243,7 @@ int tri_ivf_list_sizes(tri_ivf* v, int64_t* sizes) {
   return TRI_OK;
 }
 
-static int ivf_search_enqueue(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe,
-                              int32_t ldo, int64_t* ids, double* dists, void* stream) {
+static int ivf_validate(tri_ivf* v, int32_t B, const int32_t* k, const int32_t* nprobe, int32_t ldo) {
   if (!v) return fail(TRI_EINVAL, "index is NULL");
   if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
   if (B == 0) return TRI_OK;
@@ -1194,18 +1251,21 @@ static int ivf_search_enqueue(tri_ivf* v, const double* q, int32_t B, const int3
   TRY(validate_k(nprobe, B, v->nlist, "nprobe"));
   int km = *std::max_element(k, k + B);
   if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
-  DeviceGuard g(v->device);
-  cudaStream_t st = pick(stream, v->own);
-  Workspace* wp = nullptr;
-  Workspace* cw = nullptr;
-  TRY(v->lanes.get(st, &wp));
-  TRY(v->cstore->lanes.get(st, &cw));
-  Workspace& w = *wp;
+  return TRI_OK;
+}
+
+// Enqueue one whole search on `st` (lane workspaces w / cw already chosen).
+static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double* q, int32_t B, const int32_t* k,
+                           const int32_t* nprobe, int32_t ldo, int64_t* ids, double* dists, cudaStream_t st) {
   const int npmax = *std::max_element(nprobe, nprobe + B);
   TRY(ensure_query_bufs(w, B, v->d, v->qld));
   const bool rec = v->prof && v->ev_used < kProfSearches;
   auto mark = [&](int j) -> int {
     if (!rec) return TRI_OK;
+    if (w.capturing) {  // event node; the launch points it at the profiling ring
+      CU(cudaEventRecordWithFlags(w.cap_ph[j], st, cudaEventRecordExternal));
+      return TRI_OK;
+    }
     while ((int)v->ev.size() < 7 * (v->ev_used + 1)) {
       cudaEvent_t e;
       CU(cudaEventCreate(&e));
@@ -1214,7 +1274,22 @@ static int ivf_search_enqueue(tri_ivf* v, const double* q, int32_t B, const int3
     CU(cudaEventRecord(v->ev[7 * v->ev_used + j], st));
     return TRI_OK;
   };
-  TRY(prep_queries(w, q, B, v->d, v->qld, st));
+  // per-query plan (k, kp) and scan arithmetic: fp16 tensor-core scan when the
+  // index holds the fp16 copy (scan_kernel 2 forces TF32)
+  std::vector<int> kp;
+  ScanChoice ch;
+  TRY(choose_scan(v->qld, v->d, B, k, kp, ch, false));
+  const int kp_max = ch.kp_max, k_max = ch.k_max;
+  const bool f16 = ch.tc && v->Xh && g_scan_kernel != 2;
+  // 0. queries: fp32 rows + norms (+ the fp16 scan copy) in one kernel
+  if (f16) {
+    TRY(ensure(w.Qh, (size_t)B * v->dph * 2));
+    TRY(ensure(w.qinv, (size_t)B * sizeof(float)));
+    CU(launch_prep(q, B, v->d, w.Q32.as<float>(), v->qld, w.qn32.as<float>(), w.qn64.as<double>(), nullptr, st,
+                   v->sx, w.Qh.p, v->dph, w.qinv.as<float>()));
+  } else {
+    TRY(prep_queries(w, q, B, v->d, v->qld, st));
+  }
   TRY(mark(0));
 
   // 1. coarse step: exact top-nprobe centroids per query
@@ -1223,18 +1298,7 @@ static int ivf_search_enqueue(tri_ivf* v, const double* q, int32_t B, const int3
   TRY(bruteforce_core(v->cstore, *cw, w, q, B, nprobe, npmax, w.probes.as<long long>(), w.probe_d.as<double>(),
                       st));
 
-  // 2. host-side per-query plan (k, kp, slots) -> device
-  std::vector<int> kp;
-  ScanChoice ch;
-  TRY(choose_scan(v->qld, v->d, B, k, kp, ch, false));
-  const int kp_max = ch.kp_max, k_max = ch.k_max;
-  // fp16 tensor-core scan when the index holds the fp16 copy (scan_kernel 2 forces TF32)
-  const bool f16 = ch.tc && v->Xh && g_scan_kernel != 2;
-  if (f16) {
-    TRY(ensure(w.Qh, (size_t)B * v->dph * 2));
-    TRY(ensure(w.qinv, (size_t)B * sizeof(float)));
-    CU(launch_prep_half(w.Q32.as<float>(), B, v->qld, v->d, v->sx, w.Qh.p, v->dph, w.qinv.as<float>(), st));
-  }
+  // 2. per-query plan -> device
   long long part_keys = 0, members = 0;
   const size_t meta_bytes = (size_t)B * (sizeof(QueryMeta) + sizeof(int));
   int slot = 0;
@@ -1382,26 +1446,177 @@ static int ivf_search_enqueue(tri_ivf* v, const double* q, int32_t B, const int3
   fx.k_max = k_max;
   CU(launch_fixup(fx, st));
   TRY(mark(6));
-  if (rec) v->ev_used++;
+  if (rec && !w.capturing) v->ev_used++;
   w.last_B = B;
   w.last_npmax = npmax;
   w.last_f16 = f16 ? 1 : 0;
   w.last_np.assign(nprobe, nprobe + B);
-  TRY(lane_done(*cw, st));
-  return lane_done(w, st);
+  return TRI_OK;
 }
+
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+long long graph_opts() {
+  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 +
+         g_scan_debug * 100003;
+}
+
+// Runs `body` (which enqueues one whole search on st) through the lane's CUDA
+// graph cache.  A shape (mode, B, k[], nprobe[], ldo, buffers, options) seen
+// once runs eagerly; the second time it is captured, instantiated and from
+// then on replayed with one cudaGraphLaunch -- no host planning, no per-kernel
+// launch latency.  Graph-owned pinned staging holds the uploaded plan, so
+// replays never read a buffer another shape may overwrite; any scratch
+// reallocation or plan rewrite (g_epoch) retires the graph.
+}  // extern "C"
+
+template <class Body>
+static int graph_run(tri_ivf* v, Workspace& w, Workspace& cw, cudaStream_t st, int mode, int B, const int* k,
+                     const int* np, int ldo, const void* q, const void* ids, const void* dists, Body&& body) {
+  if (!g_graphs) return body();
+  const bool prof = v->prof && v->ev_used < kProfSearches;
+  const long long opts = graph_opts();
+  Workspace::Graph* e = nullptr;
+  for (auto& gr : w.graphs)
+    if (gr.mode == mode && gr.B == B && gr.ldo == ldo && gr.q == q && gr.ids == ids && gr.dists == dists &&
+        gr.prof == prof && gr.opts == opts && std::equal(gr.k.begin(), gr.k.end(), k) &&
+        std::equal(gr.np.begin(), gr.np.end(), np)) {
+      e = &gr;
+      break;
+    }
+  if (!e) {
+    if (w.graphs.size() >= 8) {  // evict the least recently used shape
+      auto lru = std::min_element(w.graphs.begin(), w.graphs.end(),
+                                  [](const Workspace::Graph& a, const Workspace::Graph& b) { return a.used < b.used; });
+      lru->destroy();
+      w.graphs.erase(lru);
+    }
+    w.graphs.emplace_back();
+    e = &w.graphs.back();
+    e->mode = mode;
+    e->B = B;
+    e->ldo = ldo;
+    e->k.assign(k, k + B);
+    e->np.assign(np, np + B);
+    e->q = q;
+    e->ids = ids;
+    e->dists = dists;
+    e->prof = prof;
+    e->opts = opts;
+  }
+  e->used = ++w.graph_clock;
+  if (e->state == 2 && e->epoch != g_epoch) {  // scratch moved or plan rewritten since capture
+    e->destroy();
+    e->state = 0;
+  }
+  if (e->state == 0 || e->state == 3 || (e->state == 1 && e->epoch != g_epoch)) {
+    const int rc = body();
+    if (e->state != 3) {
+      e->state = 1;
+      e->epoch = g_epoch;
+    }
+    return rc;
+  }
+  if (e->state == 1) {
+    // capture the second sighting of this shape
+    TRY(ensure_host(e->host, (size_t)B * (sizeof(QueryMeta) + sizeof(int)) + 64));
+    if (prof)
+      for (auto& ev : e->ph)
+        if (!ev) CU(cudaEventCreate(&ev));
+    const long long ep0 = g_epoch;
+    w.capturing = cw.capturing = true;
+    w.cap_host = &e->host;
+    w.cap_ph = e->ph;
+    cudaGraph_t gr = nullptr;
+    cudaError_t ce = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed);
+    int rc = ce == cudaSuccess ? body() : TRI_ECUDA;
+    if (ce == cudaSuccess) ce = cudaStreamEndCapture(st, &gr);
+    w.capturing = cw.capturing = false;
+    w.cap_host = nullptr;
+    w.cap_ph = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    if (rc == TRI_OK && ce == cudaSuccess && g_epoch == ep0) ce = cudaGraphInstantiate(&ex, gr, 0);
+    if (rc != TRI_OK || ce != cudaSuccess || g_epoch != ep0 || !ex) {
+      cudaGetLastError();
+      if (gr) cudaGraphDestroy(gr);
+      if (ex) cudaGraphExecDestroy(ex);
+      e->state = (g_epoch != ep0 && rc == TRI_OK && ce == cudaSuccess) ? 1 : 3;
+      e->epoch = g_epoch;
+      return body();  // not capturable: stay eager
+    }
+    if (prof) {
+      size_t nn = 0;
+      cudaGraphGetNodes(gr, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      cudaGraphGetNodes(gr, nodes.data(), &nn);
+      for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t evx = nullptr;
+        cudaGraphEventRecordNodeGetEvent(nd, &evx);
+        for (int j = 0; j < 7; ++j)
+          if (evx == e->ph[j]) e->evnode[j] = nd;
+      }
+    }
+    // node handles stay valid for exec updates only while the graph lives; keep it
+    // alive by instantiating from it and destroying it with the entry
+    e->exec = ex;
+    e->state = 2;
+    e->epoch = g_epoch;
+    e->last_B = w.last_B;
+    e->last_npmax = w.last_npmax;
+    e->last_f16 = w.last_f16;
+    e->last_np = w.last_np;
+    e->graph = gr;
+  }
+  // replay
+  w.last_B = e->last_B;
+  w.last_npmax = e->last_npmax;
+  w.last_f16 = e->last_f16;
+  w.last_np = e->last_np;
+  if (prof) {
+    while ((int)v->ev.size() < 7 * (v->ev_used + 1)) {
+      cudaEvent_t ev;
+      CU(cudaEventCreate(&ev));
+      v->ev.push_back(ev);
+    }
+    for (int j = 0; j < 7; ++j)
+      CU(cudaGraphExecEventRecordNodeSetEvent(e->exec, e->evnode[j], v->ev[7 * v->ev_used + j]));
+  }
+  CU(cudaGraphLaunch(e->exec, st));
+  if (prof) v->ev_used++;
+  return TRI_OK;
+}
+
+extern "C" {
 
 int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe,
                        int32_t ldo, int64_t* ids, double* dists, void* stream) {
-  if (!v) return fail(TRI_EINVAL, "index is NULL");
+  TRY(ivf_validate(v, B, k, nprobe, ldo));
+  if (B == 0) return TRI_OK;
   std::lock_guard<std::mutex> lk(v->mu);
-  return ivf_search_enqueue(v, q, B, k, nprobe, ldo, ids, dists, stream);
+  DeviceGuard g(v->device);
+  cudaStream_t st = pick(stream, v->own);
+  Workspace* wp = nullptr;
+  Workspace* cw = nullptr;
+  TRY(v->lanes.get(st, &wp));
+  TRY(v->cstore->lanes.get(st, &cw));
+  TRY(graph_run(v, *wp, *cw, st, 0, B, k, nprobe, ldo, q, ids, dists,
+                [&] { return ivf_search_body(v, *wp, cw, q, B, k, nprobe, ldo, ids, dists, st); }));
+  TRY(lane_done(*cw, st));
+  return lane_done(*wp, st);
 }
 
 int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe, int32_t ldo,
                    int64_t* ids, double* dists, void* stream) {
-  if (!v) return fail(TRI_EINVAL, "index is NULL");
-  if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
+  TRY(ivf_validate(v, B, k, nprobe, ldo));
   if (B == 0) return TRI_OK;
   TRY(check_queries(q, (long long)B * v->d));
   DeviceGuard g(v->device);
@@ -1409,19 +1624,29 @@ int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, con
   {
     std::lock_guard<std::mutex> lk(v->mu);
     Workspace* wp = nullptr;
+    Workspace* cw = nullptr;
     TRY(v->lanes.get(st, &wp));
+    TRY(v->cstore->lanes.get(st, &cw));
     Workspace& w = *wp;
-    int km = 0;
-    for (int i = 0; i < B; ++i) km = std::max(km, k[i]);
-    if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
     TRY(ensure(w.q64, (size_t)B * v->d * sizeof(double)));
     TRY(ensure(w.out_ids, (size_t)B * ldo * sizeof(long long)));
     TRY(ensure(w.out_d, (size_t)B * ldo * sizeof(double)));
-    CU(cudaMemcpyAsync(w.q64.p, q, (size_t)B * v->d * sizeof(double), cudaMemcpyHostToDevice, st));
-    TRY(ivf_search_enqueue(v, w.q64.as<double>(), B, k, nprobe, ldo, reinterpret_cast<int64_t*>(w.out_ids.p),
-                           w.out_d.as<double>(), st));
-    CU(cudaMemcpyAsync(ids, w.out_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(dists, w.out_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+    auto body = [&]() -> int {
+      CU(cudaMemcpyAsync(w.q64.p, q, (size_t)B * v->d * sizeof(double), cudaMemcpyHostToDevice, st));
+      TRY(ivf_search_body(v, w, cw, w.q64.as<double>(), B, k, nprobe, ldo, reinterpret_cast<int64_t*>(w.out_ids.p),
+                          w.out_d.as<double>(), st));
+      CU(cudaMemcpyAsync(ids, w.out_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
+      CU(cudaMemcpyAsync(dists, w.out_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+      return TRI_OK;
+    };
+    // graph replay needs pinned host buffers (pageable copies cannot be captured)
+    if (host_pinned(q) && host_pinned(ids) && host_pinned(dists)) {
+      TRY(graph_run(v, w, *cw, st, 1, B, k, nprobe, ldo, q, ids, dists, body));
+    } else {
+      TRY(body());
+    }
+    TRY(lane_done(*cw, st));
+    TRY(lane_done(w, st));
   }
   CU(cudaStreamSynchronize(st));
   return TRI_OK;

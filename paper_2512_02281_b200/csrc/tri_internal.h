@@ -83,8 +83,11 @@ size_t tc_scan_smem_bytes(int row_bytes);  // minimum (kTcMinStages ring); row_b
 int tc_scan_stages(int row_bytes, int smem_limit, int want);  // deepest ring that fits (want > 0 caps it)
 cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st);
 
+// fp64 queries -> fp32 rows + norms; with Qh != nullptr also the fp16 scan
+// copy (scale sx of the index's fp16 rows) in the same kernel.
 cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,
-                        int* bad, cudaStream_t st);
+                        int* bad, cudaStream_t st, float sx = 1.f, void* Qh = nullptr, int ldh = 0,
+                        float* qinv = nullptr);
 cudaError_t launch_absmax(const float* X, long long n, int d, long long ldx, unsigned int* bits, cudaStream_t st);
 cudaError_t launch_to_half(const float* X, long long n, int d, long long ldx, float sx, void* Xh, int ldh,
                            cudaStream_t st);
@@ -97,7 +100,7 @@ cudaError_t launch_norms(const float* X, long long n, int d, long long ldx, floa
 // then per-query top-kp (kp <= kDenseMaxKp) straight into `merged`.
 constexpr long long kDenseMaxN = 4096;
 constexpr int kDenseMaxKp = 256;
-constexpr int kDenseSlices = 2;  // split-K slices of the distance GEMM (D holds kDenseSlices x B x ldd partials)
+constexpr int kDenseSlices = 8;  // split-K slices of the distance GEMM (D holds kDenseSlices x B x ldd partials)
 cudaError_t launch_dense(const float* Q, int qld, const float* qn, int B, const float* X, long long ldx,
                          const float* xn, long long n, int dp, float* D, long long ldd, const QueryMeta* meta,
                          unsigned long long* merged, int ld_merged, int kp_max, cudaStream_t st);

@@ -23,47 +23,89 @@ constexpr int kThreads = 256;
 // ---------------------------------------------------------------------------
 // Query preparation and row norms.
 
-__global__ void prep_kernel(const double* __restrict__ q64, int d, float* __restrict__ Q32, int qld,
-                            float* __restrict__ qn32, double* __restrict__ qn64, int* bad) {
-  const int q = blockIdx.x;
-  double s32 = 0.0, s64 = 0.0;
-  bool finite = true;
-  for (int j = threadIdx.x; j < qld; j += blockDim.x) {
-    double v = j < d ? q64[(long long)q * d + j] : 0.0;
-    finite = finite && isfinite(v);
-    float f = __double2float_rn(v);
-    Q32[(long long)q * qld + j] = f;
-    s32 += (double)f * (double)f;
-    s64 += v * v;
+// One CTA (128 threads) per query; every element load is issued before any
+// store (<= 16 per thread, qld <= 2048), then: fp32 row + |q32|^2 (fp32 of an
+// fp64 sum), |q64| (fp64), and -- when Qh != nullptr -- the fp16 scan copy
+// (see prep_half_kernel) in the same pass.
+constexpr int kPrepThreads = 128, kPrepMaxU = 16;
+
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double* __restrict__ q64, int d,
+                                                            float* __restrict__ Q32, int qld, float* __restrict__ qn32,
+                                                            double* __restrict__ qn64, int* bad, float sx,
+                                                            __half* __restrict__ Qh, int ldh,
+                                                            float* __restrict__ qinv) {
+  const int q = blockIdx.x, tid = threadIdx.x;
+  double v[kPrepMaxU];
+#pragma unroll
+  for (int u = 0; u < kPrepMaxU; ++u) {
+    const int j = tid + u * kPrepThreads;
+    v[u] = j < d ? q64[(long long)q * d + j] : 0.0;
   }
-  __shared__ double r32[32], r64[32];
+  double s32 = 0.0, s64 = 0.0;
+  float m = 0.f;
+  bool finite = true;
+  float f[kPrepMaxU];
+#pragma unroll
+  for (int u = 0; u < kPrepMaxU; ++u) {
+    const int j = tid + u * kPrepThreads;
+    finite = finite && isfinite(v[u]);
+    f[u] = __double2float_rn(v[u]);
+    if (j < qld) Q32[(long long)q * qld + j] = f[u];
+    s32 += (double)f[u] * (double)f[u];
+    s64 += v[u] * v[u];
+    m = fmaxf(m, fabsf(f[u]));
+  }
+  __shared__ double r32[kPrepThreads / 32], r64[kPrepThreads / 32];
+  __shared__ float rm[kPrepThreads / 32];
   for (int o = 16; o > 0; o >>= 1) {
     s32 += __shfl_xor_sync(0xffffffffu, s32, o);
     s64 += __shfl_xor_sync(0xffffffffu, s64, o);
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   }
-  int nf = __syncthreads_or(!finite);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nf = __syncthreads_or(!finite);
+  const int lane = tid & 31, warp = tid >> 5;
   if (lane == 0) {
     r32[warp] = s32;
     r64[warp] = s64;
+    rm[warp] = m;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      a += r32[w];
-      b += r64[w];
-    }
+  double a = 0.0, b = 0.0;
+  m = 0.f;
+#pragma unroll
+  for (int w = 0; w < kPrepThreads / 32; ++w) {
+    a += r32[w];
+    b += r64[w];
+    m = fmaxf(m, rm[w]);
+  }
+  if (tid == 0) {
     qn32[q] = __double2float_rn(a);
     qn64[q] = sqrt(b);
     if (nf && bad) atomicExch(bad, 1);
   }
+  if (Qh) {
+    bool badh = false;
+    float sq = 1.f;
+    if (m > 0.f) {
+      const int e = ilogbf(m);
+      badh = e < -60 || e > 60;
+      sq = badh ? 0.f : ldexpf(1.f, 14 - e);
+    }
+#pragma unroll
+    for (int u = 0; u < kPrepMaxU; ++u) {
+      const int j = tid + u * kPrepThreads;
+      if (j < ldh) Qh[(long long)q * ldh + j] = __float2half_rn(j < d ? f[u] * sq : 0.f);
+    }
+    if (tid == 0) qinv[q] = badh ? -1.f : 1.f / (sq * sx);
+  }
 }
 
 cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,
-                        int* bad, cudaStream_t st) {
+                        int* bad, cudaStream_t st, float sx, void* Qh, int ldh, float* qinv) {
   if (B <= 0) return cudaSuccess;
-  prep_kernel<<<B, 128, 0, st>>>(q64, d, Q32, qld, qn32, qn64, bad);
+  if (qld > kPrepThreads * kPrepMaxU || (Qh && ldh > kPrepThreads * kPrepMaxU)) return cudaErrorInvalidValue;
+  prep_kernel<<<B, kPrepThreads, 0, st>>>(q64, d, Q32, qld, qn32, qn64, bad, sx, static_cast<__half*>(Qh), ldh,
+                                          qinv);
   return cudaGetLastError();
 }
 
@@ -557,6 +599,25 @@ __global__ void __launch_bounds__(128) finalize_kernel(RerankLaunch r) {
 
 // One 1-D bulk copy per candidate row per slab, issued by the candidate's own
 // pair-leader thread (all rows in flight at once, no per-16B address math).
+// Stage an fp64 query row (zero-padded to dpad) in shared memory with every
+// global load issued before the first store: a strided load/store loop would
+// pay one memory latency per iteration.
+constexpr int kStageMaxU = 32;
+__device__ __forceinline__ void stage_query(const double* __restrict__ qg, int d, int dpad, double* qs, int tid, int nthr) {
+  for (int base = 0; base < dpad; base += kStageMaxU * nthr) {
+    double v[kStageMaxU];
+#pragma unroll
+    for (int u = 0; u < kStageMaxU; ++u) {
+      const int j = base + tid + u * nthr;
+      v[u] = j < d ? qg[j] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kStageMaxU; ++u) {
+      const int j = base + tid + u * nthr;
+      if (j < dpad) qs[j] = v[u];
+    }
+  }
+}
 __device__ __forceinline__ void rf_issue(float* buf, uint64_t* bar, int S, int c, long long pos, const float* X,
                                          long long ldx, int s0, int dpad, int nvalid, bool leader) {
   const int w = min(S, dpad - s0);
@@ -607,8 +668,7 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bars[1]))));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  const double* qg = r.q64 + (long long)q * d;
-  for (int j = tid; j < dpad; j += nthr) qs[j] = j < d ? qg[j] : 0.0;
+  stage_query(r.q64 + (long long)q * d, d, dpad, qs, tid, nthr);
   const int nvalid = __syncthreads_count(leader && active);
   const int nslab = (dpad + S - 1) / S;
   const int buf_floats = kpm * (S + 4);

@@ -228,3 +228,41 @@ def test_ivf_scaled_data_and_extreme_queries(scale):
         oi, od = orc.ivf_search(data, art, q, k, npb)
         assert np.array_equal(ids[i, : oi.size], oi), i
         assert np.array_equal(d[i, : od.size], od), i
+
+
+def test_ivf_graph_replay_tracks_inputs(small):
+    """Repeated shapes run eagerly, then captured, then replayed as CUDA graphs:
+    every call must see the CURRENT query contents (device and pinned-host
+    paths), and a new shape or a scratch reallocation must not replay a stale
+    graph."""
+    import torch
+
+    g, data, idx = small
+    art = orc.IVFArtifact(g["centroids"], g["assign"])
+    ks = np.array([10, 100] * 8)
+    nps = np.array([4, 16] * 8)
+    q_dev = torch.empty((16, 32), dtype=torch.float64, device="cuda")
+    ids_dev = torch.empty((16, 100), dtype=torch.int64, device="cuda")
+    d_dev = torch.empty((16, 100), dtype=torch.float64, device="cuda")
+    q_pin = torch.empty((16, 32), dtype=torch.float64).pin_memory()
+    ids_pin = torch.empty((16, 100), dtype=torch.int64).pin_memory()
+    d_pin = torch.empty((16, 100), dtype=torch.float64).pin_memory()
+    st = torch.cuda.Stream()
+    for rep in range(5):
+        qs = gen_matrix(16, 32, 100 + rep).astype(np.float64)
+        q_dev.copy_(torch.from_numpy(qs))
+        q_pin.copy_(torch.from_numpy(qs))
+        torch.cuda.synchronize()
+        idx.search_device(q_dev, ks, nps, ids_dev, d_dev, st)
+        st.synchronize()
+        idx.search_into(q_pin, ks, nps, ids_pin, d_pin, stream=st)
+        for out_ids, out_d in ((ids_dev.cpu().numpy(), d_dev.cpu().numpy()), (ids_pin.numpy(), d_pin.numpy())):
+            for i in range(16):
+                oi, od = orc.ivf_search(data, art, qs[i], int(ks[i]), int(nps[i]))
+                assert np.array_equal(out_ids[i, :oi.size], oi), (rep, i)
+                assert np.array_equal(out_d[i, :oi.size], od), (rep, i)
+        if rep == 2:  # a different, larger shape on the same lane reallocates scratch
+            big = gen_matrix(64, 32, 9).astype(np.float64)
+            bi, bd = idx.search(big, 100, 32)
+            oi, od = orc.ivf_search(data, art, big[5], 100, 32)
+            assert np.array_equal(bi[5, :oi.size], oi)
