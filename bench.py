@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=24, help="queries timed for cpu_baseline")
     ap.add_argument("--tc-stages", type=int, default=0, help="tensor-core scan ring depth cap (0 = deepest)")
     ap.add_argument("--scan-reserve", type=int, default=0, help="SMs the list scan leaves to other lanes")
+    ap.add_argument("--no-configs", action="store_true", help="skip the secondary-config measurements (C1/C3/C5/engine)")
     ap.add_argument("--lanes", type=int, default=3,
                     help="independent batches in flight (one CUDA stream + library workspace each)")
     return ap.parse_args()
@@ -343,9 +344,13 @@ def run_ours(args):
     if dist:
         dist.barrier()
 
+    call_ms = [[] for _ in range(L)]
+
     def lane_loop(j, n):
         for _ in range(n):
+            t = time.perf_counter()
             idx.search_into(q_pin, K, NPROBE, *pins[j], stream=lanes[j])
+            call_ms[j].append((time.perf_counter() - t) * 1e3)
 
     t0 = time.perf_counter()
     if L > 1:
@@ -355,6 +360,7 @@ def run_ours(args):
         for th in ths:
             th.join()
     for _ in range(args.steps if L == 1 else 0):
+        t = time.perf_counter()
         idx.search_into(q_pin, K, NPROBE, ids_pin, d_pin, stream=stream)
         if world > 1:
             ids_dev.copy_(ids_pin, non_blocking=False)
@@ -364,6 +370,7 @@ def run_ours(args):
             merge_topk_device(g_d, g_ids, K, m_d, m_ids, stream)
             ids_pin.copy_(m_ids)
             d_pin.copy_(m_d)
+        call_ms[0].append((time.perf_counter() - t) * 1e3)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist:
@@ -378,6 +385,18 @@ def run_ours(args):
         return
 
     cpu_qps, cpu_dt = cpu_baseline_qps(data, art, queries, args.cpu_sample)
+    lat = np.concatenate([np.asarray(c) for c in call_ms if c]) if any(call_ms) else np.zeros(1)
+    configs = {}
+    if world == 1 and not args.no_configs:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_configs as bc
+
+        for name, fn in (("C1", lambda: bc.c1(peak_gbs=load_peaks()[0])), ("C3", lambda: bc.c3(idx, data, art)),
+                         ("C5", lambda: bc.c5(idx)), ("engine", bc.engine)):
+            try:
+                configs[name] = fn()
+            except Exception as exc:  # reported, never silently dropped
+                configs[name] = {"error": f"{type(exc).__name__}: {exc}"}
     peak, peak_kind = load_peaks()
     avg_scan_ms = scan_ms / max(scan_n, 1)
     achieved = scan_bytes / (avg_scan_ms / 1e3) / 1e9
@@ -398,10 +417,15 @@ def run_ours(args):
                          "sample": f"first {args.cpu_sample} of the 256 C2 queries through the numpy oracle "
                                    f"({cpu_dt:.1f} s, 1 core)"},
         "e2e": {"value": e2e_qps, "unit": UNIT, "h2d_bytes_per_step": BATCH * DIM * 8,
-                "d2h_bytes_per_step": BATCH * K * 16},
+                "d2h_bytes_per_step": BATCH * K * 16,
+                "batch_latency_ms": {"p50": float(np.percentile(lat, 50)), "p95": float(np.percentile(lat, 95)),
+                                     "p99": float(np.percentile(lat, 99)),
+                                     "what": f"wall time of one blocking search_into call (256 queries), {L} host "
+                                             f"threads / lanes in flight"}},
         "gpu_launches": kernels_per_step * args.steps,
         "clocks": sampler.summary(),
         "host_cores": os.cpu_count(),
+        "configs": configs,
     }
     print(json.dumps(line), flush=True)
     if dist:

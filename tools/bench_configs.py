@@ -1,0 +1,190 @@
+"""Secondary BASELINE.json configurations, measured briefly beside the C2 headline.
+
+bench.py (N=1, rank 0) calls these after its timed region and reports them
+under "configs" in its JSON line; each is a bounded run (seconds), on the GPU
+through the package's public API, with a parity spot-check against the CPU
+oracle or the reference-generated golden vectors.
+
+* c1  brute-force exact kNN, 100K x 128 fp32, B=64, k=10 (BASELINE config 1)
+* c3  continuous batching of heterogeneous retrievals over the C2 index:
+      prefill (k=100, nprobe=64) and decode (k=10, nprobe=16) probes of a
+      ``gen_trace`` workload, ragged batches of 256 in arrival order
+* c5  stage-aware scheduled trace (RAG retrievals + prompt-cache lookups),
+      TwoQueueScheduler with the reference policy and with decode priority
+* engine  graph search engine (tools/bench_engine.py)
+"""
+
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _pct(a):
+    a = np.asarray(a, dtype=np.float64)
+    return {"p50_ms": float(np.percentile(a, 50)), "p95_ms": float(np.percentile(a, 95)),
+            "p99_ms": float(np.percentile(a, 99))}
+
+
+def c1(steps: int = 200, peak_gbs: float | None = None) -> dict:
+    """Brute force 100K x 128, 64 queries, k=10: device-resident batches on one stream."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2512_02281_b200 import _lib
+    from paper_2512_02281_b200.ann_graph import _DeviceStore
+    from paper_2512_02281_b200.workload import gen_matrix
+
+    g = np.load(os.path.join(ROOT, "tests", "golden", "bf_c1.npz"))
+    data = gen_matrix(100_000, 128, 1)
+    qs = gen_matrix(64, 128, 2).astype(np.float64)
+    store = _DeviceStore(data)
+    lib = _lib.gpu()
+    q = torch.from_numpy(qs).cuda()
+    ks = np.full(64, 10, np.int32)
+    ids = torch.empty((64, 10), dtype=torch.int64, device="cuda")
+    d = torch.empty((64, 10), dtype=torch.float64, device="cuda")
+    st = torch.cuda.Stream()
+
+    def one():
+        _lib.check(lib.tri_knn_bruteforce_dev(store.handle, _lib.ptr(q), 64, ks.ctypes.data, 10, _lib.ptr(ids),
+                                              _lib.ptr(d), C.c_void_p(st.cuda_stream)))
+
+    for _ in range(5):
+        one()
+    st.synchronize()
+    ok = np.array_equal(ids.cpu().numpy(), g["ids"]) and np.array_equal(d.cpu().numpy(), g["dists"])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        one()
+    e1.record(st)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    # e2e: host queries in, host results out, through the public batch API
+    from paper_2512_02281_b200.ann_graph import VectorStore, brute_force_knn_batch
+
+    vs = VectorStore(data=data)
+    brute_force_knn_batch(vs, qs, 10)
+    t0 = time.perf_counter()
+    n_e2e = 50
+    for _ in range(n_e2e):
+        brute_force_knn_batch(vs, qs, 10)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
+    bytes_per_batch = 100_000 * (128 * 4 + 4)
+    out = {
+        "workload": "C1: brute-force exact kNN, gen_vectors(100000,128,seed=1), 64 queries (seed=2), k=10",
+        "qps": 64 / (ms / 1e3), "ms_per_batch": ms, "e2e_qps": 64 / (e2e_ms / 1e3),
+        "parity": f"{'ok' if ok else 'MISMATCH'}: 64 x 10 ids and f64 dists == reference golden (tests/golden/bf_c1.npz)",
+        "store_bytes_per_batch": bytes_per_batch,
+        "store_gbs": bytes_per_batch / (ms / 1e3) / 1e9,
+        "fixups": store.last_fixups(),
+    }
+    if peak_gbs:
+        out["frac_of_hbm_peak_whole_batch"] = out["store_gbs"] / peak_gbs
+    store.close()
+    return out
+
+
+def c3(idx, data, art, n_requests: int = 1200, batch: int = 256) -> dict:
+    """Ragged prefill/decode batches from a gen_trace workload over the C2 index."""
+    import torch
+
+    from oracle import trinity_oracle as orc
+    from paper_2512_02281_b200.workload import WorkloadSpec, gen_trace
+
+    spec = WorkloadSpec(n_db=data.shape[0], dim=data.shape[1], n_requests=n_requests, arrival_rate=1e4, seed=7)
+    trace = gen_trace(spec)
+    items = []  # (arrival, query, stage)
+    for r in trace:
+        for j in range(r.queries.shape[0]):
+            items.append((r.arrival_time, r.queries[j], "prefill" if j == 0 else "decode"))
+    qs = np.stack([it[1] for it in items]).astype(np.float64)
+    stage = np.array([it[2] for it in items])
+    ks = np.where(stage == "prefill", 100, 10).astype(np.int32)
+    nps = np.where(stage == "prefill", 64, 16).astype(np.int32)
+    n = qs.shape[0]
+    q_dev = torch.from_numpy(qs).cuda()
+    ids = torch.empty((n, 100), dtype=torch.int64, device="cuda")
+    d = torch.empty((n, 100), dtype=torch.float64, device="cuda")
+    st = torch.cuda.Stream()
+    starts = list(range(0, n, batch))
+
+    def run_all(times=None):
+        for s in starts:
+            e = min(n, s + batch)
+            if times is not None:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record(st)
+            idx.search_device(q_dev[s:e], ks[s:e], nps[s:e], ids[s:e], d[s:e], st)
+            if times is not None:
+                ev[1].record(st)
+                times.append(ev)
+
+    run_all()
+    st.synchronize()
+    times = []
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(st)
+    run_all(times)
+    t1.record(st)
+    t1.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    lat = {"prefill": [], "decode": []}
+    for bi, (a, b) in enumerate(times):
+        ms = a.elapsed_time(b)
+        s = starts[bi]
+        for i in range(s, min(n, s + batch)):
+            lat[stage[i]].append(ms)
+    hid, hd = ids.cpu().numpy(), d.cpu().numpy()
+    ok = True
+    for i in range(0, n, max(1, n // 12)):
+        oi, od = orc.ivf_search(data, art, qs[i], int(ks[i]), int(nps[i]))
+        ok = ok and np.array_equal(hid[i, :oi.size], oi) and np.array_equal(hd[i, :oi.size], od)
+    n_pre = int((stage == "prefill").sum())
+    return {
+        "workload": f"C3: gen_trace(seed=7) over the C2 index, {n} retrievals ({n_pre} prefill k=100 nprobe=64, "
+                    f"{n - n_pre} decode k=10 nprobe=16), ragged batches of {batch} in arrival order",
+        "qps": n / (total_ms / 1e3), "batches": len(starts), "ms_per_batch": total_ms / len(starts),
+        "batch_latency": {k: _pct(v) for k, v in lat.items()},
+        "parity": f"{'ok' if ok else 'MISMATCH'}: every {max(1, n // 12)}th retrieval == CPU oracle (ids, f64 dists)",
+        "timed": "device-resident queries, one stream, CUDA events per batch",
+    }
+
+
+def c5(idx, n_requests: int = 2000, arrival_rate: float = 40_000.0) -> dict:
+    """Scheduled RAG trace: prefill + decode probes + prompt-cache lookups, p50/p95/p99 per stage."""
+    from paper_2512_02281_b200.ann_graph import VectorStore
+    from paper_2512_02281_b200.scheduler import SchedulerConfig
+    from paper_2512_02281_b200.trace import run_trace
+    from paper_2512_02281_b200.workload import WorkloadSpec, gen_matrix
+
+    cache = VectorStore(data=gen_matrix(10_000, idx.dim, 62))
+    spec = WorkloadSpec(n_db=idx.count, dim=idx.dim, n_requests=n_requests, arrival_rate=arrival_rate, seed=7)
+    out = {"workload": f"C5: gen_trace({n_requests} requests, Poisson {arrival_rate:.0f}/s, output 64, delta 32, "
+                       f"seed 7) over the C2 index + 10K x {idx.dim} prompt cache (k=1); simulated clock advanced by "
+                       f"measured device time per batch", "policies": {}}
+    for policy in ("prefill_reserved", "decode_priority"):
+        cfg = SchedulerConfig(slots_n=256, r=0.25, tau_pre=2e-4, tau_global=1e-3, policy=policy)
+        t0 = time.perf_counter()
+        res = run_trace(idx, cache, spec, cfg, tpot=1e-3)
+        out["policies"][policy] = {
+            "latency": res.percentiles(), "batches": res.batches, "retrievals": res.retrievals,
+            "gpu_ms": res.gpu_ms, "sim_seconds": res.sim_seconds, "wall_s": time.perf_counter() - t0,
+        }
+    return out
+
+
+def engine() -> dict:
+    import sys
+
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from bench_engine import run
+
+    return run(n=100_000, d=128, nq=4096, reps=3)
