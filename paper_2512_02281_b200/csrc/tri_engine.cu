@@ -39,7 +39,6 @@
 namespace tri {
 namespace {
 
-constexpr int kEngThreads = 128;
 constexpr int kEngMaxM = 256;     // top-M capacity per request
 constexpr int kEngMaxEmit = 512;  // p * degree per extend
 constexpr int kStats = 4;         // per-step counters: emissions, retired, active after, error
@@ -70,6 +69,7 @@ struct EngineLaunch {
   long long vw;
   int* stats;  // this step's kStats counters
   int step;
+  int n_slots;  // slots [0, n_slots) are launched
   // retirements (host drains after each chunk)
   int* res_n;
   long long* res_rid;
@@ -85,161 +85,230 @@ __device__ __forceinline__ bool lt(double da, int ia, double db, int ib) {
   return da < db || (da == db && ia < ib);
 }
 
-__global__ void __launch_bounds__(kEngThreads) engine_step_kernel(EngineLaunch L) {
-  const int s = blockIdx.x;
+// Squared L2 in the reference's float64 order (see tri_common.cuh
+// exact_sq_dist) with 16-byte loads: per 8-element block two float4 of the
+// row and four double2 of the query, then sub-blocks 3..0, unfused mul/add.
+__device__ __forceinline__ double exact_sq_dist_v4(const double* __restrict__ q, const float* __restrict__ x, int d) {
+  double l0 = 0.0, l1 = 0.0;
+  int i = 0;
+  for (; i + 8 <= d; i += 8) {
+    const float4 lo = *reinterpret_cast<const float4*>(x + i);
+    const float4 hi = *reinterpret_cast<const float4*>(x + i + 4);
+    const double2 q0 = *reinterpret_cast<const double2*>(q + i);
+    const double2 q1 = *reinterpret_cast<const double2*>(q + i + 2);
+    const double2 q2 = *reinterpret_cast<const double2*>(q + i + 4);
+    const double2 q3 = *reinterpret_cast<const double2*>(q + i + 6);
+    const double a6 = __dsub_rn(q3.x, (double)hi.z), a7 = __dsub_rn(q3.y, (double)hi.w);
+    const double a4 = __dsub_rn(q2.x, (double)hi.x), a5 = __dsub_rn(q2.y, (double)hi.y);
+    const double a2 = __dsub_rn(q1.x, (double)lo.z), a3 = __dsub_rn(q1.y, (double)lo.w);
+    const double a0 = __dsub_rn(q0.x, (double)lo.x), a1 = __dsub_rn(q0.y, (double)lo.y);
+    l0 = __dadd_rn(__dmul_rn(a6, a6), l0);
+    l1 = __dadd_rn(__dmul_rn(a7, a7), l1);
+    l0 = __dadd_rn(__dmul_rn(a4, a4), l0);
+    l1 = __dadd_rn(__dmul_rn(a5, a5), l1);
+    l0 = __dadd_rn(__dmul_rn(a2, a2), l0);
+    l1 = __dadd_rn(__dmul_rn(a3, a3), l1);
+    l0 = __dadd_rn(__dmul_rn(a0, a0), l0);
+    l1 = __dadd_rn(__dmul_rn(a1, a1), l1);
+  }
+  for (; i < d; i += 2) {
+    const double t0 = __dsub_rn(q[i], (double)x[i]);
+    l0 = __dadd_rn(__dmul_rn(t0, t0), l0);
+    if (i + 1 < d) {
+      const double t1 = __dsub_rn(q[i + 1], (double)x[i + 1]);
+      l1 = __dadd_rn(__dmul_rn(t1, t1), l1);
+    }
+  }
+  return __dadd_rn(l0, l1);
+}
+
+// One WARP per request slot (kEngWarps slots per CTA): no block barriers, the
+// request's lists live in the warp's slice of shared memory.
+//   seed      strided entries floor(i*n/E) deduplicated, exact distances,
+//             visited bits, sorted by rank counting
+//   parents   ballot over the expanded flags, first p unexpanded in order
+//   expand    one neighbour slot per lane: atomicOr test-and-set on the
+//             visited bitmap, ballot compaction of the new ids
+//   distances one candidate per lane, exact fp64 in the reference order
+//   merge     old entry i -> rank i + #(new before it); new entry -> binary
+//             search in the old list + #(new before it); entries past M drop
+//   stop      ballots for "order changed" / "all expanded"
+constexpr int kEngWarps = 4;
+
+__global__ void __launch_bounds__(32 * kEngWarps) engine_step_kernel(EngineLaunch L) {
+  extern __shared__ __align__(16) unsigned char eng_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kEngWarps + warp;
+  if (s >= L.n_slots) return;
   const int st = L.status[s];
   if (st != kSeed && st != kActive) return;
-  const int tid = threadIdx.x;
-
-  // combined list: [0, cnt) the current top-M, [cnt, cnt + ne) this extend's emissions
-  __shared__ double cd[kEngMaxM + kEngMaxEmit];
-  __shared__ int ci[kEngMaxM + kEngMaxEmit];
-  __shared__ unsigned char ce[kEngMaxM + kEngMaxEmit];
-  __shared__ double od[kEngMaxM];
-  __shared__ int oi[kEngMaxM];
-  __shared__ unsigned char oe[kEngMaxM];
-  __shared__ int parents[kEngMaxEmit];
-  __shared__ int s_cnt, s_ne, s_np, s_err;
-
+  const int m = L.m, cap = m + L.p * L.D;
+  // per-warp region: combined list (cap), merged list (m), parents (p)
+  const size_t per_warp = (size_t)cap * 13 + (size_t)m * 13 + (size_t)L.p * 4 + 64;
+  unsigned char* base = eng_smem + warp * ((per_warp + 15) & ~(size_t)15);
+  double* cd = reinterpret_cast<double*>(base);
+  double* od = cd + cap;
+  int* ci = reinterpret_cast<int*>(od + m);
+  int* oi = ci + cap;
+  int* par = oi + m;
+  unsigned char* ce = reinterpret_cast<unsigned char*>(par + L.p);
+  unsigned char* oe = ce + cap;
+  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
   const double* q = L.q64 + (long long)s * L.d;
   unsigned* vis = L.vis + (long long)s * L.vw;
-  const int m = L.m;
+  const bool vec = (L.d & 1) == 0;  // double2 query loads need an even row stride
+  auto dist_of = [&](int id) -> double {
+    const float* x = L.X + (long long)id * L.ldx;
+    return vec ? exact_sq_dist_v4(q, x, L.d) : exact_sq_dist(q, x, L.d);
+  };
+  auto less = [](double da, int ia, double db, int ib) { return da < db || (da == db && ia < ib); };
 
-  if (tid == 0) {
-    s_err = kErrNone;
-    s_ne = 0;
-  }
+  int cnt;
   if (st == kSeed) {
-    // strided entry points floor(i*n/E), deduplicated (engine.py:136-143); the
-    // sequence is non-decreasing, so duplicates are adjacent
-    if (tid == 0) {
-      int c = 0;
-      long long last = -1;
-      for (int i = 0; i < L.E; ++i) {
-        long long v = (long long)i * L.n / L.E;
-        if (v != last) {
-          ci[kEngMaxM + c++] = (int)v;
-          last = v;
-        }
+    // entries floor(i*n/E), non-decreasing in i: keep the first of equal runs
+    int c = 0;
+    for (int b0 = 0; b0 < L.E; b0 += 32) {
+      const int i = b0 + lane;
+      bool keep = false;
+      long long v = 0;
+      if (i < L.E) {
+        v = (long long)i * L.n / L.E;
+        keep = i == 0 || v != (long long)(i - 1) * L.n / L.E;
       }
-      s_ne = c;
+      const unsigned mk = __ballot_sync(FULL, keep);
+      if (keep) ci[c + __popc(mk & lt)] = (int)v;
+      c += __popc(mk);
     }
-    __syncthreads();
-    const int c = s_ne;
-    for (int i = tid; i < c; i += kEngThreads) {
-      const int v = ci[kEngMaxM + i];
-      cd[kEngMaxM + i] = exact_sq_dist(q, L.X + (long long)v * L.ldx, L.d);
+    __syncwarp();
+    for (int i = lane; i < c; i += 32) {
+      const int v = ci[i];
+      cd[i] = dist_of(v);
       atomicOr(&vis[v >> 5], 1u << (v & 31));
     }
-    __syncthreads();
-    // rank placement of the entries (ids unique) -> sorted top list
-    for (int i = tid; i < c; i += kEngThreads) {
-      const double di = cd[kEngMaxM + i];
-      const int ii = ci[kEngMaxM + i];
+    __syncwarp();
+    for (int i = lane; i < c; i += 32) {  // rank counting (ids unique)
+      const double di = cd[i];
+      const int ii = ci[i];
       int r = 0;
-      for (int j = 0; j < c; ++j) r += lt(cd[kEngMaxM + j], ci[kEngMaxM + j], di, ii);
+      for (int j = 0; j < c; ++j) r += less(cd[j], ci[j], di, ii);
       od[r] = di;
       oi[r] = ii;
     }
-    __syncthreads();
-    for (int i = tid; i < c; i += kEngThreads) {
+    __syncwarp();
+    for (int i = lane; i < c; i += 32) {
       cd[i] = od[i];
       ci[i] = oi[i];
       ce[i] = 0;
     }
-    if (tid == 0) {
-      s_cnt = c;
-      s_ne = 0;
-    }
-    __syncthreads();
+    cnt = c;
   } else {
-    const int c = L.cnt[s];
-    const long long base = (long long)s * m;
-    for (int i = tid; i < c; i += kEngThreads) {
-      cd[i] = L.topd[base + i];
-      ci[i] = L.topi[base + i];
-      ce[i] = L.tope[base + i];
-    }
-    if (tid == 0) s_cnt = c;
-    __syncthreads();
-  }
-  const int cnt = s_cnt;
-
-  // select parents: the first <= p unexpanded entries, best first (engine.py:176-184)
-  if (tid == 0) {
-    int np = 0;
-    for (int r = 0; r < cnt && np < L.p; ++r)
-      if (!ce[r]) parents[np++] = r;
-    s_np = np;
-  }
-  __syncthreads();
-  const int np = s_np;
-
-  // expand: neighbours of each parent, test-and-set on the visited bitmap so an
-  // id shared by two parents is emitted once (engine.py:187-205)
-  for (int t = tid; t < np * L.D; t += kEngThreads) {
-    const int pi = t / L.D;
-    const unsigned nid = L.adj[(long long)ci[parents[pi]] * L.D + (t - pi * L.D)];
-    if ((long long)nid >= L.n) {
-      s_err = kErrRange;
-      continue;
-    }
-    const unsigned bit = 1u << (nid & 31);
-    if (!(atomicOr(&vis[nid >> 5], bit) & bit)) {
-      const int e = atomicAdd(&s_ne, 1);
-      ci[cnt + e] = (int)nid;
-      ce[cnt + e] = 0;
+    cnt = L.cnt[s];
+    const long long b = (long long)s * m;
+    for (int i = lane; i < cnt; i += 32) {
+      cd[i] = L.topd[b + i];
+      ci[i] = L.topi[b + i];
+      ce[i] = L.tope[b + i];
     }
   }
-  __syncthreads();
-  for (int i = tid; i < np; i += kEngThreads) ce[parents[i]] = 1;
-  const int ne = s_ne;
+  __syncwarp();
 
-  // exact float64 distances of the emissions, reference operation order
-  for (int i = tid; i < ne; i += kEngThreads)
-    cd[cnt + i] = exact_sq_dist(q, L.X + (long long)ci[cnt + i] * L.ldx, L.d);
-  __syncthreads();
+  // parents: the first <= p unexpanded entries in (dist, id) order
+  int np = 0;
+  for (int b0 = 0; b0 < cnt && np < L.p; b0 += 32) {
+    unsigned mk = __ballot_sync(FULL, b0 + lane < cnt && !ce[b0 + lane]);
+    while (mk && np < L.p) {
+      const int bit = __ffs(mk) - 1;
+      if (lane == 0) par[np] = b0 + bit;
+      ++np;
+      mk &= mk - 1;
+    }
+  }
+  __syncwarp();
 
-  // merge into top-M by (dist, id): rank placement over the combined list
-  const int nc = cnt + ne;
-  const int newcnt = nc < m ? nc : m;
-  for (int i = tid; i < nc; i += kEngThreads) {
+  // expand: test-and-set on the visited bitmap, ballot-compacted emissions
+  int ne = 0, err = 0;
+  const int slots = np * L.D;
+  for (int t0 = 0; t0 < slots; t0 += 32) {
+    const int t = t0 + lane;
+    bool fresh = false;
+    unsigned nid = 0;
+    if (t < slots) {
+      const int pi = t / L.D;
+      nid = L.adj[(long long)ci[par[pi]] * L.D + (t - pi * L.D)];
+      if ((long long)nid >= L.n) {
+        err = 1;
+      } else {
+        const unsigned bit = 1u << (nid & 31);
+        fresh = !(atomicOr(&vis[nid >> 5], bit) & bit);
+      }
+    }
+    const unsigned mk = __ballot_sync(FULL, fresh);
+    if (fresh) {
+      ci[cnt + ne + __popc(mk & lt)] = (int)nid;
+      ce[cnt + ne + __popc(mk & lt)] = 0;
+    }
+    ne += __popc(mk);
+  }
+  err = __any_sync(FULL, err);
+  __syncwarp();
+  if (lane < np) ce[par[lane]] = 1;
+
+  // exact distances of the emissions, one candidate per lane
+  for (int e = lane; e < ne; e += 32) cd[cnt + e] = dist_of(ci[cnt + e]);
+  __syncwarp();
+
+  // merge: ranks in the combined order; old list sorted, new ones unsorted
+  const int newcnt = min(cnt + ne, m);
+  for (int i = lane; i < cnt; i += 32) {
     const double di = cd[i];
     const int ii = ci[i];
-    int r = 0;
-    for (int j = 0; j < nc; ++j) r += lt(cd[j], ci[j], di, ii);
+    int r = i;
+    for (int j = 0; j < ne; ++j) r += less(cd[cnt + j], ci[cnt + j], di, ii);
     if (r < m) {
       od[r] = di;
       oi[r] = ii;
       oe[r] = ce[i];
     }
   }
-  __syncthreads();
-  // changed = the ordered id list differs (engine.py:259-275; no results -> unchanged)
+  for (int j = lane; j < ne; j += 32) {
+    const double dj = cd[cnt + j];
+    const int ij = ci[cnt + j];
+    int lo = 0, hi = cnt;  // # old entries before it
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (less(cd[mid], ci[mid], dj, ij)) lo = mid + 1;
+      else hi = mid;
+    }
+    int r = lo;
+    for (int l = 0; l < ne; ++l) r += less(cd[cnt + l], ci[cnt + l], dj, ij);
+    if (r < m) {
+      od[r] = dj;
+      oi[r] = ij;
+      oe[r] = 0;
+    }
+  }
+  __syncwarp();
   int diff = 0, unexp = 0;
-  for (int r = tid; r < newcnt; r += kEngThreads) {
+  for (int r = lane; r < newcnt; r += 32) {
     diff |= (r >= cnt) || (oi[r] != ci[r]);
     unexp |= !oe[r];
   }
-  const int any_diff = __syncthreads_or(diff);
-  const bool all_expanded = !__syncthreads_or(unexp);
-  const bool changed = (ne > 0) && (any_diff || newcnt != cnt);
+  const bool changed = ne > 0 && (__any_sync(FULL, diff) || newcnt != cnt);
+  const bool all_expanded = !__any_sync(FULL, unexp);
 
-  if (tid == 0) {
+  if (lane == 0) {
     if (ne) atomicAdd(&L.stats[0], ne);
-    if (s_err) atomicMax(&L.stats[3], s_err);
+    if (err) atomicMax(&L.stats[3], kErrRange);
   }
   const int extends = (st == kSeed ? 0 : L.ext[s]) + 1;
   const int streak = changed ? 0 : (st == kSeed ? 0 : L.streak[s]) + 1;
   const bool converged = streak >= L.stop_streak || all_expanded || extends >= L.max_extends;
   const int k = L.kq[s];
-  if (converged) {
-    // finalize (engine.py:293-302): first k entries
-    __shared__ int slot;
-    if (tid == 0) {
+  if (converged) {  // finalize (engine.py:293-302): the first k entries
+    int slot = -1;
+    if (lane == 0) {
       if (k > newcnt) {
         atomicMax(&L.stats[3], kErrK);
-        slot = -1;
       } else {
         slot = atomicAdd(L.res_n, 1);
         L.res_rid[slot] = L.rid[s];
@@ -249,31 +318,36 @@ __global__ void __launch_bounds__(kEngThreads) engine_step_kernel(EngineLaunch L
         L.res_slot[slot] = s;
         atomicAdd(&L.stats[1], 1);
       }
-      // the slot is free on the device now; the host reuses it only after it
-      // has read this retirement record
+      // free on the device; the host reuses it only after reading the record
       L.status[s] = kFree;
     }
-    __syncthreads();
+    slot = __shfl_sync(FULL, slot, 0);
     if (slot >= 0)
-      for (int r = tid; r < k; r += kEngThreads) {
+      for (int r = lane; r < k; r += 32) {
         L.res_ids[(long long)slot * m + r] = oi[r];
         L.res_d[(long long)slot * m + r] = od[r];
       }
     return;
   }
-  const long long base = (long long)s * m;
-  for (int r = tid; r < newcnt; r += kEngThreads) {
-    L.topd[base + r] = od[r];
-    L.topi[base + r] = oi[r];
-    L.tope[base + r] = oe[r];
+  const long long b = (long long)s * m;
+  for (int r = lane; r < newcnt; r += 32) {
+    L.topd[b + r] = od[r];
+    L.topi[b + r] = oi[r];
+    L.tope[b + r] = oe[r];
   }
-  if (tid == 0) {
+  if (lane == 0) {
     L.cnt[s] = newcnt;
     L.ext[s] = extends;
     L.streak[s] = streak;
     L.status[s] = kActive;
     atomicAdd(&L.stats[2], 1);
   }
+}
+
+size_t engine_smem(int m, int p, int D) {
+  const size_t cap = (size_t)m + (size_t)p * D;
+  const size_t per_warp = cap * 13 + (size_t)m * 13 + (size_t)p * 4 + 64;
+  return kEngWarps * ((per_warp + 15) & ~(size_t)15);
 }
 
 // Admission: copy the staged queries into their slots, reset counters and the
@@ -364,6 +438,7 @@ struct tri_engine {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double dev_ms = 0.0;
   long long dev_steps = 0;
+  size_t smem = 0;  // dynamic shared memory of the step kernel
 };
 
 namespace {
@@ -578,6 +653,10 @@ int tri_engine_create(tri_store* s, const uint32_t* adjacency, int32_t degree, i
       cudaMallocHost(&e->h_stats, kMaxChunk * kStats * sizeof(int)) != cudaSuccess ||
       cudaEventCreate(&e->ev0) != cudaSuccess || cudaEventCreate(&e->ev1) != cudaSuccess)
     return bail(set_error(TRI_ECUDA, "engine allocation failed"));
+  e->smem = engine_smem(m, p, degree);
+  if (e->smem > 48 * 1024 &&
+      cudaFuncSetAttribute(engine_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem) != cudaSuccess)
+    return bail(set_error(TRI_ECUDA, "engine shared memory %zu bytes not available", e->smem));
   rc = grow_slots(e, 64);
   if (rc) return bail(rc);
   *out = e;
@@ -663,11 +742,13 @@ int tri_engine_run(tri_engine* e, int32_t max_steps, int32_t until_idle, int32_t
     const int n = std::min({chunk, kMaxChunk, max_steps - done});
     ECU(cudaMemsetAsync(e->stats, 0, n * kStats * sizeof(int), e->st));
     EngineLaunch L = launch_of(e);
+    L.n_slots = e->hw;
     ECU(cudaEventRecord(e->ev0, e->st));
     for (int i = 0; i < n; ++i) {
       L.stats = e->stats + i * kStats;
       L.step = done + i;
-      if (e->hw > 0) engine_step_kernel<<<e->hw, kEngThreads, 0, e->st>>>(L);
+      if (e->hw > 0)
+        engine_step_kernel<<<(e->hw + kEngWarps - 1) / kEngWarps, 32 * kEngWarps, e->smem, e->st>>>(L);
     }
     ECU(cudaGetLastError());
     ECU(cudaEventRecord(e->ev1, e->st));
