@@ -215,12 +215,19 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
+    # BENCH_DEVICE / BENCH_BACKEND: test hooks that let a 1-GPU box exercise the
+    # N>1 code path (every rank on one device, gloo); never set by the driver
+    local = int(os.environ.get("BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from oracle import trinity_oracle as orc
     from paper_2512_02281_b200 import _build
@@ -259,16 +266,16 @@ def run_ours(args):
         store = _DeviceStore(data[shard_lo:shard_hi], device=local)
         idx = IVFFlatIndex.from_artifact(store, cen, asg[shard_lo:shard_hi], id_offset=shard_lo)
 
-    L = max(1, args.lanes) if world == 1 else 1
+    L = max(1, args.lanes)
     q_dev = torch.from_numpy(queries).cuda()
     lane_ids = [torch.empty((BATCH, K), dtype=torch.int64, device="cuda") for _ in range(L)]
     lane_d = [torch.empty((BATCH, K), dtype=torch.float64, device="cuda") for _ in range(L)]
     ids_dev, d_dev = lane_ids[0], lane_d[0]
-    if world > 1:
-        g_ids = torch.empty((world, BATCH, K), dtype=torch.int64, device="cuda")
-        g_d = torch.empty((world, BATCH, K), dtype=torch.float64, device="cuda")
-        m_ids = torch.empty((BATCH, K), dtype=torch.int64, device="cuda")
-        m_d = torch.empty((BATCH, K), dtype=torch.float64, device="cuda")
+    if world > 1:  # per-lane gather and merge buffers
+        g_ids = [torch.empty((world, BATCH, K), dtype=torch.int64, device="cuda") for _ in range(L)]
+        g_d = [torch.empty((world, BATCH, K), dtype=torch.float64, device="cuda") for _ in range(L)]
+        m_ids = [torch.empty((BATCH, K), dtype=torch.int64, device="cuda") for _ in range(L)]
+        m_d = [torch.empty((BATCH, K), dtype=torch.float64, device="cuda") for _ in range(L)]
     # explicit non-default streams: the library launches on the caller's
     # stream and keeps one workspace per stream, so batches on different lanes
     # overlap on the device (one batch's scan with the next one's coarse step)
@@ -282,10 +289,11 @@ def run_ours(args):
         j = step_no[0] % L
         step_no[0] += 1
         idx.search_device(q_dev, K, NPROBE, lane_ids[j], lane_d[j], lanes[j])
-        if world > 1:
-            dist.all_gather_into_tensor(g_ids.view(-1), ids_dev.view(-1))
-            dist.all_gather_into_tensor(g_d.view(-1), d_dev.view(-1))
-            merge_topk_device(g_d, g_ids, K, m_d, m_ids, stream)
+        if world > 1:  # every rank issues the collectives in the same lane order
+            with torch.cuda.stream(lanes[j]):
+                dist.all_gather_into_tensor(g_ids[j].view(-1), lane_ids[j].view(-1))
+                dist.all_gather_into_tensor(g_d[j].view(-1), lane_d[j].view(-1))
+            merge_topk_device(g_d[j], g_ids[j], K, m_d[j], m_ids[j], lanes[j])
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -294,8 +302,8 @@ def run_ours(args):
     # correctness spot-check against the CPU oracle (untimed)
     art = orc.IVFArtifact(cen, asg)
     for j in range(L):
-        res_ids = (m_ids if world > 1 else lane_ids[j]).cpu().numpy()
-        res_d = (m_d if world > 1 else lane_d[j]).cpu().numpy()
+        res_ids = (m_ids[j] if world > 1 else lane_ids[j]).cpu().numpy()
+        res_d = (m_d[j] if world > 1 else lane_d[j]).cpu().numpy()
         if rank == 0:
             for i in (0, 97, 255):
                 oi, od = orc.ivf_search(data, art, queries[i], K, NPROBE)
@@ -353,23 +361,24 @@ def run_ours(args):
             call_ms[j].append((time.perf_counter() - t) * 1e3)
 
     t0 = time.perf_counter()
-    if L > 1:
+    threaded = L > 1 and world == 1  # N>1: collectives must be issued in one order on every rank
+    if threaded:
         ths = [threading.Thread(target=lane_loop, args=(j, len(range(j, args.steps, L)))) for j in range(L)]
         for th in ths:
             th.start()
         for th in ths:
             th.join()
-    for _ in range(args.steps if L == 1 else 0):
+    for _ in range(0 if threaded else args.steps):
         t = time.perf_counter()
         idx.search_into(q_pin, K, NPROBE, ids_pin, d_pin, stream=stream)
         if world > 1:
             ids_dev.copy_(ids_pin, non_blocking=False)
             d_dev.copy_(d_pin, non_blocking=False)
-            dist.all_gather_into_tensor(g_ids.view(-1), ids_dev.view(-1))
-            dist.all_gather_into_tensor(g_d.view(-1), d_dev.view(-1))
-            merge_topk_device(g_d, g_ids, K, m_d, m_ids, stream)
-            ids_pin.copy_(m_ids)
-            d_pin.copy_(m_d)
+            dist.all_gather_into_tensor(g_ids[0].view(-1), ids_dev.view(-1))
+            dist.all_gather_into_tensor(g_d[0].view(-1), d_dev.view(-1))
+            merge_topk_device(g_d[0], g_ids[0], K, m_d[0], m_ids[0], stream)
+            ids_pin.copy_(m_ids[0])
+            d_pin.copy_(m_d[0])
         call_ms[0].append((time.perf_counter() - t) * 1e3)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -408,7 +417,7 @@ def run_ours(args):
         "config": dict(CONFIG, parallelism=f"vector-shard x{world}" if world > 1 else "dp1", lanes=L),
         "roofline": {
             "bound": "hbm", "kernel": f"tri::scan_tc_kernel ({scan_kind} tcgen05 IVF list scan)", "achieved": achieved, "peak": peak,
-            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(),
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic() if world == 1 else None,
             "algorithmic_bytes_per_launch": scan_bytes, "scan_ms_per_launch": avg_scan_ms,
             "scan_share_of_step": avg_scan_ms / (total_ms / args.steps),
             "query_vector_pairs_per_launch": pairs,
@@ -420,8 +429,9 @@ def run_ours(args):
                 "d2h_bytes_per_step": BATCH * K * 16,
                 "batch_latency_ms": {"p50": float(np.percentile(lat, 50)), "p95": float(np.percentile(lat, 95)),
                                      "p99": float(np.percentile(lat, 99)),
-                                     "what": f"wall time of one blocking search_into call (256 queries), {L} host "
-                                             f"threads / lanes in flight"}},
+                                     "what": f"wall time of one blocking search_into call (256 queries), "
+                                             + (f"{L} host threads / lanes in flight" if threaded else
+                                                "sequential calls (gather + merge included when N>1)")}},
         "gpu_launches": kernels_per_step * args.steps,
         "clocks": sampler.summary(),
         "host_cores": os.cpu_count(),

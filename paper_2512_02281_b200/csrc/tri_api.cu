@@ -889,25 +889,6 @@ int tri_store_set_id_offset(tri_store* s, int64_t id_offset) {
   return TRI_OK;
 }
 
-int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32_t* k, int32_t ldo, int64_t* ids,
-                           double* dists, void* stream) {
-  if (!s) return fail(TRI_EINVAL, "store is NULL");
-  if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
-  if (B == 0) return TRI_OK;
-  TRY(validate_k(k, B, s->n, "k"));
-  int km = *std::max_element(k, k + B);
-  if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
-  std::lock_guard<std::mutex> lk(s->mu);
-  DeviceGuard g(s->device);
-  cudaStream_t st = pick(stream, s->own);
-  Workspace* w = nullptr;
-  TRY(s->lanes.get(st, &w));
-  TRY(ensure_query_bufs(*w, B, s->d, s->qld));
-  TRY(prep_queries(*w, q, B, s->d, s->qld, st));
-  TRY(bruteforce_core(s, *w, *w, q, B, k, ldo, reinterpret_cast<long long*>(ids), dists, st));
-  return lane_done(*w, st);
-}
-
 int tri_knn_bruteforce(tri_store* s, const double* q, int32_t B, const int32_t* k, int32_t ldo, int64_t* ids,
                        double* dists, void* stream) {
   if (!s) return fail(TRI_EINVAL, "store is NULL");
@@ -1478,10 +1459,10 @@ long long graph_opts() {
 }  // extern "C"
 
 template <class Body>
-static int graph_run(tri_ivf* v, Workspace& w, Workspace& cw, cudaStream_t st, int mode, int B, const int* k,
+static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, int mode, int B, const int* k,
                      const int* np, int ldo, const void* q, const void* ids, const void* dists, Body&& body) {
   if (!g_graphs) return body();
-  const bool prof = v->prof && v->ev_used < kProfSearches;
+  const bool prof = v && v->prof && v->ev_used < kProfSearches;
   const long long opts = graph_opts();
   Workspace::Graph* e = nullptr;
   for (auto& gr : w.graphs)
@@ -1531,14 +1512,16 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace& cw, cudaStream_t st, i
       for (auto& ev : e->ph)
         if (!ev) CU(cudaEventCreate(&ev));
     const long long ep0 = g_epoch;
-    w.capturing = cw.capturing = true;
+    w.capturing = true;
+    if (cw) cw->capturing = true;
     w.cap_host = &e->host;
     w.cap_ph = e->ph;
     cudaGraph_t gr = nullptr;
     cudaError_t ce = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed);
     int rc = ce == cudaSuccess ? body() : TRI_ECUDA;
     if (ce == cudaSuccess) ce = cudaStreamEndCapture(st, &gr);
-    w.capturing = cw.capturing = false;
+    w.capturing = false;
+    if (cw) cw->capturing = false;
     w.cap_host = nullptr;
     w.cap_ph = nullptr;
     cudaGraphExec_t ex = nullptr;
@@ -1597,6 +1580,27 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace& cw, cudaStream_t st, i
 
 extern "C" {
 
+int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32_t* k, int32_t ldo, int64_t* ids,
+                           double* dists, void* stream) {
+  if (!s) return fail(TRI_EINVAL, "store is NULL");
+  if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
+  if (B == 0) return TRI_OK;
+  TRY(validate_k(k, B, s->n, "k"));
+  int km = *std::max_element(k, k + B);
+  if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
+  std::lock_guard<std::mutex> lk(s->mu);
+  DeviceGuard g(s->device);
+  cudaStream_t st = pick(stream, s->own);
+  Workspace* w = nullptr;
+  TRY(s->lanes.get(st, &w));
+  TRY(ensure_query_bufs(*w, B, s->d, s->qld));
+  TRY(graph_run(nullptr, *w, nullptr, st, 2, B, k, k, ldo, q, ids, dists, [&]() -> int {
+    TRY(prep_queries(*w, q, B, s->d, s->qld, st));
+    return bruteforce_core(s, *w, *w, q, B, k, ldo, reinterpret_cast<long long*>(ids), dists, st);
+  }));
+  return lane_done(*w, st);
+}
+
 int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe,
                        int32_t ldo, int64_t* ids, double* dists, void* stream) {
   TRY(ivf_validate(v, B, k, nprobe, ldo));
@@ -1608,7 +1612,7 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   Workspace* cw = nullptr;
   TRY(v->lanes.get(st, &wp));
   TRY(v->cstore->lanes.get(st, &cw));
-  TRY(graph_run(v, *wp, *cw, st, 0, B, k, nprobe, ldo, q, ids, dists,
+  TRY(graph_run(v, *wp, cw, st, 0, B, k, nprobe, ldo, q, ids, dists,
                 [&] { return ivf_search_body(v, *wp, cw, q, B, k, nprobe, ldo, ids, dists, st); }));
   TRY(lane_done(*cw, st));
   return lane_done(*wp, st);
@@ -1641,7 +1645,7 @@ int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, con
     };
     // graph replay needs pinned host buffers (pageable copies cannot be captured)
     if (host_pinned(q) && host_pinned(ids) && host_pinned(dists)) {
-      TRY(graph_run(v, w, *cw, st, 1, B, k, nprobe, ldo, q, ids, dists, body));
+      TRY(graph_run(v, w, cw, st, 1, B, k, nprobe, ldo, q, ids, dists, body));
     } else {
       TRY(body());
     }
