@@ -107,11 +107,22 @@ long long g_tc_stages = 0;   // tensor-core scan ring depth cap (0 = as deep as 
 long long g_scan_kernel = 0;  // 0 auto (IVF: fp16 tensor core), 1 fp32 SIMT, 2 TF32 tensor core
 long long g_scan_debug = 0;   // timing experiments only (results invalid when set)
 long long g_dense_off = 0;    // 1: never use the dense small-store brute force
+long long g_gthr = 1;         // cross-item per-query threshold in the tensor-core scan
 
 // Candidate capacity: over-fetch so the certified re-rank almost never falls
 // back.  TF32 candidates carry ~2^-9 relative dot error, so they over-fetch 2x.
 int kp_for(int k, bool tc) {
   long long want = (long long)k + (tc ? std::max<long long>(16, k) : std::max<long long>(16, k / 4)) + g_kp_extra;
+  int kp = kMinKp;
+  while (kp < want) kp <<= 1;
+  return kp;
+}
+
+// fp16 candidates carry half the TF32 dot error (2^-10 vs 2^-9 relative), so
+// they over-fetch like fp32 by default (k + max(16, k / g_f16_div)).
+long long g_f16_div = 4;
+int kp_for_f16(int k) {
+  long long want = (long long)k + std::max<long long>(16, k / std::max<long long>(1, g_f16_div)) + g_kp_extra;
   int kp = kMinKp;
   while (kp < want) kp <<= 1;
   return kp;
@@ -208,6 +219,8 @@ struct Workspace {
   // IVF per-search buffers
   DevBuf probes, probe_d, counts, fill, mbase, items, members, counters, meta;
   DevBuf Qh, qinv;  // fp16 scan: scaled fp16 queries + 1/(s_q s_x)
+  DevBuf gthr;      // per-query cross-item scan threshold
+  DevBuf fxs;       // fix-up partial lists
   HostBuf h_plan;
   HostBuf h_stage[kStaging];
   cudaEvent_t staged[kStaging] = {nullptr, nullptr, nullptr, nullptr};
@@ -269,7 +282,8 @@ struct Workspace {
     for (auto& g : graphs) g.destroy();
     graphs.clear();
     for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat,
-                      &probes, &probe_d, &counts, &fill, &mbase, &items, &members, &counters, &meta, &Qh, &qinv})
+                      &probes, &probe_d, &counts, &fill, &mbase, &items, &members, &counters, &meta, &Qh, &qinv,
+                      &gthr, &fxs})
       release(*b);
     if (h_plan.p) cudaFreeHost(h_plan.p);
     h_plan.p = nullptr;
@@ -711,6 +725,11 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   sl.dbg = 0;
   sl.stages = tc_scan_stages(s->qld * 4, kSmemLimit, (int)g_tc_stages);
   sl.box_rows = s->box_rows;
+  if (g_gthr && w.tc) {
+    TRY(ensure(w.gthr, (size_t)B * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(w.gthr.p, 0xff, (size_t)B * sizeof(unsigned long long), st));
+    sl.gthr = w.gthr.as<unsigned long long>();
+  }
   CU(w.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
   CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
                   st));
@@ -766,6 +785,8 @@ int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Wo
   fx.ldo = ldo;
   fx.B = B;
   fx.k_max = w.k_max;
+  TRY(ensure(w.fxs, fixup_scratch_bytes(B, w.k_max)));
+  fx.scratch = w.fxs.as<Exact>();
   CU(launch_fixup(fx, st));
   return TRI_OK;
 }
@@ -835,6 +856,8 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "tc_stages")) g_tc_stages = value;
   else if (!std::strcmp(name, "scan_reserve")) g_scan_reserve = value;
   else if (!std::strcmp(name, "graphs")) g_graphs = value;
+  else if (!std::strcmp(name, "gthr")) g_gthr = value;
+  else if (!std::strcmp(name, "f16_div")) g_f16_div = value;
   else if (!std::strcmp(name, "tc_box_rows")) {
     if (value != 32 && value != 64 && value != 128) return fail(TRI_EINVAL, "tc_box_rows must be 32, 64 or 128");
     g_box_rows = value;
@@ -1260,8 +1283,16 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   std::vector<int> kp;
   ScanChoice ch;
   TRY(choose_scan(v->qld, v->d, B, k, kp, ch, false));
-  const int kp_max = ch.kp_max, k_max = ch.k_max;
   const bool f16 = ch.tc && v->Xh && g_scan_kernel != 2;
+  if (f16) {
+    ch.kp_max = kMinKp;
+    for (int i = 0; i < B; ++i) {
+      kp[i] = kp_for_f16(k[i]);
+      ch.kp_max = std::max(ch.kp_max, kp[i]);
+    }
+    ch.cap = sel_cap(ch.kp_max);
+  }
+  const int kp_max = ch.kp_max, k_max = ch.k_max;
   // 0. queries: fp32 rows + norms (+ the fp16 scan copy) in one kernel
   if (f16) {
     TRY(ensure(w.Qh, (size_t)B * v->dph * 2));
@@ -1349,6 +1380,11 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   sl.Qh = f16 ? w.Qh.p : nullptr;
   sl.qldh = v->dph;
   sl.qinv = f16 ? w.qinv.as<float>() : nullptr;
+  if (g_gthr && ch.tc) {
+    TRY(ensure(w.gthr, (size_t)B * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(w.gthr.p, 0xff, (size_t)B * sizeof(unsigned long long), st));
+    sl.gthr = w.gthr.as<unsigned long long>();
+  }
   sl.X = v->Xl;
   sl.ldx = v->dp;
   sl.xnorm = v->xnl;
@@ -1425,6 +1461,8 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   fx.ldo = ldo;
   fx.B = B;
   fx.k_max = k_max;
+  TRY(ensure(w.fxs, fixup_scratch_bytes(B, k_max)));
+  fx.scratch = w.fxs.as<Exact>();
   CU(launch_fixup(fx, st));
   TRY(mark(6));
   if (rec && !w.capturing) v->ev_used++;
@@ -1445,7 +1483,7 @@ static bool host_pinned(const void* p) {
 }
 
 long long graph_opts() {
-  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 +
+  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_f16_div * 131 +
          g_scan_debug * 100003;
 }
 

@@ -85,43 +85,6 @@ __device__ __forceinline__ bool lt(double da, int ia, double db, int ib) {
   return da < db || (da == db && ia < ib);
 }
 
-// Squared L2 in the reference's float64 order (see tri_common.cuh
-// exact_sq_dist) with 16-byte loads: per 8-element block two float4 of the
-// row and four double2 of the query, then sub-blocks 3..0, unfused mul/add.
-__device__ __forceinline__ double exact_sq_dist_v4(const double* __restrict__ q, const float* __restrict__ x, int d) {
-  double l0 = 0.0, l1 = 0.0;
-  int i = 0;
-  for (; i + 8 <= d; i += 8) {
-    const float4 lo = *reinterpret_cast<const float4*>(x + i);
-    const float4 hi = *reinterpret_cast<const float4*>(x + i + 4);
-    const double2 q0 = *reinterpret_cast<const double2*>(q + i);
-    const double2 q1 = *reinterpret_cast<const double2*>(q + i + 2);
-    const double2 q2 = *reinterpret_cast<const double2*>(q + i + 4);
-    const double2 q3 = *reinterpret_cast<const double2*>(q + i + 6);
-    const double a6 = __dsub_rn(q3.x, (double)hi.z), a7 = __dsub_rn(q3.y, (double)hi.w);
-    const double a4 = __dsub_rn(q2.x, (double)hi.x), a5 = __dsub_rn(q2.y, (double)hi.y);
-    const double a2 = __dsub_rn(q1.x, (double)lo.z), a3 = __dsub_rn(q1.y, (double)lo.w);
-    const double a0 = __dsub_rn(q0.x, (double)lo.x), a1 = __dsub_rn(q0.y, (double)lo.y);
-    l0 = __dadd_rn(__dmul_rn(a6, a6), l0);
-    l1 = __dadd_rn(__dmul_rn(a7, a7), l1);
-    l0 = __dadd_rn(__dmul_rn(a4, a4), l0);
-    l1 = __dadd_rn(__dmul_rn(a5, a5), l1);
-    l0 = __dadd_rn(__dmul_rn(a2, a2), l0);
-    l1 = __dadd_rn(__dmul_rn(a3, a3), l1);
-    l0 = __dadd_rn(__dmul_rn(a0, a0), l0);
-    l1 = __dadd_rn(__dmul_rn(a1, a1), l1);
-  }
-  for (; i < d; i += 2) {
-    const double t0 = __dsub_rn(q[i], (double)x[i]);
-    l0 = __dadd_rn(__dmul_rn(t0, t0), l0);
-    if (i + 1 < d) {
-      const double t1 = __dsub_rn(q[i + 1], (double)x[i + 1]);
-      l1 = __dadd_rn(__dmul_rn(t1, t1), l1);
-    }
-  }
-  return __dadd_rn(l0, l1);
-}
-
 // One WARP per request slot (kEngWarps slots per CTA): no block barriers, the
 // request's lists live in the warp's slice of shared memory.
 //   seed      strided entries floor(i*n/E) deduplicated, exact distances,

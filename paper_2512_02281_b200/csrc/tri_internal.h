@@ -68,6 +68,10 @@ struct ScanLaunch {
   const void* Qh;
   int qldh;
   const float* qinv;
+  // per-query cross-item threshold (B keys, TRI_KEY_MAX at start; nullptr =
+  // off): the tensor-core scan publishes each full partial list's kp-th key
+  // with atomicMin and filters against the smallest one seen
+  unsigned long long* gthr;
 };
 
 size_t scan_smem_bytes(int gmax, int qld, int cap);
@@ -156,7 +160,9 @@ struct FixupLaunch {
   int ldo;
   int B;
   int k_max;
+  Exact* scratch;  // fixup_scratch_bytes(B, k_max): per-(query, slice) partial top-k
 };
+size_t fixup_scratch_bytes(int B, int k_max);
 cudaError_t launch_fixup(const FixupLaunch& f, cudaStream_t st);
 
 cudaError_t launch_distance_tasks(const int* owner, const long long* cand, int n_tasks, const double* q64, int d,

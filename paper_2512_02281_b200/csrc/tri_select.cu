@@ -805,71 +805,134 @@ cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // Exact fix-up for uncertified queries: fp64 scan of the full candidate set.
 
-__global__ void __launch_bounds__(kThreads) fixup_kernel(FixupLaunch f, int cap) {
+// Split fix-up.  Each uncertified query's candidate set (the concatenation of
+// its probed lists, or all rows) is cut into S slices; a persistent grid walks
+// the (flagged query, slice) units, computes exact float64 distances of its
+// slice (the reference order) and keeps the slice's top-k (threshold +
+// compaction + smem sort), then a second persistent kernel merges the S
+// partial lists of each flagged query.  With no flagged query both kernels
+// exit at once.
+__device__ __forceinline__ long long fx_total(const FixupLaunch& f, int q) {
+  if (!f.probes) return f.n_rows;
+  long long t = 0;
+  for (int j = 0; j < f.nprobe[q]; ++j) {
+    const long long l = f.probes[(long long)q * f.ld_probes + j];
+    t += f.list_off[l + 1] - f.list_off[l];
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(kThreads) fixup_part_kernel(FixupLaunch f, int S, int cap, Exact* part, int ldp) {
   extern __shared__ Exact fbuf[];
   __shared__ int s_cnt;
   __shared__ Exact s_thr;
-  if ((int)blockIdx.x >= *f.n_flag) return;
-  const int q = f.flag_list[blockIdx.x];
-  const int k = f.meta[q].k;
-  const double* qv = f.q64 + (long long)q * f.d;
-  if (threadIdx.x == 0) {
-    s_cnt = 0;
-    s_thr = exact_max();
-  }
-  __syncthreads();
-  const int nranges = f.probes ? f.nprobe[q] : 1;
-  for (int rg = 0; rg < nranges; ++rg) {
-    long long lo = 0, hi = f.n_rows;
-    if (f.probes) {
-      long long l = f.probes[(long long)q * f.ld_probes + rg];
-      lo = f.list_off[l];
-      hi = f.list_off[l + 1];
+  const int units = *f.n_flag * S;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int fi = u / S, sl = u - fi * S;
+    const int q = f.flag_list[fi];
+    const int k = f.meta[q].k;
+    const double* qv = f.q64 + (long long)q * f.d;
+    const long long total = fx_total(f, q);
+    const long long c0 = total * sl / S, c1 = total * (sl + 1) / S;
+    if (threadIdx.x == 0) {
+      s_cnt = 0;
+      s_thr = exact_max();
     }
-    for (long long base = lo; base < hi; base += kThreads) {
-      const long long row = base + threadIdx.x;
-      const Exact thr = s_thr;
-      if (row < hi) {
-        Exact e;
-        e.d = exact_sq_dist(qv, f.X + row * f.ldx, f.d);
-        e.id = (f.idmap ? f.idmap[row] : row) + f.id_offset;
-        if (exact_less(e, thr)) fbuf[atomicAdd(&s_cnt, 1)] = e;
+    __syncthreads();
+    // walk the ranges overlapping [c0, c1) of the concatenated candidate order
+    const int nranges = f.probes ? f.nprobe[q] : 1;
+    long long before = 0;
+    for (int rg = 0; rg < nranges && before < c1; ++rg) {
+      long long lo = 0, hi = f.n_rows;
+      if (f.probes) {
+        const long long l = f.probes[(long long)q * f.ld_probes + rg];
+        lo = f.list_off[l];
+        hi = f.list_off[l + 1];
       }
-      __syncthreads();
-      const int n = s_cnt;
-      if (n > cap - kThreads) {
-        const int p2 = next_pow2(n);
-        for (int i = n + threadIdx.x; i < p2; i += kThreads) fbuf[i] = exact_max();
-        __syncthreads();
-        block_sort(fbuf, p2, ExactLess());
-        if (threadIdx.x == 0 && n >= k) {
-          s_cnt = k;
-          s_thr = fbuf[k - 1];
+      const long long len = hi - lo;
+      const long long a = max(c0, before), b = min(c1, before + len);
+      if (a < b) {
+        const long long r0 = lo + (a - before), r1 = lo + (b - before);
+        for (long long base = r0; base < r1; base += kThreads) {
+          const long long row = base + threadIdx.x;
+          const Exact thr = s_thr;
+          if (row < r1) {
+            Exact e;
+            e.d = exact_sq_dist_any(qv, f.X + row * f.ldx, f.d);
+            e.id = (f.idmap ? f.idmap[row] : row) + f.id_offset;
+            if (exact_less(e, thr)) fbuf[atomicAdd(&s_cnt, 1)] = e;
+          }
+          __syncthreads();
+          const int n = s_cnt;
+          if (n > cap - kThreads) {
+            const int p2 = next_pow2(n);
+            for (int i = n + threadIdx.x; i < p2; i += kThreads) fbuf[i] = exact_max();
+            __syncthreads();
+            block_sort(fbuf, p2, ExactLess());
+            if (threadIdx.x == 0 && n >= k) {
+              s_cnt = k;
+              s_thr = fbuf[k - 1];
+            }
+          }
+          __syncthreads();
         }
       }
-      __syncthreads();
+      before += len;
     }
-  }
-  const int n = s_cnt;
-  const int p2 = next_pow2(n > 0 ? n : 1);
-  for (int i = n + threadIdx.x; i < p2; i += kThreads) fbuf[i] = exact_max();
-  __syncthreads();
-  block_sort(fbuf, p2, ExactLess());
-  for (int j = threadIdx.x; j < k; j += kThreads) {
-    const Exact e = j < n ? fbuf[j] : exact_max();
-    const bool ok = j < n;
-    f.out_ids[(long long)q * f.ldo + j] = ok ? e.id : -1;
-    f.out_d[(long long)q * f.ldo + j] = e.d;
+    const int n = s_cnt;
+    const int p2 = next_pow2(n > 0 ? n : 1);
+    for (int i = n + threadIdx.x; i < p2; i += kThreads) fbuf[i] = exact_max();
+    __syncthreads();
+    block_sort(fbuf, p2, ExactLess());
+    Exact* dst = part + ((long long)fi * S + sl) * ldp;
+    for (int j = threadIdx.x; j < k; j += kThreads) dst[j] = j < n ? fbuf[j] : exact_max();
+    __syncthreads();
   }
 }
 
+__global__ void __launch_bounds__(kThreads) fixup_merge_kernel(FixupLaunch f, int S, const Exact* part, int ldp) {
+  extern __shared__ Exact mbuf2[];
+  for (int fi = blockIdx.x; fi < *f.n_flag; fi += gridDim.x) {
+    const int q = f.flag_list[fi];
+    const int k = f.meta[q].k;
+    const int n = S * k, p2 = next_pow2(n);
+    for (int i = threadIdx.x; i < p2; i += kThreads) {
+      const int sl = i / k, j = i - sl * k;
+      mbuf2[i] = i < n ? part[((long long)fi * S + sl) * ldp + j] : exact_max();
+    }
+    __syncthreads();
+    block_sort(mbuf2, p2, ExactLess());
+    for (int j = threadIdx.x; j < k; j += kThreads) {
+      const Exact e = mbuf2[j];
+      const bool ok = e.id != 0x7fffffffffffffffll;
+      f.out_ids[(long long)q * f.ldo + j] = ok ? e.id : -1;
+      f.out_d[(long long)q * f.ldo + j] = e.d;
+    }
+    __syncthreads();
+  }
+}
+
+int fixup_slices(int k_max) { return std::max(1, std::min(32, 4096 / std::max(1, k_max))); }
+
+size_t fixup_scratch_bytes(int B, int k_max) { return (size_t)B * fixup_slices(k_max) * k_max * sizeof(Exact); }
+
 cudaError_t launch_fixup(const FixupLaunch& f, cudaStream_t st) {
   if (f.B <= 0) return cudaSuccess;
-  int cap = next_pow2(f.k_max + kThreads);
-  size_t smem = (size_t)cap * sizeof(Exact);
-  cudaError_t e = cudaFuncSetAttribute(fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int S = fixup_slices(f.k_max);
+  const int cap = next_pow2(f.k_max + kThreads);
+  const size_t smem = (size_t)cap * sizeof(Exact);
+  cudaError_t e = cudaFuncSetAttribute(fixup_part_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fixup_kernel<<<f.B, kThreads, smem, st>>>(f, cap);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  fixup_part_kernel<<<nsm, kThreads, smem, st>>>(f, S, cap, f.scratch, f.k_max);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t msmem = (size_t)next_pow2(S * f.k_max) * sizeof(Exact);
+  e = cudaFuncSetAttribute(fixup_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
+  if (e != cudaSuccess) return e;
+  fixup_merge_kernel<<<nsm, kThreads, msmem, st>>>(f, S, f.scratch, f.k_max);
   return cudaGetLastError();
 }
 
@@ -888,7 +951,7 @@ __global__ void distance_tasks_kernel(const int* __restrict__ owner, const long 
     out[i] = __longlong_as_double(0x7ff8000000000000ll);
     return;
   }
-  out[i] = exact_sq_dist(q64 + (long long)owner[i] * d, X + c * ldx, d);
+  out[i] = exact_sq_dist_any(q64 + (long long)owner[i] * d, X + c * ldx, d);
 }
 
 cudaError_t launch_distance_tasks(const int* owner, const long long* cand, int n_tasks, const double* q64, int d,

@@ -112,6 +112,7 @@ struct TcSmem {
   uint32_t tmem_base;
   int cnt[2][kTcN];
   unsigned long long thr[kTcN];
+  int qid[kTcN];
   float qn[kTcN];
   float qinv[kTcN];
 };
@@ -378,8 +379,19 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
           list_merge32<KL>(L[qi], x, lane);
         }
         if (n > 0) {
-          const unsigned long long t = __shfl_sync(0xffffffffu, L[qi][KL - 1], 31);
-          if (lane == 0) thr[g] = t;
+          unsigned long long t = __shfl_sync(0xffffffffu, L[qi][KL - 1], 31);
+          if (lane == 0) {
+            if (a.gthr) {
+              // cross-item threshold: a full list's kp-th key bounds the query's
+              // final kp-th key, so every CTA scanning this query may drop rows
+              // at or above it (publish without waiting; pick up others' bounds)
+              unsigned long long* gq = a.gthr + sh.qid[g];
+              const unsigned long long gt = __ldcg(gq);
+              if (t != TRI_KEY_MAX && t < gt) atomicMin(gq, t);
+              t = t < gt ? t : gt;
+            }
+            thr[g] = t;
+          }
         }
         __syncwarp();
         if (lane == 0) sh.cnt[buf][g] = 0;
@@ -412,7 +424,8 @@ __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned long long*
       const int q = e < gc ? a.members[w.member_begin + e].q : -1;
       sh.cnt[0][e] = 0;
       sh.cnt[1][e] = 0;
-      sh.thr[e] = TRI_KEY_MAX;
+      sh.thr[e] = (a.gthr && q >= 0) ? __ldcg(a.gthr + q) : TRI_KEY_MAX;
+      sh.qid[e] = q < 0 ? 0 : q;
       sh.qn[e] = q >= 0 ? a.qnorm[q] : 0.f;
       sh.qinv[e] = (H && q >= 0) ? a.qinv[q] : 0.f;
     }
