@@ -1,2 +1,5 @@
 mkdir -p gpurun_out
-timeout 600 python tools/c1_experiment.py "" "gthr=0" "gthr=1,tc_box_rows=32" "tc_box_rows=64" "tc_box_rows=128,tc_stages=4" "tc_stages=0,scan_kernel=1" "scan_kernel=0,dense_off=0" > gpurun_out/c1x.log 2>&1; echo x=$?; cat gpurun_out/c1x.log | tail -8
+NCU=/usr/local/cuda/bin/ncu
+export TRI_GRAPHS=0
+$NCU --metrics gpu__time_duration.sum --clock-control none -k regex:'scan_|merge_|rerank|fixup|prep_|pack_|dense_' -c 60 --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 2 --warmup 3 --lanes 1 --cpu-sample 1 --no-configs > gpurun_out/ncu_b.log 2>&1; echo launches=$?
+$NCU --set full --clock-control none --import-source on -k regex:'scan_tc_kernel|dense_gemm|dense_select|rerank_fused' --launch-skip 12 -c 4 -o gpurun_out/final_full -f python bench.py --steps 2 --warmup 3 --lanes 1 --cpu-sample 1 --no-configs > gpurun_out/ncu_full.log 2>&1; echo full=$?

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -65,7 +66,13 @@ struct DevBuf {
 // Bumped whenever a device scratch buffer moves or a cached plan is rewritten:
 // captured CUDA graphs bake in pointers and plan contents, so any bump retires them.
 long long g_epoch = 0;
-long long g_graphs = 1;  // capture repeated search shapes into CUDA graphs (option "graphs")
+// capture repeated search shapes into CUDA graphs (option "graphs"; the
+// environment variable TRI_GRAPHS=0 turns it off at load, e.g. under ncu,
+// whose kernel replay does not support the graphs' host-memory nodes)
+long long g_graphs = [] {
+  const char* e = std::getenv("TRI_GRAPHS");
+  return (e && e[0] == '0') ? 0LL : 1LL;
+}();
 
 int ensure(DevBuf& b, size_t bytes) {
   if (bytes <= b.cap && b.p) return TRI_OK;
@@ -858,6 +865,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "graphs")) g_graphs = value;
   else if (!std::strcmp(name, "gthr")) g_gthr = value;
   else if (!std::strcmp(name, "f16_div")) g_f16_div = value;
+  else if (!std::strcmp(name, "dense_slices")) tri::g_dense_slices = (int)value;
   else if (!std::strcmp(name, "tc_box_rows")) {
     if (value != 32 && value != 64 && value != 128) return fail(TRI_EINVAL, "tc_box_rows must be 32, 64 or 128");
     g_box_rows = value;
@@ -1483,7 +1491,7 @@ static bool host_pinned(const void* p) {
 }
 
 long long graph_opts() {
-  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_f16_div * 131 +
+  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_f16_div * 131 + tri::g_dense_slices * 17 +
          g_scan_debug * 100003;
 }
 

@@ -8,6 +8,8 @@
 //   dense_select_kernel one CTA per query: slice sum + dot-form distance keys,
 //                       shared-memory bitonic sort, first kp keys -> the
 //                       `merged` candidate list consumed by the exact re-rank.
+#include <algorithm>
+
 #include "tri_common.cuh"
 #include "tri_internal.h"
 
@@ -23,6 +25,7 @@ namespace tri {
 // summed dot stays within gamma_d (the select kernel adds the slices in a
 // fixed order).
 constexpr int kGq = 64, kGr = 128, kGk = 16, kGThreads = 128;
+int g_dense_slices = 8;
 
 struct GemmRegs {
   float4 q[2], x[4];
@@ -231,7 +234,7 @@ cudaError_t launch_dense(const float* Q, int qld, const float* qn, int B, const 
                          const float* xn, long long n, int dp, float* D, long long ldd, const QueryMeta* meta,
                          unsigned long long* merged, int ld_merged, int kp_max, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  const int nsl = kDenseSlices;
+  const int nsl = std::max(1, std::min(kDenseSlices, g_dense_slices));
   const int kslice = ((dp + nsl - 1) / nsl + kGk - 1) / kGk * kGk;
   const int used = (dp + kslice - 1) / kslice;
   dim3 grid((B + kGq - 1) / kGq, (unsigned)((n + kGr - 1) / kGr), used);

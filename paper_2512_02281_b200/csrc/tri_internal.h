@@ -104,7 +104,8 @@ cudaError_t launch_norms(const float* X, long long n, int d, long long ldx, floa
 // then per-query top-kp (kp <= kDenseMaxKp) straight into `merged`.
 constexpr long long kDenseMaxN = 4096;
 constexpr int kDenseMaxKp = 256;
-constexpr int kDenseSlices = 8;  // split-K slices of the distance GEMM (D holds kDenseSlices x B x ldd partials)
+constexpr int kDenseSlices = 16;  // max split-K slices of the distance GEMM (D holds up to this many B x ldd partials)
+extern int g_dense_slices;       // slices used (option "dense_slices", <= kDenseSlices)
 cudaError_t launch_dense(const float* Q, int qld, const float* qn, int B, const float* X, long long ldx,
                          const float* xn, long long n, int dp, float* D, long long ldd, const QueryMeta* meta,
                          unsigned long long* merged, int ld_merged, int kp_max, cudaStream_t st);
