@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-NCU=/usr/local/cuda/bin/ncu
-export TRI_GRAPHS=0
-$NCU --metrics gpu__time_duration.sum --clock-control none -k regex:'scan_|merge_|rerank|fixup|prep_|pack_|dense_' -c 60 --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 2 --warmup 3 --lanes 1 --cpu-sample 1 --no-configs > gpurun_out/ncu_b.log 2>&1; echo launches=$?
-$NCU --set full --clock-control none --import-source on -k regex:'scan_tc_kernel|dense_gemm|dense_select|rerank_fused' --launch-skip 12 -c 4 -o gpurun_out/final_full -f python bench.py --steps 2 --warmup 3 --lanes 1 --cpu-sample 1 --no-configs > gpurun_out/ncu_full.log 2>&1; echo full=$?
+timeout 900 python -m pytest tests/test_gpu_engine.py tests/test_gpu_engine_device.py -x -q --timeout 600 -p no:randomly > gpurun_out/eng_tests.log 2>&1; echo tests=$?; tail -3 gpurun_out/eng_tests.log
+timeout 600 python tools/engine_host_profile.py 2>&1 | tail -3
+timeout 600 python tools/bench_engine.py > gpurun_out/eng1.json 2>gpurun_out/eng1.err; echo e1=$?; python -c "
+import json; d=json.load(open('gpurun_out/eng1.json')); print({k: d[k] for k in ('qps','us_per_step','e2e_qps','e2e_batched_qps','parity','steps')})"; tail -3 gpurun_out/eng1.err

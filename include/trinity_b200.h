@@ -162,6 +162,13 @@ int tri_engine_run(tri_engine* e, int32_t max_steps, int32_t until_idle, int32_t
  * distances per row (row stride ld). */
 int tri_engine_retired(tri_engine* e, int32_t cap, int32_t ld, int32_t* n, int64_t* rids, int32_t* extends,
                        int32_t* ks, int32_t* steps, int64_t* ids, double* dists);
+/* Same results scattered by request id into caller arrays indexed [rid]
+ * (rows of ld for ids/dists; capacity = rows available): the form a
+ * long-lived server keeps.  rids (optional, length = retired count) lists the
+ * drained ids in retirement order. */
+int tri_engine_retired_by_id(tri_engine* e, int64_t capacity, int32_t ld, int32_t* n, int64_t* rids, int32_t* ids,
+                             double* dists, int32_t* extends, int32_t* ks);
+int tri_engine_pending_retired(tri_engine* e, int32_t* n);
 
 /* Exact merge of G per-shard result lists (device buffers, G x B x k_in,
  * id -1 = empty) into the global top-k_out by (dist, id). */

@@ -63,6 +63,8 @@ _SIGS = {
     "tri_engine_device_time": [_vp, _f64p, _i64p],
     "tri_engine_run": [_vp, _i32, _i32, _i32p, _vp, _vp, _vp],
     "tri_engine_retired": [_vp, _i32, _i32, _i32p, _vp, _vp, _vp, _vp, _vp, _vp],
+    "tri_engine_retired_by_id": [_vp, _i64, _i32, _i32p, _vp, _vp, _vp, _vp, _vp],
+    "tri_engine_pending_retired": [_vp, _i32p],
     "tri_merge_topk": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp],
 }
 _RESTYPE = {"tri_last_error": C.c_char_p}

@@ -388,13 +388,16 @@ struct tri_engine {
   std::vector<double> p_q;
   long long next_rid = 0;
   int n_active = 0;
-  struct Done {
-    long long rid;
-    int ext, k, step;
-    std::vector<int> ids;
-    std::vector<double> d;
-  };
-  std::vector<Done> retired;
+  // retired results not yet drained (flat, row stride m; drained from r_head)
+  std::vector<long long> r_rid;
+  std::vector<int> r_ext, r_k, r_step, r_ids;
+  std::vector<double> r_d;
+  size_t r_head = 0;
+  // pinned staging: admission queries and retirement read-back
+  double* h_q = nullptr;
+  size_t h_q_cap = 0;
+  void* h_res = nullptr;
+  size_t h_res_cap = 0;
   // pinned read-back
   int* h_stats = nullptr;
   // device time of the step launches (CUDA events around each chunk)
@@ -422,6 +425,17 @@ struct Guard {
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
+
+int ensure_pinned(void** p, size_t* cap, size_t bytes) {
+  if (bytes <= *cap && *p) return TRI_OK;
+  if (*p) cudaFreeHost(*p);
+  *p = nullptr;
+  *cap = 0;
+  const size_t want = std::max<size_t>(bytes + bytes / 2, 4096);
+  ECU(cudaMallocHost(p, want));
+  *cap = want;
+  return TRI_OK;
+}
 
 int grow_slots(tri_engine* e, int need) {
   if (need <= e->cap) return TRI_OK;
@@ -478,7 +492,14 @@ int admit(tri_engine* e, int* admitted) {
   ECU(cudaMemcpyAsync(e->a_slot, slots.data(), na * sizeof(int), cudaMemcpyHostToDevice, e->st));
   ECU(cudaMemcpyAsync(e->a_rid, e->p_rid.data(), na * sizeof(long long), cudaMemcpyHostToDevice, e->st));
   ECU(cudaMemcpyAsync(e->a_k, e->p_k.data(), na * sizeof(int), cudaMemcpyHostToDevice, e->st));
-  ECU(cudaMemcpyAsync(e->a_q, e->p_q.data(), e->p_q.size() * sizeof(double), cudaMemcpyHostToDevice, e->st));
+  {
+    void* hp = e->h_q;
+    int rc = ensure_pinned(&hp, &e->h_q_cap, e->p_q.size() * sizeof(double));
+    if (rc) return rc;
+    e->h_q = static_cast<double*>(hp);
+    std::memcpy(e->h_q, e->p_q.data(), e->p_q.size() * sizeof(double));
+    ECU(cudaMemcpyAsync(e->a_q, e->h_q, e->p_q.size() * sizeof(double), cudaMemcpyHostToDevice, e->st));
+  }
   engine_admit_kernel<<<na, 256, 0, e->st>>>(e->a_slot, e->a_rid, e->a_k, e->a_q, e->sv.d, e->status, e->q64,
                                              e->kq, e->rid, e->vis, e->vw);
   ECU(cudaGetLastError());
@@ -527,26 +548,36 @@ EngineLaunch launch_of(tri_engine* e) {
   return L;
 }
 
-// Read back this chunk's retirements and return their slots to the free list.
+// Read back this chunk's retirements (one pinned copy per field) and return
+// their slots to the free list.
 int collect(tri_engine* e) {
   int n = 0;
   ECU(cudaMemcpyAsync(&n, e->res_n, sizeof(int), cudaMemcpyDeviceToHost, e->st));
   ECU(cudaStreamSynchronize(e->st));
   if (!n) return TRI_OK;
   const int m = e->m;
-  std::vector<long long> rid(n);
-  std::vector<int> ext(n), k(n), step(n), slot(n), ids((size_t)n * m);
-  std::vector<double> d((size_t)n * m);
-  ECU(cudaMemcpyAsync(rid.data(), e->res_rid, n * sizeof(long long), cudaMemcpyDeviceToHost, e->st));
-  ECU(cudaMemcpyAsync(ext.data(), e->res_ext, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
-  ECU(cudaMemcpyAsync(k.data(), e->res_k, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
-  ECU(cudaMemcpyAsync(step.data(), e->res_step, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
-  ECU(cudaMemcpyAsync(slot.data(), e->res_slot, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
-  ECU(cudaMemcpyAsync(ids.data(), e->res_ids, ids.size() * sizeof(int), cudaMemcpyDeviceToHost, e->st));
-  ECU(cudaMemcpyAsync(d.data(), e->res_d, d.size() * sizeof(double), cudaMemcpyDeviceToHost, e->st));
+  const size_t scal = (size_t)n * (sizeof(long long) + 4 * sizeof(int));
+  const size_t rows = (size_t)n * m * (sizeof(int) + sizeof(double));
+  int rc = ensure_pinned(&e->h_res, &e->h_res_cap, scal + rows + 64);
+  if (rc) return rc;
+  char* h = static_cast<char*>(e->h_res);
+  long long* rid = reinterpret_cast<long long*>(h);
+  double* d = reinterpret_cast<double*>(rid + n);
+  int* ext = reinterpret_cast<int*>(d + (size_t)n * m);
+  int* k = ext + n;
+  int* step = k + n;
+  int* slot = step + n;
+  int* ids = slot + n;
+  ECU(cudaMemcpyAsync(rid, e->res_rid, n * sizeof(long long), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(d, e->res_d, (size_t)n * m * sizeof(double), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(ext, e->res_ext, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(k, e->res_k, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(step, e->res_step, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(slot, e->res_slot, n * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  ECU(cudaMemcpyAsync(ids, e->res_ids, (size_t)n * m * sizeof(int), cudaMemcpyDeviceToHost, e->st));
   ECU(cudaMemsetAsync(e->res_n, 0, sizeof(int), e->st));
   ECU(cudaStreamSynchronize(e->st));
-  for (int s : slot) e->free_slots.push_back(s);
+  for (int i = 0; i < n; ++i) e->free_slots.push_back(slot[i]);
   e->n_active -= n;
   // reuse the lowest slots first so the step grid stays compact
   std::sort(e->free_slots.begin(), e->free_slots.end(), std::greater<int>());
@@ -556,15 +587,22 @@ int collect(tri_engine* e) {
   for (int i = 0; i < n; ++i) order[i] = i;
   std::sort(order.begin(), order.end(),
             [&](int a, int b) { return step[a] != step[b] ? step[a] < step[b] : rid[a] < rid[b]; });
+  if (e->r_head > 0 && e->r_head == e->r_rid.size()) {  // everything drained: restart the buffers
+    e->r_rid.clear();
+    e->r_ext.clear();
+    e->r_k.clear();
+    e->r_step.clear();
+    e->r_ids.clear();
+    e->r_d.clear();
+    e->r_head = 0;
+  }
   for (int i : order) {
-    tri_engine::Done r;
-    r.rid = rid[i];
-    r.ext = ext[i];
-    r.k = k[i];
-    r.step = step[i];
-    r.ids.assign(ids.begin() + (size_t)i * m, ids.begin() + (size_t)i * m + k[i]);
-    r.d.assign(d.begin() + (size_t)i * m, d.begin() + (size_t)i * m + k[i]);
-    e->retired.push_back(std::move(r));
+    e->r_rid.push_back(rid[i]);
+    e->r_ext.push_back(ext[i]);
+    e->r_k.push_back(k[i]);
+    e->r_step.push_back(step[i]);
+    e->r_ids.insert(e->r_ids.end(), ids + (size_t)i * m, ids + (size_t)(i + 1) * m);
+    e->r_d.insert(e->r_d.end(), d + (size_t)i * m, d + (size_t)(i + 1) * m);
   }
   return TRI_OK;
 }
@@ -636,6 +674,8 @@ int tri_engine_destroy(tri_engine* e) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (e->h_stats) cudaFreeHost(e->h_stats);
+  if (e->h_q) cudaFreeHost(e->h_q);
+  if (e->h_res) cudaFreeHost(e->h_res);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
   if (e->st) cudaStreamDestroy(e->st);
@@ -747,20 +787,52 @@ int tri_engine_run(tri_engine* e, int32_t max_steps, int32_t until_idle, int32_t
 int tri_engine_retired(tri_engine* e, int32_t cap, int32_t ld, int32_t* n, int64_t* rids, int32_t* extends,
                        int32_t* ks, int32_t* steps, int64_t* ids, double* dists) {
   if (!e || !n) return set_error(TRI_EINVAL, "null argument");
-  const int cnt = std::min<int>(cap, (int)e->retired.size());
+  const int m = e->m;
+  const int cnt = std::min<int>(cap, (int)(e->r_rid.size() - e->r_head));
   for (int i = 0; i < cnt; ++i) {
-    const auto& r = e->retired[i];
-    if (rids) rids[i] = r.rid;
-    if (extends) extends[i] = r.ext;
-    if (ks) ks[i] = r.k;
-    if (steps) steps[i] = r.step;
-    for (int j = 0; j < r.k && j < ld; ++j) {
-      if (ids) ids[(size_t)i * ld + j] = r.ids[j];
-      if (dists) dists[(size_t)i * ld + j] = r.d[j];
+    const size_t r = e->r_head + i;
+    const int k = e->r_k[r];
+    if (rids) rids[i] = e->r_rid[r];
+    if (extends) extends[i] = e->r_ext[r];
+    if (ks) ks[i] = k;
+    if (steps) steps[i] = e->r_step[r];
+    const int w = std::min(k, (int)ld);
+    for (int j = 0; j < w; ++j) {
+      if (ids) ids[(size_t)i * ld + j] = e->r_ids[r * m + j];
+      if (dists) dists[(size_t)i * ld + j] = e->r_d[r * m + j];
     }
   }
-  e->retired.erase(e->retired.begin(), e->retired.begin() + cnt);
+  e->r_head += cnt;
   *n = cnt;
+  return TRI_OK;
+}
+
+int tri_engine_retired_by_id(tri_engine* e, int64_t capacity, int32_t ld, int32_t* n, int64_t* rids, int32_t* ids,
+                             double* dists, int32_t* extends, int32_t* ks) {
+  if (!e || !n) return set_error(TRI_EINVAL, "null argument");
+  const int m = e->m;
+  const size_t avail = e->r_rid.size() - e->r_head;
+  for (size_t i = 0; i < avail; ++i)
+    if (e->r_rid[e->r_head + i] >= capacity)
+      return set_error(TRI_EINVAL, "request id %lld >= capacity %lld", e->r_rid[e->r_head + i], (long long)capacity);
+  for (size_t i = 0; i < avail; ++i) {
+    const size_t r = e->r_head + i;
+    const long long id = e->r_rid[r];
+    const int k = e->r_k[r], w = std::min(k, (int)ld);
+    if (rids) rids[i] = id;
+    if (ids) std::memcpy(ids + id * ld, e->r_ids.data() + r * m, w * sizeof(int32_t));
+    if (dists) std::memcpy(dists + id * ld, e->r_d.data() + r * m, w * sizeof(double));
+    if (extends) extends[id] = e->r_ext[r];
+    if (ks) ks[id] = k;
+  }
+  e->r_head += avail;
+  *n = (int32_t)avail;
+  return TRI_OK;
+}
+
+int tri_engine_pending_retired(tri_engine* e, int32_t* n) {
+  if (!e || !n) return set_error(TRI_EINVAL, "null argument");
+  *n = (int32_t)(e->r_rid.size() - e->r_head);
   return TRI_OK;
 }
 
