@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=24, help="queries timed for cpu_baseline")
     ap.add_argument("--tc-stages", type=int, default=0, help="tensor-core scan ring depth cap (0 = deepest)")
     ap.add_argument("--scan-reserve", type=int, default=0, help="SMs the list scan leaves to other lanes")
+    ap.add_argument("--opt", action="append", default=[], help="library option name=value (experiments)")
     ap.add_argument("--no-configs", action="store_true", help="skip the secondary-config measurements (C1/C3/C5/engine)")
     ap.add_argument("--lanes", type=int, default=3,
                     help="independent batches in flight (one CUDA stream + library workspace each)")
@@ -239,6 +240,9 @@ def run_ours(args):
 
     _lib.set_option("tc_stages", args.tc_stages)
     _lib.set_option("scan_reserve", args.scan_reserve)
+    for kv in args.opt:
+        name, val = kv.split("=")
+        _lib.set_option(name, int(val))
     data, queries = make_inputs()
 
     # index: rank 0 trains on the full database, the artifact is broadcast

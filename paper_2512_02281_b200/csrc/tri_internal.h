@@ -140,6 +140,7 @@ struct RerankLaunch {
   const float* qinv;        // fp16 scan: qinv[q] < 0 marks a query the scan could not scale (never certified)
 };
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st);
+extern long long g_rerank_smem_cap;  // bytes; 0 = no cap
 
 struct FixupLaunch {
   const int* n_flag;

@@ -19,6 +19,7 @@
 namespace tri {
 
 constexpr int kThreads = 256;
+long long g_rerank_smem_cap = 0;
 
 // ---------------------------------------------------------------------------
 // Query preparation and row norms.
@@ -773,7 +774,12 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
   if (r.B <= 0) return cudaSuccess;
   // slab width: 2 buffers x kp x (S+4) floats <= ~72 KB (several CTAs per SM)
-  const int S = std::max(32, std::min(256, 8192 / r.kp_max));
+  int S = std::max(32, std::min(256, 8192 / r.kp_max));
+  if (g_rerank_smem_cap > 0) {  // leave room for co-resident CTAs (option "rerank_smem_cap")
+    const long long fixed = (long long)((r.d + 15) & ~15) * 8 + (long long)r.kp_max * 16;
+    const long long fit = (g_rerank_smem_cap - fixed) / (2LL * r.kp_max * 4) - 4;
+    S = (int)std::max<long long>(32, std::min<long long>(S, fit / 16 * 16));
+  }
   const size_t rf_smem = (size_t)((r.d + 15) & ~15) * sizeof(double) + (size_t)r.kp_max * 16 +
                          (size_t)2 * r.kp_max * (S + 4) * sizeof(float);
   if (r.kp_max <= 256 && rf_smem <= 200 * 1024) {

@@ -266,3 +266,31 @@ def test_ivf_graph_replay_tracks_inputs(small):
             bi, bd = idx.search(big, 100, 32)
             oi, od = orc.ivf_search(data, art, big[5], 100, 32)
             assert np.array_equal(bi[5, :oi.size], oi)
+
+
+def test_c3_scale_ragged_parity(scan_kernel):
+    """BASELINE C3 at full scale: prefill (k=100, nprobe=64) and decode (k=10,
+    nprobe=16) retrievals in ONE ragged batch over the C2 index; exercises the
+    cross-item threshold and the fp16 over-fetch at k=100.  Oracle on a subset,
+    exact-distance and ordering properties on every row."""
+    if scan_kernel != "auto":
+        pytest.skip("full-scale ragged case runs on the default path only")
+    data = gen_vectors_chunked(1_000_000, 768, seed=3)
+    idx = IVFFlatIndex.train(VectorStore(data=data), nlist=1024, iters=5, seed=4)
+    qs = gen_matrix(256, 768, 77)
+    pre = np.arange(256) % 3 == 0
+    ks = np.where(pre, 100, 10)
+    nps = np.where(pre, 64, 16)
+    ids, d = idx.search(qs, ks, nps)
+    cen, asg = idx.export()
+    art = orc.IVFArtifact(cen, asg)
+    for i in list(range(0, 256, 23)) + [3, 4]:
+        oi, od = orc.ivf_search(data, art, qs[i], int(ks[i]), int(nps[i]))
+        assert np.array_equal(ids[i, :oi.size], oi) and np.array_equal(d[i, :oi.size], od), i
+    for i in range(256):
+        k = int(ks[i])
+        sel = ids[i, :k]
+        assert (sel >= 0).all()
+        diff = qs[i].astype(np.float64)[None, :] - data[sel].astype(np.float64)
+        assert np.array_equal(np.einsum("ij,ij->i", diff, diff), d[i, :k])
+        assert np.array_equal(np.lexsort((sel, d[i, :k])), np.arange(k))
