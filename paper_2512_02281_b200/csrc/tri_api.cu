@@ -867,6 +867,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "f16_div")) g_f16_div = value;
   else if (!std::strcmp(name, "dense_slices")) tri::g_dense_slices = (int)value;
   else if (!std::strcmp(name, "rerank_smem_cap")) tri::g_rerank_smem_cap = value;
+  else if (!std::strcmp(name, "rerank_f2f")) tri::g_rerank_f2f = value;
   else if (!std::strcmp(name, "tc_box_rows")) {
     if (value != 32 && value != 64 && value != 128) return fail(TRI_EINVAL, "tc_box_rows must be 32, 64 or 128");
     g_box_rows = value;
@@ -1492,7 +1493,7 @@ static bool host_pinned(const void* p) {
 }
 
 long long graph_opts() {
-  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 +
+  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 +
          g_scan_debug * 100003;
 }
 

@@ -141,6 +141,7 @@ struct RerankLaunch {
 };
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st);
 extern long long g_rerank_smem_cap;  // bytes; 0 = no cap
+extern long long g_rerank_f2f;       // 1: hardware F2F conversions in the re-rank (else integer bit moves)
 
 struct FixupLaunch {
   const int* n_flag;

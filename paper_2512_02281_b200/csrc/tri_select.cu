@@ -20,6 +20,7 @@ namespace tri {
 
 constexpr int kThreads = 256;
 long long g_rerank_smem_cap = 0;
+long long g_rerank_f2f = 1;
 
 // ---------------------------------------------------------------------------
 // Query preparation and row norms.
@@ -646,6 +647,7 @@ __device__ __forceinline__ double f2d_bits(float x, bool& sub) {
                           (int)((u << 29) & nz));
 }
 
+template <bool F2F>
 __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S) {
   extern __shared__ __align__(16) unsigned char rf_smem[];
   __shared__ double s_dk;
@@ -702,7 +704,7 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
           const float xs[4] = {ln ? hi.w : hi.z, ln ? hi.y : hi.x, ln ? lo.w : lo.z, ln ? lo.y : lo.x};
 #pragma unroll
           for (int t = 0; t < 4; ++t) {  // sub = 3 - t -> element 2*(3-t) + ln
-            const double df = __dsub_rn(qb[8 * (b + bb) + 2 * (3 - t) + ln], f2d_bits(xs[t], sub));
+            const double df = __dsub_rn(qb[8 * (b + bb) + 2 * (3 - t) + ln], F2F ? (double)xs[t] : f2d_bits(xs[t], sub));
             t2[bb * 4 + t] = __dmul_rn(df, df);
           }
         }
@@ -784,9 +786,15 @@ cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
                          (size_t)2 * r.kp_max * (S + 4) * sizeof(float);
   if (r.kp_max <= 256 && rf_smem <= 200 * 1024) {
     const size_t smem = rf_smem;
-    cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    rerank_fused_kernel<<<r.B, 2 * r.kp_max, smem, st>>>(r, S);
+    if (g_rerank_f2f) {
+      cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      rerank_fused_kernel<true><<<r.B, 2 * r.kp_max, smem, st>>>(r, S);
+    } else {
+      cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      rerank_fused_kernel<false><<<r.B, 2 * r.kp_max, smem, st>>>(r, S);
+    }
     return cudaGetLastError();
   }
   const int slab = std::min(kPairSlab, (r.d + 15) & ~15);
