@@ -918,6 +918,7 @@ int tri_store_info(const tri_store* s, int64_t* n, int32_t* d, double* max_norm)
 
 int tri_store_set_id_offset(tri_store* s, int64_t id_offset) {
   if (!s) return fail(TRI_EINVAL, "store is NULL");
+  if (s->id_offset != id_offset) ++g_epoch;  // captured graphs bake the offset into kernel arguments
   s->id_offset = id_offset;
   return TRI_OK;
 }
