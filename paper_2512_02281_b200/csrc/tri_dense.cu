@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kGThreads) dense_gemm_kernel(const float* __re
 // thread in registers.  Sums the split-K slices in a fixed order and forms the
 // dot-form distance fl(fl(|q|^2 + |x|^2) - 2 q.x) exactly as the scans do;
 // then a bisection on the order-preserving distance bits finds a threshold T
-// with kp <= #{dist <= T} <= cap (one block count per step), the survivors are
+// with kp <= #{dist <= T} <= 2 kp (one block count per step), the survivors are
 // compacted and bitonic-sorted in shared memory, and the first kp keys are the
 // query's candidate list.  If ties make the window unreachable (> cap equal
 // distances) the list is left empty: the re-rank cannot certify it and the
@@ -155,18 +155,33 @@ __global__ void __launch_bounds__(kSelThreads) dense_select_kernel(const float* 
   const long long slice_ld = (long long)B * ldd;
   const float qv = qn[q];
   const int kp = meta[q].kp;
+  // thread t owns rows 4t..4t+3 of every 1024-row block (float4 loads; ldd and
+  // the slices are 4-aligned), slices summed in order as before
   uint32_t ord[kSelPer];
   uint32_t lo = 0xffffffffu, hi = 0u;
 #pragma unroll
-  for (int u = 0; u < kSelPer; ++u) {
-    const long long i = tid + (long long)u * kSelThreads;
-    ord[u] = 0xffffffffu;
-    if (i < n) {
-      float acc = 0.f;
-      for (int z = 0; z < nsl; ++z) acc = __fadd_rn(acc, row[z * slice_ld + i]);
-      ord[u] = f2ord(__fmaf_rn(-2.f, acc, __fadd_rn(qv, xn[i])));
-      lo = min(lo, ord[u]);
-      hi = max(hi, ord[u]);
+  for (int g = 0; g < kSelPer / 4; ++g) {
+    const long long i0 = (long long)g * 4 * kSelThreads + 4 * tid;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i0 < n) {
+      for (int z = 0; z < nsl; ++z) {
+        const float4 v = *reinterpret_cast<const float4*>(row + z * slice_ld + i0);
+        acc.x = __fadd_rn(acc.x, v.x);
+        acc.y = __fadd_rn(acc.y, v.y);
+        acc.z = __fadd_rn(acc.z, v.z);
+        acc.w = __fadd_rn(acc.w, v.w);
+      }
+    }
+    const float av[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const long long i = i0 + j;
+      ord[4 * g + j] = 0xffffffffu;
+      if (i < n) {
+        ord[4 * g + j] = f2ord(__fmaf_rn(-2.f, av[j], __fadd_rn(qv, xn[i])));
+        lo = min(lo, ord[4 * g + j]);
+        hi = max(hi, ord[4 * g + j]);
+      }
     }
   }
   // block min / max of the keys' distance bits
@@ -202,7 +217,7 @@ __global__ void __launch_bounds__(kSelThreads) dense_select_kernel(const float* 
       for (int w = 0; w < kSelThreads / 32; ++w) c += red[0][w];
       if (c >= kp) {
         b = mid;
-        if (c <= kSelCap) break;
+        if (c <= max(2 * kp, 64)) break;  // small sort window; the cap only guards ties
       } else {
         a = mid + 1;
       }
@@ -214,7 +229,7 @@ __global__ void __launch_bounds__(kSelThreads) dense_select_kernel(const float* 
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < kSelPer; ++u) {
-    const long long i = tid + (long long)u * kSelThreads;
+    const long long i = (long long)(u >> 2) * 4 * kSelThreads + 4 * tid + (u & 3);
     if (i < n && ord[u] <= T) {
       const int p = atomicAdd(&s_cnt, 1);
       if (p < kSelCap) cand[p] = ((unsigned long long)ord[u] << 32) | (unsigned long long)i;
