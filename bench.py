@@ -336,6 +336,18 @@ def run_ours(args):
     scan_ms, scan_n = idx.scan_time()
     idx.set_profiling(False)
     total_ms = ev0.elapsed_time(ev1)
+    # supplementary: the same scan with no other lane beside it (one stream,
+    # 50 searches), i.e. the kernel's own bandwidth rather than its share of a mix
+    n_iso = 50
+    for _ in range(3):
+        idx.search_device(q_dev, K, NPROBE, lane_ids[0], lane_d[0], lanes[0])
+    torch.cuda.synchronize()
+    idx.set_profiling(True)
+    for _ in range(n_iso):
+        idx.search_device(q_dev, K, NPROBE, lane_ids[0], lane_d[0], lanes[0])
+    torch.cuda.synchronize()
+    iso_ms, iso_n = idx.scan_time()
+    idx.set_profiling(False)
     if dist:
         t = torch.tensor([total_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -424,6 +436,11 @@ def run_ours(args):
             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic() if world == 1 else None,
             "algorithmic_bytes_per_launch": scan_bytes, "scan_ms_per_launch": avg_scan_ms,
             "scan_share_of_step": avg_scan_ms / (total_ms / args.steps),
+            "isolated": {"scan_ms_per_launch": iso_ms / max(iso_n, 1),
+                         "achieved": scan_bytes / (iso_ms / max(iso_n, 1) / 1e3) / 1e9,
+                         "frac": scan_bytes / (iso_ms / max(iso_n, 1) / 1e3) / 1e9 / peak,
+                         "what": f"{n_iso} searches on one stream after the timed region (no other lane "
+                                 f"running beside the scan)"},
             "query_vector_pairs_per_launch": pairs,
         },
         "cpu_baseline": {"value": cpu_qps, "unit": UNIT, "cores": 1, "kind": "port",
