@@ -109,8 +109,19 @@ class IVFFlatIndex:
         return cen, asg
 
     def save(self, path: str) -> None:
-        cen, asg = self.export()
-        np.savez(path, centroids=cen, assign=asg)
+        """IVF index file, little-endian like the reference's vector / graph files
+        (ann_graph.py:186-244): magic b"TRIVF001", `<u8 nlist`, `<u8 n`, `<u8 d`,
+        nlist x d `<f4` centroids, n `<i4` list ids (the shared artifact)."""
+        write_ivf(path, *self.export())
+
+    @classmethod
+    def load(cls, store, path: str, id_offset: int = 0) -> "IVFFlatIndex":
+        """Rebuild the device lists of ``store`` from an index file (see ``save``)."""
+        cen, asg = read_ivf(path)
+        dev = store.device() if isinstance(store, VectorStore) else store
+        if asg.shape[0] != dev.n or cen.shape[1] != dev.d:
+            raise ValueError(f"{path}: index for {asg.shape[0]} x {cen.shape[1]} vectors, store is {dev.n} x {dev.d}")
+        return cls.from_artifact(store, cen, asg, id_offset=id_offset)
 
     def list_sizes(self) -> np.ndarray:
         out = np.empty(self.nlist, dtype=np.int64)
@@ -216,6 +227,39 @@ class IVFFlatIndex:
         k = C.c_int32(0)
         _lib.check(_lib.gpu().tri_ivf_last_scan_kind(self.handle, C.byref(k)))
         return {2: "f16", 1: "f32"}.get(k.value, "none")
+
+
+IVF_MAGIC = b"TRIVF001"
+
+
+def write_ivf(path: str, centroids: np.ndarray, assign: np.ndarray) -> None:
+    cen = np.ascontiguousarray(centroids, dtype="<f4")
+    asg = np.ascontiguousarray(assign, dtype="<i4")
+    if cen.ndim != 2 or asg.ndim != 1:
+        raise ValueError("centroids must be 2-D and assign 1-D")
+    if asg.size and (asg.min() < 0 or asg.max() >= cen.shape[0]):
+        raise ValueError("assign holds list ids outside [0, nlist)")
+    with open(path, "wb") as f:
+        f.write(IVF_MAGIC)
+        f.write(np.array([cen.shape[0], asg.shape[0], cen.shape[1]], dtype="<u8").tobytes())
+        f.write(cen.tobytes())
+        f.write(asg.tobytes())
+
+
+def read_ivf(path: str):
+    with open(path, "rb") as f:
+        raw = f.read()
+    if len(raw) < 32 or raw[:8] != IVF_MAGIC:
+        raise ValueError(f"{path}: not an IVF index file")
+    nlist, n, d = (int(v) for v in np.frombuffer(raw[8:32], dtype="<u8"))
+    want = 32 + 4 * nlist * d + 4 * n
+    if len(raw) != want:
+        raise ValueError(f"{path}: expected {want} bytes for nlist={nlist}, n={n}, d={d}, got {len(raw)}")
+    cen = np.frombuffer(raw[32:32 + 4 * nlist * d], dtype="<f4").reshape(nlist, d).astype(np.float32)
+    asg = np.frombuffer(raw[32 + 4 * nlist * d:], dtype="<i4").astype(np.int32)
+    if asg.size and (asg.min() < 0 or asg.max() >= nlist):
+        raise ValueError(f"{path}: list ids outside [0, {nlist})")
+    return cen, asg
 
 
 def merge_topk_device(dists, ids, k_out: int, out_dists, out_ids, stream=None) -> None:

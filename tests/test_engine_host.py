@@ -83,3 +83,28 @@ def test_config_validation():
         EngineConfig(m=2, p=3)
     with pytest.raises(ValueError):
         EngineConfig(batch_capacity=0)
+
+
+def test_ivf_file_roundtrip_and_errors(tmp_path):
+    """IVF index file (ivf.py write_ivf / read_ivf): exact round trip, corrupt files rejected."""
+    import numpy as np
+    import pytest
+
+    from paper_2512_02281_b200.ivf import read_ivf, write_ivf
+
+    rng = np.random.default_rng(0)
+    cen = rng.standard_normal((7, 5)).astype(np.float32)
+    asg = rng.integers(0, 7, 100).astype(np.int32)
+    p = tmp_path / "x.ivf"
+    write_ivf(str(p), cen, asg)
+    c2, a2 = read_ivf(str(p))
+    assert np.array_equal(c2, cen) and np.array_equal(a2, asg)
+    raw = p.read_bytes()
+    (tmp_path / "short.ivf").write_bytes(raw[:-4])
+    with pytest.raises(ValueError):
+        read_ivf(str(tmp_path / "short.ivf"))
+    (tmp_path / "magic.ivf").write_bytes(b"XXXXXXXX" + raw[8:])
+    with pytest.raises(ValueError):
+        read_ivf(str(tmp_path / "magic.ivf"))
+    with pytest.raises(ValueError):
+        write_ivf(str(tmp_path / "bad.ivf"), cen, np.array([0, 9], np.int32))

@@ -294,3 +294,14 @@ def test_c3_scale_ragged_parity(scan_kernel):
         diff = qs[i].astype(np.float64)[None, :] - data[sel].astype(np.float64)
         assert np.array_equal(np.einsum("ij,ij->i", diff, diff), d[i, :k])
         assert np.array_equal(np.lexsort((sel, d[i, :k])), np.arange(k))
+
+
+def test_ivf_save_load_same_results(small, tmp_path):
+    g, data, idx = small
+    path = str(tmp_path / "small.ivf")
+    idx.save(path)
+    idx2 = IVFFlatIndex.load(VectorStore(data=data), path)
+    qs = gen_matrix(40, 32, 7)
+    a = idx.search(qs, g["ks"], g["nprobes"])
+    b = idx2.search(qs, g["ks"], g["nprobes"])
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
