@@ -533,9 +533,11 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
     }
     if (!g_dense_off && s->n <= kDenseMaxN && kpd <= kDenseMaxKp) {
       const size_t bytes = (((size_t)B * sizeof(QueryMeta) + 255) & ~(size_t)255) + 256;
-      TRY(ensure_host(w.h_plan, bytes));
       TRY(ensure(w.plan, bytes));
-      QueryMeta* hm = static_cast<QueryMeta*>(w.h_plan.p);
+      int slot = 0;
+      void* hp = nullptr;
+      TRY(stage_host(w, bytes, &slot, &hp));  // ring of pinned buffers: no host sync
+      QueryMeta* hm = static_cast<QueryMeta*>(hp);
       for (int i = 0; i < B; ++i) {
         hm[i].k = k[i];
         hm[i].kp = kp_for(k[i], false);
@@ -544,8 +546,7 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
         hm[i].part_off = 0;
         hm[i].n_total = s->n;
       }
-      CU(cudaMemcpyAsync(w.plan.p, hm, bytes, cudaMemcpyHostToDevice, st));
-      CU(cudaStreamSynchronize(st));
+      TRY(staged_upload(w, slot, w.plan.p, bytes, st));
       w.plan_bytes = bytes;
       w.plan_B = B;
       w.plan_n = s->n;
@@ -619,9 +620,11 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
   w.off_members = w.off_items + (((size_t)n_items * sizeof(WorkItem) + 255) & ~(size_t)255);
   size_t counters_off = w.off_members + (((size_t)n_members * sizeof(Member) + 255) & ~(size_t)255);
   w.plan_bytes = counters_off + 256;
-  TRY(ensure_host(w.h_plan, w.plan_bytes));
   TRY(ensure(w.plan, w.plan_bytes));
-  unsigned char* h = static_cast<unsigned char*>(w.h_plan.p);
+  int slot = 0;
+  void* hp = nullptr;
+  TRY(stage_host(w, w.plan_bytes, &slot, &hp));  // ring of pinned buffers: no host sync
+  unsigned char* h = static_cast<unsigned char*>(hp);
   std::memcpy(h, meta.data(), B * sizeof(QueryMeta));
   WorkItem* items = reinterpret_cast<WorkItem*>(h + w.off_items);
   Member* members = reinterpret_cast<Member*>(h + w.off_members);
@@ -648,8 +651,7 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
   }
   int* ctr = reinterpret_cast<int*>(h + counters_off);
   ctr[0] = (int)n_items;
-  CU(cudaMemcpyAsync(w.plan.p, h, w.plan_bytes, cudaMemcpyHostToDevice, st));
-  CU(cudaStreamSynchronize(st));  // h_plan is reused by the next plan
+  TRY(staged_upload(w, slot, w.plan.p, w.plan_bytes, st));
   w.plan_B = B;
   w.plan_n = s->n;
   w.plan_opts = plan_opts();

@@ -142,8 +142,8 @@ class IVFFlatIndex:
         """Ragged batched search with host buffers.
 
         Returns (ids int64[B, kmax], dists f64[B, kmax]); row i holds the exact
-        top-k[i] over its nprobe[i] lists, padded with id -1 / inf when those
-        lists hold fewer than k[i] vectors.
+        top-k[i] over its nprobe[i] lists, padded with id -1 / inf (when those
+        lists hold fewer than k[i] vectors, and in the columns past k[i]).
         """
         q = np.ascontiguousarray(np.atleast_2d(np.asarray(queries, dtype=np.float64)))
         if q.shape[1] != self.dim:
@@ -151,8 +151,8 @@ class IVFFlatIndex:
         B = q.shape[0]
         ks, nps = self._ragged(B, k, nprobe)
         kmax = int(ks.max()) if B else 1
-        ids = np.empty((B, kmax), dtype=np.int64)
-        dists = np.empty((B, kmax), dtype=np.float64)
+        ids = np.full((B, kmax), -1, dtype=np.int64)  # columns past k[i] stay -1 / inf
+        dists = np.full((B, kmax), np.inf, dtype=np.float64)
         if B:
             _lib.check(_lib.gpu().tri_ivf_search(self.handle, q.ctypes.data, B, ks.ctypes.data, nps.ctypes.data,
                                                   kmax, ids.ctypes.data, dists.ctypes.data, None))
