@@ -1,1 +1,1 @@
-timeout 300 python tools/_dbg_saveload.py
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 600 -p no:randomly > gpurun_out/t.log 2>&1; echo tests=$?; tail -2 gpurun_out/t.log

@@ -102,8 +102,9 @@ int tri_ivf_list_sizes(tri_ivf* v, int64_t* sizes);
 /* Ragged batched IVF search: query i wants k[i] results over its nprobe[i]
  * closest lists (coarse step = exact kNN over the centroids).  This is the
  * continuous-batch entry: prefill (large k / nprobe) and decode (small)
- * queries share one launch sequence.  Outputs B x ldo; rows shorter than
- * k[i] (probed lists hold fewer vectors) are padded with id -1. */
+ * queries share one launch sequence.  Outputs B x ldo; entries past the
+ * results (probed lists hold fewer than k[i] vectors, or columns >= k[i]) are
+ * id -1 / distance +inf. */
 int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe, int32_t ldo,
                    int64_t* ids, double* dists, void* stream);
 int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe,

@@ -470,6 +470,15 @@ __global__ void __launch_bounds__(2 * kPairCands) exact_pairs_kernel(RerankLaunc
   }
 }
 
+// Columns [k, ldo) of an output row: id -1, distance +inf (a defined result
+// row whatever the caller's buffer held).
+__device__ __forceinline__ void pad_row(long long* ids, double* d, int k, int ldo, int t, int nt) {
+  for (int j = k + t; j < ldo; j += nt) {
+    ids[j] = -1;
+    d[j] = __longlong_as_double(0x7ff0000000000000ll);
+  }
+}
+
 // finalize: one warp per query sorts its kp exact (dist, id) entries in
 // registers (bitonic network over element j*32 + lane), certifies, writes k.
 __device__ __forceinline__ bool ex_less(double ad, long long ai, double bd, long long bi) {
@@ -546,6 +555,7 @@ __device__ __forceinline__ void finalize_query(const RerankLaunch& r, int q, int
       r.out_d[(long long)q * r.ldo + e] = d[j];
     }
   }
+  pad_row(r.out_ids + (long long)q * r.ldo, r.out_d + (long long)q * r.ldo, m.k, r.ldo, lane, 32);
 }
 
 __global__ void __launch_bounds__(128) finalize_warp_kernel(RerankLaunch r) {
@@ -581,6 +591,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(RerankLaunch r) {
     r.out_ids[(long long)q * r.ldo + j] = ok ? e.id : -1;
     r.out_d[(long long)q * r.ldo + j] = e.d;
   }
+  pad_row(r.out_ids + (long long)q * r.ldo, r.out_d + (long long)q * r.ldo, m.k, r.ldo, threadIdx.x, blockDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -763,6 +774,7 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
     }
     if (rank == m.k - 1) s_dk = md;
   }
+  pad_row(r.out_ids + (long long)q * r.ldo, r.out_d + (long long)q * r.ldo, m.k, r.ldo, tid, nthr);
   __syncthreads();
   if (tid == 0) {
     bool cert = true;
