@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 600 -p no:randomly > gpurun_out/t.log 2>&1; echo tests=$?; tail -2 gpurun_out/t.log
+free -g | head -2; nproc
+timeout 1500 python tools/bench_c4.py > gpurun_out/c4.log 2> gpurun_out/c4.err; echo c4=$?; tail -6 gpurun_out/c4.log | cut -c1-600; tail -3 gpurun_out/c4.err
