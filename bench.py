@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--scan-reserve", type=int, default=0, help="SMs the list scan leaves to other lanes")
     ap.add_argument("--opt", action="append", default=[], help="library option name=value (experiments)")
     ap.add_argument("--no-configs", action="store_true", help="skip the secondary-config measurements (C1/C3/C5/engine)")
-    ap.add_argument("--lanes", type=int, default=3,
+    ap.add_argument("--lanes", type=int, default=4,
                     help="independent batches in flight (one CUDA stream + library workspace each)")
     return ap.parse_args()
 
