@@ -330,9 +330,17 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
   const int nchunk = (w.row_count + kTcRows - 1) / kTcRows;
   float xn_next = row_in_chunk < w.row_count ? a.xnorm[w.row_begin + row_in_chunk] : 0.f;
   volatile unsigned long long* thr = sh.thr;
+  unsigned long long gpre[2] = {TRI_KEY_MAX, TRI_KEY_MAX};  // owner lane 0: cross-item bound, loaded ahead
   for (int c = 0; c < nchunk; ++c) {
     const int buf = c & 1;
     const int rows = min(kTcRows, w.row_count - c * kTcRows);
+    if (a.gthr && lane == 0) {  // issued before the TMEM wait: the L2 round trip overlaps it
+#pragma unroll
+      for (int qi = 0; qi < 2; ++qi) {
+        const int g = ew + kEpiWarps * qi;
+        if (g < gc) gpre[qi] = __ldcg(a.gthr + sh.qid[g]);
+      }
+    }
     const long long row = w.row_begin + (long long)c * kTcRows + row_in_chunk;
     const bool valid = row_in_chunk < rows;
     const float xn = xn_next;  // loaded one chunk ahead (HBM latency off the critical path)
@@ -386,7 +394,7 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
               // final kp-th key, so every CTA scanning this query may drop rows
               // at or above it (publish without waiting; pick up others' bounds)
               unsigned long long* gq = a.gthr + sh.qid[g];
-              const unsigned long long gt = __ldcg(gq);
+              const unsigned long long gt = gpre[qi];
               if (t != TRI_KEY_MAX && t < gt) atomicMin(gq, t);
               t = t < gt ? t : gt;
             }
