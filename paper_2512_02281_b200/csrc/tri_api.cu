@@ -115,6 +115,7 @@ long long g_scan_kernel = 0;  // 0 auto (IVF: fp16 tensor core), 1 fp32 SIMT, 2 
 long long g_scan_debug = 0;   // timing experiments only (results invalid when set)
 long long g_dense_off = 0;    // 1: never use the dense small-store brute force
 long long g_gthr = 1;         // cross-item per-query threshold in the tensor-core scan
+long long g_coarse_tc = 1;    // IVF coarse GEMM on tensor cores (split fp16) when the index allows
 
 // Candidate capacity: over-fetch so the certified re-rank almost never falls
 // back.  TF32 candidates carry ~2^-9 relative dot error, so they over-fetch 2x.
@@ -165,7 +166,11 @@ struct Bound {
 //          2^-25 of a 2^14-scaled element on each side (<= 2^-38 sqrt(d)),
 //          accumulation as for TF32; csum gains 2^-80 for an fp32 subnormal
 //          product after the exact 1/(s_q s_x) rescale.
-enum ScanMode { kSimt = 0, kTf32 = 1, kF16 = 2 };
+//   kSplit tensor-core coarse GEMM on split fp16 (hi + lo) copies of both
+//          sides: residual of the split 3 x 2^-22 (+ 2^-24 query -> fp32),
+//          subnormal floor, 96-product K slices accumulated in fp32 (2x the
+//          RN bound, as for the scans) and the slices summed in fp32.
+enum ScanMode { kSimt = 0, kTf32 = 1, kF16 = 2, kSplit = 3 };
 Bound bound_for(int d, int mode) {
   const double u = std::ldexp(1.0, -24);
   Bound b;
@@ -173,6 +178,12 @@ Bound bound_for(int d, int mode) {
   const double acc = 2.0 * d * std::ldexp(1.0, -23);
   if (mode == kTf32) {
     b.cdot = std::ldexp(1.0, -9) + std::ldexp(1.0, -19) + acc;
+  } else if (mode == kSplit) {
+    const int nacc = 2 * ((d + 63) / 64);
+    b.cdot = 3 * std::ldexp(1.0, -22) * (1.0 + std::ldexp(1.0, -10)) + u +
+             2.0 * 96 * std::ldexp(1.0, -23) * (1.0 + std::ldexp(1.0, -9)) + nacc * std::ldexp(1.0, -23) +
+             std::ldexp(1.0, -36) * std::sqrt((double)d);
+    b.csum += std::ldexp(1.0, -80);
   } else if (mode == kF16) {
     const double u16 = std::ldexp(1.0, -11);
     b.cdot = 2 * u16 + u + 3 * u16 * u16 + acc * (1.0 + 4 * u16) + std::ldexp(1.0, -37) * std::sqrt((double)d);
@@ -227,6 +238,8 @@ struct Workspace {
   DevBuf probes, probe_d, counts, fill, mbase, items, members, counters, meta;
   DevBuf Qh, qinv;  // fp16 scan: scaled fp16 queries + 1/(s_q s_x)
   DevBuf gthr;      // per-query cross-item scan threshold
+  DevBuf Ql;        // lo half of the split fp16 queries (tensor-core coarse GEMM)
+  bool split_q = false;  // this search prepared Qh/Ql/qinv for the split coarse GEMM
   DevBuf fxs;       // fix-up partial lists
   HostBuf h_plan;
   HostBuf h_stage[kStaging];
@@ -290,7 +303,7 @@ struct Workspace {
     graphs.clear();
     for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat,
                       &probes, &probe_d, &counts, &fill, &mbase, &items, &members, &counters, &meta, &Qh, &qinv,
-                      &gthr, &fxs})
+                      &gthr, &fxs, &Ql})
       release(*b);
     if (h_plan.p) cudaFreeHost(h_plan.p);
     h_plan.p = nullptr;
@@ -388,6 +401,12 @@ struct tri_store {
   double xmax = 0.0;
   CUtensorMap tmap, tmap_tc, tmap_tc_tail;
   int box_rows = 32;
+  // split fp16 copies for the tensor-core coarse GEMM (IVF centroid stores)
+  void* Ch = nullptr;
+  void* Cl = nullptr;
+  int dph = 0;
+  float split_ratio = 1.f;  // s_list / s_centroid
+  CUtensorMap tmap_ch, tmap_cl;
   cudaStream_t own = nullptr;
   Lanes lanes;
   std::mutex mu;  // enqueue is serialised per handle; waits happen outside it
@@ -677,7 +696,7 @@ int ensure_query_bufs(Workspace& w, int B, int d, int qld) {
 }
 
 int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Workspace& qw, const QueryMeta* meta,
-                      int B, int ldo, long long* ids, double* dists, bool tc, cudaStream_t st);
+                      int B, int ldo, long long* ids, double* dists, int mode, cudaStream_t st);
 
 // Dense small-store brute force: distance matrix + warp select -> merged.
 int dense_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q64dev, int B, int ldo, long long* ids,
@@ -689,9 +708,28 @@ int dense_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q6
   TRY(ensure(w.flags, (size_t)(B + 64) * sizeof(int)));
   const QueryMeta* meta = static_cast<const QueryMeta*>(w.plan.p);
   CU(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
+  if (s->Ch && qw.split_q) {  // tensor-core coarse GEMM on the split fp16 copies
+    CoarseLaunch c;
+    c.map_h = &s->tmap_ch;
+    c.map_l = &s->tmap_cl;
+    c.Qh = qw.Qh.p;
+    c.Ql = qw.Ql.p;
+    c.ldq = s->dph;
+    c.qinv = qw.qinv.as<float>();
+    c.ratio = s->split_ratio;
+    c.B = B;
+    c.n = s->n;
+    c.nslab = s->dph / 64;
+    c.P = w.dmat.as<float>();
+    c.ldd = ldd;
+    CU(launch_coarse_tc(c, st));
+    CU(launch_dense_select(w.dmat.as<float>(), coarse_tc_slices(c.nslab), ldd, B, qw.qn32.as<float>(), s->xnorm, s->n, meta,
+                           w.merged.as<unsigned long long>(), w.kp_max, w.kp_max, st));
+    return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, kSplit, st);
+  }
   CU(launch_dense(qw.Q32.as<float>(), s->qld, qw.qn32.as<float>(), B, s->X, s->dp, s->xnorm, s->n, s->dp,
                   w.dmat.as<float>(), ldd, meta, w.merged.as<unsigned long long>(), w.kp_max, w.kp_max, st));
-  return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, false, st);
+  return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, kSimt, st);
 }
 
 // Run the brute-force pipeline on prepared queries (Q32/qn32/qn64 in `qw`,
@@ -742,12 +780,12 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   CU(w.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
   CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
                   st));
-  return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, w.tc, st);
+  return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, w.tc ? kTf32 : kSimt, st);
 }
 
 // Exact re-rank + certification + fix-up shared by the scan and dense paths.
 int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Workspace& qw, const QueryMeta* meta,
-                      int B, int ldo, long long* ids, double* dists, bool tc, cudaStream_t st) {
+                      int B, int ldo, long long* ids, double* dists, int mode, cudaStream_t st) {
   int* n_flag = w.flags.as<int>();
   int* flag_list = n_flag + 64;
   RerankLaunch rr{};
@@ -763,9 +801,10 @@ int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Wo
   rr.idmap = nullptr;
   rr.id_offset = s->id_offset;
   rr.xmax = s->xmax;
-  const Bound bd = bound_for(s->d, tc ? kTf32 : kSimt);
+  const Bound bd = bound_for(s->d, mode);
   rr.cdot = g_force_fixup ? 1e30 : bd.cdot;
   rr.csum = bd.csum;
+  rr.qinv = mode == kSplit ? qw.qinv.as<float>() : nullptr;  // unscalable queries are never certified
   rr.out_ids = ids;
   rr.out_d = dists;
   rr.ldo = ldo;
@@ -866,6 +905,11 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "scan_reserve")) g_scan_reserve = value;
   else if (!std::strcmp(name, "graphs")) g_graphs = value;
   else if (!std::strcmp(name, "gthr")) g_gthr = value;
+  else if (!std::strcmp(name, "coarse_tc")) g_coarse_tc = value;
+  else if (!std::strcmp(name, "coarse_split")) {
+    if (value < 1 || value > kDenseSlices) return fail(TRI_EINVAL, "coarse_split must be in [1, %d]", kDenseSlices);
+    tri::g_coarse_split = (int)value;
+  }
   else if (!std::strcmp(name, "f16_div")) g_f16_div = value;
   else if (!std::strcmp(name, "dense_slices")) tri::g_dense_slices = (int)value;
   else if (!std::strcmp(name, "rerank_smem_cap")) tri::g_rerank_smem_cap = value;
@@ -904,6 +948,8 @@ int tri_store_destroy(tri_store* s) {
   if (s->own) cudaStreamSynchronize(s->own);
   if (s->X) cudaFree(s->X);
   if (s->xnorm) cudaFree(s->xnorm);
+  if (s->Ch) cudaFree(s->Ch);
+  if (s->Cl) cudaFree(s->Cl);
   s->lanes.free_all();
   if (s->own) cudaStreamDestroy(s->own);
   delete s;
@@ -1090,6 +1136,35 @@ static tri_ivf* ivf_new(tri_store* s, int nlist) {
   return v;
 }
 
+// Split fp16 copies of the centroids for the tensor-core coarse GEMM, scaled
+// by sc = 2^(14 - ilogb(max|C|)); only when the lists carry the fp16 copy
+// (the queries' split comes from the same prep pass) and the rows fit TMEM.
+static int coarse_split_copy(tri_ivf* v, cudaStream_t st) {
+  tri_store* c = v->cstore;
+  if (!v->Xh || v->dph > 1024 || v->nlist > kDenseMaxN) return TRI_OK;
+  unsigned int* mb = nullptr;
+  CU(cudaMalloc(&mb, sizeof(unsigned int)));
+  CU(cudaMemsetAsync(mb, 0, sizeof(unsigned int), st));
+  CU(launch_absmax(c->X, c->n, c->d, c->dp, mb, st));
+  unsigned int bits = 0;
+  CU(cudaMemcpyAsync(&bits, mb, sizeof(bits), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  cudaFree(mb);
+  float m;
+  std::memcpy(&m, &bits, sizeof(m));
+  if (!(m >= std::ldexp(1.0f, -30) && m <= std::ldexp(1.0f, 30))) return TRI_OK;
+  const float sc = std::ldexp(1.0f, 14 - std::ilogb(m));
+  c->dph = v->dph;
+  c->split_ratio = v->sx / sc;  // both powers of two: exact
+  CU(cudaMalloc(&c->Ch, (size_t)c->n * c->dph * 2));
+  CU(cudaMalloc(&c->Cl, (size_t)c->n * c->dph * 2));
+  CU(launch_to_half(c->X, c->n, c->d, c->dp, sc, c->Ch, c->dph, st));
+  CU(launch_to_half_lo(c->X, c->n, c->d, c->dp, sc, c->Cl, c->dph, st));
+  TRY(make_tmap(&c->tmap_ch, c->Ch, c->n, c->dph, true, true, 128));
+  TRY(make_tmap(&c->tmap_cl, c->Cl, c->n, c->dph, true, true, 128));
+  return TRI_OK;
+}
+
 static int ivf_finish(tri_ivf* v, tri_store* s, const float* Cdev, const int* assign_dev, cudaStream_t st) {
   // counts -> offsets (host) -> ordered members -> layout
   DevBuf cnt;
@@ -1122,6 +1197,7 @@ static int ivf_finish(tri_ivf* v, tri_store* s, const float* Cdev, const int* as
   // singleton lists give centroids data-point norms, so the TF32 bound would
   // rarely certify (measured: 251/256 fix-ups); fp32 certifies every query.
   v->cstore->prefer_simt = 1;
+  TRY(coarse_split_copy(v, st));
   CU(cudaStreamCreateWithFlags(&v->own, cudaStreamNonBlocking));
   CU(cudaStreamSynchronize(st));
   return TRI_OK;
@@ -1310,9 +1386,12 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   if (f16) {
     TRY(ensure(w.Qh, (size_t)B * v->dph * 2));
     TRY(ensure(w.qinv, (size_t)B * sizeof(float)));
+    w.split_q = g_coarse_tc && v->cstore->Ch && v->cstore->dph == v->dph;
+    if (w.split_q) TRY(ensure(w.Ql, (size_t)B * v->dph * 2));
     CU(launch_prep(q, B, v->d, w.Q32.as<float>(), v->qld, w.qn32.as<float>(), w.qn64.as<double>(), nullptr, st,
-                   v->sx, w.Qh.p, v->dph, w.qinv.as<float>()));
+                   v->sx, w.Qh.p, v->dph, w.qinv.as<float>(), w.split_q ? w.Ql.p : nullptr));
   } else {
+    w.split_q = false;
     TRY(prep_queries(w, q, B, v->d, v->qld, st));
   }
   TRY(mark(0));
@@ -1496,7 +1575,7 @@ static bool host_pinned(const void* p) {
 }
 
 long long graph_opts() {
-  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 +
+  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 +
          g_scan_debug * 100003;
 }
 

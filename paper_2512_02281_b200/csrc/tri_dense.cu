@@ -256,8 +256,15 @@ cudaError_t launch_dense(const float* Q, int qld, const float* qn, int B, const 
   dense_gemm_kernel<<<grid, kGThreads, 0, st>>>(Q, qld, B, X, ldx, n, dp, kslice, D, ldd);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  return launch_dense_select(D, used, ldd, B, qn, xn, n, meta, merged, ld_merged, kp_max, st);
+}
+
+cudaError_t launch_dense_select(const float* D, int nsl, long long ldd, int B, const float* qn, const float* xn,
+                                long long n, const QueryMeta* meta, unsigned long long* merged, int ld_merged,
+                                int kp_max, cudaStream_t st) {
+  if (B <= 0) return cudaSuccess;
   if (n > (long long)kSelThreads * kSelPer || kp_max > kSelCap / 2) return cudaErrorInvalidValue;
-  dense_select_kernel<<<B, kSelThreads, 0, st>>>(D, used, ldd, B, qn, xn, n, meta, merged, ld_merged);
+  dense_select_kernel<<<B, kSelThreads, 0, st>>>(D, nsl, ldd, B, qn, xn, n, meta, merged, ld_merged);
   return cudaGetLastError();
 }
 

@@ -91,7 +91,7 @@ cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st);
 // copy (scale sx of the index's fp16 rows) in the same kernel.
 cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,
                         int* bad, cudaStream_t st, float sx = 1.f, void* Qh = nullptr, int ldh = 0,
-                        float* qinv = nullptr);
+                        float* qinv = nullptr, void* Ql = nullptr);
 cudaError_t launch_absmax(const float* X, long long n, int d, long long ldx, unsigned int* bits, cudaStream_t st);
 cudaError_t launch_to_half(const float* X, long long n, int d, long long ldx, float sx, void* Xh, int ldh,
                            cudaStream_t st);
@@ -109,6 +109,36 @@ extern int g_dense_slices;       // slices used (option "dense_slices", <= kDens
 cudaError_t launch_dense(const float* Q, int qld, const float* qn, int B, const float* X, long long ldx,
                          const float* xn, long long n, int dp, float* D, long long ldd, const QueryMeta* meta,
                          unsigned long long* merged, int ld_merged, int kp_max, cudaStream_t st);
+
+// tensor-core coarse GEMM (tri_coarse.cu): split-fp16 operands, K-split
+// TMEM accumulators; writes the fp32 dot of every (query, centroid) to P.
+struct CoarseLaunch {
+  const void* map_h;  // CUtensorMap over the centroids' fp16 hi copy (64-half x 128-row SW128 boxes)
+  const void* map_l;  // ... and the lo copy
+  const void* Qh;     // B x ldq fp16 hi of the scaled queries (prep)
+  const void* Ql;     // ... lo
+  int ldq;            // halves per query row (multiple of 64)
+  const float* qinv;  // 1 / (s_q * s_list) per query (< 0: unscalable)
+  float ratio;        // s_list / s_centroid (power of two): qinv * ratio = 1 / (s_q * s_centroid)
+  int B;
+  long long n;        // centroids
+  int nslab;          // ldq / 64
+  float* P;           // coarse_tc_slices(nslab) x B x ldd partial dots (split-K)
+  long long ldd;
+  int slab_cap;       // set by launch_coarse_tc
+  int tmem_cols;      // set by launch_coarse_tc
+};
+extern int g_coarse_split;
+int coarse_tc_slices(int nslab);
+size_t coarse_tc_smem(int slab_cap);
+cudaError_t launch_coarse_tc(const CoarseLaunch& a, cudaStream_t st);
+cudaError_t launch_to_half_lo(const float* X, long long n, int d, long long ldx, float sx, void* Xl, int ldh,
+                              cudaStream_t st);
+
+// per-query top-kp of nsl summed dot slices (D: nsl x B x ldd fp32)
+cudaError_t launch_dense_select(const float* D, int nsl, long long ldd, int B, const float* qn, const float* xn,
+                                long long n, const QueryMeta* meta, unsigned long long* merged, int ld_merged,
+                                int kp_max, cudaStream_t st);
 
 cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, unsigned long long* merged,
                          int ld_merged, int B, int kp_max, cudaStream_t st);

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double* __rest
                                                             float* __restrict__ Q32, int qld, float* __restrict__ qn32,
                                                             double* __restrict__ qn64, int* bad, float sx,
                                                             __half* __restrict__ Qh, int ldh,
-                                                            float* __restrict__ qinv) {
+                                                            float* __restrict__ qinv, __half* __restrict__ Ql) {
   const int q = blockIdx.x, tid = threadIdx.x;
   double v[kPrepMaxU];
 #pragma unroll
@@ -96,18 +96,23 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double* __rest
 #pragma unroll
     for (int u = 0; u < kPrepMaxU; ++u) {
       const int j = tid + u * kPrepThreads;
-      if (j < ldh) Qh[(long long)q * ldh + j] = __float2half_rn(j < d ? f[u] * sq : 0.f);
+      if (j < ldh) {
+        const float v = j < d ? f[u] * sq : 0.f;  // exact (power-of-two scale)
+        const __half h = __float2half_rn(v);
+        Qh[(long long)q * ldh + j] = h;
+        if (Ql) Ql[(long long)q * ldh + j] = __float2half_rn(v - __half2float(h));  // exact difference
+      }
     }
     if (tid == 0) qinv[q] = badh ? -1.f : 1.f / (sq * sx);
   }
 }
 
 cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,
-                        int* bad, cudaStream_t st, float sx, void* Qh, int ldh, float* qinv) {
+                        int* bad, cudaStream_t st, float sx, void* Qh, int ldh, float* qinv, void* Ql) {
   if (B <= 0) return cudaSuccess;
   if (qld > kPrepThreads * kPrepMaxU || (Qh && ldh > kPrepThreads * kPrepMaxU)) return cudaErrorInvalidValue;
   prep_kernel<<<B, kPrepThreads, 0, st>>>(q64, d, Q32, qld, qn32, qn64, bad, sx, static_cast<__half*>(Qh), ldh,
-                                          qinv);
+                                          qinv, static_cast<__half*>(Ql));
   return cudaGetLastError();
 }
 
