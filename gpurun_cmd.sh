@@ -1,4 +1,3 @@
 timeout 900 python -m pytest tests -m gpu -x -q --timeout 600 -p no:randomly > gpurun_out/t.log 2>&1; echo tests=$?; tail -2 gpurun_out/t.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo bench=$?; python -c "
-import json;d=json.load(open('gpurun_out/bench_full.json'));r=d['roofline'];print(round(d['value']), round(d['e2e']['value']), round(d['ms_per_step'],4), round(r['frac'],3), round(r['isolated']['frac'],3)); c=d['configs']; print({k:(round(v.get('qps',0)) if isinstance(v,dict) else v) for k,v in c.items()}); print(c['C3']['parity'])"
+timeout 600 python tools/stage_experiment.py --opts "force_fixup=1" "force_fixup=0" > gpurun_out/s.log 2>&1; tail -2 gpurun_out/s.log
+timeout 600 python tools/c3_stages.py "coarse_tc=0" "coarse_tc=1" > gpurun_out/c3.log 2>&1; tail -2 gpurun_out/c3.log

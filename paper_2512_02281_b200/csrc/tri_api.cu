@@ -707,7 +707,7 @@ int dense_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q6
   TRY(ensure(w.exact, (size_t)B * w.kp_max * 16));
   TRY(ensure(w.flags, (size_t)(B + 64) * sizeof(int)));
   const QueryMeta* meta = static_cast<const QueryMeta*>(w.plan.p);
-  CU(cudaMemsetAsync(w.flags.p, 0, sizeof(int), st));
+  CU(cudaMemsetAsync(w.flags.p, 0, 2 * sizeof(int), st));  // flag count + fix-up completion counter
   if (s->Ch && qw.split_q) {  // tensor-core coarse GEMM on the split fp16 copies
     CoarseLaunch c;
     c.map_h = &s->tmap_ch;
@@ -748,7 +748,7 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   int* n_flag = w.flags.as<int>();
   int* flag_list = n_flag + 64;
   CU(cudaMemsetAsync(ctr + 1, 0, sizeof(int), st));
-  CU(cudaMemsetAsync(n_flag, 0, sizeof(int), st));
+  CU(cudaMemsetAsync(n_flag, 0, 2 * sizeof(int), st));  // flag count + fix-up completion counter
 
   ScanLaunch sl{};
   sl.tmap = &s->tmap;
@@ -1506,7 +1506,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   TRY(mark(4));
   int* n_flag = w.flags.as<int>();
   int* flag_list = n_flag + 64;
-  CU(cudaMemsetAsync(n_flag, 0, sizeof(int), st));
+  CU(cudaMemsetAsync(n_flag, 0, 2 * sizeof(int), st));  // flag count + fix-up completion counter
   RerankLaunch rr{};
   rr.merged = w.merged.as<unsigned long long>();
   rr.exact = reinterpret_cast<Exact*>(w.exact.p);

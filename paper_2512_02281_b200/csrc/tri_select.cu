@@ -853,11 +853,15 @@ __device__ __forceinline__ long long fx_total(const FixupLaunch& f, int q) {
   return t;
 }
 
+__device__ void fixup_merge_all(const FixupLaunch& f, int S, const Exact* part, int ldp, Exact* mbuf2);
+
 __global__ void __launch_bounds__(kThreads) fixup_part_kernel(FixupLaunch f, int S, int cap, Exact* part, int ldp) {
   extern __shared__ Exact fbuf[];
   __shared__ int s_cnt;
   __shared__ Exact s_thr;
+  __shared__ int s_last;
   const int units = *f.n_flag * S;
+  if (units == 0) return;  // every query certified: nothing to do (the common case)
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int fi = u / S, sl = u - fi * S;
     const int q = f.flag_list[fi];
@@ -919,11 +923,19 @@ __global__ void __launch_bounds__(kThreads) fixup_part_kernel(FixupLaunch f, int
     for (int j = threadIdx.x; j < k; j += kThreads) dst[j] = j < n ? fbuf[j] : exact_max();
     __syncthreads();
   }
+  // the last CTA to finish merges every flagged query's slices (partials
+  // published with a fence before the completion ticket)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(const_cast<int*>(f.n_flag) + 1, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  fixup_merge_all(f, S, part, ldp, fbuf);
 }
 
-__global__ void __launch_bounds__(kThreads) fixup_merge_kernel(FixupLaunch f, int S, const Exact* part, int ldp) {
-  extern __shared__ Exact mbuf2[];
-  for (int fi = blockIdx.x; fi < *f.n_flag; fi += gridDim.x) {
+__device__ void fixup_merge_all(const FixupLaunch& f, int S, const Exact* part, int ldp, Exact* mbuf2) {
+  for (int fi = 0; fi < *f.n_flag; ++fi) {
     const int q = f.flag_list[fi];
     const int k = f.meta[q].k;
     const int n = S * k, p2 = next_pow2(n);
@@ -951,19 +963,13 @@ cudaError_t launch_fixup(const FixupLaunch& f, cudaStream_t st) {
   if (f.B <= 0) return cudaSuccess;
   const int S = fixup_slices(f.k_max);
   const int cap = next_pow2(f.k_max + kThreads);
-  const size_t smem = (size_t)cap * sizeof(Exact);
+  const size_t smem = std::max((size_t)cap, (size_t)next_pow2(S * f.k_max)) * sizeof(Exact);
   cudaError_t e = cudaFuncSetAttribute(fixup_part_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   fixup_part_kernel<<<nsm, kThreads, smem, st>>>(f, S, cap, f.scratch, f.k_max);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  const size_t msmem = (size_t)next_pow2(S * f.k_max) * sizeof(Exact);
-  e = cudaFuncSetAttribute(fixup_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
-  if (e != cudaSuccess) return e;
-  fixup_merge_kernel<<<nsm, kThreads, msmem, st>>>(f, S, f.scratch, f.k_max);
   return cudaGetLastError();
 }
 
