@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 600 -p no:randomly > gpurun_out/t.log 2>&1; echo tests=$?; tail -2 gpurun_out/t.log
-timeout 600 python tools/stage_experiment.py --opts "force_fixup=1" "force_fixup=0" > gpurun_out/s.log 2>&1; tail -2 gpurun_out/s.log
-timeout 600 python tools/c3_stages.py "coarse_tc=0" "coarse_tc=1" > gpurun_out/c3.log 2>&1; tail -2 gpurun_out/c3.log
+timeout 600 python tools/bench_engine.py > gpurun_out/eng1.json 2>gpurun_out/eng1.err; echo e1=$?; python -c "
+import json; d=json.load(open('gpurun_out/eng1.json')); print({k: d[k] for k in ('qps','e2e_batched_qps','sequential_qps','sequential_device_qps','batch_fill','parity')})"; tail -2 gpurun_out/eng1.err

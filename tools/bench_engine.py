@@ -77,6 +77,17 @@ def run(n=100_000, d=128, nq=4096, reps=5, check=64, cpu_sample=32, degree=16):
     bdt = float(np.median(btimes))
     dev = float(np.median(devs)) / 1e3
 
+    # the reference CLI's other mode (cli.py:255-270): one request at a time
+    n_seq = 64
+    ms0, _ = eng.device_time()
+    t0 = time.perf_counter()
+    for q in queries[:n_seq]:
+        eng.submit(q, k=10)
+        eng.run_to_completion()
+    seq_dt = time.perf_counter() - t0
+    ms1, _ = eng.device_time()
+    fill = eng.stats.real_tasks / max(1, eng.stats.real_tasks + eng.stats.dummy_tasks)
+
     ids, dd, ext, _, _ = orc.engine_run(data, graph.adjacency, queries[:check], np.full(check, 10),
                                         np.zeros(check, np.int64))
     # the oracle runs the first `check` queries alone; trajectories are per
@@ -96,6 +107,9 @@ def run(n=100_000, d=128, nq=4096, reps=5, check=64, cpu_sample=32, degree=16):
         "us_per_step": dev * 1e6 / max(steps, 1),
         "e2e_qps": nq / dt, "e2e_note": "submit() per query + run_to_completion() + result() objects",
         "e2e_batched_qps": nq / bdt, "e2e_batched_note": "submit_many() + run_to_completion() + result_arrays()",
+        "sequential_qps": n_seq / seq_dt, "sequential_device_qps": n_seq / ((ms1 - ms0) / 1e3),
+        "sequential_note": "one request at a time (submit + run_to_completion), the reference CLI's per-request mode",
+        "batch_fill": fill,
         "distance_evals": evals,
         "distance_evals_per_s": evals / dev,
         "parity": f"{'ok' if ok else 'MISMATCH'}: first {check} results == CPU engine oracle (ids, f64 dists, extends)",
