@@ -425,10 +425,10 @@ def run_ours(args):
     peak, peak_kind = load_peaks()
     avg_scan_ms = scan_ms / max(scan_n, 1)
     achieved = scan_bytes / (avg_scan_ms / 1e3) / 1e9
-    # prep, dense GEMM, dense select, re-rank, fix-up part + merge (coarse);
-    # 3 packer kernels; list scan; merge; re-rank; fix-up part + merge (fine);
-    # + the shard merge when N > 1 (NCCL's own kernels not counted)
-    kernels_per_step = 14 + (1 if world > 1 else 0)
+    # prep, coarse tensor-core GEMM, select, re-rank, fix-up (coarse); 3 packer
+    # kernels; list scan; merge; re-rank; fix-up (fine); + the shard merge
+    # when N > 1 (NCCL's own kernels not counted)
+    kernels_per_step = 12 + (1 if world > 1 else 0)
     line = {
         "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
