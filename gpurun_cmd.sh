@@ -1,4 +1,1 @@
-s=$(date +%s); timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo bench=$? secs=$(( $(date +%s) - s )); python -c "
-import json;d=json.load(open('gpurun_out/bench_full.json'));r=d['roofline'];print(round(d['value']), round(d['e2e']['value']), round(d['ms_per_step'],4), round(r['frac'],3), round(r['isolated']['frac'],3), d['gpu_launches'], d['clocks'], d['e2e']['batch_latency_ms']['p99'])"
-s=$(date +%s); timeout 900 python bench.py --impl reference > gpurun_out/ref.json 2> gpurun_out/ref.err; echo ref=$? secs=$(( $(date +%s) - s )); python -c "
-import json;d=json.load(open('gpurun_out/ref.json')); print(d['value'], d['cpu_baseline'])"
+timeout 900 python -m pytest tests/test_gpu_ivf.py -x -q --timeout 600 -p no:randomly -k odd_and_wide > gpurun_out/t.log 2>&1; echo tests=$?; tail -15 gpurun_out/t.log

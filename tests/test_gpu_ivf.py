@@ -305,3 +305,25 @@ def test_ivf_save_load_same_results(small, tmp_path):
     a = idx.search(qs, g["ks"], g["nprobes"])
     b = idx2.search(qs, g["ks"], g["nprobes"])
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("d", [3, 33, 130, 1100])
+def test_ivf_odd_and_wide_dims(d, scan_kernel):
+    """Row widths off the fast paths: odd d (scalar exact distances), d not a
+    multiple of 16 or 64 (padding), d > 1024 (no tensor-core scan / split
+    coarse copies: SIMT paths)."""
+    if scan_kernel not in ("auto", "simt"):
+        pytest.skip("one accelerated and one SIMT configuration are enough here")
+    n = 6000
+    data = gen_matrix(n, d, 900 + d)
+    idx = IVFFlatIndex.train(VectorStore(data=data), nlist=48, iters=3, seed=2)
+    cen, asg = idx.export()
+    art = orc.IVFArtifact(cen, asg)
+    qs = gen_matrix(20, d, 901 + d)
+    ks = np.array([1, 10, 50, 7] * 5)
+    nps = np.array([1, 4, 12, 48] * 5)
+    ids, dist = idx.search(qs, ks, nps)
+    for i in range(20):
+        oi, od = orc.ivf_search(data, art, qs[i], int(ks[i]), int(nps[i]))
+        assert np.array_equal(ids[i, :oi.size], oi), (d, i)
+        assert np.array_equal(dist[i, :oi.size], od), (d, i)
