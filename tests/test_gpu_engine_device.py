@@ -127,3 +127,21 @@ def test_device_engine_errors():
     with pytest.raises(ValueError):
         e2.run_to_completion()
     assert eng.run_to_completion() == 0
+
+
+def test_device_engine_limits_and_bad_graph():
+    """Config limits of the device engine and an adjacency id out of range
+    (the reference raises RuntimeError for such a candidate, engine.py:249-250)."""
+    store = VectorStore(data=gen_matrix(40, 4, 3))
+    good = build_knn_graph(store, 4)
+    with pytest.raises(ValueError):
+        ContinuousBatchEngine(store, good, EngineConfig(m=300, p=1, entry_count=2))
+    wide = NeighborGraph(degree=4, adjacency=good.adjacency)
+    with pytest.raises(ValueError):
+        ContinuousBatchEngine(store, wide, EngineConfig(m=256, p=200, entry_count=2))
+    bad_adj = good.adjacency.copy()
+    bad_adj[:, 0] = 10_000
+    eng = ContinuousBatchEngine(store, NeighborGraph(degree=4, adjacency=bad_adj), EngineConfig(m=8, p=1, entry_count=2))
+    eng.submit(gen_matrix(1, 4, 5)[0], k=3)
+    with pytest.raises(RuntimeError):
+        eng.run_to_completion()
