@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_engine_device.py -x -q --timeout 600 -p no:randomly > gpurun_out/t.log 2>&1; echo tests=$?; tail -15 gpurun_out/t.log
+timeout 900 python -m pytest tests/test_gpu_ivf.py -x -q --timeout 600 -p no:randomly -k duplicate > gpurun_out/t.log 2>&1; echo tests=$?; tail -15 gpurun_out/t.log

@@ -327,3 +327,22 @@ def test_ivf_odd_and_wide_dims(d, scan_kernel):
         oi, od = orc.ivf_search(data, art, qs[i], int(ks[i]), int(nps[i]))
         assert np.array_equal(ids[i, :oi.size], oi), (d, i)
         assert np.array_equal(dist[i, :oi.size], od), (d, i)
+
+
+def test_ivf_duplicate_rows_tie_break(scan_kernel):
+    """Every vector stored four times: equal float64 distances everywhere, so the
+    order is decided by the (dist, id) tie rule alone (ann_graph.py:136) and the
+    certificate's strict inequality must route boundary ties to the exact path."""
+    base = gen_matrix(1500, 24, 31)
+    data = np.concatenate([base, base, base, base])  # ids i, i+1500, i+3000, i+4500 identical
+    idx = IVFFlatIndex.train(VectorStore(data=data), nlist=32, iters=3, seed=3)
+    cen, asg = idx.export()
+    art = orc.IVFArtifact(cen, asg)
+    qs = np.concatenate([gen_matrix(12, 24, 32), base[:4].astype(np.float64)])  # the last 4 hit exact copies
+    ks = np.array([10, 3, 40, 9] * 4)
+    nps = np.array([4, 32, 8, 1] * 4)
+    ids, dist = idx.search(qs, ks, nps)
+    for i in range(qs.shape[0]):
+        oi, od = orc.ivf_search(data, art, qs[i], int(ks[i]), int(nps[i]))
+        assert np.array_equal(ids[i, :oi.size], oi), i
+        assert np.array_equal(dist[i, :oi.size], od), i
