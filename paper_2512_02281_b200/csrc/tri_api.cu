@@ -117,6 +117,7 @@ long long g_dense_off = 0;    // 1: never use the dense small-store brute force
 long long g_gthr = 1;         // cross-item per-query threshold in the tensor-core scan
 long long g_coarse_tc = 1;    // IVF coarse GEMM on tensor cores (split fp16) when the index allows
 
+
 // Candidate capacity: over-fetch so the certified re-rank almost never falls
 // back.  TF32 candidates carry ~2^-9 relative dot error, so they over-fetch 2x.
 int kp_for(int k, bool tc) {
@@ -240,6 +241,7 @@ struct Workspace {
   DevBuf gthr;      // per-query cross-item scan threshold
   DevBuf Ql;        // lo half of the split fp16 queries (tensor-core coarse GEMM)
   bool split_q = false;  // this search prepared Qh/Ql/qinv for the split coarse GEMM
+
   DevBuf fxs;       // fix-up partial lists
   HostBuf h_plan;
   HostBuf h_stage[kStaging];
@@ -405,7 +407,8 @@ struct tri_store {
   void* Ch = nullptr;
   void* Cl = nullptr;
   int dph = 0;
-  float split_ratio = 1.f;  // s_list / s_centroid
+  float sc = 1.f;           // power-of-two scale of the split copies
+  float split_ratio = 1.f;  // s_list / s_centroid (IVF centroid stores)
   CUtensorMap tmap_ch, tmap_cl;
   cudaStream_t own = nullptr;
   Lanes lanes;
@@ -536,6 +539,34 @@ int choose_scan(int qld, int d, int B, const int* k, std::vector<int>& kp, ScanC
 }
 
 long long plan_opts() { return g_dense_off * 10000000 + g_scan_kernel * 100000 + g_kp_extra; }
+
+// Split fp16 (hi + lo) copies of a store's rows for the tensor-core GEMM
+// (tri_coarse.cu), scaled by sc = 2^(14 - ilogb(max|x|)), rows of dph halves.
+// Returns TRI_OK without copies when the data's magnitude is out of range.
+static int store_split_copy(tri_store* c, int dph, cudaStream_t st) {
+  if (c->Ch) return TRI_OK;
+  unsigned int* mb = nullptr;
+  CU(cudaMalloc(&mb, sizeof(unsigned int)));
+  CU(cudaMemsetAsync(mb, 0, sizeof(unsigned int), st));
+  CU(launch_absmax(c->X, c->n, c->d, c->dp, mb, st));
+  unsigned int bits = 0;
+  CU(cudaMemcpyAsync(&bits, mb, sizeof(bits), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  cudaFree(mb);
+  float m;
+  std::memcpy(&m, &bits, sizeof(m));
+  if (!(m >= std::ldexp(1.0f, -30) && m <= std::ldexp(1.0f, 30))) return TRI_OK;
+  ++g_epoch;
+  c->sc = std::ldexp(1.0f, 14 - std::ilogb(m));
+  c->dph = dph;
+  CU(cudaMalloc(&c->Ch, (size_t)c->n * dph * 2));
+  CU(cudaMalloc(&c->Cl, (size_t)c->n * dph * 2));
+  CU(launch_to_half(c->X, c->n, c->d, c->dp, c->sc, c->Ch, dph, st));
+  CU(launch_to_half_lo(c->X, c->n, c->d, c->dp, c->sc, c->Cl, dph, st));
+  TRY(make_tmap(&c->tmap_ch, c->Ch, c->n, dph, true, true, 128));
+  TRY(make_tmap(&c->tmap_cl, c->Cl, c->n, dph, true, true, 128));
+  return TRI_OK;
+}
 
 int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_t st) {
   if (w.plan_B == B && w.plan_n == s->n && w.plan_opts == plan_opts() && (int)w.plan_k.size() == B &&
@@ -906,6 +937,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "graphs")) g_graphs = value;
   else if (!std::strcmp(name, "gthr")) g_gthr = value;
   else if (!std::strcmp(name, "coarse_tc")) g_coarse_tc = value;
+
   else if (!std::strcmp(name, "coarse_split")) {
     if (value < 1 || value > kDenseSlices) return fail(TRI_EINVAL, "coarse_split must be in [1, %d]", kDenseSlices);
     tri::g_coarse_split = (int)value;
@@ -1136,32 +1168,12 @@ static tri_ivf* ivf_new(tri_store* s, int nlist) {
   return v;
 }
 
-// Split fp16 copies of the centroids for the tensor-core coarse GEMM, scaled
-// by sc = 2^(14 - ilogb(max|C|)); only when the lists carry the fp16 copy
-// (the queries' split comes from the same prep pass) and the rows fit TMEM.
+// IVF centroid store: split copies sharing the lists' fp16 row width, so the
+// queries' split comes from the fine scan's prep pass (scale ratio s_list / sc).
 static int coarse_split_copy(tri_ivf* v, cudaStream_t st) {
-  tri_store* c = v->cstore;
   if (!v->Xh || v->dph > 1024 || v->nlist > kDenseMaxN) return TRI_OK;
-  unsigned int* mb = nullptr;
-  CU(cudaMalloc(&mb, sizeof(unsigned int)));
-  CU(cudaMemsetAsync(mb, 0, sizeof(unsigned int), st));
-  CU(launch_absmax(c->X, c->n, c->d, c->dp, mb, st));
-  unsigned int bits = 0;
-  CU(cudaMemcpyAsync(&bits, mb, sizeof(bits), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  cudaFree(mb);
-  float m;
-  std::memcpy(&m, &bits, sizeof(m));
-  if (!(m >= std::ldexp(1.0f, -30) && m <= std::ldexp(1.0f, 30))) return TRI_OK;
-  const float sc = std::ldexp(1.0f, 14 - std::ilogb(m));
-  c->dph = v->dph;
-  c->split_ratio = v->sx / sc;  // both powers of two: exact
-  CU(cudaMalloc(&c->Ch, (size_t)c->n * c->dph * 2));
-  CU(cudaMalloc(&c->Cl, (size_t)c->n * c->dph * 2));
-  CU(launch_to_half(c->X, c->n, c->d, c->dp, sc, c->Ch, c->dph, st));
-  CU(launch_to_half_lo(c->X, c->n, c->d, c->dp, sc, c->Cl, c->dph, st));
-  TRY(make_tmap(&c->tmap_ch, c->Ch, c->n, c->dph, true, true, 128));
-  TRY(make_tmap(&c->tmap_cl, c->Cl, c->n, c->dph, true, true, 128));
+  TRY(store_split_copy(v->cstore, v->dph, st));
+  if (v->cstore->Ch) v->cstore->split_ratio = v->sx / v->cstore->sc;  // both powers of two: exact
   return TRI_OK;
 }
 
