@@ -115,6 +115,7 @@ long long g_scan_kernel = 0;  // 0 auto (IVF: fp16 tensor core), 1 fp32 SIMT, 2 
 long long g_scan_debug = 0;   // timing experiments only (results invalid when set)
 long long g_dense_off = 0;    // 1: never use the dense small-store brute force
 long long g_gthr = 1;         // cross-item per-query threshold in the tensor-core scan
+long long g_scan_qbufs = 2;   // tensor-core scan query tiles (option "scan_qbufs": 1 or 2)
 long long g_coarse_tc = 1;    // IVF coarse GEMM on tensor cores (split fp16) when the index allows
 
 
@@ -801,7 +802,8 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   sl.cap = w.cap;
   sl.grid = w.grid;
   sl.dbg = 0;
-  sl.stages = tc_scan_stages(s->qld * 4, kSmemLimit, (int)g_tc_stages);
+  sl.qbufs = (int)g_scan_qbufs;
+  sl.stages = tc_scan_stages(s->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs);
   sl.box_rows = s->box_rows;
   if (g_gthr && w.tc) {
     TRY(ensure(w.gthr, (size_t)B * sizeof(unsigned long long)));
@@ -936,6 +938,10 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "scan_reserve")) g_scan_reserve = value;
   else if (!std::strcmp(name, "graphs")) g_graphs = value;
   else if (!std::strcmp(name, "gthr")) g_gthr = value;
+  else if (!std::strcmp(name, "scan_qbufs")) {
+    if (value != 1 && value != 2) return fail(TRI_EINVAL, "scan_qbufs must be 1 or 2");
+    g_scan_qbufs = value;
+  }
   else if (!std::strcmp(name, "coarse_tc")) g_coarse_tc = value;
 
   else if (!std::strcmp(name, "coarse_split")) {
@@ -1507,7 +1513,8 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   // batches in flight on other streams (the scan is HBM-bound, they are not)
   sl.grid = (int)std::max<long long>(1, std::min<long long>(sm_count(v->device) - g_scan_reserve, members));
   sl.dbg = (int)g_scan_debug;
-  sl.stages = tc_scan_stages(f16 ? v->dph * 2 : v->qld * 4, kSmemLimit, (int)g_tc_stages);
+  sl.qbufs = (int)g_scan_qbufs;
+  sl.stages = tc_scan_stages(f16 ? v->dph * 2 : v->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs);
   sl.box_rows = v->box_rows;
   TRY(mark(2));
   CU(ch.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
@@ -1587,7 +1594,7 @@ static bool host_pinned(const void* p) {
 }
 
 long long graph_opts() {
-  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 +
+  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 +
          g_scan_debug * 100003;
 }
 

@@ -72,6 +72,7 @@ struct ScanLaunch {
   // off): the tensor-core scan publishes each full partial list's kp-th key
   // with atomicMin and filters against the smallest one seen
   unsigned long long* gthr;
+  int qbufs;  // tensor-core scan: query tiles (2 = next item staged during this one; 1 frees a ring stage)
 };
 
 size_t scan_smem_bytes(int gmax, int qld, int cap);
@@ -84,7 +85,7 @@ constexpr int kTcGroup = 16;
 constexpr int kTcMaxKp = 256;  // register-resident top-kp lists in the epilogue
 constexpr int kTcMinStages = 4;
 size_t tc_scan_smem_bytes(int row_bytes);  // minimum (kTcMinStages ring); row_bytes = qld*4 or qldh*2
-int tc_scan_stages(int row_bytes, int smem_limit, int want);  // deepest ring that fits (want > 0 caps it)
+int tc_scan_stages(int row_bytes, int smem_limit, int want, int qbufs);  // deepest ring that fits (want > 0 caps it)
 cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st);
 
 // fp64 queries -> fp32 rows + norms; with Qh != nullptr also the fp16 scan

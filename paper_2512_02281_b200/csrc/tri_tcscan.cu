@@ -118,14 +118,15 @@ struct TcSmem {
 };
 
 // alignment pad + two query tiles + double-buffered append lists
-static size_t tc_fixed_smem(int row_bytes) {
-  return 1024 + (size_t)2 * tc_nslab(row_bytes) * kTcQTile + (size_t)2 * kTcN * kTcRows * 8;
+// alignment pad + qbufs query tiles + double-buffered append lists
+static size_t tc_fixed_smem(int row_bytes, int qbufs) {
+  return 1024 + (size_t)qbufs * tc_nslab(row_bytes) * kTcQTile + (size_t)2 * kTcN * kTcRows * 8;
 }
 
-size_t tc_scan_smem_bytes(int row_bytes) { return tc_fixed_smem(row_bytes) + (size_t)kTcMinStages * kTcSlabBytes; }
+size_t tc_scan_smem_bytes(int row_bytes) { return tc_fixed_smem(row_bytes, 2) + (size_t)kTcMinStages * kTcSlabBytes; }
 
-int tc_scan_stages(int row_bytes, int smem_limit, int want) {
-  int n = (int)(((long long)smem_limit - (long long)tc_fixed_smem(row_bytes)) / kTcSlabBytes);
+int tc_scan_stages(int row_bytes, int smem_limit, int want, int qbufs) {
+  int n = (int)(((long long)smem_limit - (long long)tc_fixed_smem(row_bytes, qbufs)) / kTcSlabBytes);
   if (want > 0) n = std::min(n, want);
   return std::max(std::min(n, kTcMaxStages), 0);
 }
@@ -221,8 +222,8 @@ __device__ void tc_qstage(const ScanLaunch& a, TcSmem& sh, unsigned char* qs, in
   ItemRing r;
   WorkItem w;
   for (int j = 0; next_item(sh, r, w, lane); ++j) {
-    const int qb = j & 1;
-    tmb_wait(&sh.qempty[qb], ((j >> 1) & 1) ^ 1);
+    const int qb = j % a.qbufs;
+    tmb_wait(&sh.qempty[qb], ((j / a.qbufs) & 1) ^ 1);
     unsigned char* dst = qs + qb * qtile_bytes;
     const int gc = w.member_count;
     const int myq = lane < gc ? a.members[w.member_begin + lane].q : 0;
@@ -260,8 +261,8 @@ __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, uns
   ItemRing r;
   WorkItem w;
   for (int j = 0; next_item(sh, r, w, lane); ++j) {
-    const int qb = j & 1;
-    tmb_wait(&sh.qfull[qb], (j >> 1) & 1);
+    const int qb = j % a.qbufs;
+    tmb_wait(&sh.qfull[qb], (j / a.qbufs) & 1);
     const uint32_t qs_s = tsu32(qs + qb * qtile_bytes);
     const int nchunk = (w.row_count + kTcRows - 1) / kTcRows;
     for (int c = 0; c < nchunk; ++c) {
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
   unsigned char* ring = base;
   unsigned char* qs = ring + (size_t)a.stages * kTcSlabBytes;
   const int qtile_bytes = tc_nslab(row_bytes_of<H>(a)) * kTcQTile;
-  unsigned long long* sel = reinterpret_cast<unsigned long long*>(qs + 2 * (size_t)qtile_bytes);
+  unsigned long long* sel = reinterpret_cast<unsigned long long*>(qs + (size_t)a.qbufs * qtile_bytes);
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
@@ -505,7 +506,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
 template <bool H>
 cudaError_t launch_tc(const ScanLaunch& s, cudaStream_t st) {
   if (s.stages < kTcMinStages || s.stages > kTcMaxStages) return cudaErrorInvalidValue;
-  const size_t smem = tc_fixed_smem(H ? s.qldh * 2 : s.qld * 4) + (size_t)s.stages * kTcSlabBytes;
+  if (s.qbufs < 1 || s.qbufs > 2) return cudaErrorInvalidValue;
+  const size_t smem = tc_fixed_smem(H ? s.qldh * 2 : s.qld * 4, s.qbufs) + (size_t)s.stages * kTcSlabBytes;
   cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   scan_tc_kernel<H><<<s.grid, kTcThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(s.tmap_tc),
