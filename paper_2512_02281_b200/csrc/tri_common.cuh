@@ -65,6 +65,7 @@ __device__ __forceinline__ double exact_sq_dist(const double* __restrict__ q, co
 __device__ __forceinline__ double exact_sq_dist_v4(const double* __restrict__ q, const float* __restrict__ x, int d) {
   double l0 = 0.0, l1 = 0.0;
   int i = 0;
+#pragma unroll 4
   for (; i + 8 <= d; i += 8) {
     const float4 lo = *reinterpret_cast<const float4*>(x + i);
     const float4 hi = *reinterpret_cast<const float4*>(x + i + 4);
