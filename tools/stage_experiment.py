@@ -1,6 +1,6 @@
 """Per-stage timings of the C2 search pipeline under library option sets (not a benchmark of record).
 
-python tools/stage_experiment.py --opts "rerank_kernel=0" "rerank_kernel=1" [--n 1000000] [--k 10 --nprobe 32]
+python tools/stage_experiment.py --opts "gthr=0" "gthr=1" [--n 1000000] [--k 10 --nprobe 32]
 
 Each option set: 3 warm-up searches, then 20 profiled ones (CUDA events per
 stage), parity of 4 queries against the CPU oracle, fix-up count.
