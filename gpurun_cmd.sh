@@ -1,5 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_engine.py tests/test_gpu_engine_device.py tests/test_gpu_bruteforce.py -x -q --timeout 600 -p no:randomly > gpurun_out/t.log 2>&1; echo tests=$?; tail -2 gpurun_out/t.log
-timeout 600 python tools/bench_engine.py > gpurun_out/eng1.json 2>/dev/null; python -c "
-import json; d=json.load(open('gpurun_out/eng1.json')); print({k: d[k] for k in ('qps','us_per_step','parity')})"
-timeout 600 python tools/bench_engine.py --n 20000 --d 768 --nq 1024 > gpurun_out/eng2.json 2>/dev/null; python -c "
-import json; d=json.load(open('gpurun_out/eng2.json')); print({k: d[k] for k in ('qps','us_per_step','parity')})"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:randomly > gpurun_out/t.log 2>&1; echo tests=$?; tail -1 gpurun_out/t.log
+s=$(date +%s); timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo bench=$? secs=$(( $(date +%s) - s )); python -c "
+import json;d=json.load(open('gpurun_out/bench_full.json'));r=d['roofline'];print(round(d['value']), round(d['e2e']['value']), round(d['ms_per_step'],4), round(r['frac'],3), round(r['isolated']['frac'],3), d['clocks']['samples']); c=d['configs']; print({k:(round(v.get('qps',0)) if isinstance(v,dict) else v) for k,v in c.items()}); print(c['C1']['ms_per_batch'], c['C3']['qps_one_stream'])"
