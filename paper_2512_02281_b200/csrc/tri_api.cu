@@ -138,6 +138,15 @@ int kp_for_f16(int k) {
   return kp;
 }
 
+// Dense small-store path: its select and re-rank take any capacity, so the
+// over-fetch is rounded to 16 instead of a power of two (nprobe 32 -> 48).
+long long g_dense_pow2 = 0;
+int kp_dense(int k) {
+  if (g_dense_pow2) return kp_for(k, false);
+  const long long want = (long long)k + std::max<long long>(16, k / 4) + g_kp_extra;
+  return (int)std::max<long long>(kMinKp, (want + 15) / 16 * 16);
+}
+
 int cls_of(int kp) {
   int c = 0;
   while ((kMinKp << c) < kp) ++c;
@@ -539,7 +548,7 @@ int choose_scan(int qld, int d, int B, const int* k, std::vector<int>& kp, ScanC
   return TRI_OK;
 }
 
-long long plan_opts() { return g_dense_off * 10000000 + g_scan_kernel * 100000 + g_kp_extra; }
+long long plan_opts() { return g_dense_pow2 * 100000000 + g_dense_off * 10000000 + g_scan_kernel * 100000 + g_kp_extra; }
 
 // Split fp16 (hi + lo) copies of a store's rows for the tensor-core GEMM
 // (tri_coarse.cu), scaled by sc = 2^(14 - ilogb(max|x|)), rows of dph halves.
@@ -579,7 +588,7 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
   {
     int kpd = kMinKp, kmx = 1;
     for (int i = 0; i < B; ++i) {
-      kpd = std::max(kpd, kp_for(k[i], false));
+      kpd = std::max(kpd, kp_dense(k[i]));
       kmx = std::max(kmx, k[i]);
     }
     if (!g_dense_off && s->n <= kDenseMaxN && kpd <= kDenseMaxKp) {
@@ -591,7 +600,7 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
       QueryMeta* hm = static_cast<QueryMeta*>(hp);
       for (int i = 0; i < B; ++i) {
         hm[i].k = k[i];
-        hm[i].kp = kp_for(k[i], false);
+        hm[i].kp = kp_dense(k[i]);
         hm[i].n_slots = 1;
         hm[i].cls = cls_of(hm[i].kp);
         hm[i].part_off = 0;
@@ -943,6 +952,7 @@ int tri_set_option(const char* name, int64_t value) {
     g_scan_qbufs = value;
   }
   else if (!std::strcmp(name, "coarse_tc")) g_coarse_tc = value;
+  else if (!std::strcmp(name, "dense_pow2")) g_dense_pow2 = value;
 
   else if (!std::strcmp(name, "coarse_split")) {
     if (value < 1 || value > kDenseSlices) return fail(TRI_EINVAL, "coarse_split must be in [1, %d]", kDenseSlices);

@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
   if (r.B <= 0) return cudaSuccess;
   // slab width: 2 buffers x kp x (S+4) floats <= ~72 KB (several CTAs per SM)
-  int S = std::max(32, std::min(256, 8192 / r.kp_max));
+  int S = std::max(32, std::min(256, 8192 / r.kp_max)) / 16 * 16;  // slabs hold whole 8-element blocks, 16B rows
   if (g_rerank_smem_cap > 0) {  // leave room for co-resident CTAs (option "rerank_smem_cap")
     const long long fixed = (long long)((r.d + 15) & ~15) * 8 + (long long)r.kp_max * 16;
     const long long fit = (g_rerank_smem_cap - fixed) / (2LL * r.kp_max * 4) - 4;
