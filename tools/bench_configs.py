@@ -87,6 +87,28 @@ def c1(steps: int = 200, peak_gbs: float | None = None) -> dict:
     }
     if peak_gbs:
         out["frac_of_hbm_peak_whole_batch"] = out["store_gbs"] / peak_gbs
+    # batch-size sweep as extra data (queries gen_vectors(B, 128, seed=2))
+    sweep = {}
+    for Bs in (256, 1024):
+        qb = torch.from_numpy(gen_matrix(Bs, 128, 2).astype(np.float64)).cuda()
+        kb = np.full(Bs, 10, np.int32)
+        ib = torch.empty((Bs, 10), dtype=torch.int64, device="cuda")
+        db = torch.empty((Bs, 10), dtype=torch.float64, device="cuda")
+
+        def oneb():
+            _lib.check(lib.tri_knn_bruteforce_dev(store.handle, _lib.ptr(qb), Bs, kb.ctypes.data, 10, _lib.ptr(ib),
+                                                  _lib.ptr(db), C.c_void_p(st.cuda_stream)))
+
+        for _ in range(10):
+            oneb()
+        e0.record(st)
+        for _ in range(50):
+            oneb()
+        e1.record(st)
+        e1.synchronize()
+        msb = e0.elapsed_time(e1) / 50
+        sweep[f"B={Bs}"] = {"qps": Bs / (msb / 1e3), "ms_per_batch": msb}
+    out["batch_sweep"] = sweep
     store.close()
     return out
 
