@@ -810,7 +810,7 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   sl.gmax = w.gmax;
   sl.cap = w.cap;
   sl.grid = w.grid;
-  sl.dbg = 0;
+  sl.dbg = (int)g_scan_debug;
   sl.qbufs = (int)g_scan_qbufs;
   sl.stages = tc_scan_stages(s->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs);
   sl.box_rows = s->box_rows;

@@ -213,6 +213,46 @@ __device__ __forceinline__ void list_merge32(unsigned long long (&v)[KL], unsign
   bitonic_merge_regs<KL>(v, lane);
 }
 
+// v (sorted, 32*KL distinct keys) <- smallest 32*KL of v U {x}: x lands at
+// pos = #{v < x}, the tail shifts up one (a no-op when pos == 32*KL).  A few
+// shuffles per key instead of a 32-wide sort + merge: the fold for chunks that
+// admit only a handful of candidates.
+template <int KL>
+__device__ __forceinline__ void list_insert(unsigned long long (&v)[KL], unsigned long long x, int lane) {
+  int pos = 0;
+#pragma unroll
+  for (int j = 0; j < KL; ++j) pos += __popc(__ballot_sync(0xffffffffu, v[j] < x));
+  unsigned long long carry = 0;
+#pragma unroll
+  for (int j = 0; j < KL; ++j) {
+    unsigned long long up = __shfl_up_sync(0xffffffffu, v[j], 1);
+    const unsigned long long last = __shfl_sync(0xffffffffu, v[j], 31);
+    if (lane == 0) up = carry;
+    const int i = j * 32 + lane;
+    v[j] = i < pos ? v[j] : (i == pos ? x : up);
+    carry = last;
+  }
+}
+
+// Fold up to 32 candidates (one per lane, TRI_KEY_MAX = none) into the sorted
+// list: by insertion when at most kInsMax of them beat the list's last key,
+// else by sort + bitonic merge.
+constexpr int kInsMax = 8;
+template <int KL>
+__device__ __forceinline__ void list_fold32(unsigned long long (&v)[KL], unsigned long long x, int lane) {
+  const unsigned long long kth = __shfl_sync(0xffffffffu, v[KL - 1], 31);
+  unsigned m = __ballot_sync(0xffffffffu, x < kth);
+  if (__popc(m) <= kInsMax) {
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      list_insert<KL>(v, __shfl_sync(0xffffffffu, x, src), lane);
+    }
+  } else {
+    list_merge32<KL>(v, warp_sort32(x, lane), lane);
+  }
+}
+
 // v (sorted) <- smallest 32*KL of v U p where p is a sorted list of the same
 // size given REVERSED (p_rev[j] on lane l = p[KP-1 - (j*32+l)]).
 template <int KL>

@@ -308,7 +308,8 @@ __device__ void tc_mma(const ScanLaunch& a, TcSmem& sh, unsigned char* ring, uns
 // kp = 32*KL).  Per 128-row chunk, all 256 threads append the candidates that
 // beat the query's threshold to its smem buffer (double-buffered by chunk
 // parity); after ONE named barrier each owner folds its buffer in 32 at a
-// time: register bitonic sort (shuffles), bitonic split against the list's
+// time: by insertion when few of them beat the list's last key (list_insert),
+// else register bitonic sort (shuffles), bitonic split against the list's
 // last 32, bitonic merge.  Thresholds are published by the owner and read
 // (possibly one chunk stale, which only admits more candidates) by appenders.
 constexpr int kEpiWarps = 8;
@@ -383,9 +384,7 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
         const int n = sh.cnt[buf][g];
         const unsigned long long* sb = sel + (size_t)buf * kTcN * kTcRows + g * kTcRows;
         for (int b = 0; b < n; b += 32) {
-          unsigned long long x = b + lane < n ? sb[b + lane] : TRI_KEY_MAX;
-          x = warp_sort32(x, lane);
-          list_merge32<KL>(L[qi], x, lane);
+          list_fold32<KL>(L[qi], b + lane < n ? sb[b + lane] : TRI_KEY_MAX, lane);
         }
         if (n > 0) {
           unsigned long long t = __shfl_sync(0xffffffffu, L[qi][KL - 1], 31);

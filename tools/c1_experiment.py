@@ -33,7 +33,7 @@ for spec in sys.argv[1:] or [""]:
         _lib.check(lib.tri_knn_bruteforce_dev(store.handle, _lib.ptr(q), 64, ks.ctypes.data, 10, _lib.ptr(ids),
                                               _lib.ptr(d), C.c_void_p(st.cuda_stream)))
 
-    for _ in range(5):
+    for _ in range(60):  # the first tens of batches after a store's creation run slower
         one()
     st.synchronize()
     ok = np.array_equal(ids.cpu().numpy(), g["ids"]) and np.array_equal(d.cpu().numpy(), g["dists"])
