@@ -112,6 +112,7 @@ long long g_box_rows = 128;     // rows per TMA box of the tensor-core scan maps
 long long g_scan_reserve = 0;  // SMs the IVF list scan leaves to other streams
 long long g_tc_stages = 0;   // tensor-core scan ring depth cap (0 = as deep as shared memory allows)
 long long g_scan_kernel = 0;  // 0 auto (IVF: fp16 tensor core), 1 fp32 SIMT, 2 TF32 tensor core
+long long g_scan_l2hint = 1;  // L2 policy of the IVF tensor-core scan's row loads (option "scan_l2hint")
 long long g_scan_debug = 0;   // timing experiments only (results invalid when set)
 long long g_dense_off = 0;    // 1: never use the dense small-store brute force
 long long g_gthr = 1;         // cross-item per-query threshold in the tensor-core scan
@@ -507,6 +508,7 @@ int store_from_device(const float* Xdev, long long ldx, long long n, int d, int 
     return fail(TRI_ECUDA, "store creation failed: %s", cudaGetErrorString(e));
   }
   std::memcpy(&s->xmax, &bits, sizeof(double));
+  if (std::getenv("TRI_DEBUG_ALLOC")) std::fprintf(stderr, "[tri] store X=%p xnorm=%p\n", (void*)s->X, (void*)s->xnorm);
   int rc = make_tmap(&s->tmap, s->X, n, s->dp, false);
   if (rc == TRI_OK) rc = make_tmap(&s->tmap_tc, s->X, n, s->dp, true, false, (int)g_box_rows);
   if (rc == TRI_OK) rc = make_tmap(&s->tmap_tc_tail, s->X, n, s->dp, true, false, 32);
@@ -811,6 +813,7 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   sl.cap = w.cap;
   sl.grid = w.grid;
   sl.dbg = (int)g_scan_debug;
+  sl.l2hint = 0;  // rows re-read by the batch's other query groups: default L2 policy
   sl.qbufs = (int)g_scan_qbufs;
   sl.stages = tc_scan_stages(s->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs);
   sl.box_rows = s->box_rows;
@@ -947,6 +950,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "scan_reserve")) g_scan_reserve = value;
   else if (!std::strcmp(name, "graphs")) g_graphs = value;
   else if (!std::strcmp(name, "gthr")) g_gthr = value;
+  else if (!std::strcmp(name, "scan_l2hint")) g_scan_l2hint = value;
   else if (!std::strcmp(name, "scan_qbufs")) {
     if (value != 1 && value != 2) return fail(TRI_EINVAL, "scan_qbufs must be 1 or 2");
     g_scan_qbufs = value;
@@ -1523,6 +1527,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   // batches in flight on other streams (the scan is HBM-bound, they are not)
   sl.grid = (int)std::max<long long>(1, std::min<long long>(sm_count(v->device) - g_scan_reserve, members));
   sl.dbg = (int)g_scan_debug;
+  sl.l2hint = (int)g_scan_l2hint;  // lists stream once per batch: evict_first keeps centroids / queries in L2
   sl.qbufs = (int)g_scan_qbufs;
   sl.stages = tc_scan_stages(f16 ? v->dph * 2 : v->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs);
   sl.box_rows = v->box_rows;

@@ -73,6 +73,7 @@ struct ScanLaunch {
   // with atomicMin and filters against the smallest one seen
   unsigned long long* gthr;
   int qbufs;  // tensor-core scan: query tiles (2 = next item staged during this one; 1 frees a ring stage)
+  int l2hint;  // tensor-core scan TMA loads: 0 default, 1 L2 evict_first, 2 L2 evict_last
 };
 
 size_t scan_smem_bytes(int gmax, int qld, int cap);

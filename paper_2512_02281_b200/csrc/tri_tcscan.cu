@@ -75,6 +75,14 @@ __device__ __forceinline__ void ttma_2d(void* dst, const CUtensorMap* map, int c
       "l"(map), "r"(c0), "r"(c1), "r"(tsu32(bar))
       : "memory");
 }
+__device__ __forceinline__ void ttma_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                             uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(tsu32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(tsu32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 2, 256;\n" ::: "memory"); }
 
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
@@ -174,6 +182,9 @@ __device__ void tc_producer(const ScanLaunch& a, const CUtensorMap* map, const C
     }
     return ok;
   };
+  uint64_t pol = 0;
+  if (a.l2hint == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  if (a.l2hint == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
   int cur = atomicAdd(a.counter, 1);
   if (!publish(cur)) return;
   for (;;) {
@@ -195,8 +206,12 @@ __device__ void tc_producer(const ScanLaunch& a, const CUtensorMap* map, const C
         tmb_wait(&sh.empty[stage], sphase ^ 1);
         unsigned char* dst = ring + (size_t)stage * kTcSlabBytes;
         tmb_expect(&sh.full[stage], (uint32_t)(nbox * br * kTcRowB));
-        for (int b = 0; b < nbox; ++b)
-          ttma_2d(dst + b * br * kTcRowB, m, s * slab_elems<H>(), row0 + b * br, &sh.full[stage]);
+        for (int b = 0; b < nbox; ++b) {
+          if (a.l2hint)
+            ttma_2d_hint(dst + b * br * kTcRowB, m, s * slab_elems<H>(), row0 + b * br, &sh.full[stage], pol);
+          else
+            ttma_2d(dst + b * br * kTcRowB, m, s * slab_elems<H>(), row0 + b * br, &sh.full[stage]);
+        }
         if (++stage == a.stages) {
           stage = 0;
           sphase ^= 1;
