@@ -53,7 +53,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=24, help="queries timed for cpu_baseline")
     ap.add_argument("--tc-stages", type=int, default=0, help="tensor-core scan ring depth cap (0 = deepest)")
-    ap.add_argument("--scan-reserve", type=int, default=0, help="SMs the list scan leaves to other lanes")
+    ap.add_argument("--scan-reserve", type=int, default=-1,
+                    help="SMs the list scan leaves to other lanes (-1: the library's choice, 8 with > 1 lane)")
     ap.add_argument("--opt", action="append", default=[], help="library option name=value (experiments)")
     ap.add_argument("--no-configs", action="store_true", help="skip the secondary-config measurements (C1/C3/C5/engine)")
     ap.add_argument("--lanes", type=int, default=4,
@@ -337,8 +338,11 @@ def run_ours(args):
     idx.set_profiling(False)
     total_ms = ev0.elapsed_time(ev1)
     # supplementary: the same scan with no other lane beside it (one stream,
-    # 50 searches), i.e. the kernel's own bandwidth rather than its share of a mix
+    # 50 searches), i.e. the kernel's own bandwidth rather than its share of a mix;
+    # every SM goes to the scan (no SMs reserved for other lanes)
     n_iso = 50
+    reserve_opt = dict(o.split("=", 1) for o in args.opt).get("scan_reserve")
+    _lib.set_option("scan_reserve", 0)
     for _ in range(3):
         idx.search_device(q_dev, K, NPROBE, lane_ids[0], lane_d[0], lanes[0])
     torch.cuda.synchronize()
@@ -348,6 +352,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     iso_ms, iso_n = idx.scan_time()
     idx.set_profiling(False)
+    _lib.set_option("scan_reserve", int(reserve_opt) if reserve_opt is not None else args.scan_reserve)
     if dist:
         t = torch.tensor([total_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
