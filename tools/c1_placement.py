@@ -1,3 +1,10 @@
+"""C1 brute-force time per batch for several allocations of the same store (not a benchmark of record).
+
+python tools/c1_placement.py   (TRI_DEBUG_ALLOC=1 prints each store's device addresses)
+
+Each store: 100 + 300 batches per L2 policy of the scan loads (scan_l2hint 0, 1, 2, 0).
+Shows the per-allocation fast / slow modes described in DESIGN.md section 9.
+"""
 import ctypes as C, os, sys, time
 import numpy as np, torch
 sys.path.insert(0, os.getcwd())
