@@ -26,5 +26,5 @@ for spec in sys.argv[1:] or [""]:
     r = b.c3(idx, data, art)
     st, n = idx.stage_times()
     idx.set_profiling(False)
-    print(f"[{spec or 'defaults'}] qps {r['qps']:.0f} ms/batch {r['ms_per_batch']:.3f} fixups(last) {idx.last_fixups()} "
+    print(f"[{spec or 'defaults'}] qps {r['qps']:.0f} ms/batch(1 stream) {r['ms_per_batch_one_stream']:.3f} fixups(last) {idx.last_fixups()} "
           + json.dumps({k: round(v / n * 1e3, 1) for k, v in st.items()}) + " " + r["parity"], flush=True)
