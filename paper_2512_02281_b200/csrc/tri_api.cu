@@ -116,6 +116,7 @@ long long g_scan_l2hint = 1;  // L2 policy of the IVF tensor-core scan's row loa
 long long g_scan_debug = 0;   // timing experiments only (results invalid when set)
 long long g_dense_off = 0;    // 1: never use the dense small-store brute force
 long long g_gthr = 1;         // cross-item per-query threshold in the tensor-core scan
+long long g_scan_abufs = 1;  // IVF tensor-core scan append-list buffers (option "scan_abufs": 1 or 2)
 long long g_scan_qbufs = 2;   // tensor-core scan query tiles (option "scan_qbufs": 1 or 2)
 long long g_coarse_tc = 1;    // IVF coarse GEMM on tensor cores (split fp16) when the index allows
 
@@ -826,7 +827,8 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   sl.dbg = (int)g_scan_debug;
   sl.l2hint = 0;  // rows re-read by the batch's other query groups: default L2 policy
   sl.qbufs = (int)g_scan_qbufs;
-  sl.stages = tc_scan_stages(s->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs);
+  sl.abufs = 2;  // brute force: selection-bound (L2-resident rows), keep one barrier per chunk
+  sl.stages = tc_scan_stages(s->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs, sl.abufs);
   sl.box_rows = s->box_rows;
   if (g_gthr && w.tc) {
     TRY(ensure(w.gthr, (size_t)B * sizeof(unsigned long long)));
@@ -962,6 +964,10 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "graphs")) g_graphs = value;
   else if (!std::strcmp(name, "gthr")) g_gthr = value;
   else if (!std::strcmp(name, "scan_l2hint")) g_scan_l2hint = value;
+  else if (!std::strcmp(name, "scan_abufs")) {
+    if (value != 1 && value != 2) return fail(TRI_EINVAL, "scan_abufs must be 1 or 2");
+    g_scan_abufs = value;
+  }
   else if (!std::strcmp(name, "scan_qbufs")) {
     if (value != 1 && value != 2) return fail(TRI_EINVAL, "scan_qbufs must be 1 or 2");
     g_scan_qbufs = value;
@@ -1540,7 +1546,9 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   sl.dbg = (int)g_scan_debug;
   sl.l2hint = (int)g_scan_l2hint;  // lists stream once per batch: evict_first keeps centroids / queries in L2
   sl.qbufs = (int)g_scan_qbufs;
-  sl.stages = tc_scan_stages(f16 ? v->dph * 2 : v->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs);
+  // one append buffer: the list scan is stream-bound, and the 16 KB buy a ring stage
+  sl.abufs = (int)g_scan_abufs;
+  sl.stages = tc_scan_stages(f16 ? v->dph * 2 : v->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs, sl.abufs);
   sl.box_rows = v->box_rows;
   TRY(mark(2));
   CU(ch.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
@@ -1621,7 +1629,7 @@ static bool host_pinned(const void* p) {
 
 long long graph_opts() {
   return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 +
-         g_scan_debug * 100003 + g_scan_l2hint * 1000003;
+         g_scan_debug * 100003 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
 }
 
 

@@ -73,6 +73,7 @@ struct ScanLaunch {
   // with atomicMin and filters against the smallest one seen
   unsigned long long* gthr;
   int qbufs;  // tensor-core scan: query tiles (2 = next item staged during this one; 1 frees a ring stage)
+  int abufs;  // tensor-core scan: append-list buffers (2 = one barrier per chunk; 1 = two barriers, frees a ring stage)
   int l2hint;  // tensor-core scan TMA loads: 0 default, 1 L2 evict_first, 2 L2 evict_last
 };
 
@@ -86,7 +87,7 @@ constexpr int kTcGroup = 16;
 constexpr int kTcMaxKp = 256;  // register-resident top-kp lists in the epilogue
 constexpr int kTcMinStages = 4;
 size_t tc_scan_smem_bytes(int row_bytes);  // minimum (kTcMinStages ring); row_bytes = qld*4 or qldh*2
-int tc_scan_stages(int row_bytes, int smem_limit, int want, int qbufs);  // deepest ring that fits (want > 0 caps it)
+int tc_scan_stages(int row_bytes, int smem_limit, int want, int qbufs, int abufs);  // deepest ring that fits (want > 0 caps it)
 cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st);
 
 // fp64 queries -> fp32 rows + norms; with Qh != nullptr also the fp16 scan

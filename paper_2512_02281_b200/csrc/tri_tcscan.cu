@@ -125,16 +125,15 @@ struct TcSmem {
   float qinv[kTcN];
 };
 
-// alignment pad + two query tiles + double-buffered append lists
-// alignment pad + qbufs query tiles + double-buffered append lists
-static size_t tc_fixed_smem(int row_bytes, int qbufs) {
-  return 1024 + (size_t)qbufs * tc_nslab(row_bytes) * kTcQTile + (size_t)2 * kTcN * kTcRows * 8;
+// alignment pad + qbufs query tiles + abufs append-list buffers
+static size_t tc_fixed_smem(int row_bytes, int qbufs, int abufs) {
+  return 1024 + (size_t)qbufs * tc_nslab(row_bytes) * kTcQTile + (size_t)abufs * kTcN * kTcRows * 8;
 }
 
-size_t tc_scan_smem_bytes(int row_bytes) { return tc_fixed_smem(row_bytes, 2) + (size_t)kTcMinStages * kTcSlabBytes; }
+size_t tc_scan_smem_bytes(int row_bytes) { return tc_fixed_smem(row_bytes, 2, 2) + (size_t)kTcMinStages * kTcSlabBytes; }
 
-int tc_scan_stages(int row_bytes, int smem_limit, int want, int qbufs) {
-  int n = (int)(((long long)smem_limit - (long long)tc_fixed_smem(row_bytes, qbufs)) / kTcSlabBytes);
+int tc_scan_stages(int row_bytes, int smem_limit, int want, int qbufs, int abufs) {
+  int n = (int)(((long long)smem_limit - (long long)tc_fixed_smem(row_bytes, qbufs, abufs)) / kTcSlabBytes);
   if (want > 0) n = std::min(n, want);
   return std::max(std::min(n, kTcMaxStages), 0);
 }
@@ -349,7 +348,7 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
   volatile unsigned long long* thr = sh.thr;
   unsigned long long gpre[2] = {TRI_KEY_MAX, TRI_KEY_MAX};  // owner lane 0: cross-item bound, loaded ahead
   for (int c = 0; c < nchunk; ++c) {
-    const int buf = c & 1;
+    const int buf = a.abufs == 2 ? (c & 1) : 0;
     const int rows = min(kTcRows, w.row_count - c * kTcRows);
     if (a.gthr && lane == 0) {  // issued before the TMEM wait: the L2 round trip overlaps it
 #pragma unroll
@@ -420,6 +419,7 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
         if (lane == 0) sh.cnt[buf][g] = 0;
       }
     }
+    if (a.abufs == 1) epi_sync();  // single append buffer: drained before the next chunk appends
   }
 #pragma unroll
   for (int qi = 0; qi < 2; ++qi) {
@@ -520,8 +520,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
 template <bool H>
 cudaError_t launch_tc(const ScanLaunch& s, cudaStream_t st) {
   if (s.stages < kTcMinStages || s.stages > kTcMaxStages) return cudaErrorInvalidValue;
-  if (s.qbufs < 1 || s.qbufs > 2) return cudaErrorInvalidValue;
-  const size_t smem = tc_fixed_smem(H ? s.qldh * 2 : s.qld * 4, s.qbufs) + (size_t)s.stages * kTcSlabBytes;
+  if (s.qbufs < 1 || s.qbufs > 2 || s.abufs < 1 || s.abufs > 2) return cudaErrorInvalidValue;
+  const size_t smem = tc_fixed_smem(H ? s.qldh * 2 : s.qld * 4, s.qbufs, s.abufs) + (size_t)s.stages * kTcSlabBytes;
   cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   scan_tc_kernel<H><<<s.grid, kTcThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(s.tmap_tc),
