@@ -346,3 +346,37 @@ def test_ivf_duplicate_rows_tie_break(scan_kernel):
         oi, od = orc.ivf_search(data, art, qs[i], int(ks[i]), int(nps[i]))
         assert np.array_equal(ids[i, :oi.size], oi), i
         assert np.array_equal(dist[i, :oi.size], od), i
+
+
+_SCAN_OPTS = [
+    {"scan_abufs": 2},
+    {"scan_l2hint": 0},
+    {"scan_l2hint": 2},
+    {"scan_reserve": 16},
+    {"scan_reserve": 0},
+    {"scan_qbufs": 1, "tc_stages": 4},
+]
+_SCAN_DEFAULTS = {"scan_abufs": 1, "scan_l2hint": 1, "scan_reserve": -1, "scan_qbufs": 2, "tc_stages": 0}
+
+
+@pytest.mark.parametrize("opts", _SCAN_OPTS, ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
+def test_ivf_scan_options_parity(small, opts):
+    """Scan tuning options (append buffers, L2 policy, reserved SMs, ring depth)
+    change scheduling only: results stay equal to the golden vectors, also with
+    batches on several streams (the automatic SM reservation)."""
+    import torch
+
+    g, data, idx = small
+    qs = gen_matrix(40, 32, 7)
+    try:
+        for k, v in opts.items():
+            _lib.set_option(k, v)
+        streams = [torch.cuda.Stream() for _ in range(3)]
+        for st in streams:
+            ids = np.full((40, int(g["ks"].max())), -1, np.int64)
+            d = np.full(ids.shape, np.inf)
+            idx.search_into(qs.astype(np.float64), g["ks"], g["nprobes"], ids, d, stream=st)
+            _check_rows(ids, d, g, g["ks"])
+    finally:
+        for k, v in _SCAN_DEFAULTS.items():
+            _lib.set_option(k, v)
