@@ -866,6 +866,8 @@ int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Wo
   rr.out_ids = ids;
   rr.out_d = dists;
   rr.ldo = ldo;
+  TRY(ensure(w.fxs, fixup_scratch_bytes(B, w.k_max)));  // fix-up bounds + partial lists
+  rr.fx_thr = static_cast<unsigned long long*>(w.fxs.p);
   rr.n_flag = n_flag;
   rr.flag_list = flag_list;
   rr.B = B;
@@ -891,8 +893,23 @@ int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Wo
   fx.ldo = ldo;
   fx.B = B;
   fx.k_max = w.k_max;
-  TRY(ensure(w.fxs, fixup_scratch_bytes(B, w.k_max)));
-  fx.scratch = w.fxs.as<Exact>();
+  fx.fx_thr = static_cast<unsigned long long*>(w.fxs.p);
+  fx.fx_cnt = reinterpret_cast<int*>(static_cast<unsigned char*>(w.fxs.p) + fixup_thr_bytes(B));
+  fx.scratch = reinterpret_cast<Exact*>(static_cast<unsigned char*>(w.fxs.p) + fixup_thr_bytes(B) +
+                                        fixup_cnt_bytes(B, w.k_max));
+  fx.max_units = fixup_max_units(B, w.k_max);
+  fx.slice_rows = (int)tri::g_fx_slice_rows;
+  {
+    const Bound bs = bound_for(s->d, kSimt);
+    fx.Q32 = qw.Q32.as<float>();
+    fx.qld = s->qld;
+    fx.qn32 = qw.qn32.as<float>();
+    fx.qn64 = qw.qn64.as<double>();
+    fx.xnorm = s->xnorm;
+    fx.xmax = s->xmax;
+    fx.cdot = bs.cdot;
+    fx.csum = bs.csum;
+  }
   CU(launch_fixup(fx, st));
   return TRI_OK;
 }
@@ -983,6 +1000,10 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "dense_slices")) tri::g_dense_slices = (int)value;
   else if (!std::strcmp(name, "rerank_smem_cap")) tri::g_rerank_smem_cap = value;
   else if (!std::strcmp(name, "rerank_f2f")) tri::g_rerank_f2f = value;
+  else if (!std::strcmp(name, "fx_slice_rows")) {
+    if (value < 32) return fail(TRI_EINVAL, "fx_slice_rows must be >= 32");
+    tri::g_fx_slice_rows = value;
+  }
   else if (!std::strcmp(name, "tc_box_rows")) {
     if (value != 32 && value != 64 && value != 128) return fail(TRI_EINVAL, "tc_box_rows must be 32, 64 or 128");
     g_box_rows = value;
@@ -1580,6 +1601,8 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   rr.out_ids = reinterpret_cast<long long*>(ids);
   rr.out_d = dists;
   rr.ldo = ldo;
+  TRY(ensure(w.fxs, fixup_scratch_bytes(B, k_max)));  // fix-up bounds + partial lists
+  rr.fx_thr = static_cast<unsigned long long*>(w.fxs.p);
   rr.n_flag = n_flag;
   rr.flag_list = flag_list;
   rr.B = B;
@@ -1606,8 +1629,23 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   fx.ldo = ldo;
   fx.B = B;
   fx.k_max = k_max;
-  TRY(ensure(w.fxs, fixup_scratch_bytes(B, k_max)));
-  fx.scratch = w.fxs.as<Exact>();
+  fx.fx_thr = static_cast<unsigned long long*>(w.fxs.p);
+  fx.fx_cnt = reinterpret_cast<int*>(static_cast<unsigned char*>(w.fxs.p) + fixup_thr_bytes(B));
+  fx.scratch = reinterpret_cast<Exact*>(static_cast<unsigned char*>(w.fxs.p) + fixup_thr_bytes(B) +
+                                        fixup_cnt_bytes(B, k_max));
+  fx.max_units = fixup_max_units(B, k_max);
+  fx.slice_rows = (int)tri::g_fx_slice_rows;
+  {
+    const Bound bs = bound_for(v->d, kSimt);
+    fx.Q32 = w.Q32.as<float>();
+    fx.qld = v->qld;
+    fx.qn32 = w.qn32.as<float>();
+    fx.qn64 = w.qn64.as<double>();
+    fx.xnorm = v->xnl;
+    fx.xmax = v->xmax;
+    fx.cdot = bs.cdot;
+    fx.csum = bs.csum;
+  }
   CU(launch_fixup(fx, st));
   TRY(mark(6));
   if (rec && !w.capturing) v->ev_used++;
@@ -1628,7 +1666,7 @@ static bool host_pinned(const void* p) {
 }
 
 long long graph_opts() {
-  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 +
+  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_fx_slice_rows * 7919 +
          g_scan_debug * 100003 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
 }
 

@@ -168,13 +168,15 @@ struct RerankLaunch {
   int ldo;
   int* n_flag;
   int* flag_list;
+  unsigned long long* fx_thr;  // per flagged query: the fix-up's exact k-th bound (set to +inf when flagged)
   int B;
   int kp_max;
   const float* qinv;        // fp16 scan: qinv[q] < 0 marks a query the scan could not scale (never certified)
 };
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st);
 extern long long g_rerank_smem_cap;  // bytes; 0 = no cap
-extern long long g_rerank_f2f;       // 1: hardware F2F conversions in the re-rank (else integer bit moves)
+extern long long g_rerank_f2f;
+extern long long g_fx_slice_rows;  // fix-up: minimum rows per slice       // 1: hardware F2F conversions in the re-rank (else integer bit moves)
 
 struct FixupLaunch {
   const int* n_flag;
@@ -196,9 +198,28 @@ struct FixupLaunch {
   int ldo;
   int B;
   int k_max;
-  Exact* scratch;  // fixup_scratch_bytes(B, k_max): per-(query, slice) partial top-k
+  Exact* scratch;  // per-(flagged query, slice) partial top-k (fixup_part_bytes(B, k_max) from fixup_scratch)
+  unsigned long long* fx_thr;  // per flagged query: smallest slice k-th exact distance (double bits)
+  int* fx_cnt;                 // per (flagged query, slice): entries in its partial list
+  int max_units;               // partial lists the scratch holds (slices x flagged queries)
+  int slice_rows;              // minimum rows per slice (option "fx_slice_rows")
+  // fp32 pre-filter: a row's exact distance is computed only when its fp32
+  // distance (the SIMT scan's arithmetic) is within 4x the SIMT error bound of
+  // the current fix-up bound
+  const float* Q32;
+  int qld;
+  const float* qn32;
+  const double* qn64;
+  const float* xnorm;  // norms of the rows of X
+  double xmax;
+  double cdot, csum;   // bound_for(d, kSimt)
 };
+// Fix-up scratch: fx_thr (B x 8 bytes), fx_cnt (max_units ints), each
+// 256-aligned, then the partial lists.
 size_t fixup_scratch_bytes(int B, int k_max);
+size_t fixup_thr_bytes(int B);
+size_t fixup_cnt_bytes(int B, int k_max);
+int fixup_max_units(int B, int k_max);
 cudaError_t launch_fixup(const FixupLaunch& f, cudaStream_t st);
 
 cudaError_t launch_distance_tasks(const int* owner, const long long* cand, int n_tasks, const double* q64, int d,

@@ -21,6 +21,7 @@ namespace tri {
 constexpr int kThreads = 256;
 long long g_rerank_smem_cap = 0;
 long long g_rerank_f2f = 1;
+long long g_fx_slice_rows = 256;
 
 // ---------------------------------------------------------------------------
 // Query preparation and row norms.
@@ -218,6 +219,15 @@ cudaError_t launch_prep_half(const float* Q32, int B, int qld, int d, float sx, 
   if (B <= 0) return cudaSuccess;
   prep_half_kernel<<<B, 128, 0, st>>>(Q32, qld, d, sx, static_cast<__half*>(Qh), ldh, qinv);
   return cudaGetLastError();
+}
+
+// Queue an uncertified query for the exact fix-up.  Its fix-up bound starts
+// at dk, the k-th exact distance among the re-ranked candidates: k real rows
+// lie at or below it, so the exact top-k does too (+inf when dk is not finite).
+__device__ __forceinline__ void flag_query(const RerankLaunch& r, int q, double dk) {
+  const int fi = atomicAdd(r.n_flag, 1);
+  r.flag_list[fi] = q;
+  r.fx_thr[fi] = (dk >= 0.0 && dk < INFINITY) ? (unsigned long long)__double_as_longlong(dk) : 0x7ff0000000000000ull;
 }
 
 // Certification test (k-th exact distance dk, kp-th kept approx distance T).
@@ -540,9 +550,9 @@ __device__ __forceinline__ void finalize_query(const RerankLaunch& r, int q, int
     }
   // certification: every dropped candidate has approx distance >= T
   bool cert = true;
+  double dk = INFINITY;
   if (m.n_total > m.kp) {
     const int kk = m.k - 1;
-    double dk = 0.0;
 #pragma unroll
     for (int j = 0; j < KL; ++j) {
       const double t = __shfl_sync(0xffffffffu, d[j], kk & 31);
@@ -550,7 +560,7 @@ __device__ __forceinline__ void finalize_query(const RerankLaunch& r, int q, int
     }
     cert = certified(r, q, dk, (double)key_dist(r.merged[(long long)q * r.ld_merged + m.kp - 1]));
   }
-  if (!cert && lane == 0) r.flag_list[atomicAdd(r.n_flag, 1)] = q;
+  if (!cert && lane == 0) flag_query(r, q, dk);
 #pragma unroll
   for (int j = 0; j < KL; ++j) {
     const int e = j * 32 + lane;
@@ -588,7 +598,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(RerankLaunch r) {
     if (m.n_total > kp) {
       cert = certified(r, q, ebuf[m.k - 1].d, (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]));
     }
-    if (!cert) r.flag_list[atomicAdd(r.n_flag, 1)] = q;
+    if (!cert) flag_query(r, q, ebuf[m.k - 1].d);
   }
   for (int j = threadIdx.x; j < m.k; j += blockDim.x) {
     const Exact e = ebuf[j];
@@ -786,7 +796,7 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
     if (m.n_total > kp) {
       cert = certified(r, q, s_dk, (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]));
     }
-    if (!cert) r.flag_list[atomicAdd(r.n_flag, 1)] = q;
+    if (!cert) flag_query(r, q, s_dk);
   }
 }
 
@@ -837,116 +847,311 @@ cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
 // Exact fix-up for uncertified queries: fp64 scan of the full candidate set.
 
 // Split fix-up.  Each uncertified query's candidate set (the concatenation of
-// its probed lists, or all rows) is cut into S slices; a persistent grid walks
-// the (flagged query, slice) units, computes exact float64 distances of its
-// slice (the reference order) and keeps the slice's top-k (threshold +
-// compaction + smem sort), then a second persistent kernel merges the S
-// partial lists of each flagged query.  With no flagged query both kernels
-// exit at once.
-__device__ __forceinline__ long long fx_total(const FixupLaunch& f, int q) {
-  if (!f.probes) return f.n_rows;
+// its probed lists, or all rows) is cut into slices of >= kThreads rows, at
+// most S per query, S chosen on the device from the flagged count so that the
+// units fill about kFxWaves x the grid (one flagged query alone spreads over
+// every SM).  The query's bound fx_thr starts at the re-rank's k-th exact
+// distance (flag_query), so only rows at or below it can enter the top-k.
+// A unit screens its rows with the fp32 distance of the SIMT scan: only rows
+// within 4x the SIMT error bound of the bound get the exact float64 distance
+// (the reference order), because fp64 runs at a small fraction of the fp32
+// rate.  Survivors are kept as the slice's top-k (threshold + compaction +
+// smem sort), and a full slice publishes its k-th distance to fx_thr
+// (atomicMin on the double's bits, d >= 0).  The last CTA merges each
+// query's slice lists, keeping only entries at or below the final bound.
+// With no flagged query the kernel exits at once.
+constexpr int kFxWaves = 3;
+constexpr int kFxSurv = 1024;  // screened rows per slice awaiting their exact distance
+
+// Block-wide sum over the block of a 64-bit value (every thread gets it).
+__device__ __forceinline__ long long fx_block_sum(long long v, long long* s_w) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+  __syncthreads();
   long long t = 0;
-  for (int j = 0; j < f.nprobe[q]; ++j) {
-    const long long l = f.probes[(long long)q * f.ld_probes + j];
-    t += f.list_off[l + 1] - f.list_off[l];
-  }
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) t += s_w[w];
+  __syncthreads();
   return t;
 }
 
-__device__ void fixup_merge_all(const FixupLaunch& f, int S, const Exact* part, int ldp, Exact* mbuf2);
+// Candidate-set size of query q: its probed lists' lengths summed by the block
+// (one parallel round of loads instead of a chain of nprobe dependent ones).
+__device__ __forceinline__ long long fx_total(const FixupLaunch& f, int q, long long* s_w) {
+  if (!f.probes) return f.n_rows;
+  long long t = 0;
+  for (int j = threadIdx.x; j < f.nprobe[q]; j += kThreads) {
+    const long long l = f.probes[(long long)q * f.ld_probes + j];
+    t += f.list_off[l + 1] - f.list_off[l];
+  }
+  return fx_block_sum(t, s_w);
+}
 
-__global__ void __launch_bounds__(kThreads) fixup_part_kernel(FixupLaunch f, int S, int cap, Exact* part, int ldp) {
+// Slices of a query's candidate set: >= rows_min rows each, at most S.
+__device__ __forceinline__ int fx_slices_of(long long total, int S, int rows_min) {
+  return (int)max(1LL, min((long long)S, total / rows_min));
+}
+
+// The query's current fix-up bound as an Exact (ties at the bound distance pass).
+__device__ __forceinline__ Exact fx_bound(const FixupLaunch& f, int fi) {
+  Exact e;
+  e.d = __longlong_as_double((long long)__ldcg(f.fx_thr + fi));
+  e.id = 0x7fffffffffffffffll;
+  return e;
+}
+
+// Stream-compacted candidates in fbuf (count s_cnt, capacity cap): sort and keep
+// the k best once fewer than kThreads free slots remain (or when forced).
+// Returns the count, negative when fbuf was left unsorted.
+__device__ __forceinline__ int fx_compact(Exact* fbuf, int* s_cnt, int cap, int k, bool force) {
+  const int n = *s_cnt;
+  if (force || n > cap - kThreads) {
+    const int p2 = next_pow2(n > 0 ? n : 1);
+    for (int i = n + threadIdx.x; i < p2; i += kThreads) fbuf[i] = exact_max();
+    __syncthreads();
+    block_sort(fbuf, p2, ExactLess());
+    __syncthreads();
+    if (threadIdx.x == 0 && n > k) *s_cnt = k;
+    __syncthreads();
+    return min(n, k);
+  }
+  return -1 - n;
+}
+
+// After a round of appends (and a barrier): compact if needed, publish a full
+// list's k-th distance to the query's bound, pick up a tighter bound.  Ends
+// with a barrier.
+__device__ __forceinline__ void fx_update(const FixupLaunch& f, int fi, int k, Exact* fbuf, int* s_cnt, int cap,
+                                          Exact* s_thr) {
+  const int n = fx_compact(fbuf, s_cnt, cap, k, false);  // < 0: not sorted this round
+  if (threadIdx.x == 0) {
+    if (n >= k && exact_less(fbuf[k - 1], *s_thr)) {
+      *s_thr = fbuf[k - 1];
+      atomicMin(f.fx_thr + fi, (unsigned long long)__double_as_longlong(fbuf[k - 1].d));
+    }
+    const Exact g = fx_bound(f, fi);  // tighter bound from another slice
+    if (exact_less(g, *s_thr)) *s_thr = g;
+  }
+  __syncthreads();
+}
+
+__device__ void fixup_merge_all(const FixupLaunch& f, int S, const Exact* part, int ldp, Exact* fbuf, int cap,
+                                int* s_cnt, long long* s_w);
+
+__global__ void __launch_bounds__(kThreads) fixup_part_kernel(FixupLaunch f, int cap, Exact* part, int ldp) {
   extern __shared__ Exact fbuf[];
   __shared__ int s_cnt;
   __shared__ Exact s_thr;
   __shared__ int s_last;
-  const int units = *f.n_flag * S;
-  if (units == 0) return;  // every query certified: nothing to do (the common case)
+  __shared__ long long s_w[kThreads / 32];
+  __shared__ long long s_rlo[kThreads], s_rlen[kThreads], s_rpre[kThreads];
+  __shared__ long long s_surv[kFxSurv];
+  __shared__ int s_ns, s_ovf;
+  const int nf = *f.n_flag;
+  if (nf == 0) return;  // every query certified: nothing to do (the common case)
+  const int S = max(1, min((kFxWaves * (int)gridDim.x + nf - 1) / nf, f.max_units / nf));
+  const int units = nf * S;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int fi = u / S, sl = u - fi * S;
     const int q = f.flag_list[fi];
     const int k = f.meta[q].k;
     const double* qv = f.q64 + (long long)q * f.d;
-    const long long total = fx_total(f, q);
-    const long long c0 = total * sl / S, c1 = total * (sl + 1) / S;
+    const long long total = fx_total(f, q, s_w);
+    const int Sq = fx_slices_of(total, S, f.slice_rows);
+    if (sl >= Sq) continue;  // uniform per CTA
+    const long long c0 = total * sl / Sq, c1 = total * (sl + 1) / Sq;
+    const float4* q4 = reinterpret_cast<const float4*>(f.Q32 + (size_t)q * f.qld);
+    const float qn = f.qn32[q];
+    const double sn = f.qn64[q] + f.xmax;
+    const double Epre = 4.0 * (f.cdot * 2.0 * f.qn64[q] * f.xmax + f.csum * sn * sn) + 1e-30;
     if (threadIdx.x == 0) {
       s_cnt = 0;
-      s_thr = exact_max();
+      s_thr = fx_bound(f, fi);
     }
     __syncthreads();
-    // walk the ranges overlapping [c0, c1) of the concatenated candidate order
-    const int nranges = f.probes ? f.nprobe[q] : 1;
-    long long before = 0;
-    for (int rg = 0; rg < nranges && before < c1; ++rg) {
-      long long lo = 0, hi = f.n_rows;
-      if (f.probes) {
-        const long long l = f.probes[(long long)q * f.ld_probes + rg];
-        lo = f.list_off[l];
-        hi = f.list_off[l + 1];
+    // Pass 0 screens every row of the slice with its fp32 distance, one warp
+    // per 4 rows (coalesced row loads), and records survivors in s_surv; pass
+    // 1 (only if s_surv overflowed) computes the exact distance of every row.
+    if (threadIdx.x == 0) {
+      s_ns = 0;
+      s_ovf = 0;
+    }
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1 && !s_ovf) break;  // uniform: read after a barrier
+      // walk the ranges overlapping [c0, c1) of the concatenated candidate
+      // order, kThreads probes at a time: lengths loaded in parallel, block prefix sum
+      const int nranges = f.probes ? f.nprobe[q] : 1;
+      long long before = 0;
+      for (int cs = 0; cs < nranges && before < c1; cs += kThreads) {
+        const int j = cs + threadIdx.x;
+        long long lo = 0, len = 0;
+        if (j < nranges) {
+          if (f.probes) {
+            const long long l = f.probes[(long long)q * f.ld_probes + j];
+            lo = f.list_off[l];
+            len = f.list_off[l + 1] - lo;
+          } else {
+            len = f.n_rows;
+          }
+        }
+        long long inc = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+          if ((threadIdx.x & 31) >= o) inc += y;
+        }
+        if ((threadIdx.x & 31) == 31) s_w[threadIdx.x >> 5] = inc;
+        __syncthreads();
+        long long off = 0, chunk = 0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) {
+          if (w < (threadIdx.x >> 5)) off += s_w[w];
+          chunk += s_w[w];
+        }
+        s_rlo[threadIdx.x] = lo;
+        s_rlen[threadIdx.x] = len;
+        s_rpre[threadIdx.x] = before + off + inc - len;
+        __syncthreads();
+        const int nr = min(kThreads, nranges - cs);
+        for (int rg = 0; rg < nr; ++rg) {
+          const long long pre = s_rpre[rg], rlen = s_rlen[rg], rlo = s_rlo[rg];
+          const long long a = max(c0, pre), b = min(c1, pre + rlen);
+          if (a >= b) continue;  // uniform: shared-memory values
+          const long long r0 = rlo + (a - pre), r1 = rlo + (b - pre);
+          if (pass == 0) {
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            const double lim = fx_bound(f, fi).d + Epre;
+            for (long long row0 = r0 + warp * 4; row0 < r1; row0 += kThreads / 32 * 4) {
+              // the 4 rows' loads issue together (rows past r1 re-read row r1 - 1)
+              float acc[4] = {0.f, 0.f, 0.f, 0.f};
+              const float4* x4[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                x4[i] = reinterpret_cast<const float4*>(f.X + min(row0 + i, r1 - 1) * f.ldx);
+#pragma unroll 2
+              for (int c = lane; c < (f.qld >> 2); c += 32) {
+                const float4 y = __ldg(q4 + c);
+                float4 x[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) x[i] = __ldg(x4[i] + c);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  acc[i] = __fmaf_rn(x[i].x, y.x, acc[i]);
+                  acc[i] = __fmaf_rn(x[i].y, y.y, acc[i]);
+                  acc[i] = __fmaf_rn(x[i].z, y.z, acc[i]);
+                  acc[i] = __fmaf_rn(x[i].w, y.w, acc[i]);
+                }
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int o = 16; o; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+              if (lane < 4 && row0 + lane < r1) {
+                const long long row = row0 + lane;
+                const float dot = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+                const float d32 = __fmaf_rn(-2.f, dot, __fadd_rn(qn, f.xnorm[row]));
+                if (!isfinite(d32) || (double)d32 <= lim) {
+                  const int idx = atomicAdd(&s_ns, 1);
+                  if (idx < kFxSurv) s_surv[idx] = row;
+                  else s_ovf = 1;
+                }
+              }
+            }
+          } else {
+            for (long long base = r0; base < r1; base += kThreads) {
+              const long long row = base + threadIdx.x;
+              const Exact thr = s_thr;
+              if (row < r1) {
+                Exact e;
+                e.d = exact_sq_dist_any(qv, f.X + row * f.ldx, f.d);
+                e.id = (f.idmap ? f.idmap[row] : row) + f.id_offset;
+                if (exact_less(e, thr)) fbuf[atomicAdd(&s_cnt, 1)] = e;
+              }
+              __syncthreads();
+              fx_update(f, fi, k, fbuf, &s_cnt, cap, &s_thr);
+            }
+          }
+        }
+        before += chunk;
+        __syncthreads();  // s_w / s_r* are rewritten by the next chunk
       }
-      const long long len = hi - lo;
-      const long long a = max(c0, before), b = min(c1, before + len);
-      if (a < b) {
-        const long long r0 = lo + (a - before), r1 = lo + (b - before);
-        for (long long base = r0; base < r1; base += kThreads) {
-          const long long row = base + threadIdx.x;
+      if (pass == 0 && !s_ovf) {
+        // exact distances of the survivors, kThreads at a time
+        const int ns = s_ns;
+        for (int b0 = 0; b0 < ns; b0 += kThreads) {
           const Exact thr = s_thr;
-          if (row < r1) {
+          if (b0 + (int)threadIdx.x < ns) {
+            const long long row = s_surv[b0 + threadIdx.x];
             Exact e;
             e.d = exact_sq_dist_any(qv, f.X + row * f.ldx, f.d);
             e.id = (f.idmap ? f.idmap[row] : row) + f.id_offset;
             if (exact_less(e, thr)) fbuf[atomicAdd(&s_cnt, 1)] = e;
           }
           __syncthreads();
-          const int n = s_cnt;
-          if (n > cap - kThreads) {
-            const int p2 = next_pow2(n);
-            for (int i = n + threadIdx.x; i < p2; i += kThreads) fbuf[i] = exact_max();
-            __syncthreads();
-            block_sort(fbuf, p2, ExactLess());
-            if (threadIdx.x == 0 && n >= k) {
-              s_cnt = k;
-              s_thr = fbuf[k - 1];
-            }
-          }
-          __syncthreads();
+          fx_update(f, fi, k, fbuf, &s_cnt, cap, &s_thr);
         }
       }
-      before += len;
+      __syncthreads();
     }
-    const int n = s_cnt;
-    const int p2 = next_pow2(n > 0 ? n : 1);
-    for (int i = n + threadIdx.x; i < p2; i += kThreads) fbuf[i] = exact_max();
-    __syncthreads();
-    block_sort(fbuf, p2, ExactLess());
+    const int n = fx_compact(fbuf, &s_cnt, cap, k, true);
+    if (threadIdx.x == 0 && n >= k)
+      atomicMin(f.fx_thr + fi, (unsigned long long)__double_as_longlong(fbuf[k - 1].d));
     Exact* dst = part + ((long long)fi * S + sl) * ldp;
-    for (int j = threadIdx.x; j < k; j += kThreads) dst[j] = j < n ? fbuf[j] : exact_max();
+    for (int j = threadIdx.x; j < n; j += kThreads) dst[j] = fbuf[j];
+    if (threadIdx.x == 0) f.fx_cnt[fi * S + sl] = n;
     __syncthreads();
   }
-  // the last CTA to finish merges every flagged query's slices (partials
-  // published with a fence before the completion ticket)
+  // the last CTA to finish merges every flagged query's slices (partials and
+  // bounds published with a fence before the completion ticket)
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(const_cast<int*>(f.n_flag) + 1, 1) == (int)gridDim.x - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  fixup_merge_all(f, S, part, ldp, fbuf);
+  fixup_merge_all(f, S, part, ldp, fbuf, cap, &s_cnt, s_w);
 }
 
-__device__ void fixup_merge_all(const FixupLaunch& f, int S, const Exact* part, int ldp, Exact* mbuf2) {
+__device__ void fixup_merge_all(const FixupLaunch& f, int S, const Exact* part, int ldp, Exact* fbuf, int cap,
+                                int* s_cnt, long long* s_w) {
   for (int fi = 0; fi < *f.n_flag; ++fi) {
     const int q = f.flag_list[fi];
     const int k = f.meta[q].k;
-    const int n = S * k, p2 = next_pow2(n);
-    for (int i = threadIdx.x; i < p2; i += kThreads) {
-      const int sl = i / k, j = i - sl * k;
-      mbuf2[i] = i < n ? part[((long long)fi * S + sl) * ldp + j] : exact_max();
-    }
+    const Exact bound = fx_bound(f, fi);
+    if (threadIdx.x == 0) *s_cnt = 0;
     __syncthreads();
-    block_sort(mbuf2, p2, ExactLess());
+    // slice lists are sorted: thread t walks slices t, t + kThreads, ... one
+    // entry per round (at most kThreads appends between compactions) and
+    // stops at the first entry above the bound
+    const int Sq = fx_slices_of(fx_total(f, q, s_w), S, f.slice_rows);
+    for (int s0 = 0; s0 < Sq; s0 += kThreads) {
+      const int sl = s0 + threadIdx.x;
+      const int cnt = sl < Sq ? f.fx_cnt[fi * S + sl] : 0;
+      const Exact* src = part + ((long long)fi * S + sl) * ldp;
+      int j = 0;
+      for (;;) {
+        bool more = false;
+        if (j < cnt) {
+          const Exact e = src[j];
+          if (!exact_less(bound, e)) {
+            fbuf[atomicAdd(s_cnt, 1)] = e;
+            more = ++j < cnt;
+          } else {
+            j = cnt;
+          }
+        }
+        if (!__syncthreads_or(more)) break;
+        fx_compact(fbuf, s_cnt, cap, k, false);
+        __syncthreads();  // the count is read before anyone appends again
+      }
+      fx_compact(fbuf, s_cnt, cap, k, false);
+      __syncthreads();
+    }
+    const int n = fx_compact(fbuf, s_cnt, cap, k, true);
     for (int j = threadIdx.x; j < k; j += kThreads) {
-      const Exact e = mbuf2[j];
+      const Exact e = j < n ? fbuf[j] : exact_max();
       const bool ok = e.id != 0x7fffffffffffffffll;
       f.out_ids[(long long)q * f.ldo + j] = ok ? e.id : -1;
       f.out_d[(long long)q * f.ldo + j] = e.d;
@@ -957,19 +1162,28 @@ __device__ void fixup_merge_all(const FixupLaunch& f, int S, const Exact* part, 
 
 int fixup_slices(int k_max) { return std::max(1, std::min(32, 4096 / std::max(1, k_max))); }
 
-size_t fixup_scratch_bytes(int B, int k_max) { return (size_t)B * fixup_slices(k_max) * k_max * sizeof(Exact); }
+size_t fixup_thr_bytes(int B) { return ((size_t)B * sizeof(unsigned long long) + 255) & ~(size_t)255; }
+
+int fixup_max_units(int B, int k_max) { return B * fixup_slices(k_max); }
+
+size_t fixup_cnt_bytes(int B, int k_max) {
+  return ((size_t)fixup_max_units(B, k_max) * sizeof(int) + 255) & ~(size_t)255;
+}
+
+size_t fixup_scratch_bytes(int B, int k_max) {
+  return fixup_thr_bytes(B) + fixup_cnt_bytes(B, k_max) + (size_t)fixup_max_units(B, k_max) * k_max * sizeof(Exact);
+}
 
 cudaError_t launch_fixup(const FixupLaunch& f, cudaStream_t st) {
   if (f.B <= 0) return cudaSuccess;
-  const int S = fixup_slices(f.k_max);
   const int cap = next_pow2(f.k_max + kThreads);
-  const size_t smem = std::max((size_t)cap, (size_t)next_pow2(S * f.k_max)) * sizeof(Exact);
+  const size_t smem = (size_t)cap * sizeof(Exact);
   cudaError_t e = cudaFuncSetAttribute(fixup_part_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  fixup_part_kernel<<<nsm, kThreads, smem, st>>>(f, S, cap, f.scratch, f.k_max);
+  fixup_part_kernel<<<4 * nsm, kThreads, smem, st>>>(f, cap, f.scratch, f.k_max);
   return cudaGetLastError();
 }
 

@@ -132,6 +132,30 @@ def test_exact_ties_break_by_id():
         assert np.array_equal(ids[i], oi) and np.array_equal(d[i], od)
 
 
+@pytest.mark.parametrize("slice_rows", [256, 8192])
+def test_fixup_screening_and_overflow(slice_rows):
+    """Fix-up internals: 6000 duplicate rows tie exactly with the k-th distance,
+    so every row of a slice survives the fp32 screen; slices of 8192 rows
+    overflow the survivor buffer and take the exact-every-row pass."""
+    rng = np.random.Generator(np.random.Philox(77))
+    far = rng.standard_normal((14_000, 24)).astype(np.float32) + 6.0
+    dup = np.tile(rng.standard_normal((1, 24)).astype(np.float32), (6000, 1))
+    data = np.concatenate([far[:7000], dup, far[7000:]])
+    store = VectorStore(data=data)
+    qs = np.concatenate([dup[:1].astype(np.float64) + 0.01, rng.standard_normal((3, 24)) + 6.0])
+    try:
+        _lib.set_option("force_fixup", 1)
+        _lib.set_option("fx_slice_rows", slice_rows)
+        ids, d = brute_force_knn_batch(store, qs, np.array([40, 10, 1, 200]))
+        assert store.device().last_fixups() == 4
+    finally:
+        _lib.set_option("fx_slice_rows", 256)
+    for i, k in enumerate([40, 10, 1, 200]):
+        oi, od = orc.exact_knn(data, qs[i], k)
+        assert np.array_equal(ids[i, :k], oi), i
+        assert np.array_equal(d[i, :k], od), i
+
+
 def test_nonfinite_query_rejected():
     store = VectorStore(data=np.eye(4, dtype=np.float32))
     with pytest.raises(ValueError, match="finite"):
