@@ -113,6 +113,7 @@ long long g_scan_reserve = -1;  // SMs the IVF list scan leaves to other streams
 long long g_tc_stages = 0;   // tensor-core scan ring depth cap (0 = as deep as shared memory allows)
 long long g_scan_kernel = 0;  // 0 auto (IVF: fp16 tensor core), 1 fp32 SIMT, 2 TF32 tensor core
 long long g_scan_l2hint = 1;  // L2 policy of the IVF tensor-core scan's row loads (option "scan_l2hint")
+long long g_pack_mixed = 1;  // IVF tensor-core scan: one group sequence per list for all k classes (option "pack_mixed")
 long long g_scan_debug = 0;   // timing experiments only (results invalid when set)
 long long g_dense_off = 0;    // 1: never use the dense small-store brute force
 long long g_gthr = 1;         // cross-item per-query threshold in the tensor-core scan
@@ -717,7 +718,7 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
       for (int q : g) {
         Member m;
         m.q = q;
-        m.pad = (int)r;
+        m.pad = kp[q];
         m.slot = meta[q].part_off + r * kp[q];
         members[mb++] = m;
       }
@@ -980,6 +981,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "scan_reserve")) g_scan_reserve = value;
   else if (!std::strcmp(name, "graphs")) g_graphs = value;
   else if (!std::strcmp(name, "gthr")) g_gthr = value;
+  else if (!std::strcmp(name, "pack_mixed")) g_pack_mixed = value;
   else if (!std::strcmp(name, "scan_l2hint")) g_scan_l2hint = value;
   else if (!std::strcmp(name, "scan_abufs")) {
     if (value != 1 && value != 2) return fail(TRI_EINVAL, "scan_abufs must be 1 or 2");
@@ -1531,6 +1533,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   pk.members = w.members.as<Member>();
   pk.gmax = gmax;
   pk.cls_mask = cls_mask;
+  pk.mixed = (ch.tc && g_pack_mixed) ? 1 : 0;  // the SIMT scan keeps per-class groups
   CU(launch_pack(pk, st));
 
   // 4. list scan (persistent, one CTA per SM)
@@ -1667,7 +1670,7 @@ static bool host_pinned(const void* p) {
 
 long long graph_opts() {
   return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_fx_slice_rows * 7919 +
-         g_scan_debug * 100003 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
+         g_scan_debug * 100003 + g_pack_mixed * 104729 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
 }
 
 

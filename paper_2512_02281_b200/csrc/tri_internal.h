@@ -22,7 +22,7 @@ struct WorkItem {
 // A (query, partial-list slot) pair; slot is a key offset into the partial buffer.
 struct Member {
   int q;
-  int pad;
+  int pad;  // the query's kp (tensor-core scan: per-member threshold / output size)
   long long slot;
 };
 
@@ -247,6 +247,7 @@ struct PackLaunch {
   int* n_items;
   Member* members;
   int gmax;
+  int mixed;  // 1: one group sequence per list for all capacity classes (item kp = members' max)
 };
 cudaError_t launch_pack(const PackLaunch& p, cudaStream_t st);
 

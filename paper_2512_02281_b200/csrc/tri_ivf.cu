@@ -19,7 +19,7 @@ namespace tri {
 __global__ void pack_hist_kernel(PackLaunch p) {
   const int q = blockIdx.x;
   const int np = p.nprobe[q];
-  const int cls = p.meta[q].cls;
+  const int cls = p.mixed ? 0 : p.meta[q].cls;
   long long tot = 0;
   for (int j = threadIdx.x; j < np; j += blockDim.x) {
     long long l = p.probes[(long long)q * p.ld_probes + j];
@@ -46,9 +46,9 @@ __global__ void __launch_bounds__(1024) pack_items_kernel(PackLaunch p) {
     carry_grp = 0;
   }
   __syncthreads();
-  int pc[kNumCls], npc = 0;  // capacity classes present in this batch
+  int pc[kNumCls], npc = 0;  // capacity classes present in this batch (one slot when mixed)
   for (int c = 0; c < kNumCls; ++c)
-    if (p.cls_mask & (1 << c)) pc[npc++] = c;
+    if (p.mixed ? c == 0 : (p.cls_mask & (1 << c))) pc[npc++] = c;
   const int E = p.nlist * npc;
   for (int base = 0; base < E; base += 1024) {
     const int e = base + tid;
@@ -92,13 +92,14 @@ __global__ void __launch_bounds__(1024) pack_items_kernel(PackLaunch p) {
     const int grp_before = carry_grp + (warp ? s_grp[warp - 1] : 0) + ig - ngrp;
     if (e < E) {
       p.member_base[l * kNumCls + cls] = mem_before;
+      if (p.mixed) p.counts[l * kNumCls + 1] = grp_before;  // class slot 1 is unused when mixed
       for (int g = 0; g < ngrp; ++g) {
         WorkItem w;
         w.row_begin = p.list_off[l];
         w.row_count = (int)lsize;
         w.member_begin = mem_before + g * p.gmax;
         w.member_count = min(p.gmax, cnt - g * p.gmax);
-        w.kp = kMinKp << cls;
+        w.kp = p.mixed ? kMinKp : kMinKp << cls;  // mixed: raised to the members' max by pack_fill
         w.pad0 = l;
         w.pad1 = 0;
         p.items[grp_before + g] = w;
@@ -118,14 +119,16 @@ __global__ void pack_fill_kernel(PackLaunch p) {
   const int q = blockIdx.x;
   const int np = p.nprobe[q];
   const QueryMeta m = p.meta[q];
+  const int cls = p.mixed ? 0 : m.cls;
   for (int j = threadIdx.x; j < np; j += blockDim.x) {
     long long l = p.probes[(long long)q * p.ld_probes + j];
-    int slot = atomicAdd(&p.fill[l * kNumCls + m.cls], 1);
+    int slot = atomicAdd(&p.fill[l * kNumCls + cls], 1);
     Member mb;
     mb.q = q;
-    mb.pad = j;
+    mb.pad = m.kp;
     mb.slot = m.part_off + (long long)j * m.kp;
-    p.members[p.member_base[l * kNumCls + m.cls] + slot] = mb;
+    p.members[p.member_base[l * kNumCls + cls] + slot] = mb;
+    if (p.mixed) atomicMax(&p.items[p.counts[l * kNumCls + 1] + slot / p.gmax].kp, m.kp);
   }
 }
 

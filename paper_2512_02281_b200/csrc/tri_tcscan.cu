@@ -121,6 +121,7 @@ struct TcSmem {
   int cnt[2][kTcN];
   unsigned long long thr[kTcN];
   int qid[kTcN];
+  int kpq[kTcN];  // each member's kp (Member::pad): <= the item's kp in mixed-class groups
   float qn[kTcN];
   float qinv[kTcN];
 };
@@ -401,7 +402,14 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
           list_fold32<KL>(L[qi], b + lane < n ? sb[b + lane] : TRI_KEY_MAX, lane);
         }
         if (n > 0) {
-          unsigned long long t = __shfl_sync(0xffffffffu, L[qi][KL - 1], 31);
+          // the member's own kp-th key (a mixed-class group runs at the largest kp)
+          const int jq = (sh.kpq[g] >> 5) - 1;
+          unsigned long long t = TRI_KEY_MAX;
+#pragma unroll
+          for (int j = 0; j < KL; ++j) {
+            const unsigned long long y = __shfl_sync(0xffffffffu, L[qi][j], 31);
+            if (j == jq) t = y;
+          }
           if (lane == 0) {
             if (a.gthr) {
               // cross-item threshold: a full list's kp-th key bounds the query's
@@ -427,7 +435,8 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
     if (g < gc) {
       unsigned long long* out = a.part + a.members[w.member_begin + g].slot;
 #pragma unroll
-      for (int j = 0; j < KL; ++j) out[j * 32 + lane] = L[qi][j];
+      for (int j = 0; j < KL; ++j)
+        if (j * 32 < sh.kpq[g]) out[j * 32 + lane] = L[qi][j];  // the member's kp entries
     }
   }
   return acc | (aphase << 8);
@@ -449,6 +458,7 @@ __device__ void tc_epilogue(const ScanLaunch& a, TcSmem& sh, unsigned long long*
       sh.cnt[1][e] = 0;
       sh.thr[e] = (a.gthr && q >= 0) ? __ldcg(a.gthr + q) : TRI_KEY_MAX;
       sh.qid[e] = q < 0 ? 0 : q;
+      sh.kpq[e] = q >= 0 ? a.members[w.member_begin + e].pad : kMinKp;
       sh.qn[e] = q >= 0 ? a.qnorm[q] : 0.f;
       sh.qinv[e] = (H && q >= 0) ? a.qinv[q] : 0.f;
     }
