@@ -355,14 +355,16 @@ _SCAN_OPTS = [
     {"scan_reserve": 16},
     {"scan_reserve": 0},
     {"scan_qbufs": 1, "tc_stages": 4},
+    {"pack_mixed": 0},
 ]
-_SCAN_DEFAULTS = {"scan_abufs": 1, "scan_l2hint": 1, "scan_reserve": -1, "scan_qbufs": 2, "tc_stages": 0}
+_SCAN_DEFAULTS = {"scan_abufs": 1, "scan_l2hint": 1, "scan_reserve": -1, "scan_qbufs": 2, "tc_stages": 0,
+                  "pack_mixed": 1}
 
 
 @pytest.mark.parametrize("opts", _SCAN_OPTS, ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
 def test_ivf_scan_options_parity(small, opts):
-    """Scan tuning options (append buffers, L2 policy, reserved SMs, ring depth)
-    change scheduling only: results stay equal to the golden vectors, also with
+    """Scan tuning options (append buffers, L2 policy, reserved SMs, ring depth,
+    per-class instead of mixed-k list groups) change scheduling only: results stay equal to the golden vectors, also with
     batches on several streams (the automatic SM reservation)."""
     import torch
 
