@@ -563,7 +563,10 @@ int choose_scan(int qld, int d, int B, const int* k, std::vector<int>& kp, ScanC
   return TRI_OK;
 }
 
-long long plan_opts() { return g_dense_pow2 * 100000000 + g_dense_off * 10000000 + g_scan_kernel * 100000 + g_kp_extra; }
+long long plan_opts() {
+  return g_pack_mixed * 1000000000 + g_dense_pow2 * 100000000 + g_dense_off * 10000000 + g_scan_kernel * 100000 +
+         g_kp_extra;
+}
 
 // Split fp16 (hi + lo) copies of a store's rows for the tensor-core GEMM
 // (tri_coarse.cu), scaled by sc = 2^(14 - ilogb(max|x|)), rows of dph halves.
@@ -658,12 +661,13 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
     };
     while (gmax > 4 && n_groups(gmax) * max_ranges < nsm) gmax >>= 1;
   }
-  // groups: consecutive same-class queries in index order
+  // groups: consecutive same-class queries in index order (the tensor-core
+  // scan takes mixed-k groups at the members' largest kp: one pass per group)
   std::vector<std::vector<int>> groups;
   for (int c = 0; c < kNumCls; ++c) {
     std::vector<int> cur;
     for (int i = 0; i < B; ++i)
-      if (cls[i] == c) {
+      if ((ch.tc && g_pack_mixed) ? c == 0 : cls[i] == c) {
         cur.push_back(i);
         if ((int)cur.size() == gmax) {
           groups.push_back(cur);
@@ -711,7 +715,8 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
       wi.row_count = (int)std::min<long long>(R, s->n - r * R);
       wi.member_begin = (int)mb;
       wi.member_count = (int)g.size();
-      wi.kp = kp[g[0]];
+      wi.kp = 0;
+      for (int q : g) wi.kp = std::max(wi.kp, kp[q]);
       wi.pad0 = 0;
       wi.pad1 = 0;
       items[it++] = wi;

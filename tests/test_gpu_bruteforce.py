@@ -108,6 +108,26 @@ def test_ragged_k_and_capacity_classes():
         assert np.array_equal(d[i, : ks[i]], od), i
 
 
+@pytest.mark.parametrize("mixed", [1, 0])
+def test_ragged_k_mixed_groups(mixed):
+    """Tensor-core scan groups queries of different k classes together
+    (pack_mixed=1: each member keeps its own kp) or per class (0)."""
+    rng = np.random.Generator(np.random.Philox(31))
+    data = rng.standard_normal((30_000, 64)).astype(np.float32)
+    store = VectorStore(data=data)
+    qs = rng.standard_normal((40, 64))
+    ks = np.array([1, 10, 100, 50, 200, 7, 33, 128] * 5)
+    try:
+        _lib.set_option("pack_mixed", mixed)
+        ids, d = brute_force_knn_batch(store, qs, ks)
+    finally:
+        _lib.set_option("pack_mixed", 1)
+    for i in range(qs.shape[0]):
+        oi, od = orc.exact_knn(data, qs[i], int(ks[i]))
+        assert np.array_equal(ids[i, : ks[i]], oi), i
+        assert np.array_equal(d[i, : ks[i]], od), i
+
+
 @pytest.mark.parametrize("dim", [1, 3, 5, 16, 17, 100, 768, 1000])
 def test_odd_dimensions(dim):
     rng = np.random.Generator(np.random.Philox(dim))
