@@ -55,8 +55,16 @@ int tri_device_count(int32_t* count);
  * SIMT scan; 2 TF32 tensor-core scan, no fp16), "dense_off" (1 = no dense
  * small-store path), "tc_stages" (cap on the tensor-core scan ring depth,
  * 0 = deepest that fits), "scan_reserve" (SMs the IVF list scan leaves free
- * for batches on other streams), "scan_debug" (timing experiments only: results are
- * invalid while set). */
+ * for batches on other streams; -1 default = 8 once an index runs on more
+ * than one stream), "scan_abufs" (1 default / 2 append-list buffers of the IVF
+ * tensor-core scan), "scan_qbufs" (1 / 2 default query tiles), "scan_l2hint"
+ * (IVF scan row loads: 0 default policy, 1 default = L2 evict_first, 2
+ * evict_last), "pack_mixed" (1 default: tensor-core scan groups mix k classes),
+ * "gthr" (1 default: cross-item thresholds), "fx_slice_rows" (fix-up: minimum
+ * rows per slice, default 256), "graphs" (1 default: CUDA graph replay of
+ * repeated search shapes), "scan_debug" (timing experiments only: results are
+ * invalid while set).  Every option changes scheduling or tuning only; results
+ * stay bit-identical. */
 int tri_set_option(const char* name, int64_t value);
 
 /* Vector store: replaces ann_graph.VectorStore (ann_graph.py:21-48).
