@@ -450,6 +450,9 @@ def run_ours(args):
                          "what": f"{n_iso} searches on one stream after the timed region (no other lane "
                                  f"running beside the scan)"},
             "query_vector_pairs_per_launch": pairs,
+            "scan_sms": "148 minus the IVF scan's reserved SMs: 8 when more than one lane runs (library default "
+                        "scan_reserve=-1; +2% QPS, in-mix frac about 0.66 vs 0.76 with all 148 SMs, "
+                        "--opt scan_reserve=0); the isolated pass uses all 148",
         },
         "cpu_baseline": {"value": cpu_qps, "unit": UNIT, "cores": 1, "kind": "port",
                          "sample": f"first {args.cpu_sample} of the 256 C2 queries through the numpy oracle "
