@@ -874,6 +874,7 @@ int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Wo
   rr.ldo = ldo;
   TRY(ensure(w.fxs, fixup_scratch_bytes(B, w.k_max)));  // fix-up bounds + partial lists
   rr.fx_thr = static_cast<unsigned long long*>(w.fxs.p);
+  rr.skip_far = (int)tri::g_rerank_skip;
   rr.n_flag = n_flag;
   rr.flag_list = flag_list;
   rr.B = B;
@@ -1007,6 +1008,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "dense_slices")) tri::g_dense_slices = (int)value;
   else if (!std::strcmp(name, "rerank_smem_cap")) tri::g_rerank_smem_cap = value;
   else if (!std::strcmp(name, "rerank_f2f")) tri::g_rerank_f2f = value;
+  else if (!std::strcmp(name, "rerank_skip")) tri::g_rerank_skip = value;
   else if (!std::strcmp(name, "fx_slice_rows")) {
     if (value < 32) return fail(TRI_EINVAL, "fx_slice_rows must be >= 32");
     tri::g_fx_slice_rows = value;
@@ -1611,6 +1613,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   rr.ldo = ldo;
   TRY(ensure(w.fxs, fixup_scratch_bytes(B, k_max)));  // fix-up bounds + partial lists
   rr.fx_thr = static_cast<unsigned long long*>(w.fxs.p);
+  rr.skip_far = (int)tri::g_rerank_skip;
   rr.n_flag = n_flag;
   rr.flag_list = flag_list;
   rr.B = B;
@@ -1674,7 +1677,7 @@ static bool host_pinned(const void* p) {
 }
 
 long long graph_opts() {
-  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_fx_slice_rows * 7919 +
+  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_rerank_skip * 11 + tri::g_fx_slice_rows * 7919 +
          g_scan_debug * 100003 + g_pack_mixed * 104729 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
 }
 

@@ -169,6 +169,7 @@ struct RerankLaunch {
   int* n_flag;
   int* flag_list;
   unsigned long long* fx_thr;  // per flagged query: the fix-up's exact k-th bound (set to +inf when flagged)
+  int skip_far;                // fused re-rank: skip candidates 2E above the k-th approx key (option "rerank_skip")
   int B;
   int kp_max;
   const float* qinv;        // fp16 scan: qinv[q] < 0 marks a query the scan could not scale (never certified)
@@ -176,6 +177,7 @@ struct RerankLaunch {
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st);
 extern long long g_rerank_smem_cap;  // bytes; 0 = no cap
 extern long long g_rerank_f2f;
+extern long long g_rerank_skip;
 extern long long g_fx_slice_rows;  // fix-up: minimum rows per slice       // 1: hardware F2F conversions in the re-rank (else integer bit moves)
 
 struct FixupLaunch {

@@ -21,6 +21,7 @@ namespace tri {
 constexpr int kThreads = 256;
 long long g_rerank_smem_cap = 0;
 long long g_rerank_f2f = 1;
+long long g_rerank_skip = 1;
 long long g_fx_slice_rows = 256;
 
 // ---------------------------------------------------------------------------
@@ -689,7 +690,18 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
   const int tid = threadIdx.x, nthr = blockDim.x, c = tid >> 1, ln = tid & 1;
   unsigned long long key = TRI_KEY_MAX;
   if (c < kp) key = r.merged[(long long)q * r.ld_merged + c];
-  const bool active = key != TRI_KEY_MAX;
+  bool active = key != TRI_KEY_MAX;
+  // A candidate whose approx key exceeds the k-th approx key by more than 2E
+  // cannot enter the exact top-k.  Its exact distance is > approx(k) + E >= D_k,
+  // since the k smallest-key candidates have exact <= approx + E.  So its fp64
+  // row is neither loaded nor computed.  (merged is sorted; unscalable fp16
+  // queries keep every candidate.)
+  if (active && r.skip_far && m.k < kp && !(r.qinv && r.qinv[q] < 0.f)) {
+    const unsigned long long kk = r.merged[(long long)q * r.ld_merged + m.k - 1];
+    const double sn = r.qn64[q] + r.xmax;
+    const double E = (r.cdot * 2.0 * r.qn64[q] * r.xmax + r.csum * sn * sn) * 1.001 + 1e-30;
+    if (kk != TRI_KEY_MAX && (double)key_dist(key) > (double)key_dist(kk) + 2.0 * E) active = false;
+  }
   const long long pos = active ? (long long)key_pos(key) : -1;
   const bool leader = ln == 0 && c < kp;
   if (tid == 0) {
