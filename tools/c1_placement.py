@@ -33,6 +33,10 @@ def run(store, tag):
         res.setdefault(h, []).append(round(e0.elapsed_time(e1) / 300 * 1e3, 1))
     _lib.set_option("scan_l2hint", 0)
     print(tag, res, flush=True)
+if len(sys.argv) > 1:
+    for kv in sys.argv[1:]:
+        k, v = kv.split("=")
+        _lib.set_option(k, int(v))
 A = _DeviceStore(data); run(A, "A")
 B = _DeviceStore(data); run(B, "B (A alive)")
 run(A, "A again")
