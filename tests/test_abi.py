@@ -25,6 +25,18 @@ def test_version_and_error_plumbing():
     assert b"unknown option" in lib.tri_last_error()
 
 
+def test_option_ranges_validated():
+    """Tuning knobs reject out-of-range values (host-side, no device work)."""
+    for name, bad in (("scan_abufs", 3), ("scan_qbufs", 0), ("fx_slice_rows", 8), ("coarse_split", 0),
+                      ("tc_box_rows", 48)):
+        with pytest.raises(ValueError):
+            _lib.set_option(name, bad)
+    for name, good, default in (("scan_abufs", 2, 1), ("pack_mixed", 0, 1), ("scan_l2hint", 2, 1),
+                                ("scan_reserve", 16, -1), ("rerank_skip", 0, 1), ("fx_slice_rows", 512, 256)):
+        _lib.set_option(name, good)
+        _lib.set_option(name, default)
+
+
 def test_invalid_arguments_rejected_before_device_work():
     lib = _lib.load_library()
     h = C.c_void_p()
