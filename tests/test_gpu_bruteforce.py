@@ -95,6 +95,25 @@ def test_forced_fixup_path_is_exact(golden_dir):
     assert np.array_equal(ids, g["ids"][:8]) and np.array_equal(d, g["dists"][:8])
 
 
+def test_host_calls_replay_graphs_exactly(golden_dir):
+    """Repeated host-buffer calls of one shape are captured (2nd call) and
+    replayed (3rd on) as CUDA graphs through pinned staging; interleaved
+    shapes and fresh query values must still come back exact."""
+    g = np.load(os.path.join(golden_dir, "bf_c1.npz"))
+    store = VectorStore(data=gen_matrix(100_000, 128, 1))
+    qs = gen_matrix(64, 128, 2)
+    for it in range(5):
+        ids, d = brute_force_knn_batch(store, qs, 10)
+        assert np.array_equal(ids, g["ids"]) and np.array_equal(d, g["dists"]), it
+        sub_ids, sub_d = brute_force_knn_batch(store, qs[it : it + 3], 10)  # a second shape in between
+        assert np.array_equal(sub_ids, g["ids"][it : it + 3]) and np.array_equal(sub_d, g["dists"][it : it + 3])
+    # new values in the same shape (the staged copy must be refreshed each call)
+    rev = qs[::-1].copy()
+    for _ in range(3):
+        ids, d = brute_force_knn_batch(store, rev, 10)
+        assert np.array_equal(ids, g["ids"][::-1]) and np.array_equal(d, g["dists"][::-1])
+
+
 def test_ragged_k_and_capacity_classes():
     rng = np.random.Generator(np.random.Philox(21))
     data = rng.standard_normal((20_000, 40)).astype(np.float32)
