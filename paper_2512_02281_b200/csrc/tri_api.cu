@@ -373,9 +373,9 @@ int staged_upload(Workspace& w, int slot, void* dst, size_t bytes, cudaStream_t 
 // taken the least recently assigned one is recycled after its last search
 // (its `done` event) has completed.
 struct Lanes {
-  static constexpr int kMax = 4;
+  static constexpr int kMax = 8;
   Workspace w[kMax];
-  cudaStream_t st[kMax] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t st[kMax] = {};
   int used = 0, next_victim = 0, last = 0;
   int get(cudaStream_t s, Workspace** out) {
     for (int i = 0; i < used; ++i)
