@@ -457,6 +457,10 @@ def run_ours(args):
                          "what": f"{n_iso} searches on one stream after the timed region (no other lane "
                                  f"running beside the scan)"},
             "query_vector_pairs_per_launch": pairs,
+            "step_achieved": scan_bytes / (total_ms / args.steps / 1e3) / 1e9,
+            "step_frac": scan_bytes / (total_ms / args.steps / 1e3) / 1e9 / peak,
+            "step_what": "the scan's algorithmic bytes per step / the step time (all lanes overlapped): the HBM rate "
+                         "the whole pipeline sustains, where per-launch durations overlap",
             "scan_sms": "148 minus the IVF scan's reserved SMs: 8 when more than one lane runs (library default "
                         "scan_reserve=-1; +2% QPS, in-mix frac about 0.66 vs 0.76 with all 148 SMs, "
                         "--opt scan_reserve=0); the isolated pass uses all 148",
