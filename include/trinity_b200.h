@@ -87,6 +87,13 @@ int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32
  * for the rows of the store named by `rows` (host buffers). */
 int tri_rowwise_sq_dists(tri_store* s, const double* q, const int64_t* rows, int64_t n, double* out, void* stream);
 
+/* rowwise_sq_dists on arbitrary float64 rows (ann_graph.py:97-105), host
+ * buffers: q is 1 x d (broadcast) or n x d (row i paired with query i, numpy
+ * broadcasting), rows n x d float64; same operation order, computed on
+ * `device`.  Used when the rows do not come from a float32 store. */
+int tri_rowwise_sq_dists_f64(const double* q, int32_t q_rows, const double* rows, int64_t n, int32_t d, int32_t device,
+                             double* out);
+
 /* Fixed-shape distance batch: replaces engine.execute_distance_batch
  * (engine.py:229-256).  Task i pairs query row owner[i] of `queries`
  * (n_queries x d float64) with store row cand[i]; returns TRI_EINTERNAL if a

@@ -38,6 +38,7 @@ _SIGS = {
     "tri_knn_bruteforce": [_vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp],
     "tri_knn_bruteforce_dev": [_vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp],
     "tri_rowwise_sq_dists": [_vp, _vp, _vp, _i64, _vp, _vp],
+    "tri_rowwise_sq_dists_f64": [_vp, _i32, _vp, _i64, _i32, _i32, _vp],
     "tri_distance_tasks": [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp],
     "tri_ivf_train": [_vp, _i32, _i32, _vp, C.POINTER(_vp)],
     "tri_ivf_create": [_vp, _vp, _i32, _vp, _i64, C.POINTER(_vp)],

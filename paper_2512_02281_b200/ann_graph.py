@@ -73,6 +73,10 @@ class _DeviceStore:
         owner = np.ascontiguousarray(owner, dtype=np.int32)
         cand = np.ascontiguousarray(cand, dtype=np.int64)
         q = np.ascontiguousarray(queries64, dtype=np.float64)
+        if q.ndim != 2 or q.shape[1] != self.d:
+            raise ValueError(f"queries must be (n, {self.d}), got shape {q.shape}")
+        if owner.shape != cand.shape:
+            raise ValueError(f"owner {owner.shape} and cand {cand.shape} differ in length")
         out = np.empty(owner.shape[0], dtype=np.float64)
         if owner.shape[0]:
             _lib.check(lib.tri_distance_tasks(self.handle, owner.ctypes.data, cand.ctypes.data, owner.shape[0],
@@ -168,28 +172,48 @@ class GraphValidationReport:
 
 
 def rowwise_sq_dists(query64: np.ndarray, rows64: np.ndarray) -> np.ndarray:
-    """Squared L2 from one query to each row (ann_graph.py:97-105), on the GPU.
+    """Squared L2 from the query to each row (ann_graph.py:97-105), on the GPU.
 
-    The device holds float32 rows, so ``rows64`` must be float32-representable
-    (every row the reference passes comes from a float32 store).
+    Same broadcasting as the reference's ``query64 - rows64``: a (d,) or (1, d)
+    query against (n, d) rows, or one query row per row.  Float64 on both sides
+    (``tri_rowwise_sq_dists_f64``), in the reference's einsum operation order.
     """
-    rows64 = np.atleast_2d(np.asarray(rows64, dtype=np.float64))
-    rows32 = rows64.astype(np.float32)
-    if not np.array_equal(rows32.astype(np.float64), rows64):
-        raise ValueError("rows must be float32-representable (device stores hold float32)")
-    q = np.asarray(query64, dtype=np.float64).reshape(1, -1)
-    dev = _DeviceStore(rows32)
+    q = np.asarray(query64, dtype=np.float64)
+    rows = np.asarray(rows64, dtype=np.float64)
     try:
-        return dev.task_dists(np.zeros(rows32.shape[0], np.int32), np.arange(rows32.shape[0]), q)
-    finally:
-        dev.close()
+        shape = np.broadcast_shapes(q.shape, rows.shape)
+    except ValueError as exc:
+        raise ValueError(f"query {q.shape} does not broadcast against rows {rows.shape}") from exc
+    if len(shape) != 2:
+        raise ValueError(f"query - rows must be 2-D (rows, dim), got shape {shape}")
+    n, d = shape
+    if n == 0:
+        return np.empty(0, dtype=np.float64)
+    # (q - x)^2 == (x - q)^2 exactly, so either operand may play the query
+    if q.shape[-1:] == (d,) and q.size == d:
+        one, full = q.reshape(1, d), rows
+    elif rows.size == d:
+        one, full = rows.reshape(1, d), q
+    else:
+        one, full = None, None
+    if one is not None and full.shape == (n, d):
+        qb, xb, qrows = np.ascontiguousarray(one), np.ascontiguousarray(full), 1
+    else:
+        qb = np.ascontiguousarray(np.broadcast_to(q, shape))
+        xb = np.ascontiguousarray(np.broadcast_to(rows, shape))
+        qrows = n
+    out = np.empty(n, dtype=np.float64)
+    _lib.check(_lib.gpu().tri_rowwise_sq_dists_f64(qb.ctypes.data, qrows, xb.ctypes.data, n, d, 0, out.ctypes.data))
+    return out
 
 
 def store_sq_dists(store: VectorStore, query, rows) -> np.ndarray:
     """rowwise_sq_dists(query, store.data64[rows]) without materialising rows."""
-    q = np.asarray(query, dtype=np.float64).reshape(1, -1)
+    q = np.asarray(query, dtype=np.float64)
+    if q.size != store.dim:
+        raise ValueError(f"query has {q.size} values, store dim is {store.dim}")
     rows = np.asarray(rows, dtype=np.int64)
-    return store.device().task_dists(np.zeros(rows.shape[0], np.int32), rows, q)
+    return store.device().task_dists(np.zeros(rows.shape[0], np.int32), rows, q.reshape(1, -1))
 
 
 def pair_sq_dist(query64: np.ndarray, row64: np.ndarray) -> float:
@@ -205,12 +229,7 @@ def distance(a, b) -> float:
         raise ValueError(f"dimension mismatch: {a.shape} vs {b.shape}")
     if not (np.isfinite(a).all() and np.isfinite(b).all()):
         raise ValueError("vectors must be finite")
-    # put the float32-exact operand on the device side
-    if np.array_equal(b.astype(np.float32).astype(np.float64), b):
-        return pair_sq_dist(a, b)
-    if np.array_equal(a.astype(np.float32).astype(np.float64), a):
-        return pair_sq_dist(b, a)
-    raise ValueError("one operand must be float32-representable")
+    return pair_sq_dist(a, b)
 
 
 # ----------------------------------------------------------------------------

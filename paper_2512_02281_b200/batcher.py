@@ -62,14 +62,22 @@ class RetrievalBatcher:
 
     def submit(self, query, k: int | None = None, nprobe: int | None = None, stage: str = "decode",
                t_submit: float | None = None) -> int:
+        # validated here, so one bad submission cannot fail a whole batch in step()
         dk, dnp = STAGE_PARAMS.get(stage, (10, 16))
         q = np.asarray(query, dtype=np.float64).ravel()
         if q.shape[0] != self.index.dim:
             raise ValueError(f"query dim {q.shape[0]} != index dim {self.index.dim}")
+        if not np.isfinite(q).all():
+            raise ValueError("query must be finite")
+        k = dk if k is None else int(k)
+        nprobe = dnp if nprobe is None else int(nprobe)
+        if k < 1:
+            raise ValueError(f"k must be >= 1, got {k}")
+        if not 1 <= nprobe <= self.index.nlist:
+            raise ValueError(f"nprobe must be in [1, {self.index.nlist}], got {nprobe}")
         rid = self._next
         self._next += 1
-        self._queue.append(_Pending(rid, q, int(k or dk), int(nprobe or dnp), stage,
-                                    self.clock() if t_submit is None else t_submit))
+        self._queue.append(_Pending(rid, q, k, nprobe, stage, self.clock() if t_submit is None else t_submit))
         return rid
 
     @property

@@ -494,9 +494,12 @@ struct DeviceGuard {
 // Branch-free scan (vectorises): a double is non-finite iff its exponent bits
 // are all ones (no per-element branch; about 25% faster on a C2 batch).
 int check_queries(const double* q, long long count) {
-  const uint64_t* u = reinterpret_cast<const uint64_t*>(q);
   uint64_t bad = 0;
-  for (long long i = 0; i < count; ++i) bad |= (uint64_t)((u[i] & 0x7ff0000000000000ull) == 0x7ff0000000000000ull);
+  for (long long i = 0; i < count; ++i) {
+    uint64_t u;
+    std::memcpy(&u, q + i, sizeof(u));  // no type punning through the caller's buffer
+    bad |= (uint64_t)((u & 0x7ff0000000000000ull) == 0x7ff0000000000000ull);
+  }
   if (bad) return fail(TRI_EINVAL, "query must be finite");
   return TRI_OK;
 }
@@ -1157,6 +1160,33 @@ int tri_rowwise_sq_dists(tri_store* s, const double* q, const int64_t* rows, int
   if (n == 0) return TRI_OK;
   std::vector<int32_t> owner(n, 0);
   return tri_distance_tasks(s, owner.data(), rows, (int32_t)n, q, 1, out, stream);
+}
+
+int tri_rowwise_sq_dists_f64(const double* q, int32_t q_rows, const double* rows, int64_t n, int32_t d, int32_t device,
+                             double* out) {
+  if (n < 0 || d < 1) return fail(TRI_EINVAL, "bad shape (%lld, %d)", (long long)n, d);
+  if (q_rows != 1 && q_rows != n) return fail(TRI_EINVAL, "query rows must be 1 or %lld, got %d", (long long)n, q_rows);
+  if (n == 0) return TRI_OK;
+  if (!q || !rows || !out) return fail(TRI_EINVAL, "NULL argument");
+  DeviceGuard g(device);
+  cudaStream_t st = nullptr;
+  CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const size_t qb = (size_t)q_rows * d * sizeof(double), xb = (size_t)n * d * sizeof(double);
+  void* buf = nullptr;
+  cudaError_t e = cudaMallocAsync(&buf, qb + xb + (size_t)n * sizeof(double), st);
+  double* dq = static_cast<double*>(buf);
+  double* dx = dq + (size_t)q_rows * d;
+  double* dout = dx + (size_t)n * d;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dq, q, qb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dx, rows, xb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = launch_rowwise_f64(dq, q_rows == 1 ? 0 : d, dx, n, d, dout, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (buf) cudaFreeAsync(buf, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return fail(TRI_ECUDA, "rowwise_sq_dists: %s", cudaGetErrorString(e));
+  return TRI_OK;
 }
 
 int tri_distance_tasks(tri_store* s, const int32_t* owner, const int64_t* cand, int32_t n_tasks,

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(32 * kEngWarps) engine_step_kernel(EngineLaunc
   }
   err = __any_sync(FULL, err);
   __syncwarp();
-  if (lane < np) ce[par[lane]] = 1;
+  for (int i = lane; i < np; i += 32) ce[par[i]] = 1;  // every parent, p may exceed 32
 
   // exact distances of the emissions, one candidate per lane
   for (int e = lane; e < ne; e += 32) cd[cnt + e] = dist_of(ci[cnt + e]);

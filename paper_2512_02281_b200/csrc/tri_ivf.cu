@@ -23,6 +23,7 @@ __global__ void pack_hist_kernel(PackLaunch p) {
   long long tot = 0;
   for (int j = threadIdx.x; j < np; j += blockDim.x) {
     long long l = p.probes[(long long)q * p.ld_probes + j];
+    if (l < 0) continue;  // non-finite query: its coarse step returned no lists
     atomicAdd(&p.counts[l * kNumCls + cls], 1);
     tot += p.list_off[l + 1] - p.list_off[l];
   }
@@ -122,6 +123,7 @@ __global__ void pack_fill_kernel(PackLaunch p) {
   const int cls = p.mixed ? 0 : m.cls;
   for (int j = threadIdx.x; j < np; j += blockDim.x) {
     long long l = p.probes[(long long)q * p.ld_probes + j];
+    if (l < 0) continue;
     int slot = atomicAdd(&p.fill[l * kNumCls + cls], 1);
     Member mb;
     mb.q = q;

@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double* __rest
   }
   if (tid == 0) {
     qn32[q] = __double2float_rn(a);
-    qn64[q] = sqrt(b);
+    qn64[q] = nf ? __longlong_as_double(0x7ff8000000000000ll) : sqrt(b);  // NaN marks a non-finite query
     if (nf && bad) atomicExch(bad, 1);
   }
   if (Qh) {
@@ -561,7 +561,7 @@ __device__ __forceinline__ void finalize_query(const RerankLaunch& r, int q, int
     }
     cert = certified(r, q, dk, (double)key_dist(r.merged[(long long)q * r.ld_merged + m.kp - 1]));
   }
-  if (!cert && lane == 0) flag_query(r, q, dk);
+  if ((!cert || isnan(r.qn64[q])) && lane == 0) flag_query(r, q, dk);
 #pragma unroll
   for (int j = 0; j < KL; ++j) {
     const int e = j * 32 + lane;
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(RerankLaunch r) {
     if (m.n_total > kp) {
       cert = certified(r, q, ebuf[m.k - 1].d, (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]));
     }
-    if (!cert) flag_query(r, q, ebuf[m.k - 1].d);
+    if (!cert || isnan(r.qn64[q])) flag_query(r, q, ebuf[m.k - 1].d);
   }
   for (int j = threadIdx.x; j < m.k; j += blockDim.x) {
     const Exact e = ebuf[j];
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
     if (m.n_total > kp) {
       cert = certified(r, q, s_dk, (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]));
     }
-    if (!cert) flag_query(r, q, s_dk);
+    if (!cert || isnan(r.qn64[q])) flag_query(r, q, s_dk);
   }
 }
 
@@ -895,7 +895,7 @@ __device__ __forceinline__ long long fx_total(const FixupLaunch& f, int q, long 
   long long t = 0;
   for (int j = threadIdx.x; j < f.nprobe[q]; j += kThreads) {
     const long long l = f.probes[(long long)q * f.ld_probes + j];
-    t += f.list_off[l + 1] - f.list_off[l];
+    if (l >= 0) t += f.list_off[l + 1] - f.list_off[l];
   }
   return fx_block_sum(t, s_w);
 }
@@ -967,6 +967,7 @@ __global__ void __launch_bounds__(kThreads) fixup_part_kernel(FixupLaunch f, int
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int fi = u / S, sl = u - fi * S;
     const int q = f.flag_list[fi];
+    if (isnan(f.qn64[q])) continue;  // non-finite query: no rescan, the merge writes an empty row
     const int k = f.meta[q].k;
     const double* qv = f.q64 + (long long)q * f.d;
     const long long total = fx_total(f, q, s_w);
@@ -1002,8 +1003,10 @@ __global__ void __launch_bounds__(kThreads) fixup_part_kernel(FixupLaunch f, int
         if (j < nranges) {
           if (f.probes) {
             const long long l = f.probes[(long long)q * f.ld_probes + j];
-            lo = f.list_off[l];
-            len = f.list_off[l + 1] - lo;
+            if (l >= 0) {
+              lo = f.list_off[l];
+              len = f.list_off[l + 1] - lo;
+            }
           } else {
             len = f.n_rows;
           }
@@ -1131,6 +1134,13 @@ __device__ void fixup_merge_all(const FixupLaunch& f, int S, const Exact* part, 
   for (int fi = 0; fi < *f.n_flag; ++fi) {
     const int q = f.flag_list[fi];
     const int k = f.meta[q].k;
+    if (isnan(f.qn64[q])) {  // non-finite query (device-buffer entry points): id -1, distance NaN
+      for (int j = threadIdx.x; j < k; j += kThreads) {
+        f.out_ids[(long long)q * f.ldo + j] = -1;
+        f.out_d[(long long)q * f.ldo + j] = __longlong_as_double(0x7ff8000000000000ll);
+      }
+      continue;
+    }
     const Exact bound = fx_bound(f, fi);
     if (threadIdx.x == 0) *s_cnt = 0;
     __syncthreads();
@@ -1223,6 +1233,45 @@ cudaError_t launch_distance_tasks(const int* owner, const long long* cand, int n
   if (n_tasks <= 0) return cudaSuccess;
   distance_tasks_kernel<<<(n_tasks + 127) / 128, 128, 0, st>>>(owner, cand, n_tasks, q64, d, X, ldx, n_rows, out,
                                                                  err);
+  return cudaGetLastError();
+}
+
+// rowwise_sq_dists on float64 rows (ann_graph.py:97-105) for rows that are not
+// in a float32 store: same einsum operation order as exact_sq_dist, both
+// operands float64.  q_stride = 0 broadcasts one query; d pairs row i with
+// query row i (numpy broadcasting of a (n, d) query).
+__global__ void rowwise_f64_kernel(const double* __restrict__ q, long long q_stride, const double* __restrict__ X,
+                                   long long n, int d, double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* qq = q + i * q_stride;
+  const double* x = X + i * d;
+  double l0 = 0.0, l1 = 0.0;
+  int j = 0;
+  for (; j + 8 <= d; j += 8) {
+#pragma unroll
+    for (int sub = 3; sub >= 0; --sub) {
+      const double t0 = __dsub_rn(qq[j + 2 * sub], x[j + 2 * sub]);
+      const double t1 = __dsub_rn(qq[j + 2 * sub + 1], x[j + 2 * sub + 1]);
+      l0 = __dadd_rn(__dmul_rn(t0, t0), l0);
+      l1 = __dadd_rn(__dmul_rn(t1, t1), l1);
+    }
+  }
+  for (; j < d; j += 2) {
+    const double t0 = __dsub_rn(qq[j], x[j]);
+    l0 = __dadd_rn(__dmul_rn(t0, t0), l0);
+    if (j + 1 < d) {
+      const double t1 = __dsub_rn(qq[j + 1], x[j + 1]);
+      l1 = __dadd_rn(__dmul_rn(t1, t1), l1);
+    }
+  }
+  out[i] = __dadd_rn(l0, l1);
+}
+
+cudaError_t launch_rowwise_f64(const double* q, long long q_stride, const double* X, long long n, int d, double* out,
+                               cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  rowwise_f64_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(q, q_stride, X, n, d, out);
   return cudaGetLastError();
 }
 

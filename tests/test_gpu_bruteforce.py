@@ -42,6 +42,32 @@ def test_distance_kats(golden_dir):
         assert distance(np.array(c["a"], np.float32), np.array(c["b"], np.float32)) == c["dist"]
 
 
+def test_rowwise_sq_dists_broadcasting_and_f64_rows(scan_kernel):
+    """rowwise_sq_dists / distance on arbitrary float64 operands, numpy broadcasting
+    as the reference's ``query64 - rows64`` (ann_graph.py:97-105), bit-exact."""
+    from paper_2512_02281_b200.ann_graph import pair_sq_dist, rowwise_sq_dists
+
+    if scan_kernel != "auto":
+        pytest.skip("no scan involved")
+    rng = np.random.default_rng(5)
+    for d in (1, 7, 8, 13, 768):
+        rows = rng.standard_normal((37, d)) * 1e3 + 1.0 / 3.0  # not float32-representable
+        q = rng.standard_normal(d)
+        assert np.array_equal(rowwise_sq_dists(q, rows), orc.sq_dists(q, rows))
+        assert np.array_equal(rowwise_sq_dists(q.reshape(1, -1), rows), orc.sq_dists(q, rows))
+        per_row = rng.standard_normal((37, d))
+        want = np.einsum("ij,ij->i", per_row - rows, per_row - rows)
+        assert np.array_equal(rowwise_sq_dists(per_row, rows), want)
+        assert distance(q, rows[0]) == float(orc.sq_dists(q, rows[:1])[0])
+        assert pair_sq_dist(q, rows[3]) == float(orc.sq_dists(q, rows[3:4])[0])
+    with pytest.raises(ValueError):
+        rowwise_sq_dists(np.zeros(3), np.zeros((4, 5)))  # would read past the query
+    with pytest.raises(ValueError):
+        rowwise_sq_dists(np.zeros((2, 5)), np.zeros((4, 5)))
+    with pytest.raises(ValueError):
+        store_sq_dists(VectorStore(data=np.zeros((4, 5), np.float32)), np.zeros(3), [0, 1])
+
+
 def test_bruteforce_golden_small_all_k(golden_dir):
     g = np.load(os.path.join(golden_dir, "bf_small.npz"))
     store = VectorStore(data=gen_matrix(1000, 8, 11))
@@ -216,3 +242,26 @@ def test_knn_graph_matches_reference(golden_dir):
     graph = build_knn_graph(store, 16)
     assert validate_graph(graph, store.count).ok
     assert np.array_equal(graph.adjacency, g["adjacency"])
+
+
+def test_device_path_non_finite_query_rows(scan_kernel):
+    """tri_knn_bruteforce_dev: a non-finite query row -> id -1 / NaN, others exact."""
+    import torch
+
+    data = gen_matrix(3000, 24, 41)
+    store = VectorStore(data=data)
+    qs = gen_matrix(8, 24, 42).astype(np.float64)
+    qs[2, 7] = np.nan
+    q = torch.from_numpy(qs).cuda()
+    ids = torch.empty((8, 10), dtype=torch.int64, device="cuda")
+    d = torch.empty((8, 10), dtype=torch.float64, device="cuda")
+    dev = store.device()
+    ks = np.full(8, 10, np.int32)
+    _lib.check(_lib.gpu().tri_knn_bruteforce_dev(dev.handle, _lib.ptr(q), 8, ks.ctypes.data, 10, _lib.ptr(ids),
+                                                 _lib.ptr(d), None))
+    torch.cuda.synchronize()
+    hi, hd = ids.cpu().numpy(), d.cpu().numpy()
+    assert (hi[2] == -1).all() and np.isnan(hd[2]).all()
+    for i in (0, 1, 3, 7):
+        oi, od = orc.exact_knn(data, qs[i], 10)
+        assert np.array_equal(hi[i], oi) and np.array_equal(hd[i], od)

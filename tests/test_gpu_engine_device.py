@@ -50,6 +50,8 @@ def _check(eng, rids, ref):
         (8000, 768, 16, dict(m=64, p=2, entry_count=8, batch_capacity=512)),
         (6000, 32, 24, dict(m=128, p=4, entry_count=16, batch_capacity=100, stop_streak=3, max_extends=40)),
         (3000, 16, 8, dict(m=16, p=1, entry_count=3, batch_capacity=7, stop_streak=2, max_extends=5)),
+        # p > 32: parents beyond one warp's lanes must be marked expanded too
+        (4000, 16, 8, dict(m=64, p=40, entry_count=8, batch_capacity=256, stop_streak=2, max_extends=12)),
     ],
 )
 def test_device_engine_matches_oracle(n, d, deg, cfg):

@@ -382,3 +382,28 @@ def test_ivf_scan_options_parity(small, opts):
     finally:
         for k, v in _SCAN_DEFAULTS.items():
             _lib.set_option(k, v)
+
+
+def test_device_path_non_finite_query_rows(small):
+    """search_device skips the host finiteness check: a NaN / inf query row comes
+    back as id -1 / NaN (never garbage) and leaves the other rows exact."""
+    import torch
+
+    g, data, idx = small
+    qs = gen_matrix(40, 32, 7).astype(np.float64)
+    qs[3, 5] = np.nan
+    qs[17, 0] = np.inf
+    q = torch.from_numpy(qs).cuda()
+    kmax = int(g["ks"].max())
+    ids = torch.empty((40, kmax), dtype=torch.int64, device="cuda")
+    d = torch.empty((40, kmax), dtype=torch.float64, device="cuda")
+    idx.search_device(q, g["ks"], g["nprobes"], ids, d)
+    torch.cuda.synchronize()
+    hi, hd = ids.cpu().numpy(), d.cpu().numpy()
+    for i in (3, 17):
+        k = int(g["ks"][i])
+        assert (hi[i, :k] == -1).all() and np.isnan(hd[i, :k]).all()
+    keep = [i for i in range(40) if i not in (3, 17)]
+    _check_rows(hi[keep], hd[keep], {"ids": g["ids"][keep], "dists": g["dists"][keep]}, g["ks"][keep])
+    with pytest.raises(ValueError):  # the host entry point rejects it up front
+        idx.search(qs, g["ks"], g["nprobes"])
