@@ -171,6 +171,9 @@ def run_reference(args):
     from oracle import trinity_oracle as orc
 
     data, queries = make_inputs()
+    # the same deterministic k-means the GPU arm runs (oracle.kmeans restates
+    # tri_ivf_train bit-for-bit): both arms search one index artifact, whose
+    # digest goes into config
     art = orc.kmeans(data, NLIST, ITERS, KM_SEED)
     cores = os.cpu_count() or 1
     # Steps are a bounded sample of the C2 batch: about 200 x cores queries in
@@ -191,10 +194,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": dict(CONFIG, parallelism=f"cpu x{cores}"),
+        "data": "synthetic", "config": dict(CONFIG, artifact=orc.artifact_digest(art)),
         "cpu_baseline": {"value": qps, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{per_step} queries per step of the C2 batch ({per_step * args.steps} in "
-                                   f"all), numpy oracle, one process per core"},
+                                   f"all), numpy oracle, one process per core ({cores} cores)"},
         "e2e": {"value": qps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -445,7 +448,9 @@ def run_ours(args):
         "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": f"{scan_kind} candidate scan (certified bound) + f64 exact re-rank", "data": "synthetic",
-        "config": dict(CONFIG, parallelism=f"vector-shard x{world}" if world > 1 else "dp1", lanes=L),
+        "config": dict(CONFIG, parallelism=f"vector-shard x{world}" if world > 1 else "dp1",
+                       artifact=orc.artifact_digest(art)),
+        "lanes": L,
         "roofline": {
             "bound": "hbm", "kernel": f"tri::scan_tc_kernel ({scan_kind} tcgen05 IVF list scan)", "achieved": achieved, "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic() if world == 1 else None,

@@ -102,10 +102,18 @@ int tri_distance_tasks(tri_store* s, const int32_t* owner, const int64_t* cand, 
                        const double* queries, int32_t n_queries, double* out, void* stream);
 
 /* IVF-Flat (new component; the reference has no IVF).
- * train: GPU Lloyd k-means from the host-chosen init rows, `iters` updates.
+ * train: GPU Lloyd k-means from the host-chosen init rows, `iters` updates
+ * (exact assignment, float64 ascending-id centroid sums: deterministic).
  * create: from a shared artifact (fp32 centroids + the list id of each row),
  * `id_offset` = global id of the store's row 0 (shards). */
 int tri_ivf_train(tri_store* s, int32_t nlist, int32_t iters, const int64_t* init_rows, tri_ivf** out);
+/* Exact nearest-centroid assignment of every store row (host centroids
+ * nlist x d float32 -> host assign[n]): brute_force_knn over the centroids
+ * with k = 1 (ann_graph.py:124-137), ties to the smaller centroid id.  It is
+ * also the assignment step of tri_ivf_train, whose Lloyd update sums each
+ * list's rows in ascending id order in float64 -- so training is
+ * deterministic and reproducible on the CPU (oracle.kmeans). */
+int tri_kmeans_assign(tri_store* s, const float* centroids, int32_t nlist, int32_t* assign);
 int tri_ivf_create(tri_store* s, const float* centroids, int32_t nlist, const int32_t* assign, int64_t id_offset,
                    tri_ivf** out);
 int tri_ivf_destroy(tri_ivf* v);

@@ -179,35 +179,91 @@ def ivf_search(data32: np.ndarray, art: IVFArtifact, query, k: int, nprobe: int)
     return _lex_topk(dists, cand, min(k, cand.size))
 
 
-def kmeans(data32: np.ndarray, nlist: int, iters: int, seed: int):
-    """Small Lloyd k-means used to make CPU-test artifacts (no reference exists).
+def nearest_centroid(data32: np.ndarray, cent32: np.ndarray, chunk: int = 8192) -> np.ndarray:
+    """Exact nearest centroid of every row: ``brute_force_knn(VectorStore(cent), row, 1)``
+    (ann_graph.py:124-137) per row, i.e. the smallest float64 einsum-order
+    distance, ties to the smaller centroid id.
 
-    Centroids start from a seeded sample of rows; empty clusters keep their
-    previous centroid.  Not the GPU trainer -- only an artifact source.
+    Vectorised: the float64 score S = |c|^2 - 2 x.c (the row's |x|^2 is a
+    common constant) picks the candidates; rows whose runner-up lies within
+    twice the error bound of the winner are decided by the exact distances.
+    |S + |x|^2 - D| <= eps (|x| + |c|)^2 with eps = 4 (d + 4) 2^-53 covers S's
+    rounding (any BLAS order) and D's own einsum rounding, so the exact winner
+    is always among the candidates.  Chunks run on a thread pool (numpy and
+    BLAS release the GIL; BLAS pinned to one thread per chunk).
+    """
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+
+    from threadpoolctl import threadpool_limits
+
+    n, d = data32.shape
+    c64 = cent32.astype(np.float64)
+    cn = np.einsum("ij,ij->i", c64, c64)
+    c64t = np.ascontiguousarray(c64.T)
+    cmax = float(np.sqrt(cn.max()))
+    eps = 4.0 * (d + 4) * 2.0 ** -53
+    out = np.empty(n, dtype=np.int32)
+
+    def run(s):
+        x = data32[s:s + chunk].astype(np.float64)
+        S = x @ c64t
+        S *= -2.0
+        S += cn
+        win = S.argmin(axis=1).astype(np.int32)
+        smin = S[np.arange(S.shape[0]), win]
+        xn = np.einsum("ij,ij->i", x, x)
+        S -= (smin + 2.0 * eps * (np.sqrt(xn) + cmax) ** 2)[:, None]
+        multi = np.nonzero((S <= 0.0).sum(axis=1) > 1)[0]
+        for r in multi:
+            cs = np.nonzero(S[r] <= 0.0)[0]
+            dd = sq_dists(x[r], c64[cs])
+            win[r] = cs[np.lexsort((cs, dd))[0]]
+        out[s:s + chunk] = win
+
+    with threadpool_limits(1, "blas"), ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        list(ex.map(run, range(0, n, chunk)))
+    return out
+
+
+def kmeans(data32: np.ndarray, nlist: int, iters: int, seed: int):
+    """Lloyd k-means, the restatement of the GPU trainer (tri_ivf_train).
+
+    The reference has no IVF (SPEC.md:166), so there is nothing to pin it to;
+    its semantics are chosen to be deterministic so the GPU result can be
+    checked bit-for-bit: centroids start from the seeded rows
+    ``sort(choice(n, nlist))`` of a Philox(seed) generator; every iteration
+    assigns each row to its exact nearest centroid (``nearest_centroid``),
+    then each non-empty list's centroid becomes fp32(sum * (1 / count)) with
+    the sum taken in float64 over its rows in ascending id order (numpy's
+    axis-0 sum is that sequential chain); empty lists keep their centroid.
+    After ``iters`` updates a final assignment gives the artifact.
     """
     rng = np.random.Generator(np.random.Philox(seed))
     n = data32.shape[0]
-    cent = data32[np.sort(rng.choice(n, size=nlist, replace=False))].astype(np.float64)
-    assign = np.zeros(n, dtype=np.int32)
-    chunk = 1 << 16
+    cent = np.ascontiguousarray(data32[np.sort(rng.choice(n, size=nlist, replace=False))], dtype=np.float32)
     for it in range(iters + 1):
-        cn = np.einsum("ij,ij->i", cent, cent)
-        for s in range(0, n, chunk):  # row norms are constant per row: argmin of cn - 2 x.c
-            x = data32[s:s + chunk].astype(np.float64)
-            assign[s:s + chunk] = np.argmin(cn[None, :] - 2.0 * (x @ cent.T), axis=1)
+        assign = nearest_centroid(data32, cent)
         if it == iters:
             break
-        from scipy.sparse import csr_matrix
+        order = np.argsort(assign, kind="stable")
+        counts = np.bincount(assign, minlength=nlist)
+        off = np.zeros(nlist + 1, dtype=np.int64)
+        np.cumsum(counts, out=off[1:])
+        for lst in np.nonzero(counts)[0]:
+            rows = order[off[lst]:off[lst + 1]]
+            s = data32[rows].astype(np.float64).sum(axis=0)
+            cent[lst] = (s * (1.0 / counts[lst])).astype(np.float32)
+    return IVFArtifact(cent, assign)
 
-        sums = np.zeros_like(cent)
-        for s in range(0, n, chunk):
-            a = assign[s:s + chunk]
-            onehot = csr_matrix((np.ones(a.size), (a, np.arange(a.size))), shape=(nlist, a.size))
-            sums += onehot @ data32[s:s + chunk].astype(np.float64)
-        cnt = np.bincount(assign, minlength=nlist)
-        nz = cnt > 0
-        cent[nz] = sums[nz] / cnt[nz, None]
-    return IVFArtifact(cent.astype(np.float32), assign)
+
+def artifact_digest(art: "IVFArtifact") -> str:
+    """sha256 prefix of (centroids, assign): both bench arms print it."""
+    import hashlib
+
+    h = hashlib.sha256(np.ascontiguousarray(art.centroids, dtype="<f4").tobytes())
+    h.update(np.ascontiguousarray(art.assign, dtype="<i4").tobytes())
+    return h.hexdigest()[:16]
 
 
 # ----------------------------------------------------------------------------

@@ -41,6 +41,7 @@ _SIGS = {
     "tri_rowwise_sq_dists_f64": [_vp, _i32, _vp, _i64, _i32, _i32, _vp],
     "tri_distance_tasks": [_vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp],
     "tri_ivf_train": [_vp, _i32, _i32, _vp, C.POINTER(_vp)],
+    "tri_kmeans_assign": [_vp, _vp, _i32, _vp],
     "tri_ivf_create": [_vp, _vp, _i32, _vp, _i64, C.POINTER(_vp)],
     "tri_ivf_destroy": [_vp],
     "tri_ivf_info": [_vp, _i32p, _i64p, _i32p],

@@ -1352,6 +1352,79 @@ static int ivf_finish(tri_ivf* v, tri_store* s, const float* Cdev, const int* as
   return TRI_OK;
 }
 
+// Exact k-means assignment: every row of s goes to its nearest centroid by
+// the exact float64 distance in the reference's operation order, ties to the
+// smaller centroid id -- i.e. brute_force_knn(VectorStore(C), row, 1)
+// (ann_graph.py:124-137) for each row, run as the certified batched brute
+// force.  Deterministic, so the CPU oracle reproduces it bit-for-bit
+// (oracle.kmeans).  C: nlist x ldc device rows (ldc = s->dp).
+static int exact_assign(tri_store* s, const float* C, int nlist, int* asg, cudaStream_t st) {
+  tri_store* cs = nullptr;
+  TRY(store_from_device(C, s->dp, nlist, s->d, s->device, &cs));
+  cs->prefer_simt = 1;  // centroid distances sit close together: the tight fp32 bound
+  constexpr int kChunk = 4096;
+  DevBuf q64, ids, dd;
+  int rc = TRI_OK;
+  do {
+    Workspace* w = nullptr;
+    if ((rc = cs->lanes.get(st, &w))) break;
+    const long long n = s->n;
+    if ((rc = ensure(q64, (size_t)kChunk * s->d * sizeof(double)))) break;
+    if ((rc = ensure(ids, (size_t)n * sizeof(long long)))) break;
+    if ((rc = ensure(dd, (size_t)kChunk * sizeof(double)))) break;
+    std::vector<int> ones(kChunk, 1);
+    for (long long r0 = 0; r0 < n && rc == TRI_OK; r0 += kChunk) {
+      const int B = (int)std::min<long long>(kChunk, n - r0);
+      cudaError_t e = launch_rows_to_f64(s->X + r0 * s->dp, s->dp, B, s->d, q64.as<double>(), st);
+      if (e != cudaSuccess) {
+        rc = fail(TRI_ECUDA, "k-means assignment: %s", cudaGetErrorString(e));
+        break;
+      }
+      if ((rc = ensure_query_bufs(*w, B, s->d, cs->qld))) break;
+      if ((rc = prep_queries(*w, q64.as<double>(), B, s->d, cs->qld, st))) break;
+      rc = bruteforce_core(cs, *w, *w, q64.as<double>(), B, ones.data(), 1, ids.as<long long>() + r0, dd.as<double>(),
+                           st);
+    }
+    if (rc) break;
+    cudaError_t e = launch_narrow_ids(ids.as<long long>(), n, asg, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(TRI_ECUDA, "k-means assignment: %s", cudaGetErrorString(e));
+  } while (0);
+  cudaStreamSynchronize(st);
+  release(q64);
+  release(ids);
+  release(dd);
+  tri_store_destroy(cs);
+  return rc;
+}
+
+int tri_kmeans_assign(tri_store* s, const float* centroids, int32_t nlist, int32_t* assign) {
+  if (!s || !centroids || !assign) return fail(TRI_EINVAL, "NULL argument");
+  if (nlist < 1) return fail(TRI_EINVAL, "nlist must be >= 1");
+  for (long long i = 0; i < (long long)nlist * s->d; ++i)
+    if (!std::isfinite(centroids[i])) return fail(TRI_EINVAL, "centroids must be finite");
+  DeviceGuard g(s->device);
+  cudaStream_t st = s->own;
+  DevBuf C, asg;
+  int rc = ensure(C, (size_t)nlist * s->dp * sizeof(float));
+  if (!rc) rc = ensure(asg, (size_t)s->n * sizeof(int));
+  if (!rc) {
+    cudaError_t e = cudaMemset2DAsync(C.p, s->dp * sizeof(float), 0, s->dp * sizeof(float), nlist, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(C.p, s->dp * sizeof(float), centroids, s->d * sizeof(float), s->d * sizeof(float), nlist,
+                            cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) rc = fail(TRI_ECUDA, "upload: %s", cudaGetErrorString(e));
+  }
+  if (!rc) rc = exact_assign(s, C.as<float>(), nlist, asg.as<int>(), st);
+  if (!rc) {
+    cudaError_t e = cudaMemcpy(assign, asg.p, (size_t)s->n * sizeof(int), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(TRI_ECUDA, "download: %s", cudaGetErrorString(e));
+  }
+  release(C);
+  release(asg);
+  return rc;
+}
+
 int tri_ivf_train(tri_store* s, int32_t nlist, int32_t iters, const int64_t* init_rows, tri_ivf** out) {
   if (!s || !out || !init_rows) return fail(TRI_EINVAL, "NULL argument");
   if (nlist < 1 || nlist > s->n) return fail(TRI_EINVAL, "nlist must be in [1, %lld], got %d", s->n, nlist);
@@ -1380,10 +1453,7 @@ int tri_ivf_train(tri_store* s, int32_t nlist, int32_t iters, const int64_t* ini
     std::vector<int> hc(nlist);
     std::vector<long long> ho(nlist + 1);
     for (int it = 0; it <= iters && e == cudaSuccess; ++it) {
-      e = cudaMemsetAsync(xm.p, 0, sizeof(unsigned long long), st);
-      if (e == cudaSuccess) e = launch_norms(C.as<float>(), nlist, s->d, s->dp, cn.as<float>(), xm.as<unsigned long long>(), st);
-      if (e == cudaSuccess)
-        e = launch_assign(s->X, s->n, s->d, s->dp, C.as<float>(), nlist, s->dp, cn.as<float>(), asg.as<int>(), st);
+      if ((rc = exact_assign(s, C.as<float>(), nlist, asg.as<int>(), st))) break;
       if (it == iters) break;
       if (e == cudaSuccess) e = launch_counts(asg.as<int>(), s->n, nlist, cnt.as<int>(), st);
       if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), cnt.p, (size_t)nlist * sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -1397,6 +1467,7 @@ int tri_ivf_train(tri_store* s, int32_t nlist, int32_t iters, const int64_t* ini
         e = launch_centroid_update(s->X, s->dp, s->d, perm.as<long long>(), off.as<long long>(), nlist, C.as<float>(), s->dp, st);
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // ho is reused
     }
+    if (rc) break;
     if (e != cudaSuccess) {
       rc = fail(TRI_ECUDA, "k-means: %s", cudaGetErrorString(e));
       break;

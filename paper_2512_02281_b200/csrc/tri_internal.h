@@ -256,8 +256,8 @@ struct PackLaunch {
 cudaError_t launch_pack(const PackLaunch& p, cudaStream_t st);
 
 // k-means / index layout --------------------------------------------------------
-cudaError_t launch_assign(const float* X, long long n, int d, long long ldx, const float* C, int nlist,
-                          long long ldc, const float* cnorm, int* assign, cudaStream_t st);
+cudaError_t launch_rows_to_f64(const float* X, long long ldx, long long n, int d, double* out, cudaStream_t st);
+cudaError_t launch_narrow_ids(const long long* ids, long long n, int* out, cudaStream_t st);
 cudaError_t launch_counts(const int* assign, long long n, int nlist, int* counts, cudaStream_t st);
 cudaError_t launch_list_members(const int* assign, long long n, int nlist, const long long* offsets,
                                 long long* perm, cudaStream_t st);

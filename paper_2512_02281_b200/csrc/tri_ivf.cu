@@ -147,102 +147,37 @@ cudaError_t launch_pack(const PackLaunch& p, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
-// k-means assignment: nearest centroid by fp32 dot-form score cn - 2 x.c
-// (the row norm is constant per row).  64x64 register-tiled SGEMM with a
-// running (score, centroid id) argmin; ties go to the smaller id.
-
-constexpr int AB = 64, AK = 16;
-
-__global__ void __launch_bounds__(256) assign_kernel(const float* __restrict__ X, long long n, long long ldx,
-                                                     int dp, const float* __restrict__ C, int nlist, long long ldc,
-                                                     const float* __restrict__ cnorm, int* __restrict__ assign) {
-  __shared__ __align__(16) float As[AK][AB];
-  __shared__ __align__(16) float Bs[AK][AB];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const long long row0 = (long long)blockIdx.x * AB;
-  float best[4];
-  int bid[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    best[i] = __int_as_float(0x7f800000);
-    bid[i] = 0x7fffffff;
-  }
-  const int lr = tid >> 2, lk = (tid & 3) * 4;
-  for (int c0 = 0; c0 < nlist; c0 += AB) {
-    float acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-    for (int k0 = 0; k0 < dp; k0 += AK) {
-      float4 av = make_float4(0.f, 0.f, 0.f, 0.f), bv = av;
-      if (row0 + lr < n && k0 + lk < dp) av = *reinterpret_cast<const float4*>(X + (row0 + lr) * ldx + k0 + lk);
-      if (c0 + lr < nlist && k0 + lk < dp) bv = *reinterpret_cast<const float4*>(C + (long long)(c0 + lr) * ldc + k0 + lk);
-      __syncthreads();
-      As[lk + 0][lr] = av.x;
-      As[lk + 1][lr] = av.y;
-      As[lk + 2][lr] = av.z;
-      As[lk + 3][lr] = av.w;
-      Bs[lk + 0][lr] = bv.x;
-      Bs[lk + 1][lr] = bv.y;
-      Bs[lk + 2][lr] = bv.z;
-      Bs[lk + 3][lr] = bv.w;
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < AK; ++kk) {
-        float4 a = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
-        float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
-        float ar[4] = {a.x, a.y, a.z, a.w}, br[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int c = c0 + tx * 4 + j;
-      if (c < nlist) {
-        float cn = cnorm[c];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float s = __fmaf_rn(-2.f, acc[i][j], cn);
-          if (s < best[i] || (s == best[i] && c < bid[i])) {
-            best[i] = s;
-            bid[i] = c;
-          }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float s = best[i];
-    int c = bid[i];
-    for (int o = 1; o < 16; o <<= 1) {
-      float s2 = __shfl_xor_sync(0xffffffffu, s, o);
-      int c2 = __shfl_xor_sync(0xffffffffu, c, o);
-      if (s2 < s || (s2 == s && c2 < c)) {
-        s = s2;
-        c = c2;
-      }
-    }
-    long long r = row0 + ty * 4 + i;
-    if (tx == 0 && r < n) assign[r] = c;
-  }
-}
-
-cudaError_t launch_assign(const float* X, long long n, int d, long long ldx, const float* C, int nlist,
-                          long long ldc, const float* cnorm, int* assign, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  int dp = (d + 3) & ~3;
-  assign_kernel<<<(unsigned)((n + AB - 1) / AB), 256, 0, st>>>(X, n, ldx, dp, C, nlist, ldc, cnorm, assign);
-  return cudaGetLastError();
-}
 
 __global__ void counts_kernel(const int* __restrict__ assign, long long n, int* counts) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) atomicAdd(&counts[assign[i]], 1);
+}
+
+// Exact k-means assignment helpers: rows widened to the float64 queries the
+// exact brute force takes, and its int64 top-1 ids narrowed to list ids.
+__global__ void rows_to_f64_kernel(const float* __restrict__ X, long long ldx, long long n, int d,
+                                   double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * d) return;
+  const long long r = i / d;
+  out[i] = (double)X[r * ldx + (i - r * d)];
+}
+
+cudaError_t launch_rows_to_f64(const float* X, long long ldx, long long n, int d, double* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  rows_to_f64_kernel<<<(unsigned)((n * d + 255) / 256), 256, 0, st>>>(X, ldx, n, d, out);
+  return cudaGetLastError();
+}
+
+__global__ void narrow_ids_kernel(const long long* __restrict__ ids, long long n, int* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (int)ids[i];
+}
+
+cudaError_t launch_narrow_ids(const long long* ids, long long n, int* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  narrow_ids_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ids, n, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_counts(const int* assign, long long n, int nlist, int* counts, cudaStream_t st) {

@@ -67,12 +67,34 @@ class IVFFlatIndex:
     # -- construction -----------------------------------------------------
     @classmethod
     def train(cls, store, nlist: int, iters: int = 5, seed: int = 0) -> "IVFFlatIndex":
-        """GPU Lloyd k-means (``iters`` updates) from seeded initial rows."""
+        """GPU Lloyd k-means (``iters`` updates) from seeded initial rows.
+
+        Deterministic: exact nearest-centroid assignment and float64 centroid
+        sums in ascending id order, so ``oracle.kmeans`` reproduces the
+        artifact bit-for-bit (the bench's CPU arm builds the same index)."""
         dev = store.device() if isinstance(store, VectorStore) else store
         rows = init_rows(dev.n, nlist, seed)
         h = C.c_void_p()
         _lib.check(_lib.gpu().tri_ivf_train(dev.handle, int(nlist), int(iters), rows.ctypes.data, C.byref(h)))
         return cls(h, nlist, dev.n, dev.d, dev.device)
+
+    @staticmethod
+    def assign(store, centroids: np.ndarray) -> np.ndarray:
+        """Exact nearest-centroid list id of every store row (tri_kmeans_assign):
+        k = 1 brute force over the centroids, ties to the smaller id."""
+        dev = store.device() if isinstance(store, VectorStore) else store
+        cen = np.ascontiguousarray(centroids, dtype=np.float32)
+        if cen.ndim != 2 or cen.shape[1] != dev.d:
+            raise ValueError(f"centroids must be (nlist, {dev.d}), got {cen.shape}")
+        out = np.empty(dev.n, dtype=np.int32)
+        _lib.check(_lib.gpu().tri_kmeans_assign(dev.handle, cen.ctypes.data, cen.shape[0], out.ctypes.data))
+        return out
+
+    @classmethod
+    def from_centroids(cls, store, centroids: np.ndarray, id_offset: int = 0) -> "IVFFlatIndex":
+        """Lists from given centroids (each row to its exact nearest centroid):
+        how a shard of a larger database joins a shared coarse quantiser."""
+        return cls.from_artifact(store, centroids, cls.assign(store, centroids), id_offset=id_offset)
 
     @classmethod
     def from_artifact(cls, store, centroids: np.ndarray, assign: np.ndarray, id_offset: int = 0) -> "IVFFlatIndex":
