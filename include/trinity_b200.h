@@ -194,6 +194,17 @@ int tri_engine_retired_by_id(tri_engine* e, int64_t capacity, int32_t ld, int32_
                              double* dists, int32_t* extends, int32_t* ks);
 int tri_engine_pending_retired(tri_engine* e, int32_t* n);
 
+/* Test hooks for the certificate.  debug_bound: the error
+ * model constants cdot, csum of |D~ - D| <= cdot 2|q||x| + csum (|q| + |x|)^2
+ * for a scan arithmetic (0 fp32 SIMT, 1 TF32, 2 fp16, 3 split fp16 coarse).
+ * ivf_debug_keys: the last search's candidate keys ((fp32 order bits of D~)
+ * << 32 | row position), which = 0 the fine partial lists (layout[3 i ..] =
+ * part_off, kp, slots of query i; slot j holds probe j's list), which = 1 the
+ * coarse step's merged lists (layout[0] = row stride).  keys may be NULL to
+ * query the size. */
+int tri_debug_bound(int32_t d, int32_t mode, double* cdot, double* csum);
+int tri_ivf_debug_keys(tri_ivf* v, int32_t which, uint64_t* keys, int64_t cap, int64_t* n, int64_t* layout);
+
 /* Exact merge of G per-shard result lists (device buffers, G x B x k_in,
  * id -1 = empty) into the global top-k_out by (dist, id). */
 int tri_merge_topk(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t k_out,

@@ -67,6 +67,8 @@ _SIGS = {
     "tri_engine_retired": [_vp, _i32, _i32, _i32p, _vp, _vp, _vp, _vp, _vp, _vp],
     "tri_engine_retired_by_id": [_vp, _i64, _i32, _i32p, _vp, _vp, _vp, _vp, _vp],
     "tri_engine_pending_retired": [_vp, _i32p],
+    "tri_debug_bound": [_i32, _i32, _f64p, _f64p],
+    "tri_ivf_debug_keys": [_vp, _i32, _vp, _i64, _i64p, _vp],
     "tri_merge_topk": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp],
 }
 _RESTYPE = {"tri_last_error": C.c_char_p}
