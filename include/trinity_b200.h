@@ -204,6 +204,12 @@ int tri_engine_pending_retired(tri_engine* e, int32_t* n);
  * query the size. */
 int tri_debug_bound(int32_t d, int32_t mode, double* cdot, double* csum);
 int tri_ivf_debug_keys(tri_ivf* v, int32_t which, uint64_t* keys, int64_t cap, int64_t* n, int64_t* layout);
+/* Timeline probe of the tensor-core scan (option scan_debug & 8): per CTA
+ * (up to 256) eight globaltimer stamps: entry, setup done, first item
+ * published, first query tile staged, first chunk's MMAs issued, first chunk
+ * read by the epilogue, last TMA issued, epilogue done.  Synchronises the device.
+ * n = 4 instead reads and resets the scan_debug & 16 selection counters. */
+int tri_debug_scan_ts(uint64_t* out, int32_t n);
 
 /* Exact merge of G per-shard result lists (device buffers, G x B x k_in,
  * id -1 = empty) into the global top-k_out by (dist, id). */

@@ -69,6 +69,7 @@ _SIGS = {
     "tri_engine_pending_retired": [_vp, _i32p],
     "tri_debug_bound": [_i32, _i32, _f64p, _f64p],
     "tri_ivf_debug_keys": [_vp, _i32, _vp, _i64, _i64p, _vp],
+    "tri_debug_scan_ts": [_vp, _i32],
     "tri_merge_topk": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp],
 }
 _RESTYPE = {"tri_last_error": C.c_char_p}

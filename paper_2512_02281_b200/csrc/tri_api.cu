@@ -120,6 +120,9 @@ long long g_gthr = 1;         // cross-item per-query threshold in the tensor-co
 long long g_scan_abufs = 1;  // IVF tensor-core scan append-list buffers (option "scan_abufs": 1 or 2)
 long long g_scan_qbufs = 2;   // tensor-core scan query tiles (option "scan_qbufs": 1 or 2)
 long long g_coarse_tc = 1;    // IVF coarse GEMM on tensor cores (split fp16) when the index allows
+long long g_bf_wide = 1;      // brute force: 64-query groups (one row pass per 64 queries) when kp <= 64
+long long g_bf_seed = 2;      // ... with the TMEM seed pass (tri_tcscan.cu tc_seed_pass): 1 per item, 2 cross-item
+long long g_bf_qtma = 1;      // ... and TMA-loaded query tiles
 
 
 // Candidate capacity: over-fetch so the certified re-rank almost never falls
@@ -249,7 +252,7 @@ int make_tmap(CUtensorMap* map, const void* X, long long rows, int ldx, bool tc,
 // or the queries do not fit its shared-memory layout.
 bool use_tc(int qld, int kp_max_tc) {
   if (g_scan_kernel == 1) return false;
-  return kp_max_tc <= kTcMaxKp && qld <= kTcMaxQld && tc_scan_smem_bytes(qld * 4) <= (size_t)kSmemLimit;
+  return kp_max_tc <= kTcMaxKp && qld <= kTcMaxQld && tc_scan_smem_bytes(qld * 4, kTcGroup) <= (size_t)kSmemLimit;
 }
 
 // Per-search scratch shared by the brute-force and IVF pipelines.  One
@@ -261,6 +264,7 @@ struct Workspace {
   // IVF per-search buffers
   DevBuf probes, probe_d, counts, fill, mbase, items, members, counters, meta;
   DevBuf Qh, qinv;  // fp16 scan: scaled fp16 queries + 1/(s_q s_x)
+  DevBuf seedb;     // wide brute force: per (query, item) smallest distance (cross-item seed)
   DevBuf gthr;      // per-query cross-item scan threshold
   DevBuf Ql;        // lo half of the split fp16 queries (tensor-core coarse GEMM)
   bool split_q = false;  // this search prepared Qh/Ql/qinv for the split coarse GEMM
@@ -279,6 +283,9 @@ struct Workspace {
   int plan_B = -1;
   long long plan_n = -1;
   int n_items = 0, grid = 0, gmax = 0, cap = 0, kp_max = 0, k_max = 0;
+  int nq = kTcGroup;  // tensor-core scan query-group width of the plan
+  int q_tma = 0;      // groups are runs of consecutive queries
+  CUtensorMap qmap;   // over Q32 (wide brute-force groups), encoded per search
   long long plan_opts = -1;
   bool tc = false;
   bool dense = false;
@@ -329,7 +336,7 @@ struct Workspace {
     graphs.clear();
     for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat,
                       &probes, &probe_d, &counts, &fill, &mbase, &items, &members, &counters, &meta, &Qh, &qinv,
-                      &gthr, &fxs, &Ql})
+                      &gthr, &fxs, &Ql, &seedb})
       release(*b);
     for (HostBuf* b : {&h_plan, &h_bq, &h_bids, &h_bd}) {
       if (b->p) cudaFreeHost(b->p);
@@ -585,7 +592,7 @@ int choose_scan(int qld, int d, int B, const int* k, std::vector<int>& kp, ScanC
 }
 
 long long plan_opts() {
-  return g_pack_mixed * 1000000000 + g_dense_pow2 * 100000000 + g_dense_off * 10000000 + g_scan_kernel * 100000 +
+  return g_bf_wide * 10000000000LL + g_pack_mixed * 1000000000 + g_dense_pow2 * 100000000 + g_dense_off * 10000000 + g_scan_kernel * 100000 +
          g_kp_extra;
 }
 
@@ -672,6 +679,12 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
   // with the group -- small stores (the IVF coarse step) shrink groups until
   // the items cover every SM.
   int gmax = ch.gmax;
+  int nq = kTcGroup;
+  if (ch.tc && g_bf_wide && kp_max <= kTcWideMaxKp && B > kTcGroup &&
+      tc_scan_stages(s->qld * 4, kSmemLimit, 0, 1, 1, kTcGroupWide) >= kTcMinStages) {
+    gmax = kTcGroupWide;  // every row slab serves 64 queries: a quarter of the L2 reads of 16-query groups
+    nq = kTcGroupWide;
+  }
   if (!ch.tc) {
     auto n_groups = [&](int g) {
       std::vector<int> per(kNumCls, 0);
@@ -700,7 +713,9 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
   long long nr = std::max<long long>(1, ((long long)nsm + (long long)groups.size() - 1) / (long long)groups.size());
   nr = std::min(nr, max_ranges);
   long long R = (s->n + nr - 1) / nr;
-  R = ((R + 511) / 512) * 512;
+  const long long rq = ch.tc ? 32 : 512;  // tensor-core items: any multiple of the 32-row tail box
+  R = ((R + rq - 1) / rq) * rq;
+  if (nq == kTcGroupWide) R = std::min<long long>(R, (long long)kTcWideMaxChunks * 128);  // chunks stay in TMEM
   nr = (s->n + R - 1) / R;
   // sizes
   std::vector<QueryMeta> meta(B);
@@ -761,6 +776,11 @@ int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_
   w.n_items = (int)n_items;
   w.grid = (int)std::min<long long>(n_items, nsm);
   w.gmax = gmax;
+  w.nq = nq;
+  w.q_tma = 1;  // every group is a run of consecutive query indices (TMA query tiles)
+  for (const auto& g : groups)
+    for (size_t i = 1; i < g.size(); ++i)
+      if (g[i] != g[0] + (int)i) w.q_tma = 0;
   w.cap = cap;
   w.kp_max = kp_max;
   w.k_max = k_max;
@@ -814,12 +834,18 @@ int dense_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q6
   return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, kSimt, st);
 }
 
-// Run the brute-force pipeline on prepared queries (Q32/qn32/qn64 in `qw`,
-// fp64 queries at q64dev).  Results to device ids/dists with row stride ldo.
+int prep_queries(Workspace& w, const double* q64dev, int B, int d, int qld, cudaStream_t st);
+
+// Run the brute-force pipeline; prep = true prepares the fp64 queries at
+// q64dev into `w` first (w == qw), otherwise they are prepared in `qw`
+// (Q32/qn32/qn64).  Results to device ids/dists with row stride ldo.
 int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q64dev, int B, const int* k,
-                    int ldo, long long* ids, double* dists, cudaStream_t st) {
+                    int ldo, long long* ids, double* dists, cudaStream_t st, bool prep) {
   TRY(plan_bruteforce(s, w, B, k, st));
-  if (w.dense) return dense_core(s, w, qw, q64dev, B, ldo, ids, dists, st);
+  if (w.dense) {
+    if (prep) TRY(prep_queries(w, q64dev, B, s->d, s->qld, st));
+    return dense_core(s, w, qw, q64dev, B, ldo, ids, dists, st);
+  }
   TRY(ensure(w.part, (size_t)w.part_keys * sizeof(unsigned long long)));
   TRY(ensure(w.merged, (size_t)B * w.kp_max * sizeof(unsigned long long)));
   TRY(ensure(w.exact, (size_t)B * w.kp_max * 16));
@@ -829,8 +855,10 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   int* ctr = reinterpret_cast<int*>(plan + w.plan_bytes - 256);
   int* n_flag = w.flags.as<int>();
   int* flag_list = n_flag + 64;
-  CU(cudaMemsetAsync(ctr + 1, 0, sizeof(int), st));
-  CU(cudaMemsetAsync(n_flag, 0, 2 * sizeof(int), st));  // flag count + fix-up completion counter
+  // per-search fills: the prep kernel does them on the side when it runs here
+  ClearList cl{};
+  cl.add(ctr + 1, 2, 0u);   // work-item counter + seed publish counter
+  cl.add(n_flag, 2, 0u);    // flag count + fix-up completion counter
 
   ScanLaunch sl{};
   sl.tmap = &s->tmap;
@@ -853,18 +881,57 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   sl.grid = w.grid;
   sl.dbg = (int)g_scan_debug;
   sl.l2hint = 0;  // rows re-read by the batch's other query groups: default L2 policy
-  sl.qbufs = (int)g_scan_qbufs;
-  sl.abufs = 2;  // brute force: selection-bound (L2-resident rows), keep one barrier per chunk
-  sl.stages = tc_scan_stages(s->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs, sl.abufs);
+  sl.nq = w.nq;
+  // brute force: selection-bound (L2-resident rows), keep one barrier per chunk
+  // -- except 64-query groups, whose 64 KB append buffer and 32 KB query tile
+  // leave room for only one of each beside a 7-slab ring
+  sl.qbufs = w.nq == kTcGroupWide ? 1 : (int)g_scan_qbufs;
+  sl.abufs = w.nq == kTcGroupWide ? 1 : 2;
+  sl.stages = tc_scan_stages(s->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs, sl.abufs, sl.nq);
   sl.box_rows = s->box_rows;
+  if (w.nq == kTcGroupWide) {
+    sl.seed = (int)g_bf_seed;
+    // cross-item seed: one wave (every item its own CTA) of at least kp items
+    if (sl.seed == 2 && !(w.n_items <= w.grid && w.n_items <= kTcSeedItems && w.n_items >= w.kp_max)) sl.seed = 1;
+    if (sl.seed == 2) {
+      const size_t sb = ((size_t)B * w.n_items * sizeof(uint32_t) + 255) & ~(size_t)255;
+      TRY(ensure(w.seedb, sb + (size_t)B * sizeof(int)));
+      cl.add(w.seedb.p, (long long)(sb / 4), 0xffffffffu);
+      int* ccnt = reinterpret_cast<int*>(static_cast<unsigned char*>(w.seedb.p) + sb);
+      cl.add(ccnt, B, 0u);
+      sl.seed_min = static_cast<uint32_t*>(w.seedb.p);
+      sl.seed_ctr = ctr + 2;
+      sl.seed_items = w.n_items;
+      sl.grid = w.n_items;  // one CTA per item (tc_producer: fixed assignment)
+      sl.compact_cnt = ccnt;
+      sl.meta = meta;
+    }
+    if (w.q_tma && g_bf_qtma) {
+      TRY(make_tmap(&w.qmap, qw.Q32.p, B, s->qld, true, false, kTcGroupWide));
+      sl.q_tma = 1;
+      sl.tmap_q = &w.qmap;
+    }
+  }
   if (g_gthr && w.tc) {
     TRY(ensure(w.gthr, (size_t)B * sizeof(unsigned long long)));
-    CU(cudaMemsetAsync(w.gthr.p, 0xff, (size_t)B * sizeof(unsigned long long), st));
+    cl.add(w.gthr.p, 2LL * B, 0xffffffffu);
     sl.gthr = w.gthr.as<unsigned long long>();
   }
+  if (prep) {
+    CU(launch_prep(q64dev, B, s->d, w.Q32.as<float>(), s->qld, w.qn32.as<float>(), w.qn64.as<double>(), nullptr, st,
+                   1.f, nullptr, 0, nullptr, nullptr, &cl));
+  } else {
+    for (int r = 0; r < cl.n; ++r)
+      CU(cl.val[r] == 0 ? cudaMemsetAsync(cl.p[r], 0, (size_t)cl.words[r] * 4, st)
+                        : cudaMemsetAsync(cl.p[r], 0xff, (size_t)cl.words[r] * 4, st));
+  }
   CU(w.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
-  CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
-                  st));
+  if (sl.compact_cnt)
+    CU(launch_merge_compact(w.part.as<unsigned long long>(), sl.compact_cnt, meta, w.merged.as<unsigned long long>(),
+                            w.kp_max, B, w.kp_max, st));
+  else
+    CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
+                    st));
   return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, w.tc ? kTf32 : kSimt, st);
 }
 
@@ -1025,6 +1092,9 @@ int tri_set_option(const char* name, int64_t value) {
     g_scan_qbufs = value;
   }
   else if (!std::strcmp(name, "coarse_tc")) g_coarse_tc = value;
+  else if (!std::strcmp(name, "bf_wide")) g_bf_wide = value;
+  else if (!std::strcmp(name, "bf_seed")) g_bf_seed = value;
+  else if (!std::strcmp(name, "bf_qtma")) g_bf_qtma = value;
   else if (!std::strcmp(name, "dense_pow2")) g_dense_pow2 = value;
 
   else if (!std::strcmp(name, "coarse_split")) {
@@ -1137,8 +1207,8 @@ int tri_knn_bruteforce(tri_store* s, const double* q, int32_t B, const int32_t* 
   }
   auto body = [&]() -> int {
     CU(cudaMemcpyAsync(w.q64.p, qsrc, qb, cudaMemcpyHostToDevice, st));
-    TRY(prep_queries(w, w.q64.as<double>(), B, s->d, s->qld, st));
-    TRY(bruteforce_core(s, w, w, w.q64.as<double>(), B, k, ldo, w.out_ids.as<long long>(), w.out_d.as<double>(), st));
+    TRY(bruteforce_core(s, w, w, w.q64.as<double>(), B, k, ldo, w.out_ids.as<long long>(), w.out_d.as<double>(), st,
+                        true));
     CU(cudaMemcpyAsync(dst_ids, w.out_ids.p, ob, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(dst_d, w.out_d.p, ob, cudaMemcpyDeviceToHost, st));
     return TRI_OK;
@@ -1395,9 +1465,8 @@ static int exact_assign(tri_store* s, const float* C, int nlist, int* asg, cudaS
         break;
       }
       if ((rc = ensure_query_bufs(*w, B, s->d, cs->qld))) break;
-      if ((rc = prep_queries(*w, q64.as<double>(), B, s->d, cs->qld, st))) break;
       rc = bruteforce_core(cs, *w, *w, q64.as<double>(), B, ones.data(), 1, ids.as<long long>() + r0, dd.as<double>(),
-                           st);
+                           st, true);
     }
     if (rc) break;
     cudaError_t e = launch_narrow_ids(ids.as<long long>(), n, asg, st);
@@ -1634,7 +1703,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   TRY(ensure(w.probes, (size_t)B * npmax * sizeof(long long)));
   TRY(ensure(w.probe_d, (size_t)B * npmax * sizeof(double)));
   TRY(bruteforce_core(v->cstore, *cw, w, q, B, nprobe, npmax, w.probes.as<long long>(), w.probe_d.as<double>(),
-                      st));
+                      st, false));
 
   // 2. per-query plan -> device
   long long part_keys = 0, members = 0;
@@ -1734,7 +1803,8 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   sl.qbufs = (int)g_scan_qbufs;
   // one append buffer: the list scan is stream-bound, and the 16 KB buy a ring stage
   sl.abufs = (int)g_scan_abufs;
-  sl.stages = tc_scan_stages(f16 ? v->dph * 2 : v->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs, sl.abufs);
+  sl.nq = kTcGroup;
+  sl.stages = tc_scan_stages(f16 ? v->dph * 2 : v->qld * 4, kSmemLimit, (int)g_tc_stages, sl.qbufs, sl.abufs, sl.nq);
   sl.box_rows = v->box_rows;
   TRY(mark(2));
   CU(ch.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
@@ -1983,8 +2053,7 @@ int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32
   TRY(s->lanes.get(st, &w));
   TRY(ensure_query_bufs(*w, B, s->d, s->qld));
   TRY(graph_run(nullptr, *w, nullptr, st, 2, B, k, k, ldo, q, ids, dists, [&]() -> int {
-    TRY(prep_queries(*w, q, B, s->d, s->qld, st));
-    return bruteforce_core(s, *w, *w, q, B, k, ldo, reinterpret_cast<long long*>(ids), dists, st);
+    return bruteforce_core(s, *w, *w, q, B, k, ldo, reinterpret_cast<long long*>(ids), dists, st, true);
   }));
   return lane_done(*w, st);
 }
@@ -2139,6 +2208,12 @@ int tri_ivf_last_scan_kind(tri_ivf* v, int32_t* kind) {
   if (!v || !kind) return fail(TRI_EINVAL, "null handle");
   const Workspace& w = v->lanes.recent();
   *kind = w.last_f16 ? 2 : (v->lanes.used ? 1 : 0);
+  return TRI_OK;
+}
+
+int tri_debug_scan_ts(uint64_t* out, int32_t n) {
+  CU(cudaDeviceSynchronize());
+  CU(read_scan_ts(reinterpret_cast<unsigned long long*>(out), n));
   return TRI_OK;
 }
 

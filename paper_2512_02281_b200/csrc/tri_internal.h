@@ -75,7 +75,24 @@ struct ScanLaunch {
   int qbufs;  // tensor-core scan: query tiles (2 = next item staged during this one; 1 frees a ring stage)
   int abufs;  // tensor-core scan: append-list buffers (2 = one barrier per chunk; 1 = two barriers, frees a ring stage)
   int l2hint;  // tensor-core scan TMA loads: 0 default, 1 L2 evict_first, 2 L2 evict_last
+  int nq;      // tensor-core scan query-group width (MMA N): kTcGroup or kTcGroupWide
+  // brute force (nq = kTcGroupWide): items of consecutive queries load their
+  // query tile with TMA through tmap_q (a CUtensorMap over Q: 32-float x 64-row
+  // SW128 boxes); seed = 1 runs the seed pass (items <= kTcWideMaxChunks chunks)
+  int q_tma;
+  const void* tmap_q;
+  int seed;            // 1: per-item seed; 2: cross-item seed (one item per CTA, seed_items <= kTcSeedItems)
+  uint32_t* seed_min;  // seed 2: B x seed_items fp32 order bits of each item's smallest distance (0xff.. = none)
+  int* seed_ctr;       // seed 2: items that published (zeroed before the launch)
+  int seed_items;
+  // seed 2: each item appends at most kp survivors per query, unsorted, at the
+  // front of the query's partial region (part + meta part_off), counted here
+  // (B ints, zeroed before the launch); merged by launch_merge_compact
+  int* compact_cnt;
+  const QueryMeta* meta;
 };
+constexpr int kTcSeedItems = 160;
+constexpr int kTcWideMaxChunks = 8;  // 8 x 64 TMEM columns: a wide item's every chunk stays resident
 
 size_t scan_smem_bytes(int gmax, int qld, int cap);
 int scan_gmax(int qld, int cap, int smem_limit);
@@ -84,17 +101,37 @@ cudaError_t launch_scan(const ScanLaunch& s, cudaStream_t st);
 // tensor-core scan (tri_tcscan.cu): fixed groups of 16 queries, qld <= kTcMaxQld
 constexpr int kTcMaxQld = 1024;
 constexpr int kTcGroup = 16;
+constexpr int kTcGroupWide = 64;   // brute force: one row pass per 64 queries (MMA N = 64)
+constexpr int kTcWideMaxKp = 64;   // ... with register lists of at most 64 keys
 constexpr int kTcMaxKp = 256;  // register-resident top-kp lists in the epilogue
 constexpr int kTcMinStages = 4;
-size_t tc_scan_smem_bytes(int row_bytes);  // minimum (kTcMinStages ring); row_bytes = qld*4 or qldh*2
-int tc_scan_stages(int row_bytes, int smem_limit, int want, int qbufs, int abufs);  // deepest ring that fits (want > 0 caps it)
+// minimum (kTcMinStages ring) shared memory; row_bytes = qld*4 or qldh*2, nq = query-group width
+size_t tc_scan_smem_bytes(int row_bytes, int nq);
+// deepest ring that fits (want > 0 caps it)
+int tc_scan_stages(int row_bytes, int smem_limit, int want, int qbufs, int abufs, int nq);
 cudaError_t launch_scan_tc(const ScanLaunch& s, cudaStream_t st);
+cudaError_t read_scan_ts(unsigned long long* out, int n);  // dbg & 8 timeline stamps (256 CTAs x 8)
 
+// Up to six 32-bit fills the prep kernel performs on the side (the search's
+// counters and seed buffers), replacing one cudaMemsetAsync each.
+struct ClearList {
+  static constexpr int kMax = 6;
+  void* p[kMax];
+  long long words[kMax];
+  uint32_t val[kMax];
+  int n;
+  void add(void* ptr, long long w, uint32_t v) {
+    p[n] = ptr;
+    words[n] = w;
+    val[n] = v;
+    ++n;
+  }
+};
 // fp64 queries -> fp32 rows + norms; with Qh != nullptr also the fp16 scan
 // copy (scale sx of the index's fp16 rows) in the same kernel.
 cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,
                         int* bad, cudaStream_t st, float sx = 1.f, void* Qh = nullptr, int ldh = 0,
-                        float* qinv = nullptr, void* Ql = nullptr);
+                        float* qinv = nullptr, void* Ql = nullptr, const ClearList* clears = nullptr);
 cudaError_t launch_absmax(const float* X, long long n, int d, long long ldx, unsigned int* bits, cudaStream_t st);
 cudaError_t launch_to_half(const float* X, long long n, int d, long long ldx, float sx, void* Xh, int ldh,
                            cudaStream_t st);
@@ -145,6 +182,9 @@ cudaError_t launch_dense_select(const float* D, int nsl, long long ldd, int B, c
 
 cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, unsigned long long* merged,
                          int ld_merged, int B, int kp_max, cudaStream_t st);
+// cnt[q] unsorted keys at part + meta[q].part_off (ScanLaunch::compact_cnt)
+cudaError_t launch_merge_compact(const unsigned long long* part, const int* cnt, const QueryMeta* meta,
+                                 unsigned long long* merged, int ld_merged, int B, int kp_max, cudaStream_t st);
 
 struct Exact;
 

@@ -37,8 +37,14 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double* __rest
                                                             float* __restrict__ Q32, int qld, float* __restrict__ qn32,
                                                             double* __restrict__ qn64, int* bad, float sx,
                                                             __half* __restrict__ Qh, int ldh,
-                                                            float* __restrict__ qinv, __half* __restrict__ Ql) {
+                                                            float* __restrict__ qinv, __half* __restrict__ Ql,
+                                                            ClearList cl) {
   const int q = blockIdx.x, tid = threadIdx.x;
+  // per-search counters / buffers the later kernels expect filled (instead of
+  // one cudaMemsetAsync each)
+  for (int r = 0; r < cl.n; ++r)
+    for (long long i = (long long)q * kPrepThreads + tid; i < cl.words[r]; i += (long long)gridDim.x * kPrepThreads)
+      static_cast<uint32_t*>(cl.p[r])[i] = cl.val[r];
   double v[kPrepMaxU];
 #pragma unroll
   for (int u = 0; u < kPrepMaxU; ++u) {
@@ -110,11 +116,14 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double* __rest
 }
 
 cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, float* qn32, double* qn64,
-                        int* bad, cudaStream_t st, float sx, void* Qh, int ldh, float* qinv, void* Ql) {
+                        int* bad, cudaStream_t st, float sx, void* Qh, int ldh, float* qinv, void* Ql,
+                        const ClearList* clears) {
   if (B <= 0) return cudaSuccess;
   if (qld > kPrepThreads * kPrepMaxU || (Qh && ldh > kPrepThreads * kPrepMaxU)) return cudaErrorInvalidValue;
+  ClearList cl{};
+  if (clears) cl = *clears;
   prep_kernel<<<B, kPrepThreads, 0, st>>>(q64, d, Q32, qld, qn32, qn64, bad, sx, static_cast<__half*>(Qh), ldh,
-                                          qinv, static_cast<__half*>(Ql));
+                                          qinv, static_cast<__half*>(Ql), cl);
   return cudaGetLastError();
 }
 
@@ -367,6 +376,69 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_tree_kernel(const unsi
     case 128: merge_tree<4>(src, m.n_slots, dst, msm); break;
     default: merge_tree<8>(src, m.n_slots, dst, msm); break;
   }
+}
+
+// Compact merge (wide brute force with a cross-item seed): query q's
+// candidates are cnt[q] UNSORTED keys at the front of its partial region
+// (every scan CTA appended at most kp of its survivors there).  Warp w folds
+// keys w*32, w*32 + 256, ... 32 at a time, then the 8 lists merge pairwise.
+template <int KL>
+__device__ __forceinline__ void merge_compact(const unsigned long long* __restrict__ src, int n,
+                                              unsigned long long* __restrict__ dst, unsigned long long* sm) {
+  constexpr int KP = 32 * KL;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long L[KL];
+#pragma unroll
+  for (int j = 0; j < KL; ++j) L[j] = TRI_KEY_MAX;
+  for (int b = warp * 32; b < n; b += 32 * kMergeWarps) list_fold32<KL>(L, b + lane < n ? __ldcg(src + b + lane) : TRI_KEY_MAX, lane);
+  for (int stride = 1; stride < kMergeWarps; stride <<= 1) {
+    if ((warp & (2 * stride - 1)) == stride) {
+#pragma unroll
+      for (int j = 0; j < KL; ++j) sm[warp * KP + j * 32 + lane] = L[j];
+    }
+    __syncthreads();
+    if ((warp & (2 * stride - 1)) == 0 && warp + stride < kMergeWarps && stride * 32 < n) {
+      unsigned long long R[KL];
+#pragma unroll
+      for (int j = 0; j < KL; ++j) R[j] = sm[(warp + stride) * KP + (KL - 1 - j) * 32 + (31 - lane)];
+      list_merge_rev<KL>(L, R, lane);
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+#pragma unroll
+    for (int j = 0; j < KL; ++j) dst[j * 32 + lane] = L[j];
+  }
+}
+
+__global__ void __launch_bounds__(32 * kMergeWarps) merge_compact_kernel(const unsigned long long* __restrict__ part,
+                                                                         const int* __restrict__ cnt,
+                                                                         const QueryMeta* __restrict__ meta,
+                                                                         unsigned long long* __restrict__ merged,
+                                                                         int ld_merged) {
+  extern __shared__ unsigned long long msm[];
+  const int q = blockIdx.x;
+  const QueryMeta m = meta[q];
+  const unsigned long long* src = part + m.part_off;
+  unsigned long long* dst = merged + (long long)q * ld_merged;
+  const int n = min(cnt[q], m.n_slots * m.kp);
+  switch (m.kp) {
+    case 32: merge_compact<1>(src, n, dst, msm); break;
+    case 64: merge_compact<2>(src, n, dst, msm); break;
+    case 128: merge_compact<4>(src, n, dst, msm); break;
+    default: merge_compact<8>(src, n, dst, msm); break;
+  }
+}
+
+cudaError_t launch_merge_compact(const unsigned long long* part, const int* cnt, const QueryMeta* meta,
+                                 unsigned long long* merged, int ld_merged, int B, int kp_max, cudaStream_t st) {
+  if (B <= 0) return cudaSuccess;
+  if (kp_max > 256) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)kMergeWarps * kp_max * sizeof(unsigned long long);
+  cudaError_t e = cudaFuncSetAttribute(merge_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  merge_compact_kernel<<<B, 32 * kMergeWarps, smem, st>>>(part, cnt, meta, merged, ld_merged);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, unsigned long long* merged,
