@@ -496,6 +496,11 @@ __device__ __forceinline__ void tc_seed_pass(const ScanLaunch& a, const WorkItem
     // 32 rows (lane j ends with query half*32 + j), then the 4 row quadrants
     // combine with shared atomicMin on the order bits
     static_assert(QPT == 32, "cross-item seed: 32 query columns per thread");
+    // keep this thread's per-query minima (its rows of every chunk) for the
+    // selection pass: it re-reads only the columns whose minimum passes the seed
+    float* mnb = reinterpret_cast<float*>(sel);  // [QPT][256] (first 32 KB of the append buffer)
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) mnb[j * 256 + e] = mn[j];
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
       const bool up = (lane & off) != 0;
@@ -657,44 +662,43 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
     // 128-key buffer (adversarial ties) sends the item down the per-chunk path
     // below, which re-reads the same accumulators.
     if (a.seed == 2 && !(a.dbg & 1)) {
-      unsigned long long* sb = sel;
+      // sparse selection: a (thread, query) pair is revisited only when the
+      // thread's minimum over its rows (kept by the seed pass) passes the
+      // query's bound; its column is then read from every chunk (x1 TMEM
+      // loads, one wait) and each row tested exactly
+      constexpr int kApp = 64;  // append slots per query (second 32 KB of the buffer)
+      const float* mnb = reinterpret_cast<const float*>(sel);
+      unsigned long long* sb = sel + 4096;
       const unsigned long long* thr_nv = sh.thr;  // fixed during this pass: loads may be hoisted
-      int ac = acc, ap = aphase;
 #pragma unroll 1
-      for (int c = 0; c < nchunk; ++c) {
-        const int rows = min(kTcRows, w.row_count - c * kTcRows);
-        const bool valid = row_in_chunk < rows;
-        const float xn = sh.xns[c * kTcRows + row_in_chunk];  // written by the seed pass (barriers since)
-        tmb_wait(&sh.tfull[ac], ap);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        uint32_t v[QPT];
-        tmem_ld_cols<QPT>(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ac * N + half * QPT), v);
+      for (int j = 0; j < QPT; ++j) {
+        const int g = half * QPT + j;
+        const unsigned long long tk = thr_nv[g];
+        const bool hit = g < gc && !(mnb[j * 256 + e] > ord2f((uint32_t)(tk >> 32)));
+        if (!__any_sync(0xffffffffu, hit)) continue;
+        uint32_t col[kTcWideMaxChunks];
+        const uint32_t cbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * QPT + j);
+#pragma unroll
+        for (int c = 0; c < kTcWideMaxChunks; ++c) {
+          col[c] = 0u;
+          if (c < nchunk)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n"
+                         : "=r"(col[c])
+                         : "r"(cbase + (uint32_t)(((acc + c) & (kTcWideMaxChunks - 1)) * N)));
+        }
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (++ac == tc_acc<N>()) {
-          ac = 0;
-          ap ^= 1;
-        }
-        if (!valid) continue;
-        const uint32_t pos = (uint32_t)(w.row_begin + (long long)c * kTcRows + row_in_chunk);
-        uint32_t m = 0;
+        if (!hit) continue;
+        const float qng = sh.qn[g];
+        const float qig = sh.qinv[g];
 #pragma unroll
-        for (int j = 0; j < QPT; ++j) {
-          const int g = half * QPT + j;
-          const float dot = H ? __uint_as_float(v[j]) * sh.qinv[g] : __uint_as_float(v[j]);
-          const float d = __fmaf_rn(-2.f, dot, __fadd_rn(sh.qn[g], xn));
-          v[j] = __float_as_uint(d);
-          m |= (uint32_t)(!(d > ord2f((uint32_t)(thr_nv[g] >> 32))) && g < gc) << j;
-        }
-        if (m) {
-#pragma unroll
-          for (int j = 0; j < QPT; ++j) {
-            if (m & (1u << j)) {
-              const int g = half * QPT + j;
-              const unsigned long long key = make_key(__uint_as_float(v[j]), pos);
-              if (key < thr_nv[g]) {
-                const int slot = atomicAdd(&sh.cnt[0][g], 1);
-                if (slot < kTcRows) sb[g * kTcRows + slot] = key;
-              }
+        for (int c = 0; c < kTcWideMaxChunks; ++c) {
+          if (c < nchunk && c * kTcRows + row_in_chunk < w.row_count) {
+            const float dot = H ? __uint_as_float(col[c]) * qig : __uint_as_float(col[c]);
+            const float d = __fmaf_rn(-2.f, dot, __fadd_rn(qng, sh.xns[c * kTcRows + row_in_chunk]));
+            const unsigned long long key = make_key(d, (uint32_t)(w.row_begin + (long long)c * kTcRows + row_in_chunk));
+            if (key < tk) {
+              const int slot = atomicAdd(&sh.cnt[0][g], 1);
+              if (slot < kApp) sb[g * kApp + slot] = key;
             }
           }
         }
@@ -707,18 +711,12 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
 #pragma unroll
       for (int qi = 0; qi < OWN; ++qi) {
         const int g = ew + kEpiWarps * qi;
-        over |= g < gc && sh.cnt[0][g] > kTcRows;
+        over |= g < gc && sh.cnt[0][g] > kApp;
       }
       over = __syncthreads_or_epi(over);
       if (!over) {
-        // release every accumulator of the item to the MMA warp
-        for (int c = 0; c < nchunk; ++c) {
-          if (lane == 0) tmb_arrive(&sh.tempty[acc]);
-          if (++acc == tc_acc<N>()) {
-            acc = 0;
-            aphase ^= 1;
-          }
-        }
+        // one item per CTA under the cross-item seed: no later chunk needs the
+        // accumulators, so they are not handed back to the MMA warp
         // each query's survivors (or, beyond kp of them, their top kp) go
         // unsorted to the front of its partial region: launch_merge_compact
         if (threadIdx.x == 64) ts_mark(a, 14);
@@ -748,9 +746,9 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
               atomicAdd(&g_scan_cnt[1], 1ull);
             }
             if (n <= kp) {
-              for (int b = lane; b < n; b += 32) out[b] = sb[g * kTcRows + b];
+              for (int b = lane; b < n; b += 32) out[b] = sb[g * kApp + b];
             } else {
-              for (int b = 0; b < n; b += 32) list_fold32<KL>(L[qi], b + lane < n ? sb[g * kTcRows + b + lane] : TRI_KEY_MAX, lane);
+              for (int b = 0; b < n; b += 32) list_fold32<KL>(L[qi], b + lane < n ? sb[g * kApp + b + lane] : TRI_KEY_MAX, lane);
 #pragma unroll
               for (int j = 0; j < KL; ++j)
                 if (j * 32 < kp) out[j * 32 + lane] = L[qi][j];
