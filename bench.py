@@ -1,19 +1,24 @@
 """Benchmark of the Trinity vector-search pool hot path on B200.
 
-Headline (N=1): BASELINE.json config C2 -- IVF-Flat over 1M x 768 fp32 synthetic
+N=1 (default): BASELINE.json config C2 -- IVF-Flat over 1M x 768 fp32 synthetic
 vectors, nlist=1024 (5 Lloyd iterations), nprobe=32, batch 256, k=10.  A step is
 one batch of 256 queries through the whole device pipeline (exact coarse step,
 device packer, list scan, merge, exact fp64 re-rank, certified fix-up).
 
-N>1 (torchrun, one process per GPU): strong scaling of the same 1M database,
-vector-sharded by id range with the k-means artifact replicated; each rank
-searches its shard and the per-shard top-k lists are all-gathered over NCCL
-and merged on the device by (dist, id).
+N>1 (torchrun, one process per GPU): BASELINE.json config C4 -- IVF-Flat over
+10M x 768, vector-sharded by id range.  Each rank draws only its own rows,
+rank 0 trains the k-means centroids on rows [0, 1M) and broadcasts them, every
+rank lists its rows under the shared centroids (exact nearest centroid), and a
+step is one 256-query batch: local search -> ONE all-gather of the packed
+(id, dist) lists -> device merge by (dist, id) (paper_2512_02281_b200/sharded.py).
+``--config`` overrides the choice (C2 at N>1 = strong scaling of the 1M DB;
+C4 at N=1 = the whole 10M DB on one GPU).
 
 --impl reference: the CPU oracle (numpy restatement of the reference's
 algorithm, oracle/trinity_oracle.py) on the host cores, same config and metric.
 
-Prints ONE JSON line on rank 0.
+Prints ONE JSON line on rank 0; ``--full-out PATH`` also writes the complete
+records of every secondary config (the line keeps their headline numbers).
 """
 
 from __future__ import annotations
@@ -31,17 +36,26 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_DB, DIM, NLIST, ITERS, NPROBE, BATCH, K = 1_000_000, 768, 1024, 5, 32, 256, 10
-DB_SEED, Q_SEED, KM_SEED = 3, 4, 4
-METRIC = "search QPS (IVF-Flat 1M x 768, nlist 1024, nprobe 32, k 10)"
+DIM, NLIST, ITERS, NPROBE, BATCH, K = 768, 1024, 5, 32, 256, 10
+Q_SEED, KM_SEED = 4, 4
 UNIT = "queries/s"
-CONFIG = {
-    "workload": "C2: IVF-Flat 1M x 768 fp32, nlist=1024 (5 Lloyd iters), nprobe=32, batch=256, k=10",
-    "n_db": N_DB, "dim": DIM, "nlist": NLIST, "nprobe": NPROBE, "global_batch": BATCH, "k": K,
-    "db": "gen_vectors_chunked(1_000_000, 768, seed=3): 131072-row Philox chunks seeded [3, i]",
-    "queries": "gen_vectors(256, 768, seed=4) as float64",
-    "l2": "no flush: each batch scans ~3.1 GB of inverted lists (> 126 MB L2); 3 MB of centroids stay L2-resident",
-    "parallelism": "dp1",
+# C4's database size can be lowered for tests of the sharded path (BENCH_C4_N)
+C4_N = int(os.environ.get("BENCH_C4_N", 10_000_000))
+IVF_CONFIGS = {
+    "C2": {
+        "n": 1_000_000, "seed": 3, "n_train": 1_000_000,
+        "metric": "search QPS (IVF-Flat 1M x 768, nlist 1024, nprobe 32, k 10)",
+        "workload": "C2: IVF-Flat 1M x 768 fp32, nlist=1024 (5 Lloyd iters), nprobe=32, batch=256, k=10",
+        "db": "gen_vectors_chunked(1_000_000, 768, seed=3): 131072-row Philox chunks seeded [3, i]",
+    },
+    "C4": {
+        "n": C4_N, "seed": 100, "n_train": min(1_000_000, C4_N),
+        "metric": f"search QPS (IVF-Flat {C4_N / 1e6:g}M x 768 vector-sharded, nlist 1024, nprobe 32, k 10)",
+        "workload": f"C4: IVF-Flat {C4_N / 1e6:g}M x 768 fp32 vector-sharded by id range, nlist=1024 (5 Lloyd iters on "
+                    f"rows [0, {min(1_000_000, C4_N) / 1e6:g}M), every row listed under its exact nearest centroid), "
+                    "nprobe=32, batch=256, k=10, per-shard top-k merged on the device after one all-gather",
+        "db": f"gen_vectors_chunked({C4_N}, 768, seed=100); each rank draws only its own rows",
+    },
 }
 
 
@@ -51,12 +65,18 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, choices=["C2", "C4"],
+                    help="headline workload (default: C2 on one GPU, C4 when sharded over N > 1)")
     ap.add_argument("--cpu-sample", type=int, default=24, help="queries timed for cpu_baseline")
+    ap.add_argument("--parity", default="spot", choices=["spot", "full"],
+                    help="untimed oracle check: 3 queries per lane, or every query of lane 0 and the spot set")
     ap.add_argument("--tc-stages", type=int, default=0, help="tensor-core scan ring depth cap (0 = deepest)")
     ap.add_argument("--scan-reserve", type=int, default=-1,
                     help="SMs the list scan leaves to other lanes (-1: the library's choice, 8 with > 1 lane)")
     ap.add_argument("--opt", action="append", default=[], help="library option name=value (experiments)")
-    ap.add_argument("--no-configs", action="store_true", help="skip the secondary-config measurements (C1/C3/C5/engine)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the secondary configs (C1/C3/C4/C5/engine)")
+    ap.add_argument("--configs", default="C1,C3,C4,C5,engine", help="secondary configs measured at N=1")
+    ap.add_argument("--full-out", default=None, help="write every config's complete record to this JSON file")
     ap.add_argument("--lanes", type=int, default=4,
                     help="independent batches in flight (one CUDA stream + library workspace each)")
     return ap.parse_args()
@@ -140,25 +160,19 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def make_inputs():
-    from paper_2512_02281_b200.workload import gen_matrix, gen_vectors_chunked
+def queries_f64():
+    from paper_2512_02281_b200.workload import gen_matrix
 
-    data = gen_vectors_chunked(N_DB, DIM, DB_SEED)
-    queries = gen_matrix(BATCH, DIM, Q_SEED).astype(np.float64)
-    return data, queries
+    return gen_matrix(BATCH, DIM, Q_SEED).astype(np.float64)
 
 
-def cpu_baseline_qps(data, art, queries, n_sample):
-    from oracle import trinity_oracle as orc
-
-    t0 = time.perf_counter()
-    for i in range(n_sample):
-        orc.ivf_search(data, art, queries[i], K, NPROBE)
-    dt = time.perf_counter() - t0
-    return n_sample / dt, dt
+def pct(a):
+    a = np.asarray(a, dtype=np.float64)
+    return {"p50": float(np.percentile(a, 50)), "p95": float(np.percentile(a, 95)), "p99": float(np.percentile(a, 99))}
 
 
 # ----------------------------------------------------------------------------
+# reference arm
 
 
 def run_reference(args):
@@ -169,21 +183,29 @@ def run_reference(args):
     from concurrent.futures import ProcessPoolExecutor
 
     from oracle import trinity_oracle as orc
+    from paper_2512_02281_b200.workload import gen_rows_chunked
 
-    data, queries = make_inputs()
+    name = args.config or ("C2" if world == 1 else "C4")
+    cfg = IVF_CONFIGS[name]
+    data = gen_rows_chunked(0, cfg["n"], DIM, cfg["seed"])
+    queries = queries_f64()
     # the same deterministic k-means the GPU arm runs (oracle.kmeans restates
-    # tri_ivf_train bit-for-bit): both arms search one index artifact, whose
-    # digest goes into config
-    art = orc.kmeans(data, NLIST, ITERS, KM_SEED)
+    # tri_ivf_train bit-for-bit) on the same training rows, then every row's
+    # exact nearest centroid: both arms search one index artifact (digest in config)
+    art = orc.kmeans(data[:cfg["n_train"]], NLIST, ITERS, KM_SEED)
+    if cfg["n_train"] < cfg["n"]:
+        art = orc.IVFArtifact(art.centroids, orc.nearest_centroid(data, art.centroids))
     cores = os.cpu_count() or 1
-    # Steps are a bounded sample of the C2 batch: about 200 x cores queries in
-    # total (a minute on 16 cores) whatever K is, and the whole run goes to the
-    # process pool at once so every core stays busy across step boundaries.
-    per_step = max(1, -(-max(cores, 16) * 200 // max(args.steps, 1)))
+    # Steps are a bounded sample of the batch: about 200 x cores queries in all
+    # for C2 (a minute on 16 cores), 10x fewer for the 10x larger C4 lists,
+    # whatever K is; the whole run goes to the process pool at once so every
+    # core stays busy across step boundaries.
+    budget = max(cores, 16) * (200 if name == "C2" else 20)
+    per_step = max(1, -(-budget // max(args.steps, 1)))
     global _REF_STATE
     _REF_STATE = (data, art, queries)
     with ProcessPoolExecutor(max_workers=cores) as ex:  # fork: workers share the arrays copy-on-write
-        warm = [j % BATCH for j in range(args.warmup * per_step)]
+        warm = [j % BATCH for j in range(min(args.warmup * per_step, 2 * cores))]
         list(ex.map(_ref_query, warm, chunksize=1))
         timed = [(s * per_step + j) % BATCH for s in range(args.steps) for j in range(per_step)]
         t0 = time.perf_counter()
@@ -191,12 +213,14 @@ def run_reference(args):
         dt = time.perf_counter() - t0
     qps = per_step * args.steps / dt
     line = {
-        "impl": "reference", "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": cfg["metric"], "value": qps, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": dict(CONFIG, artifact=orc.artifact_digest(art)),
+        "data": "synthetic", "config": {"workload": cfg["workload"], "n_db": cfg["n"], "dim": DIM, "nlist": NLIST,
+                                        "nprobe": NPROBE, "global_batch": BATCH, "k": K, "db": cfg["db"],
+                                        "parallelism": f"cpu x{cores}", "artifact": orc.artifact_digest(art)},
         "cpu_baseline": {"value": qps, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{per_step} queries per step of the C2 batch ({per_step * args.steps} in "
+                         "sample": f"{per_step} queries per step of the {name} batch ({per_step * args.steps} in "
                                    f"all), numpy oracle, one process per core ({cores} cores)"},
         "e2e": {"value": qps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -214,6 +238,277 @@ def _ref_query(i):
 
 
 # ----------------------------------------------------------------------------
+# our arm: IVF workloads (C2 / C4), one GPU or vector-sharded over N
+
+
+class Ctx:
+    """Process-wide run context (rank, device, process groups)."""
+
+    def __init__(self, rank, world, local, dist):
+        self.rank, self.world, self.local, self.dist = rank, world, local, dist
+        self.gloo = dist is not None and dist.get_backend() == "gloo"
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        if not self.dist:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.gloo else "cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def build_ivf(cfg, ctx: Ctx):
+    """This rank's rows, the shared centroids and its device index (see module doc)."""
+    import torch
+
+    from paper_2512_02281_b200.ann_graph import _DeviceStore
+    from paper_2512_02281_b200.ivf import IVFFlatIndex
+    from paper_2512_02281_b200.sharded import shard_bounds
+    from paper_2512_02281_b200.workload import gen_rows_chunked
+
+    n, ntr = cfg["n"], cfg["n_train"]
+    lo, hi = shard_bounds(n, ctx.world, ctx.rank)
+    t0 = time.perf_counter()
+    data = gen_rows_chunked(lo, hi, DIM, cfg["seed"], procs=max(1, (os.cpu_count() or 1) // ctx.world))
+    gen_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    if ctx.world == 1 and ntr == n:
+        store = _DeviceStore(data, device=ctx.local)
+        idx = IVFFlatIndex.train(store, NLIST, ITERS, KM_SEED)
+    else:
+        cen = np.empty((NLIST, DIM), dtype=np.float32)
+        if ctx.rank == 0:
+            tr = data[:ntr] if hi - lo >= ntr else gen_rows_chunked(0, ntr, DIM, cfg["seed"])
+            ts = _DeviceStore(tr, device=ctx.local)
+            ti = IVFFlatIndex.train(ts, NLIST, ITERS, KM_SEED)
+            cen, _ = ti.export()
+            ti.close()
+            ts.close()
+            del tr
+        if ctx.dist:
+            t = torch.from_numpy(cen)
+            if not ctx.gloo:
+                t = t.cuda()
+            ctx.dist.broadcast(t, 0)
+            cen = t.cpu().numpy()
+        store = _DeviceStore(data, device=ctx.local)
+        idx = IVFFlatIndex.from_centroids(store, cen, id_offset=lo)
+    torch.cuda.synchronize()
+    cen, asg = idx.export()
+    return {"data": data, "store": store, "idx": idx, "lo": lo, "hi": hi, "cen": cen, "asg": asg,
+            "gen_s": gen_s, "build_s": time.perf_counter() - t0}
+
+
+def oracle_check(b, queries, rows, got_ids, got_d, ctx: Ctx):
+    """Untimed parity: for every checked query, the exact IVF top-k over this
+    rank's rows (numpy oracle, process pool), merged over ranks by (dist, id)
+    = the global oracle; compared bit-for-bit with the device result on rank 0.
+    Returns the number of mismatching queries (rank 0; 0 elsewhere)."""
+    from oracle import trinity_oracle as orc
+    from oracle.pool import ivf_oracle_batch
+
+    art = orc.IVFArtifact(b["cen"], b["asg"])
+    procs = max(1, min(len(rows), (os.cpu_count() or 1) // ctx.world))
+    local = ivf_oracle_batch(b["data"], art, queries[rows], K, NPROBE, procs=procs)
+    local = [(i + b["lo"], d) for i, d in local]
+    parts = [local]
+    if ctx.dist:
+        parts = [None] * ctx.world
+        ctx.dist.all_gather_object(parts, local)
+    if ctx.rank != 0:
+        return 0
+    bad = 0
+    for j, i in enumerate(rows):
+        oi, od = orc.merge_shards([p[j] for p in parts], K)
+        if not (np.array_equal(got_ids[i, :oi.size], oi) and np.array_equal(got_d[i, :od.size], od)):
+            bad += 1
+    return bad
+
+
+def run_ivf(cfg, args, ctx: Ctx, headline: bool = True, keep: bool = False):
+    """Device-resident throughput, per-launch scan roofline, e2e through the
+    host API and an oracle check for one IVF workload; returns a record (and,
+    with ``keep``, the built index for the configs that reuse it)."""
+    import torch
+
+    from paper_2512_02281_b200 import _lib
+    from paper_2512_02281_b200.sharded import ShardedIVF
+
+    b = build_ivf(cfg, ctx)
+    idx = b["idx"]
+    queries = queries_f64()
+    L = max(1, args.lanes)
+    q_dev = torch.from_numpy(queries).cuda()
+    lane_ids = [torch.empty((BATCH, K), dtype=torch.int64, device="cuda") for _ in range(L)]
+    lane_d = [torch.empty((BATCH, K), dtype=torch.float64, device="cuda") for _ in range(L)]
+    # explicit non-default streams: the library launches on the caller's
+    # stream and keeps one workspace per stream, so batches on different lanes
+    # overlap on the device (one batch's scan with the next one's coarse step)
+    lanes = [torch.cuda.Stream() for _ in range(L)]
+    stream = lanes[0]
+    shard = None
+    if ctx.world > 1:  # one process group per lane: each lane's gathers are ordered on its own communicator
+        groups = [ctx.dist.new_group(list(range(ctx.world))) for _ in range(L)]
+        shard = [ShardedIVF(idx, K, group=g) for g in groups]
+    torch.cuda.set_stream(stream)
+    torch.cuda.synchronize()
+    step_no = [0]
+
+    def step():
+        j = step_no[0] % L
+        step_no[0] += 1
+        if shard:
+            shard[j].search_device(q_dev, NPROBE, lane_ids[j], lane_d[j], lanes[j])
+        else:
+            idx.search_device(q_dev, K, NPROBE, lane_ids[j], lane_d[j], lanes[j])
+
+    # prime every lane (its workspace, plan and CUDA graph: a shape is captured
+    # on its second sighting and replayed from the third), so a small --warmup
+    # cannot leave first-use work inside the timed region
+    for _ in range(3 * L):
+        step()
+    torch.cuda.synchronize()
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # correctness against the CPU oracle (untimed): 3 queries of every lane, or
+    # with --parity full every query of lane 0 as well
+    bad, checked = 0, 0
+    for j in range(L):
+        rows = list(range(BATCH)) if (args.parity == "full" and j == 0) else [0, 97, 255]
+        if not headline and j > 0:
+            break
+        bad += oracle_check(b, queries, rows, lane_ids[j].cpu().numpy(), lane_d[j].cpu().numpy(), ctx)
+        checked += len(rows)
+    if ctx.rank == 0 and bad:
+        raise SystemExit(f"parity failure: {bad} of {checked} checked queries differ from the oracle")
+
+    # timed region: device-resident inputs
+    idx.set_profiling(True)
+    sampler = ClockSampler(ctx.local)
+    ctx.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        ev0.record(stream)
+        for ls in lanes[1:]:
+            ls.wait_event(ev0)
+        for _ in range(args.steps):
+            step()
+        for ls in lanes[1:]:
+            stream.wait_stream(ls)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ctx.barrier()
+    scan_ms, scan_n = idx.scan_time()
+    idx.set_profiling(False)
+    total_ms = ctx.max_over_ranks(ev0.elapsed_time(ev1))
+    qps = BATCH * args.steps / (total_ms / 1e3)
+    scan_bytes, pairs = idx.last_scan_bytes()
+    scan_kind = idx.last_scan_kind()
+    peak, peak_kind = load_peaks()
+    avg_scan_ms = scan_ms / max(scan_n, 1)
+    achieved = scan_bytes / (avg_scan_ms / 1e3) / 1e9
+    rec = {"value": qps, "ms_per_step": total_ms / args.steps, "scan_kind": scan_kind,
+           "parity": f"{'ok' if not bad else 'FAIL'}: {checked} queries == global oracle (ids, f64 dists)",
+           "gen_s": round(b["gen_s"], 1), "build_s": round(b["build_s"], 1), "clocks": sampler.summary(),
+           "artifact_rows": [b["lo"], b["hi"]]}
+    rec["roofline"] = {
+        "bound": "hbm", "kernel": f"scan_tc_kernel ({scan_kind} tcgen05 IVF list scan)", "achieved": achieved,
+        "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": load_traffic() if (ctx.world == 1 and cfg is IVF_CONFIGS["C2"]) else None,
+        "algorithmic_bytes_per_launch": scan_bytes, "scan_ms_per_launch": avg_scan_ms,
+        "step_frac": scan_bytes / (total_ms / args.steps / 1e3) / 1e9 / peak,
+        "query_vector_pairs_per_launch": pairs,
+    }
+    if headline and ctx.world == 1:
+        # the same scan with no other lane beside it (one stream, all 148 SMs)
+        n_iso = 50
+        reserve_opt = dict(o.split("=", 1) for o in args.opt).get("scan_reserve")
+        _lib.set_option("scan_reserve", 0)
+        for _ in range(3):
+            idx.search_device(q_dev, K, NPROBE, lane_ids[0], lane_d[0], lanes[0])
+        torch.cuda.synchronize()
+        idx.set_profiling(True)
+        for _ in range(n_iso):
+            idx.search_device(q_dev, K, NPROBE, lane_ids[0], lane_d[0], lanes[0])
+        torch.cuda.synchronize()
+        iso_ms, iso_n = idx.scan_time()
+        idx.set_profiling(False)
+        _lib.set_option("scan_reserve", int(reserve_opt) if reserve_opt is not None else args.scan_reserve)
+        iso = iso_ms / max(iso_n, 1)
+        rec["roofline"]["isolated"] = {"scan_ms_per_launch": iso, "frac": scan_bytes / (iso / 1e3) / 1e9 / peak}
+
+    # e2e: public host API, pinned host buffers, H2D of the queries and D2H of
+    # the results inside the timed region.  One host thread per lane, each a
+    # blocking call on its own stream; threads warm up, then start together.
+    q_pin = torch.from_numpy(queries).pin_memory()
+    pins = [(torch.empty((BATCH, K), dtype=torch.int64).pin_memory(),
+             torch.empty((BATCH, K), dtype=torch.float64).pin_memory()) for _ in range(L)]
+
+    def call(j):
+        if shard:
+            shard[j].search_into(q_pin, NPROBE, *pins[j], stream=lanes[j])
+        else:
+            idx.search_into(q_pin, K, NPROBE, *pins[j], stream=lanes[j])
+
+    call_ms = [[] for _ in range(L)]
+    gate = threading.Barrier(L + 1)
+    t_end = [0.0] * L
+
+    def lane_loop(j, n):
+        for _ in range(3):
+            call(j)
+        gate.wait()
+        for _ in range(n):
+            t = time.perf_counter()
+            call(j)
+            call_ms[j].append((time.perf_counter() - t) * 1e3)
+        t_end[j] = time.perf_counter()
+
+    ctx.barrier()
+    ths = [threading.Thread(target=lane_loop, args=(j, len(range(j, args.steps, L)))) for j in range(L)]
+    for th in ths:
+        th.start()
+    gate.wait()
+    t0 = time.perf_counter()
+    for th in ths:
+        th.join()
+    torch.cuda.synchronize()
+    e2e_s = ctx.max_over_ranks(max(t_end) - t0)
+    lat = np.concatenate([np.asarray(c) for c in call_ms if c])
+    rec["e2e"] = {"value": BATCH * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": BATCH * DIM * 8,
+                  "d2h_bytes_per_step": BATCH * K * 16,
+                  "batch_latency_ms": {k: round(v, 4) for k, v in pct(lat).items()}}
+    if ctx.rank == 0 and (headline or ctx.world == 1):
+        from oracle import trinity_oracle as orc
+
+        n_cpu = args.cpu_sample if cfg["n"] <= 2_000_000 else max(2, args.cpu_sample // 8)
+        t0 = time.perf_counter()
+        art = orc.IVFArtifact(b["cen"], b["asg"]) if ctx.world == 1 else None
+        if art is not None:
+            for i in range(n_cpu):
+                orc.ivf_search(b["data"], art, queries[i], K, NPROBE)
+            dt = time.perf_counter() - t0
+            rec["cpu_baseline"] = {"value": n_cpu / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                                   "sample": f"first {n_cpu} of the 256 queries, numpy oracle ({dt:.1f} s, 1 core)"}
+            rec["artifact"] = orc.artifact_digest(art)
+    if shard:
+        for s in shard:
+            s._bufs.clear()
+    if keep:
+        return rec, b
+    idx.close()
+    b["store"].close()
+    del b
+    torch.cuda.synchronize()
+    return rec
 
 
 def run_ours(args):
@@ -233,11 +528,9 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+    ctx = Ctx(rank, world, local, dist)
 
-    from oracle import trinity_oracle as orc
     from paper_2512_02281_b200 import _build
-    from paper_2512_02281_b200.ann_graph import _DeviceStore
-    from paper_2512_02281_b200.ivf import IVFFlatIndex, init_rows, merge_topk_device
 
     _build.build()
     from paper_2512_02281_b200 import _lib
@@ -247,241 +540,71 @@ def run_ours(args):
     for kv in args.opt:
         name, val = kv.split("=")
         _lib.set_option(name, int(val))
-    data, queries = make_inputs()
 
-    # index: rank 0 trains on the full database, the artifact is broadcast
-    if world == 1:
-        store = _DeviceStore(data, device=local)
-        idx = IVFFlatIndex.train(store, NLIST, ITERS, KM_SEED)
-        cen, asg = idx.export()
-        shard_lo, shard_hi = 0, N_DB
-    else:
-        cen_t = torch.empty((NLIST, DIM), dtype=torch.float32, device="cuda")
-        asg_t = torch.empty((N_DB,), dtype=torch.int32, device="cuda")
-        if rank == 0:
-            full = _DeviceStore(data, device=local)
-            tmp = IVFFlatIndex.train(full, NLIST, ITERS, KM_SEED)
-            c, a = tmp.export()
-            tmp.close()
-            full.close()
-            cen_t.copy_(torch.from_numpy(c))
-            asg_t.copy_(torch.from_numpy(a))
-        dist.broadcast(cen_t, 0)
-        dist.broadcast(asg_t, 0)
-        cen, asg = cen_t.cpu().numpy(), asg_t.cpu().numpy()
-        shard_lo = rank * N_DB // world
-        shard_hi = (rank + 1) * N_DB // world
-        store = _DeviceStore(data[shard_lo:shard_hi], device=local)
-        idx = IVFFlatIndex.from_artifact(store, cen, asg[shard_lo:shard_hi], id_offset=shard_lo)
+    name = args.config or ("C2" if world == 1 else "C4")
+    cfg = IVF_CONFIGS[name]
+    secondary = world == 1 and not args.no_configs
+    rec, b = run_ivf(cfg, args, ctx, keep=True)
 
-    L = max(1, args.lanes)
-    q_dev = torch.from_numpy(queries).cuda()
-    lane_ids = [torch.empty((BATCH, K), dtype=torch.int64, device="cuda") for _ in range(L)]
-    lane_d = [torch.empty((BATCH, K), dtype=torch.float64, device="cuda") for _ in range(L)]
-    ids_dev, d_dev = lane_ids[0], lane_d[0]
-    if world > 1:  # per-lane gather and merge buffers
-        g_ids = [torch.empty((world, BATCH, K), dtype=torch.int64, device="cuda") for _ in range(L)]
-        g_d = [torch.empty((world, BATCH, K), dtype=torch.float64, device="cuda") for _ in range(L)]
-        m_ids = [torch.empty((BATCH, K), dtype=torch.int64, device="cuda") for _ in range(L)]
-        m_d = [torch.empty((BATCH, K), dtype=torch.float64, device="cuda") for _ in range(L)]
-    # explicit non-default streams: the library launches on the caller's
-    # stream and keeps one workspace per stream, so batches on different lanes
-    # overlap on the device (one batch's scan with the next one's coarse step)
-    lanes = [torch.cuda.Stream() for _ in range(L)]
-    stream = lanes[0]
-    torch.cuda.set_stream(stream)
-    torch.cuda.synchronize()
-    step_no = [0]
+    full = {name: rec}
+    configs = {}
+    if secondary:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_configs as bc
 
-    def step():
-        j = step_no[0] % L
-        step_no[0] += 1
-        idx.search_device(q_dev, K, NPROBE, lane_ids[j], lane_d[j], lanes[j])
-        if world > 1:  # every rank issues the collectives in the same lane order
-            with torch.cuda.stream(lanes[j]):
-                dist.all_gather_into_tensor(g_ids[j].view(-1), lane_ids[j].view(-1))
-                dist.all_gather_into_tensor(g_d[j].view(-1), lane_d[j].view(-1))
-            merge_topk_device(g_d[j], g_ids[j], K, m_d[j], m_ids[j], lanes[j])
-
-    # setup: prime every lane (its workspace, plan and CUDA graph: a shape is
-    # captured on its second sighting and replayed from the third), so a small
-    # --warmup cannot leave first-use work inside the timed region
-    for _ in range(3 * L):
-        step()
-    torch.cuda.synchronize()
-    n_warm = max(3, args.warmup)
-    for _ in range(n_warm):
-        step()
-    torch.cuda.synchronize()
-
-    # correctness spot-check against the CPU oracle (untimed), every lane
-    art = orc.IVFArtifact(cen, asg)
-    for j in range(L):
-        res_ids = (m_ids[j] if world > 1 else lane_ids[j]).cpu().numpy()
-        res_d = (m_d[j] if world > 1 else lane_d[j]).cpu().numpy()
-        if rank == 0:
-            for i in (0, 97, 255):
-                oi, od = orc.ivf_search(data, art, queries[i], K, NPROBE)
-                if not (np.array_equal(res_ids[i], oi) and np.array_equal(res_d[i], od)):
-                    raise SystemExit(f"parity failure on query {i} (lane {j})")
-
-    # timed region: device-resident inputs
-    idx.set_profiling(True)
-    sampler = ClockSampler(local)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with sampler:
-        ev0.record(stream)
-        for ls in lanes[1:]:
-            ls.wait_event(ev0)
-        for _ in range(args.steps):
-            step()
-        for ls in lanes[1:]:
-            stream.wait_stream(ls)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    scan_ms, scan_n = idx.scan_time()
-    idx.set_profiling(False)
-    total_ms = ev0.elapsed_time(ev1)
-    # supplementary: the same scan with no other lane beside it (one stream,
-    # 50 searches), i.e. the kernel's own bandwidth rather than its share of a mix;
-    # every SM goes to the scan (no SMs reserved for other lanes)
-    n_iso = 50
-    reserve_opt = dict(o.split("=", 1) for o in args.opt).get("scan_reserve")
-    _lib.set_option("scan_reserve", 0)
-    for _ in range(3):
-        idx.search_device(q_dev, K, NPROBE, lane_ids[0], lane_d[0], lanes[0])
-    torch.cuda.synchronize()
-    idx.set_profiling(True)
-    for _ in range(n_iso):
-        idx.search_device(q_dev, K, NPROBE, lane_ids[0], lane_d[0], lanes[0])
-    torch.cuda.synchronize()
-    iso_ms, iso_n = idx.scan_time()
-    idx.set_profiling(False)
-    _lib.set_option("scan_reserve", int(reserve_opt) if reserve_opt is not None else args.scan_reserve)
-    if dist:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    qps = BATCH * args.steps / (total_ms / 1e3)
-    scan_bytes, pairs = idx.last_scan_bytes()
-    scan_kind = idx.last_scan_kind()
-
-    # e2e: public host API, pinned host buffers, copies inside the timed region
-    # (one host thread per lane, each a blocking search_into on its own stream)
-    q_pin = torch.from_numpy(queries).pin_memory()
-    pins = [(torch.empty((BATCH, K), dtype=torch.int64).pin_memory(),
-             torch.empty((BATCH, K), dtype=torch.float64).pin_memory()) for _ in range(L)]
-    ids_pin, d_pin = pins[0]
-    for j in range(L):
-        for _ in range(3):
-            idx.search_into(q_pin, K, NPROBE, *pins[j], stream=lanes[j])
-    if dist:
-        dist.barrier()
-
-    call_ms = [[] for _ in range(L)]
-
-    def lane_loop(j, n):
-        for _ in range(n):
-            t = time.perf_counter()
-            idx.search_into(q_pin, K, NPROBE, *pins[j], stream=lanes[j])
-            call_ms[j].append((time.perf_counter() - t) * 1e3)
-
-    t0 = time.perf_counter()
-    threaded = L > 1 and world == 1  # N>1: collectives must be issued in one order on every rank
-    if threaded:
-        ths = [threading.Thread(target=lane_loop, args=(j, len(range(j, args.steps, L)))) for j in range(L)]
-        for th in ths:
-            th.start()
-        for th in ths:
-            th.join()
-    for _ in range(0 if threaded else args.steps):
-        t = time.perf_counter()
-        idx.search_into(q_pin, K, NPROBE, ids_pin, d_pin, stream=stream)
-        if world > 1:
-            ids_dev.copy_(ids_pin, non_blocking=False)
-            d_dev.copy_(d_pin, non_blocking=False)
-            dist.all_gather_into_tensor(g_ids[0].view(-1), ids_dev.view(-1))
-            dist.all_gather_into_tensor(g_d[0].view(-1), d_dev.view(-1))
-            merge_topk_device(g_d[0], g_ids[0], K, m_d[0], m_ids[0], stream)
-            ids_pin.copy_(m_ids[0])
-            d_pin.copy_(m_d[0])
-        call_ms[0].append((time.perf_counter() - t) * 1e3)
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_qps = BATCH * args.steps / e2e_s
-
+        wanted = [c for c in args.configs.split(",") if c and c != name]
+        # C3 and C5 run over the headline's C2 index; it is closed before C4
+        order = [c for c in ("C3", "C5") if c in wanted and name == "C2"] + \
+                [c for c in wanted if c not in ("C3", "C5")]
+        for cname in order:
+            if b is not None and cname not in ("C3", "C5"):
+                b["idx"].close()
+                b["store"].close()
+                b = None
+            try:
+                if cname in ("C3", "C5"):
+                    r = getattr(bc, cname.lower())(b, load_peaks()[0])
+                elif cname == "C4":
+                    r = run_ivf(IVF_CONFIGS["C4"], argparse.Namespace(**{**vars(args), "steps": 40, "warmup": 3,
+                                                                         "parity": "spot"}), ctx, headline=False)
+                    r["workload"] = IVF_CONFIGS["C4"]["workload"] + " (all shards on this one GPU: the G=1 point)"
+                else:
+                    r = getattr(bc, cname.lower())(load_peaks()[0])
+            except Exception as exc:  # reported, never silently dropped
+                r = {"error": f"{type(exc).__name__}: {exc}"}
+            full[cname] = r
+            configs[cname] = bc.compact(r)
+    if b is not None:
+        b["idx"].close()
+        b["store"].close()
+        b = None
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
-
-    cpu_qps, cpu_dt = cpu_baseline_qps(data, art, queries, args.cpu_sample)
-    lat = np.concatenate([np.asarray(c) for c in call_ms if c]) if any(call_ms) else np.zeros(1)
-    configs = {}
-    if world == 1 and not args.no_configs:
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        import bench_configs as bc
-
-        for name, fn in (("C1", lambda: bc.c1(peak_gbs=load_peaks()[0])), ("C3", lambda: bc.c3(idx, data, art)),
-                         ("C5", lambda: bc.c5(idx)), ("engine", bc.engine)):
-            try:
-                configs[name] = fn()
-            except Exception as exc:  # reported, never silently dropped
-                configs[name] = {"error": f"{type(exc).__name__}: {exc}"}
-    peak, peak_kind = load_peaks()
-    avg_scan_ms = scan_ms / max(scan_n, 1)
-    achieved = scan_bytes / (avg_scan_ms / 1e3) / 1e9
+    if args.full_out:
+        with open(args.full_out, "w") as f:
+            json.dump(full, f, indent=1)
     # prep, coarse tensor-core GEMM, select, re-rank, fix-up (coarse); 3 packer
-    # kernels; list scan; merge; re-rank; fix-up (fine); + the shard merge
-    # when N > 1 (NCCL's own kernels not counted)
+    # kernels; list scan; merge; re-rank; fix-up (fine); + the shard merge when
+    # sharded (NCCL's own kernels not counted)
     kernels_per_step = 12 + (1 if world > 1 else 0)
     line = {
-        "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": f"{scan_kind} candidate scan (certified bound) + f64 exact re-rank", "data": "synthetic",
-        "config": dict(CONFIG, parallelism=f"vector-shard x{world}" if world > 1 else "dp1",
-                       artifact=orc.artifact_digest(art)),
-        "lanes": L,
-        "roofline": {
-            "bound": "hbm", "kernel": f"tri::scan_tc_kernel ({scan_kind} tcgen05 IVF list scan)", "achieved": achieved, "peak": peak,
-            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic() if world == 1 else None,
-            "algorithmic_bytes_per_launch": scan_bytes, "scan_ms_per_launch": avg_scan_ms,
-            "scan_share_of_step": avg_scan_ms / (total_ms / args.steps),
-            "isolated": {"scan_ms_per_launch": iso_ms / max(iso_n, 1),
-                         "achieved": scan_bytes / (iso_ms / max(iso_n, 1) / 1e3) / 1e9,
-                         "frac": scan_bytes / (iso_ms / max(iso_n, 1) / 1e3) / 1e9 / peak,
-                         "what": f"{n_iso} searches on one stream after the timed region (no other lane "
-                                 f"running beside the scan)"},
-            "query_vector_pairs_per_launch": pairs,
-            "step_achieved": scan_bytes / (total_ms / args.steps / 1e3) / 1e9,
-            "step_frac": scan_bytes / (total_ms / args.steps / 1e3) / 1e9 / peak,
-            "step_what": "the scan's algorithmic bytes per step / the step time (all lanes overlapped): the HBM rate "
-                         "the whole pipeline sustains, where per-launch durations overlap",
-            "scan_sms": "148 minus the IVF scan's reserved SMs: 8 when more than one lane runs (library default "
-                        "scan_reserve=-1; +2% QPS, in-mix frac about 0.66 vs 0.76 with all 148 SMs, "
-                        "--opt scan_reserve=0); the isolated pass uses all 148",
-        },
-        "cpu_baseline": {"value": cpu_qps, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"first {args.cpu_sample} of the 256 C2 queries through the numpy oracle "
-                                   f"({cpu_dt:.1f} s, 1 core)"},
-        "e2e": {"value": e2e_qps, "unit": UNIT, "h2d_bytes_per_step": BATCH * DIM * 8,
-                "d2h_bytes_per_step": BATCH * K * 16,
-                "batch_latency_ms": {"p50": float(np.percentile(lat, 50)), "p95": float(np.percentile(lat, 95)),
-                                     "p99": float(np.percentile(lat, 99)),
-                                     "what": f"wall time of one blocking search_into call (256 queries), "
-                                             + (f"{L} host threads / lanes in flight" if threaded else
-                                                "sequential calls (gather + merge included when N>1)")}},
+        "metric": cfg["metric"], "value": rec["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": f"{rec['scan_kind']} candidate scan (certified bound) + f64 exact re-rank",
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"], "n_db": cfg["n"], "dim": DIM, "nlist": NLIST, "nprobe": NPROBE,
+                   "global_batch": BATCH, "k": K, "db": cfg["db"], "queries": "gen_vectors(256, 768, seed=4) as f64",
+                   "l2": "no flush: every batch streams > 1.5 GB of lists (> 126 MB L2)",
+                   "parallelism": f"vector-shard x{world}" if world > 1 else "dp1", "lanes": args.lanes,
+                   "artifact": rec.get("artifact")},
+        "parity": rec["parity"],
+        "roofline": rec["roofline"],
+        "cpu_baseline": rec.get("cpu_baseline"),
+        "e2e": rec["e2e"],
         "gpu_launches": kernels_per_step * args.steps,
-        "clocks": sampler.summary(),
+        "clocks": rec["clocks"],
         "host_cores": os.cpu_count(),
         "configs": configs,
     }

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 120 python tools/c1_scan_probe.py scan_debug=8 20 > gpurun_out/c1_ts.log 2>&1
-timeout 300 python tools/c1_experiment.py "" "bf_wide=0" > gpurun_out/c1.log 2>&1
-TRI_GRAPHS=0 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 400 -c 7 --csv python tools/c1_experiment.py > gpurun_out/c1_launches.csv 2>&1
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest.log 2>&1
+for i in 1 2; do
+BENCH_DEVICE=0 BENCH_BACKEND=gloo BENCH_C4_N=300000 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 2951$i bench.py --gpus 2 --steps 4 --warmup 3 --lanes 2 --parity full > gpurun_out/sh$i.out 2> gpurun_out/sh$i.err; echo "rc=$?" >> gpurun_out/sh$i.err
+done

@@ -215,6 +215,16 @@ int tri_debug_scan_ts(uint64_t* out, int32_t n);
  * id -1 = empty) into the global top-k_out by (dist, id). */
 int tri_merge_topk(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t k_out,
                    double* out_dists, int64_t* out_ids, void* stream);
+/* Strided form for packed shard results: element (g, b, j) of the input lists
+ * is at [g * g_stride + b * ld_in + j], output row b at [b * ld_out].  A rank
+ * that writes its top-k ids and then its dists into ONE [2, B, k] block (ids
+ * at p, dists at p + B*k, ldo = k) gathers a single tensor per batch and the
+ * merge reads the gathered [G, 2, B, k] in place: ids = p, dists = p + B*k,
+ * ld_in = k, g_stride = 2*B*k.  The per-shard merge SURVEY.md 8(e) adds (the
+ * reference has none); tie rule of ann_graph.py:136. */
+int tri_merge_topk_ld(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t ld_in,
+                      int64_t g_stride, int32_t k_out, double* out_dists, int64_t* out_ids, int32_t ld_out,
+                      void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,5 +1,6 @@
 """Full-batch oracle parity at BASELINE sizes: the numpy oracle (oracle/) for
-every query of a batch, fanned out over the host cores.
+every query of a batch, fanned out over the host cores.  Test infrastructure
+(tests/ and bench.py's untimed parity checks), like the rest of oracle/.
 
 The oracle costs about 0.2 s per C2 query on one core, so a whole 256-query
 batch takes seconds on a process pool.  Workers are forked and read the

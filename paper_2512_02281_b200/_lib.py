@@ -71,6 +71,7 @@ _SIGS = {
     "tri_ivf_debug_keys": [_vp, _i32, _vp, _i64, _i64p, _vp],
     "tri_debug_scan_ts": [_vp, _i32],
     "tri_merge_topk": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp],
+    "tri_merge_topk_ld": [_vp, _vp, _i32, _i32, _i32, _i32, _i64, _i32, _vp, _vp, _i32, _vp],
 }
 _RESTYPE = {"tri_last_error": C.c_char_p}
 

@@ -68,6 +68,21 @@ class _DeviceStore:
                                               ids.ctypes.data, dists.ctypes.data, None))
         return ids, dists
 
+    def knn_into(self, q_host, ks, ids_out, dists_out, stream=None) -> None:
+        """Blocking batched exact kNN into caller-owned host arrays [B, ldo]
+        (pinned buffers let a repeated shape replay as one CUDA graph)."""
+        from .ivf import _check_buf, _stream_ptr
+
+        B = int(q_host.shape[0])
+        _check_buf("queries", q_host, "float64", cols=self.d)
+        _check_buf("ids_out", ids_out, "int64", rows=B)
+        _check_buf("dists_out", dists_out, "float64", cols=int(ids_out.shape[1]), rows=B)
+        ks = np.ascontiguousarray(np.broadcast_to(np.asarray(ks, dtype=np.int64), (B,)), dtype=np.int32)
+        if B:
+            _lib.check(_lib.gpu().tri_knn_bruteforce(self.handle, _lib.ptr(q_host), B, ks.ctypes.data,
+                                                     int(ids_out.shape[1]), _lib.ptr(ids_out), _lib.ptr(dists_out),
+                                                     _stream_ptr(stream)))
+
     def task_dists(self, owner: np.ndarray, cand: np.ndarray, queries64: np.ndarray) -> np.ndarray:
         lib = _lib.gpu()
         owner = np.ascontiguousarray(owner, dtype=np.int32)

@@ -1132,7 +1132,10 @@ int tri_store_create(const float* x, int64_t n, int32_t d, int32_t device, tri_s
   CU(cudaSetDevice(device));
   float* tmp = nullptr;
   CU(cudaMalloc(&tmp, (size_t)n * d * sizeof(float)));
+  // a synchronous H2D copy from pageable memory may return before its DMA
+  // lands; the kernels that read tmp run on a non-blocking stream, so wait
   cudaError_t e = cudaMemcpy(tmp, x, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
   if (e != cudaSuccess) {
     cudaFree(tmp);
     return fail(TRI_ECUDA, "upload: %s", cudaGetErrorString(e));
@@ -1373,7 +1376,8 @@ static int ivf_layout(tri_ivf* v, const float* X, long long ldx, const long long
     return (v->h_off[a + 1] - v->h_off[a]) > (v->h_off[b + 1] - v->h_off[b]);
   });
   CU(cudaMalloc(&v->list_by_size, (size_t)v->nlist * sizeof(int)));
-  CU(cudaMemcpy(v->list_by_size, order.data(), (size_t)v->nlist * sizeof(int), cudaMemcpyHostToDevice));
+  CU(cudaMemcpyAsync(v->list_by_size, order.data(), (size_t)v->nlist * sizeof(int), cudaMemcpyHostToDevice, st));
+  CU(cudaStreamSynchronize(st));
   return TRI_OK;
 }
 
@@ -1410,7 +1414,10 @@ static int ivf_finish(tri_ivf* v, tri_store* s, const float* Cdev, const int* as
   v->h_off.assign(v->nlist + 1, 0);
   for (int l = 0; l < v->nlist; ++l) v->h_off[l + 1] = v->h_off[l] + hc[l];
   CU(cudaMalloc(&v->list_off, (size_t)(v->nlist + 1) * sizeof(long long)));
-  CU(cudaMemcpy(v->list_off, v->h_off.data(), (size_t)(v->nlist + 1) * sizeof(long long), cudaMemcpyHostToDevice));
+  // on st, not the legacy stream: list_members_kernel (on the non-blocking st)
+  // must see the offsets, and a pageable H2D cudaMemcpy may return before its DMA lands
+  CU(cudaMemcpyAsync(v->list_off, v->h_off.data(), (size_t)(v->nlist + 1) * sizeof(long long),
+                     cudaMemcpyHostToDevice, st));
   DevBuf perm;
   TRY(ensure(perm, (size_t)v->n * sizeof(long long)));
   CU(launch_list_members(assign_dev, v->n, v->nlist, v->list_off, perm.as<long long>(), st));
@@ -1419,9 +1426,11 @@ static int ivf_finish(tri_ivf* v, tri_store* s, const float* Cdev, const int* as
   if (v->id_offset) {
     // ids are global: add the shard offset on the host-free path
     std::vector<long long> h(v->n);
-    CU(cudaMemcpy(h.data(), v->ids, (size_t)v->n * sizeof(long long), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(h.data(), v->ids, (size_t)v->n * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     for (auto& x : h) x += v->id_offset;
-    CU(cudaMemcpy(v->ids, h.data(), (size_t)v->n * sizeof(long long), cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(v->ids, h.data(), (size_t)v->n * sizeof(long long), cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
   }
   CU(cudaMalloc(&v->assign, (size_t)v->n * sizeof(int)));
   CU(cudaMemcpyAsync(v->assign, assign_dev, (size_t)v->n * sizeof(int), cudaMemcpyDeviceToDevice, st));
@@ -2264,10 +2273,20 @@ int tri_ivf_debug_keys(tri_ivf* v, int32_t which, uint64_t* keys, int64_t cap, i
 
 int tri_merge_topk(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t k_out,
                    double* out_dists, int64_t* out_ids, void* stream) {
+  return tri_merge_topk_ld(dists, ids, G, B, k_in, k_in, (int64_t)B * k_in, k_out, out_dists, out_ids, k_out, stream);
+}
+
+int tri_merge_topk_ld(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t ld_in,
+                      int64_t g_stride, int32_t k_out, double* out_dists, int64_t* out_ids, int32_t ld_out,
+                      void* stream) {
   if (G < 1 || B < 0 || k_in < 1 || k_out < 1) return fail(TRI_EINVAL, "bad merge shape");
+  if (ld_in < k_in || ld_out < k_out) return fail(TRI_EINVAL, "ld_in=%d / ld_out=%d below k_in=%d / k_out=%d", ld_in,
+                                                 ld_out, k_in, k_out);
+  if (G > 1 && g_stride < (int64_t)B * ld_in) return fail(TRI_EINVAL, "g_stride=%lld below B*ld_in", (long long)g_stride);
   if ((long long)G * k_in > 8192) return fail(TRI_EINVAL, "G*k_in=%lld exceeds 8192", (long long)G * k_in);
   CU(launch_merge_exact(dists, reinterpret_cast<const long long*>(ids), G, B, k_in, k_out, out_dists,
-                        reinterpret_cast<long long*>(out_ids), static_cast<cudaStream_t>(stream)));
+                        reinterpret_cast<long long*>(out_ids), static_cast<cudaStream_t>(stream), ld_in, ld_out,
+                        (long long)g_stride));
   return TRI_OK;
 }
 

@@ -648,8 +648,9 @@ int tri_engine_create(tri_store* s, const uint32_t* adjacency, int32_t degree, i
     return bail(set_error(TRI_ECUDA, "stream creation failed"));
   const size_t adj_bytes = (size_t)sv.n * degree * sizeof(unsigned);
   if (cudaMalloc(&e->adj, adj_bytes) != cudaSuccess ||
-      cudaMemcpy(e->adj, adjacency, adj_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMalloc(&e->res_n, sizeof(int)) != cudaSuccess || cudaMemset(e->res_n, 0, sizeof(int)) != cudaSuccess ||
+      cudaMemcpyAsync(e->adj, adjacency, adj_bytes, cudaMemcpyHostToDevice, e->st) != cudaSuccess ||
+      cudaStreamSynchronize(e->st) != cudaSuccess ||
+      cudaMalloc(&e->res_n, sizeof(int)) != cudaSuccess || cudaMemsetAsync(e->res_n, 0, sizeof(int), e->st) != cudaSuccess ||
       cudaMalloc(&e->stats, kMaxChunk * kStats * sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&e->h_stats, kMaxChunk * kStats * sizeof(int)) != cudaSuccess ||
       cudaEventCreate(&e->ev0) != cudaSuccess || cudaEventCreate(&e->ev1) != cudaSuccess)

@@ -271,7 +271,8 @@ cudaError_t launch_distance_tasks(const int* owner, const long long* cand, int n
 cudaError_t launch_rowwise_f64(const double* q, long long q_stride, const double* X, long long n, int d, double* out,
                                cudaStream_t st);
 cudaError_t launch_merge_exact(const double* dists, const long long* ids, int G, int B, int k_in, int k_out,
-                               double* out_d, long long* out_ids, cudaStream_t st);
+                               double* out_d, long long* out_ids, cudaStream_t st, int ld_in, int ld_out,
+                               long long g_stride);
 
 // IVF packer ------------------------------------------------------------------
 struct PackLaunch {

@@ -1353,7 +1353,8 @@ cudaError_t launch_rowwise_f64(const double* q, long long q_stride, const double
 __global__ void __launch_bounds__(kThreads) merge_exact_kernel(const double* __restrict__ dists,
                                                                const long long* __restrict__ ids, int G, int B,
                                                                int k_in, int k_out, double* __restrict__ out_d,
-                                                               long long* __restrict__ out_ids, int n2) {
+                                                               long long* __restrict__ out_ids, int n2, int ld_in,
+                                                               int ld_out, long long g_stride) {
   extern __shared__ Exact mbuf[];
   const int q = blockIdx.x;
   const int n = G * k_in;
@@ -1361,7 +1362,7 @@ __global__ void __launch_bounds__(kThreads) merge_exact_kernel(const double* __r
     Exact e = exact_max();
     if (i < n) {
       int g = i / k_in, j = i - g * k_in;
-      long long off = ((long long)g * B + q) * k_in + j;
+      long long off = (long long)g * g_stride + (long long)q * ld_in + j;
       long long id = ids[off];
       if (id >= 0) {
         e.d = dists[off];
@@ -1375,20 +1376,22 @@ __global__ void __launch_bounds__(kThreads) merge_exact_kernel(const double* __r
   for (int j = threadIdx.x; j < k_out; j += kThreads) {
     const Exact e = mbuf[j];
     const bool ok = e.id != 0x7fffffffffffffffll;
-    out_ids[(long long)q * k_out + j] = ok ? e.id : -1;
-    out_d[(long long)q * k_out + j] = e.d;
+    out_ids[(long long)q * ld_out + j] = ok ? e.id : -1;
+    out_d[(long long)q * ld_out + j] = e.d;
   }
 }
 
 cudaError_t launch_merge_exact(const double* dists, const long long* ids, int G, int B, int k_in, int k_out,
-                               double* out_d, long long* out_ids, cudaStream_t st) {
+                               double* out_d, long long* out_ids, cudaStream_t st, int ld_in, int ld_out,
+                               long long g_stride) {
   if (B <= 0) return cudaSuccess;
   int n2 = next_pow2(G * k_in);
   size_t smem = (size_t)n2 * sizeof(Exact);
   cudaError_t e =
       cudaFuncSetAttribute(merge_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  merge_exact_kernel<<<B, kThreads, smem, st>>>(dists, ids, G, B, k_in, k_out, out_d, out_ids, n2);
+  merge_exact_kernel<<<B, kThreads, smem, st>>>(dists, ids, G, B, k_in, k_out, out_d, out_ids, n2, ld_in, ld_out,
+                                                   g_stride);
   return cudaGetLastError();
 }
 

@@ -143,7 +143,7 @@ def test_c2_scale_parity():
     """BASELINE C2 (1M x 768, nlist 1024, nprobe 32, B 256, k 10): the GPU-trained
     artifact equals the oracle's k-means bit-for-bit, and ALL 256 queries equal
     the oracle (process pool over the host cores)."""
-    from oracle_pool import assert_rows_equal, ivf_oracle_batch
+    from oracle.pool import assert_rows_equal, ivf_oracle_batch
 
     data = gen_vectors_chunked(1_000_000, 768, seed=3)
     store = VectorStore(data=data)
@@ -313,7 +313,7 @@ def test_c3_scale_ragged_parity(scan_kernel):
     ids, d = idx.search(qs, ks, nps)
     cen, asg = idx.export()
     art = orc.IVFArtifact(cen, asg)
-    from oracle_pool import assert_rows_equal, ivf_oracle_batch
+    from oracle.pool import assert_rows_equal, ivf_oracle_batch
 
     assert_rows_equal(ids, d, ivf_oracle_batch(data, art, qs.astype(np.float64), ks, nps), ks)
 

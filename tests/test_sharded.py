@@ -87,3 +87,19 @@ def test_two_rank_gloo_sharded_equals_global(tmp_path):
     for j, q in enumerate(queries):
         i, d = orc.ivf_search(data, art, q, 7, 5)
         assert np.array_equal(got["ids"][j, : i.size], i) and np.array_equal(got["ds"][j, : d.size], d)
+
+
+def test_reference_arm_c4_small():
+    """bench.py --impl reference on a reduced C4: CPU oracle only (no GPU)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BENCH_C4_N="20000")
+    res = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "C4", "--steps", "2",
+                          "--warmup", "1"], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["config"]["n_db"] == 20000
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
