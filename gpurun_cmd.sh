@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-for i in 1 2; do
-BENCH_DEVICE=0 BENCH_BACKEND=gloo BENCH_C4_N=300000 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 2951$i bench.py --gpus 2 --steps 4 --warmup 3 --lanes 2 --parity full > gpurun_out/sh$i.out 2> gpurun_out/sh$i.err; echo "rc=$?" >> gpurun_out/sh$i.err
-done
+timeout 900 python -m pytest tests/test_gpu_padded.py -q -x > gpurun_out/pytest_pad.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_pad.log
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest.log
+timeout 600 python tools/c5_realtime.py --repeats 3 --out gpurun_out/c5.json > gpurun_out/c5.log 2>&1; echo "c5 rc=$?" >> gpurun_out/c5.log

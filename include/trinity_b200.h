@@ -48,6 +48,11 @@ typedef struct tri_ivf tri_ivf;
 /* Library ------------------------------------------------------------------ */
 const char* tri_last_error(void);
 int tri_version(void);
+/* Process-wide counts of whole-search executions: eager (host-planned
+ * launches), graph captures and graph replays.  Ragged batches replay
+ * fixed-shape padded graphs keyed by (bucket(B), max k, max nprobe); option
+ * "ragged_graphs" = 0 restores exact-shape keys. */
+int tri_graph_counters(int64_t* eager, int64_t* captured, int64_t* replayed);
 int tri_device_count(int32_t* count);
 /* Debug/test knobs: "force_fixup" (1 = treat every query as uncertified),
  * "kp_extra" (extra over-fetch added to k), "scan_kernel" (0 auto: IVF

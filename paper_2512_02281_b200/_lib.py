@@ -29,6 +29,7 @@ _i64p = C.POINTER(C.c_int64)
 _SIGS = {
     "tri_last_error": [],
     "tri_version": [],
+    "tri_graph_counters": [_i64p, _i64p, _i64p],
     "tri_device_count": [_i32p],
     "tri_set_option": [C.c_char_p, _i64],
     "tri_store_create": [_vp, _i64, _i32, _i32, C.POINTER(_vp)],
@@ -136,6 +137,13 @@ def ptr(a) -> int:
     if hasattr(a, "data_ptr"):
         return a.data_ptr()
     return a.ctypes.data
+
+
+def graph_counters() -> dict:
+    """Process-wide whole-search executions: eager, graph captures, graph replays."""
+    e, c, r = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+    check(load_library().tri_graph_counters(C.byref(e), C.byref(c), C.byref(r)))
+    return {"eager": e.value, "captured": c.value, "replayed": r.value}
 
 
 def set_option(name: str, value: int) -> None:

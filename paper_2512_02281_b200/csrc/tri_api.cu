@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -57,6 +58,7 @@ int fail(int code, const char* fmt, ...) {
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  long long* owner = nullptr;  // the owning workspace's epoch (nullptr: the global one)
   template <typename T>
   T* as() const {
     return static_cast<T*>(p);
@@ -76,8 +78,10 @@ long long g_graphs = [] {
 
 int ensure(DevBuf& b, size_t bytes) {
   if (bytes <= b.cap && b.p) return TRI_OK;
-  ++g_epoch;
-  if (b.p) cudaFree(b.p);
+  if (b.p) {  // a pointer captured graphs may bake in goes away (a fresh allocation retires nothing)
+    ++(b.owner ? *b.owner : g_epoch);
+    cudaFree(b.p);
+  }
   b.p = nullptr;
   b.cap = 0;
   size_t want = std::max<size_t>(bytes + bytes / 4, 256);
@@ -123,6 +127,8 @@ long long g_coarse_tc = 1;    // IVF coarse GEMM on tensor cores (split fp16) wh
 long long g_bf_wide = 1;      // brute force: 64-query groups (one row pass per 64 queries) when kp <= 64
 long long g_bf_seed = 2;      // ... with the TMEM seed pass (tri_tcscan.cu tc_seed_pass): 1 per item, 2 cross-item
 long long g_bf_qtma = 1;      // ... and TMA-loaded query tiles
+std::atomic<long long> g_gr_eager{0}, g_gr_captured{0}, g_gr_replayed{0};  // graph_run outcomes
+long long g_ragged_graphs = 1;  // ragged / odd-sized batches replay fixed-shape padded graphs (option "ragged_graphs")
 
 
 // Candidate capacity: over-fetch so the certified re-rank almost never falls
@@ -260,6 +266,9 @@ bool use_tc(int qld, int kp_max_tc) {
 // streams never share scratch, so they can overlap on the device.
 struct Workspace {
   static constexpr int kStaging = 4;  // pinned host staging ring depth
+  // Bumped when one of THIS workspace's buffers moves or a plan of it is
+  // dropped: only graphs that use this workspace retire (graph_run).
+  long long epoch = 0;
   DevBuf q64, Q32, qn32, qn64, flags, plan, part, merged, exact, out_ids, out_d;
   // IVF per-search buffers
   DevBuf probes, probe_d, counts, fill, mbase, items, members, counters, meta;
@@ -270,6 +279,10 @@ struct Workspace {
   bool split_q = false;  // this search prepared Qh/Ql/qinv for the split coarse GEMM
 
   DevBuf fxs;       // fix-up partial lists
+  // fixed-shape padded batches: uploaded plan input, device key total, padded
+  // queries and results
+  DevBuf rplan, rtot, qpad, pad_ids, pad_d;
+  int pad_real = -1;  // real queries of the last search when it ran padded (-1: not padded)
   HostBuf h_plan;
   HostBuf h_stage[kStaging];
   HostBuf h_bq, h_bids, h_bd;  // pinned copies of a host brute-force call's queries / results (graph replay)
@@ -331,12 +344,79 @@ struct Workspace {
   };
   std::vector<Graph> graphs;
   unsigned long long graph_clock = 0;
+  // brute-force plans not currently active (see plan_bruteforce): each keeps
+  // its own device buffer, so graphs captured against it stay valid
+  struct Plan {
+    DevBuf plan;
+    size_t plan_bytes = 0, off_items = 0, off_members = 0;
+    int plan_B = -1;
+    long long plan_n = -1, plan_opts = -1, part_keys = 0;
+    std::vector<int> plan_k;
+    bool dense = false, tc = false;
+    int n_items = 0, grid = 0, gmax = 0, cap = 0, kp_max = 0, k_max = 0, nq = kTcGroup, q_tma = 0;
+    unsigned long long used = 0;
+  };
+  std::vector<Plan> plan_cache;
+  unsigned long long plan_clock = 0;
+  void plan_out(Plan& p) const {
+    p.plan = plan;
+    p.plan_bytes = plan_bytes;
+    p.off_items = off_items;
+    p.off_members = off_members;
+    p.plan_B = plan_B;
+    p.plan_n = plan_n;
+    p.plan_opts = plan_opts;
+    p.part_keys = part_keys;
+    p.plan_k = plan_k;
+    p.dense = dense;
+    p.tc = tc;
+    p.n_items = n_items;
+    p.grid = grid;
+    p.gmax = gmax;
+    p.cap = cap;
+    p.kp_max = kp_max;
+    p.k_max = k_max;
+    p.nq = nq;
+    p.q_tma = q_tma;
+  }
+  void plan_in(const Plan& p) {
+    plan = p.plan;
+    plan_bytes = p.plan_bytes;
+    off_items = p.off_items;
+    off_members = p.off_members;
+    plan_B = p.plan_B;
+    plan_n = p.plan_n;
+    plan_opts = p.plan_opts;
+    part_keys = p.part_keys;
+    plan_k = p.plan_k;
+    dense = p.dense;
+    tc = p.tc;
+    n_items = p.n_items;
+    grid = p.grid;
+    gmax = p.gmax;
+    cap = p.cap;
+    kp_max = p.kp_max;
+    k_max = p.k_max;
+    nq = p.nq;
+    q_tma = p.q_tma;
+  }
+  Workspace() {
+    for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat,
+                      &probes, &probe_d, &counts, &fill, &mbase, &items, &members, &counters, &meta, &Qh, &qinv,
+                      &gthr, &fxs, &Ql, &seedb, &rplan, &rtot, &qpad, &pad_ids, &pad_d})
+      b->owner = &epoch;
+  }
+  Workspace(const Workspace&) = delete;
+  Workspace& operator=(const Workspace&) = delete;
   void free_all() {
     for (auto& g : graphs) g.destroy();
     graphs.clear();
+    for (auto& p : plan_cache)
+      if (p.plan.p) cudaFree(p.plan.p);
+    plan_cache.clear();
     for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat,
                       &probes, &probe_d, &counts, &fill, &mbase, &items, &members, &counters, &meta, &Qh, &qinv,
-                      &gthr, &fxs, &Ql, &seedb})
+                      &gthr, &fxs, &Ql, &seedb, &rplan, &rtot, &qpad, &pad_ids, &pad_d})
       release(*b);
     for (HostBuf* b : {&h_plan, &h_bq, &h_bids, &h_bd}) {
       if (b->p) cudaFreeHost(b->p);
@@ -624,12 +704,41 @@ static int store_split_copy(tri_store* c, int dph, cudaStream_t st) {
   return TRI_OK;
 }
 
+// Per-workspace brute-force plans.  The active plan lives in the Workspace
+// fields; up to kPlanCache others are kept with their own device buffers, so
+// alternating shapes (a serving loop's batch profiles, the IVF coarse step at
+// several nprobe) switch plans without re-planning and without touching the
+// device copy any captured graph reads.  Only evicting a plan retires graphs.
+constexpr int kPlanCache = 16;
+
 int plan_bruteforce(tri_store* s, Workspace& w, int B, const int* k, cudaStream_t st) {
-  if (w.plan_B == B && w.plan_n == s->n && w.plan_opts == plan_opts() && (int)w.plan_k.size() == B &&
-      std::equal(w.plan_k.begin(), w.plan_k.end(), k))
-    return TRI_OK;
+  auto same = [&](int pB, long long pn, long long popts, const std::vector<int>& pk) {
+    return pB == B && pn == s->n && popts == plan_opts() && (int)pk.size() == B && std::equal(pk.begin(), pk.end(), k);
+  };
+  if (same(w.plan_B, w.plan_n, w.plan_opts, w.plan_k)) return TRI_OK;
+  for (auto& p : w.plan_cache)
+    if (same(p.plan_B, p.plan_n, p.plan_opts, p.plan_k)) {  // swap the cached plan in
+      Workspace::Plan cur;
+      w.plan_out(cur);
+      w.plan_in(p);
+      p = cur;
+      p.used = ++w.plan_clock;
+      return TRI_OK;
+    }
   if (w.capturing) return fail(TRI_EINTERNAL, "re-plan during graph capture");
-  ++g_epoch;  // graphs captured against the old plan read its device copy
+  if (w.plan_B >= 0 && w.plan.p) {  // park the active plan (its buffer stays alive)
+    if ((int)w.plan_cache.size() >= kPlanCache) {
+      auto lru = std::min_element(w.plan_cache.begin(), w.plan_cache.end(),
+                                  [](const Workspace::Plan& a, const Workspace::Plan& b) { return a.used < b.used; });
+      ++w.epoch;  // graphs captured against it read its device copy
+      cudaFree(lru->plan.p);
+      w.plan_cache.erase(lru);
+    }
+    w.plan_cache.emplace_back();
+    w.plan_out(w.plan_cache.back());
+    w.plan_cache.back().used = ++w.plan_clock;
+    w.plan = DevBuf{nullptr, 0, &w.epoch};  // the new plan gets a fresh buffer
+  }
   // Dense path for small stores: the whole B x n distance matrix is cheap.
   {
     int kpd = kMinKp, kmx = 1;
@@ -1051,13 +1160,27 @@ int set_error(int code, const char* fmt, ...) {
 // entry points that use it).
 template <class Body>
 static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, int mode, int B, const int* k,
-                     const int* np, int ldo, const void* q, const void* ids, const void* dists, Body&& body);
+                     const int* np, int ldo, const void* q, const void* ids, const void* dists, Body&& body,
+                     int nk = -1);
+// fixed-shape padded batches (defined with graph_run)
+static int bucket_of(int B);
+static int ensure_padded(Workspace& w, int Bc, int d, int ldo);
+static int bf_padded(tri_store* s, Workspace& w, cudaStream_t st, int mode, const double* q_dev, int B, const int* k,
+                     int ldo, int64_t* out_ids, double* out_d);
+static bool pad_bf(int B, const int* k);
 
 extern "C" {
 
 const char* tri_last_error(void) { return g_err.c_str(); }
 
 int tri_version(void) { return 1; }
+
+int tri_graph_counters(int64_t* eager, int64_t* captured, int64_t* replayed) {
+  if (eager) *eager = g_gr_eager.load();
+  if (captured) *captured = g_gr_captured.load();
+  if (replayed) *replayed = g_gr_replayed.load();
+  return TRI_OK;
+}
 
 int tri_device_count(int32_t* count) {
   int c = 0;
@@ -1095,6 +1218,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "bf_wide")) g_bf_wide = value;
   else if (!std::strcmp(name, "bf_seed")) g_bf_seed = value;
   else if (!std::strcmp(name, "bf_qtma")) g_bf_qtma = value;
+  else if (!std::strcmp(name, "ragged_graphs")) g_ragged_graphs = value;
   else if (!std::strcmp(name, "dense_pow2")) g_dense_pow2 = value;
 
   else if (!std::strcmp(name, "coarse_split")) {
@@ -1189,6 +1313,17 @@ int tri_knn_bruteforce(tri_store* s, const double* q, int32_t B, const int32_t* 
   Workspace* wp = nullptr;
   TRY(s->lanes.get(st, &wp));
   Workspace& w = *wp;
+  if (pad_bf(B, k)) {
+    TRY(ensure_padded(w, bucket_of(B), s->d, ldo));
+    CU(cudaMemcpyAsync(w.qpad.p, q, (size_t)B * s->d * sizeof(double), cudaMemcpyHostToDevice, st));
+    TRY(bf_padded(s, w, st, 6, nullptr, B, k, ldo, nullptr, nullptr));
+    CU(cudaMemcpyAsync(ids, w.pad_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(dists, w.pad_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+    TRY(lane_done(w, st));
+    CU(cudaStreamSynchronize(st));
+    return TRI_OK;
+  }
+  w.pad_real = -1;
   TRY(ensure_query_bufs(w, B, s->d, s->qld));
   TRY(ensure(w.out_ids, (size_t)B * ldo * sizeof(long long)));
   TRY(ensure(w.out_d, (size_t)B * ldo * sizeof(double)));
@@ -1237,7 +1372,7 @@ int tri_store_last_fixups(tri_store* s, int32_t* n) {
     CU(cudaDeviceSynchronize());
     CU(cudaMemcpy(&v, w.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
   }
-  *n = v;
+  *n = w.pad_real >= 0 ? std::min(v, w.pad_real) : v;  // padded: dummies copy query 0
   return TRI_OK;
 }
 
@@ -1660,8 +1795,12 @@ static int ivf_validate(tri_ivf* v, int32_t B, const int32_t* k, const int32_t* 
 }
 
 // Enqueue one whole search on `st` (lane workspaces w / cw already chosen).
+// dplan != nullptr: a padded fixed-shape batch (see launch_ragged_plan): k and
+// nprobe are then the batch profile (max k, max nprobe for every row) that
+// sizes every buffer, and the per-query plan is built on the device.
 static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double* q, int32_t B, const int32_t* k,
-                           const int32_t* nprobe, int32_t ldo, int64_t* ids, double* dists, cudaStream_t st) {
+                           const int32_t* nprobe, int32_t ldo, int64_t* ids, double* dists, cudaStream_t st,
+                           const int* dplan = nullptr) {
   const int npmax = *std::max_element(nprobe, nprobe + B);
   TRY(ensure_query_bufs(w, B, v->d, v->qld));
   const bool rec = v->prof && v->ev_used < kProfSearches;
@@ -1717,33 +1856,56 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   // 2. per-query plan -> device
   long long part_keys = 0, members = 0;
   const size_t meta_bytes = (size_t)B * (sizeof(QueryMeta) + sizeof(int));
-  int slot = 0;
-  void* hbuf = nullptr;
-  TRY(stage_host(w, meta_bytes + 64, &slot, &hbuf));
-  QueryMeta* hm = static_cast<QueryMeta*>(hbuf);
-  int* hnp = reinterpret_cast<int*>(hm + B);
-  for (int i = 0; i < B; ++i) {
-    hm[i].k = k[i];
-    hm[i].kp = kp[i];
-    hm[i].n_slots = nprobe[i];
-    hm[i].cls = cls_of(kp[i]);
-    hm[i].part_off = part_keys;
-    hm[i].n_total = 0;
-    hnp[i] = nprobe[i];
+  for (int i = 0; i < B; ++i) {  // (padded batch: the worst case the device plan can reach)
     part_keys += (long long)nprobe[i] * kp[i];
     members += nprobe[i];
   }
   const int cap = ch.cap, gmax = ch.gmax;
-  int cls_mask = 0;
-  for (int i = 0; i < B; ++i) cls_mask |= 1 << hm[i].cls;
   TRY(ensure(w.meta, meta_bytes + 64));
-  TRY(staged_upload(w, slot, w.meta.p, meta_bytes, st));
   QueryMeta* dmeta = w.meta.as<QueryMeta>();
   int* dnp = reinterpret_cast<int*>(dmeta + B);
+  int cls_mask = 0;
+  if (dplan) {
+    cls_mask = (1 << (cls_of(kp_max) + 1)) - 1;  // any class up to the profile's
+    TRY(ensure(w.rtot, 64));
+    RaggedPlan rp;
+    rp.in = dplan;
+    rp.Bc = B;
+    rp.f16 = f16 ? 1 : 0;
+    rp.tc = ch.tc ? 1 : 0;
+    rp.f16_div = (int)std::max<long long>(1, g_f16_div);
+    rp.kp_extra = (int)g_kp_extra;
+    rp.meta = dmeta;
+    rp.nprobe = dnp;
+    rp.total_keys = w.rtot.as<long long>();
+    CU(launch_ragged_plan(rp, st));
+  } else {
+    int slot = 0;
+    void* hbuf = nullptr;
+    TRY(stage_host(w, meta_bytes + 64, &slot, &hbuf));
+    QueryMeta* hm = static_cast<QueryMeta*>(hbuf);
+    int* hnp = reinterpret_cast<int*>(hm + B);
+    long long off = 0;
+    for (int i = 0; i < B; ++i) {
+      hm[i].k = k[i];
+      hm[i].kp = kp[i];
+      hm[i].n_slots = nprobe[i];
+      hm[i].cls = cls_of(kp[i]);
+      hm[i].part_off = off;
+      hm[i].n_total = 0;
+      hnp[i] = nprobe[i];
+      off += (long long)nprobe[i] * kp[i];
+      cls_mask |= 1 << hm[i].cls;
+    }
+    TRY(staged_upload(w, slot, w.meta.p, meta_bytes, st));
+  }
   TRY(ensure(w.part, (size_t)part_keys * sizeof(unsigned long long)));
   TRY(ensure(w.merged, (size_t)B * kp_max * sizeof(unsigned long long)));
   TRY(ensure(w.exact, (size_t)B * kp_max * 16));
-  CU(cudaMemsetAsync(w.part.p, 0xff, (size_t)part_keys * sizeof(unsigned long long), st));
+  if (dplan)
+    CU(launch_fill_keys(w.part.as<unsigned long long>(), w.rtot.as<long long>(), 2 * sm_count(v->device), st));
+  else
+    CU(cudaMemsetAsync(w.part.p, 0xff, (size_t)part_keys * sizeof(unsigned long long), st));
   size_t cbytes = (size_t)v->nlist * kNumCls * sizeof(int);
   TRY(ensure(w.counts, cbytes));
   TRY(ensure(w.fill, cbytes));
@@ -1927,20 +2089,29 @@ long long graph_opts() {
 
 template <class Body>
 static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, int mode, int B, const int* k,
-                     const int* np, int ldo, const void* q, const void* ids, const void* dists, Body&& body) {
-  if (!g_graphs) return body();
+                     const int* np, int ldo, const void* q, const void* ids, const void* dists, Body&& body,
+                     int nk) {
+  if (nk < 0) nk = B;  // key entries of k[] / np[]: every query, or 1 (a padded batch's profile)
+  // validity stamp of a captured graph: the global epoch (store-level changes)
+  // plus the epochs of the workspaces it reads; all only grow, so the sum
+  // changes exactly when one of them does
+  auto stamp = [&]() { return g_epoch + w.epoch + (cw ? cw->epoch : 0); };
+  if (!g_graphs) {
+    ++g_gr_eager;
+    return body();
+  }
   const bool prof = v && v->prof && v->ev_used < kProfSearches;
   const long long opts = graph_opts() * 2 + (v && scan_reserve_for(v) > 0);
   Workspace::Graph* e = nullptr;
   for (auto& gr : w.graphs)
     if (gr.mode == mode && gr.B == B && gr.ldo == ldo && gr.q == q && gr.ids == ids && gr.dists == dists &&
-        gr.prof == prof && gr.opts == opts && std::equal(gr.k.begin(), gr.k.end(), k) &&
+        gr.prof == prof && gr.opts == opts && (int)gr.k.size() == nk && std::equal(gr.k.begin(), gr.k.end(), k) &&
         std::equal(gr.np.begin(), gr.np.end(), np)) {
       e = &gr;
       break;
     }
   if (!e) {
-    if (w.graphs.size() >= 8) {  // evict the least recently used shape
+    if (w.graphs.size() >= 32) {  // evict the least recently used shape
       auto lru = std::min_element(w.graphs.begin(), w.graphs.end(),
                                   [](const Workspace::Graph& a, const Workspace::Graph& b) { return a.used < b.used; });
       lru->destroy();
@@ -1951,8 +2122,8 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
     e->mode = mode;
     e->B = B;
     e->ldo = ldo;
-    e->k.assign(k, k + B);
-    e->np.assign(np, np + B);
+    e->k.assign(k, k + nk);
+    e->np.assign(np, np + nk);
     e->q = q;
     e->ids = ids;
     e->dists = dists;
@@ -1960,15 +2131,16 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
     e->opts = opts;
   }
   e->used = ++w.graph_clock;
-  if (e->state == 2 && e->epoch != g_epoch) {  // scratch moved or plan rewritten since capture
+  if (e->state == 2 && e->epoch != stamp()) {  // scratch moved or plan rewritten since capture
     e->destroy();
     e->state = 0;
   }
-  if (e->state == 0 || e->state == 3 || (e->state == 1 && e->epoch != g_epoch)) {
+  if (e->state == 0 || e->state == 3 || (e->state == 1 && e->epoch != stamp())) {
+    ++g_gr_eager;
     const int rc = body();
     if (e->state != 3) {
       e->state = 1;
-      e->epoch = g_epoch;
+      e->epoch = stamp();
     }
     return rc;
   }
@@ -1978,7 +2150,7 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
     if (prof)
       for (auto& ev : e->ph)
         if (!ev) CU(cudaEventCreate(&ev));
-    const long long ep0 = g_epoch;
+    const long long ep0 = stamp();
     w.capturing = true;
     if (cw) cw->capturing = true;
     w.cap_host = &e->host;
@@ -1992,13 +2164,14 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
     w.cap_host = nullptr;
     w.cap_ph = nullptr;
     cudaGraphExec_t ex = nullptr;
-    if (rc == TRI_OK && ce == cudaSuccess && g_epoch == ep0) ce = cudaGraphInstantiate(&ex, gr, 0);
-    if (rc != TRI_OK || ce != cudaSuccess || g_epoch != ep0 || !ex) {
+    if (rc == TRI_OK && ce == cudaSuccess && stamp() == ep0) ce = cudaGraphInstantiate(&ex, gr, 0);
+    if (rc != TRI_OK || ce != cudaSuccess || stamp() != ep0 || !ex) {
       cudaGetLastError();
       if (gr) cudaGraphDestroy(gr);
       if (ex) cudaGraphExecDestroy(ex);
-      e->state = (g_epoch != ep0 && rc == TRI_OK && ce == cudaSuccess) ? 1 : 3;
-      e->epoch = g_epoch;
+      e->state = (stamp() != ep0 && rc == TRI_OK && ce == cudaSuccess) ? 1 : 3;
+      e->epoch = stamp();
+      ++g_gr_eager;
       return body();  // not capturable: stay eager
     }
     if (prof) {
@@ -2019,12 +2192,13 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
     // alive by instantiating from it and destroying it with the entry
     e->exec = ex;
     e->state = 2;
-    e->epoch = g_epoch;
+    e->epoch = stamp();
     e->last_B = w.last_B;
     e->last_npmax = w.last_npmax;
     e->last_f16 = w.last_f16;
     e->last_np = w.last_np;
     e->graph = gr;
+    ++g_gr_captured;
   }
   // replay
   w.last_B = e->last_B;
@@ -2041,8 +2215,112 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
       CU(cudaGraphExecEventRecordNodeSetEvent(e->exec, e->evnode[j], v->ev[7 * v->ev_used + j]));
   }
   CU(cudaGraphLaunch(e->exec, st));
+  ++g_gr_replayed;
   if (prof) v->ev_used++;
   return TRI_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Fixed-shape padded batches.  A batch whose shape would not repeat (ragged
+// per-query k / nprobe, or a size that is not a power of two) runs as Bc =
+// bucket(B) queries: dummies copy query 0 with k = nprobe = 1, the per-query
+// plan is built on the device from an uploaded input, and the graph key is
+// (Bc, max k, max nprobe) -- so a serving loop's ever-changing prefill /
+// decode mixes replay a handful of captured graphs instead of planning every
+// batch on the host ("round up with masked dummies").
+static int bucket_of(int B) {
+  int b = 16;
+  while (b < B) b <<= 1;
+  return b;
+}
+
+static bool uniform_shape(int B, const int* k, const int* np) {
+  for (int i = 1; i < B; ++i)
+    if (k[i] != k[0] || (np && np[i] != np[0])) return false;
+  return true;
+}
+
+// plan input [B, 0, (k, nprobe) x Bc] for the next padded search on st
+static int upload_ragged(Workspace& w, int B, int Bc, const int* k, const int* np, cudaStream_t st) {
+  const size_t bytes = (size_t)(2 + 2 * Bc) * sizeof(int);
+  int slot = 0;
+  void* hp = nullptr;
+  TRY(stage_host(w, bytes, &slot, &hp));
+  int* h = static_cast<int*>(hp);
+  h[0] = B;
+  h[1] = 0;
+  for (int i = 0; i < Bc; ++i) {
+    h[2 + 2 * i] = i < B ? k[i] : 1;
+    h[3 + 2 * i] = i < B ? (np ? np[i] : 1) : 1;
+  }
+  TRY(ensure(w.rplan, bytes));
+  return staged_upload(w, slot, w.rplan.p, bytes, st);
+}
+
+static int ensure_padded(Workspace& w, int Bc, int d, int ldo) {
+  TRY(ensure(w.qpad, (size_t)Bc * d * sizeof(double)));
+  TRY(ensure(w.pad_ids, (size_t)Bc * ldo * sizeof(long long)));
+  TRY(ensure(w.pad_d, (size_t)Bc * ldo * sizeof(double)));
+  return TRI_OK;
+}
+
+// One padded IVF search on st.  q_dev: the caller's device queries (B rows),
+// or nullptr when the B rows were already copied into w.qpad.  Results land in
+// w.pad_ids / w.pad_d; with out_ids set, the first B rows are copied there.
+static int ivf_padded(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, int mode, const double* q_dev, int B,
+                      const int* k, const int* np, int ldo, int64_t* out_ids, double* out_d) {
+  const int Bc = bucket_of(B);
+  const int kmax = *std::max_element(k, k + B), npmax = *std::max_element(np, np + B);
+  TRY(upload_ragged(w, B, Bc, k, np, st));
+  TRY(ensure_padded(w, Bc, v->d, ldo));
+  TRY(ensure_query_bufs(w, Bc, v->d, v->qld));
+  std::vector<int> kprof(Bc, kmax), npprof(Bc, npmax);
+  TRY(graph_run(v, w, cw, st, mode, Bc, &kmax, &npmax, ldo, q_dev, out_ids, out_d, [&]() -> int {
+    const int* nB = w.rplan.as<int>();
+    CU(launch_pad_rows(q_dev ? q_dev : w.qpad.as<double>(), w.qpad.as<double>(), nB, Bc, v->d, st));
+    TRY(ivf_search_body(v, w, cw, w.qpad.as<double>(), Bc, kprof.data(), npprof.data(), ldo,
+                        w.pad_ids.as<int64_t>(), w.pad_d.as<double>(), st, nB));
+    if (out_ids)
+      CU(launch_copy_rows(w.pad_ids.as<long long>(), w.pad_d.as<double>(), reinterpret_cast<long long*>(out_ids),
+                          out_d, ldo, Bc, nB, st));
+    return TRI_OK;
+  }, 1));
+  w.last_B = B;  // introspection (probes, scan bytes, fix-ups) sees the real batch
+  w.last_np.assign(np, np + B);
+  w.pad_real = B;
+  if (cw) cw->pad_real = B;
+  return TRI_OK;
+}
+
+// Padded brute force (uniform k): as ivf_padded.
+static int bf_padded(tri_store* s, Workspace& w, cudaStream_t st, int mode, const double* q_dev, int B, const int* k,
+                     int ldo, int64_t* out_ids, double* out_d) {
+  const int Bc = bucket_of(B);
+  TRY(upload_ragged(w, B, Bc, k, nullptr, st));
+  TRY(ensure_padded(w, Bc, s->d, ldo));
+  TRY(ensure_query_bufs(w, Bc, s->d, s->qld));
+  std::vector<int> kk(Bc, k[0]);
+  TRY(graph_run(nullptr, w, nullptr, st, mode, Bc, k, k, ldo, q_dev, out_ids, out_d, [&]() -> int {
+    const int* nB = w.rplan.as<int>();
+    CU(launch_pad_rows(q_dev ? q_dev : w.qpad.as<double>(), w.qpad.as<double>(), nB, Bc, s->d, st));
+    TRY(bruteforce_core(s, w, w, w.qpad.as<double>(), Bc, kk.data(), ldo, w.pad_ids.as<long long>(),
+                        w.pad_d.as<double>(), st, true));
+    if (out_ids)
+      CU(launch_copy_rows(w.pad_ids.as<long long>(), w.pad_d.as<double>(), reinterpret_cast<long long*>(out_ids),
+                          out_d, ldo, Bc, nB, st));
+    return TRI_OK;
+  }, 1));
+  w.pad_real = B;
+  return TRI_OK;
+}
+
+static bool pad_ivf(int B, const int* k, const int* np, bool pinned) {
+  return g_graphs && g_ragged_graphs && !(pinned && uniform_shape(B, k, np) && B == bucket_of(B));
+}
+
+static bool pad_bf(int B, const int* k) {
+  return g_graphs && g_ragged_graphs && uniform_shape(B, k, nullptr) && B != bucket_of(B);
 }
 
 extern "C" {
@@ -2060,7 +2338,12 @@ int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32
   cudaStream_t st = pick(stream, s->own);
   Workspace* w = nullptr;
   TRY(s->lanes.get(st, &w));
+  if (pad_bf(B, k)) {
+    TRY(bf_padded(s, *w, st, 5, q, B, k, ldo, ids, dists));
+    return lane_done(*w, st);
+  }
   TRY(ensure_query_bufs(*w, B, s->d, s->qld));
+  w->pad_real = -1;
   TRY(graph_run(nullptr, *w, nullptr, st, 2, B, k, k, ldo, q, ids, dists, [&]() -> int {
     return bruteforce_core(s, *w, *w, q, B, k, ldo, reinterpret_cast<long long*>(ids), dists, st, true);
   }));
@@ -2078,8 +2361,13 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   Workspace* cw = nullptr;
   TRY(v->lanes.get(st, &wp));
   TRY(v->cstore->lanes.get(st, &cw));
-  TRY(graph_run(v, *wp, cw, st, 0, B, k, nprobe, ldo, q, ids, dists,
-                [&] { return ivf_search_body(v, *wp, cw, q, B, k, nprobe, ldo, ids, dists, st); }));
+  if (pad_ivf(B, k, nprobe, true))
+    TRY(ivf_padded(v, *wp, cw, st, 3, q, B, k, nprobe, ldo, ids, dists));
+  else {
+    wp->pad_real = cw->pad_real = -1;
+    TRY(graph_run(v, *wp, cw, st, 0, B, k, nprobe, ldo, q, ids, dists,
+                  [&] { return ivf_search_body(v, *wp, cw, q, B, k, nprobe, ldo, ids, dists, st); }));
+  }
   TRY(lane_done(*cw, st));
   return lane_done(*wp, st);
 }
@@ -2098,6 +2386,20 @@ int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, con
     TRY(v->lanes.get(st, &wp));
     TRY(v->cstore->lanes.get(st, &cw));
     Workspace& w = *wp;
+    const bool pinned = host_pinned(q) && host_pinned(ids) && host_pinned(dists);
+    if (pad_ivf(B, k, nprobe, pinned)) {
+      // queries straight into the padded buffer, one graph launch, results back
+      TRY(ensure_padded(w, bucket_of(B), v->d, ldo));
+      CU(cudaMemcpyAsync(w.qpad.p, q, (size_t)B * v->d * sizeof(double), cudaMemcpyHostToDevice, st));
+      TRY(ivf_padded(v, w, cw, st, 4, nullptr, B, k, nprobe, ldo, nullptr, nullptr));
+      CU(cudaMemcpyAsync(ids, w.pad_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
+      CU(cudaMemcpyAsync(dists, w.pad_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+      TRY(lane_done(*cw, st));
+      TRY(lane_done(w, st));
+      CU(cudaStreamSynchronize(st));
+      return TRI_OK;
+    }
+    w.pad_real = cw->pad_real = -1;
     TRY(ensure(w.q64, (size_t)B * v->d * sizeof(double)));
     TRY(ensure(w.out_ids, (size_t)B * ldo * sizeof(long long)));
     TRY(ensure(w.out_d, (size_t)B * ldo * sizeof(double)));
@@ -2110,7 +2412,7 @@ int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, con
       return TRI_OK;
     };
     // graph replay needs pinned host buffers (pageable copies cannot be captured)
-    if (host_pinned(q) && host_pinned(ids) && host_pinned(dists)) {
+    if (pinned) {
       TRY(graph_run(v, w, cw, st, 1, B, k, nprobe, ldo, q, ids, dists, body));
     } else {
       TRY(body());
@@ -2147,6 +2449,10 @@ int tri_ivf_last_fixups(tri_ivf* v, int32_t* n) {
   if (v->cstore) {
     const Workspace& c = v->cstore->lanes.recent();
     if (c.flags.p) CU(cudaMemcpy(&b, c.flags.p, sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  if (w.pad_real >= 0) {  // padded batch: dummies copy query 0
+    a = std::min(a, w.pad_real);
+    b = std::min(b, w.pad_real);
   }
   *n = a + b;
   return TRI_OK;

@@ -294,6 +294,20 @@ struct PackLaunch {
   int gmax;
   int mixed;  // 1: one group sequence per list for all capacity classes (item kp = members' max)
 };
+// Fixed-shape ragged batches (tri_ivf.cu): device-side plan of a padded batch.
+struct RaggedPlan {
+  const int* in;          // [B, unused, (k, nprobe) x Bc]
+  int Bc;
+  int f16, tc, f16_div, kp_extra;  // the host's over-fetch rule (kp_for / kp_for_f16)
+  QueryMeta* meta;
+  int* nprobe;
+  long long* total_keys;  // sum of nprobe * kp
+};
+cudaError_t launch_ragged_plan(const RaggedPlan& r, cudaStream_t st);
+cudaError_t launch_fill_keys(unsigned long long* p, const long long* count, int grid, cudaStream_t st);
+cudaError_t launch_pad_rows(const double* src, double* dst, const int* nB, int Bc, int d, cudaStream_t st);
+cudaError_t launch_copy_rows(const long long* si, const double* sd, long long* di, double* dd, int ld, int Bc,
+                             const int* nB, cudaStream_t st);
 cudaError_t launch_pack(const PackLaunch& p, cudaStream_t st);
 
 // k-means / index layout --------------------------------------------------------

@@ -4,6 +4,8 @@
 #include "tri_common.cuh"
 #include "tri_internal.h"
 
+#include <algorithm>
+
 namespace tri {
 
 // ---------------------------------------------------------------------------
@@ -143,6 +145,137 @@ cudaError_t launch_pack(const PackLaunch& p, cudaStream_t st) {
   pack_hist_kernel<<<p.B, 64, 0, st>>>(p);
   pack_items_kernel<<<1, 1024, 0, st>>>(p);
   pack_fill_kernel<<<p.B, 64, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Fixed-shape ragged batches (CUDA graphs for any prefill / decode mix).  A
+// batch of B queries runs as a padded batch of Bc = bucket(B) queries whose
+// plan is built HERE from an uploaded input, so one captured graph per
+// (Bc, max k, max nprobe) replays for every mix -- the paper's fixed-shape
+// step (engine.py:208-226: round up with masked dummies).
+//   in[0] = B (real queries), in[1] unused, in[2 + 2 i] = k_i, in[3 + 2 i] = nprobe_i
+// Dummies (i >= B) carry k = 1, nprobe = 1 and a copy of query 0, and their
+// outputs stay in the padded workspace rows.
+
+__device__ __forceinline__ int ragged_kp(int k, const RaggedPlan& r) {
+  long long want;
+  if (r.f16) want = (long long)k + max(16LL, (long long)k / max(1, r.f16_div)) + r.kp_extra;
+  else want = (long long)k + (r.tc ? max(16LL, (long long)k) : max(16LL, (long long)k / 4)) + r.kp_extra;
+  int kp = kMinKp;
+  while (kp < want) kp <<= 1;
+  return kp;
+}
+
+__global__ void __launch_bounds__(1024) ragged_plan_kernel(RaggedPlan r) {
+  __shared__ long long s_warp[32];
+  __shared__ long long s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < r.Bc; base += 1024) {
+    const int i = base + tid;
+    int k = 0, np = 0, kp = 0;
+    if (i < r.Bc) {
+      k = r.in[2 + 2 * i];
+      np = r.in[3 + 2 * i];
+      kp = ragged_kp(k, r);
+    }
+    const long long keys = (long long)np * kp;
+    long long x = keys;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      long long v = s_warp[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      s_warp[lane] = v;
+    }
+    __syncthreads();
+    const long long before = s_carry + (warp ? s_warp[warp - 1] : 0) + x - keys;
+    if (i < r.Bc) {
+      QueryMeta m;
+      m.k = k;
+      m.kp = kp;
+      m.n_slots = np;
+      int c = 0;
+      while ((kMinKp << c) < kp) ++c;
+      m.cls = c;
+      m.part_off = before;
+      m.n_total = 0;
+      r.meta[i] = m;
+      r.nprobe[i] = np;
+    }
+    __syncthreads();
+    if (tid == 0) s_carry += s_warp[31];
+    __syncthreads();
+  }
+  if (tid == 0) *r.total_keys = s_carry;
+}
+
+cudaError_t launch_ragged_plan(const RaggedPlan& r, cudaStream_t st) {
+  ragged_plan_kernel<<<1, 1024, 0, st>>>(r);
+  return cudaGetLastError();
+}
+
+// Every partial-list key starts as "empty" (all ones); the count comes from the plan.
+__global__ void fill_keys_kernel(unsigned long long* __restrict__ p, const long long* __restrict__ count) {
+  const long long n = *count;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = ~0ull;
+}
+
+cudaError_t launch_fill_keys(unsigned long long* p, const long long* count, int grid, cudaStream_t st) {
+  fill_keys_kernel<<<grid, 512, 0, st>>>(p, count);
+  return cudaGetLastError();
+}
+
+// dst row i = src row i for i < B, src row 0 otherwise (B read on the device);
+// src == dst pads in place.
+__global__ void pad_rows_kernel(const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ nB,
+                                int Bc, int d) {
+  const int B = *nB;
+  const long long total = (long long)Bc * d;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / d, c = e - r * d;
+    if (r < B) {
+      if (src != dst) dst[e] = src[e];
+    } else {
+      dst[e] = src[c];
+    }
+  }
+}
+
+cudaError_t launch_pad_rows(const double* src, double* dst, const int* nB, int Bc, int d, cudaStream_t st) {
+  const long long total = (long long)Bc * d;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 1184);
+  pad_rows_kernel<<<grid, 256, 0, st>>>(src, dst, nB, Bc, d);
+  return cudaGetLastError();
+}
+
+// The first B rows (B read on the device) of a padded result into the caller's buffers.
+__global__ void copy_rows_kernel(const long long* __restrict__ si, const double* __restrict__ sd,
+                                 long long* __restrict__ di, double* __restrict__ dd, int ld, const int* __restrict__ nB) {
+  const long long total = (long long)(*nB) * ld;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    di[e] = si[e];
+    dd[e] = sd[e];
+  }
+}
+
+cudaError_t launch_copy_rows(const long long* si, const double* sd, long long* di, double* dd, int ld, int Bc,
+                             const int* nB, cudaStream_t st) {
+  const long long total = (long long)Bc * ld;
+  const int grid = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 592));
+  copy_rows_kernel<<<grid, 256, 0, st>>>(si, sd, di, dd, ld, nB);
   return cudaGetLastError();
 }
 
