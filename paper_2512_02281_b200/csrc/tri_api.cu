@@ -1165,9 +1165,19 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
 // fixed-shape padded batches (defined with graph_run)
 static int bucket_of(int B);
 static int ensure_padded(Workspace& w, int Bc, int d, int ldo);
-static int bf_padded(tri_store* s, Workspace& w, cudaStream_t st, int mode, const double* q_dev, int B, const int* k,
-                     int ldo, int64_t* out_ids, double* out_d);
+static int bf_padded(tri_store* s, Workspace& w, cudaStream_t st, int B, const int* k, int ldo);
+static int padded_in(Workspace& w, const double* q, int B, int Bc, int d, int ldo, cudaStream_t st);
+static int padded_out(Workspace& w, int B, int ldo, int64_t* ids, double* dists, cudaStream_t st);
 static bool pad_bf(int B, const int* k);
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 
 extern "C" {
 
@@ -1307,33 +1317,38 @@ int tri_knn_bruteforce(tri_store* s, const double* q, int32_t B, const int32_t* 
   int km = *std::max_element(k, k + B);
   if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
   TRY(check_queries(q, (long long)B * s->d));
-  std::lock_guard<std::mutex> lk(s->mu);
   DeviceGuard g(s->device);
   cudaStream_t st = pick(stream, s->own);
+  const size_t qb = (size_t)B * s->d * sizeof(double), ob = (size_t)B * ldo * sizeof(double);
+  void* dst_ids = ids;
+  void* dst_d = dists;
+  bool staged = false;
   Workspace* wp = nullptr;
+  {  // the store's lock covers the enqueue, not the wait (other lanes' threads overlap)
+  std::lock_guard<std::mutex> lk(s->mu);
   TRY(s->lanes.get(st, &wp));
   Workspace& w = *wp;
   if (pad_bf(B, k)) {
-    TRY(ensure_padded(w, bucket_of(B), s->d, ldo));
-    CU(cudaMemcpyAsync(w.qpad.p, q, (size_t)B * s->d * sizeof(double), cudaMemcpyHostToDevice, st));
-    TRY(bf_padded(s, w, st, 6, nullptr, B, k, ldo, nullptr, nullptr));
-    CU(cudaMemcpyAsync(ids, w.pad_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(dists, w.pad_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+    staged = !(host_pinned(ids) && host_pinned(dists));
+    if (staged) {
+      TRY(ensure_host(w.h_bids, ob));
+      TRY(ensure_host(w.h_bd, ob));
+      dst_ids = w.h_bids.p;
+      dst_d = w.h_bd.p;
+    }
+    TRY(padded_in(w, q, B, bucket_of(B), s->d, ldo, st));
+    TRY(bf_padded(s, w, st, B, k, ldo));
+    TRY(padded_out(w, B, ldo, static_cast<int64_t*>(dst_ids), static_cast<double*>(dst_d), st));
     TRY(lane_done(w, st));
-    CU(cudaStreamSynchronize(st));
-    return TRI_OK;
-  }
+  } else {
   w.pad_real = -1;
   TRY(ensure_query_bufs(w, B, s->d, s->qld));
   TRY(ensure(w.out_ids, (size_t)B * ldo * sizeof(long long)));
   TRY(ensure(w.out_d, (size_t)B * ldo * sizeof(double)));
-  const size_t qb = (size_t)B * s->d * sizeof(double), ob = (size_t)B * ldo * sizeof(double);
   // With graphs on, the caller's (pageable) buffers are copied through the
   // lane's pinned ones, so a repeated shape replays as one graph launch.
-  const bool staged = g_graphs != 0;
+  staged = g_graphs != 0;
   const void* qsrc = q;
-  void* dst_ids = ids;
-  void* dst_d = dists;
   if (staged) {
     TRY(ensure_host(w.h_bq, qb));
     TRY(ensure_host(w.h_bids, ob));
@@ -1355,10 +1370,13 @@ int tri_knn_bruteforce(tri_store* s, const double* q, int32_t B, const int32_t* 
     TRY(graph_run(nullptr, w, nullptr, st, 2, B, k, k, ldo, qsrc, dst_ids, dst_d, body));
   else
     TRY(body());
+  TRY(lane_done(w, st));
+  }
+  }
   CU(cudaStreamSynchronize(st));
   if (staged) {
-    std::memcpy(ids, w.h_bids.p, ob);
-    std::memcpy(dists, w.h_bd.p, ob);
+    std::memcpy(ids, dst_ids, ob);
+    std::memcpy(dists, dst_d, ob);
   }
   return TRI_OK;
 }
@@ -2063,14 +2081,6 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   return TRI_OK;
 }
 
-static bool host_pinned(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
-}
 
 long long graph_opts() {
   return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + g_bound_margin * 523 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_rerank_skip * 11 + tri::g_fx_slice_rows * 7919 +
@@ -2265,26 +2275,22 @@ static int ensure_padded(Workspace& w, int Bc, int d, int ldo) {
   return TRI_OK;
 }
 
-// One padded IVF search on st.  q_dev: the caller's device queries (B rows),
-// or nullptr when the B rows were already copied into w.qpad.  Results land in
-// w.pad_ids / w.pad_d; with out_ids set, the first B rows are copied there.
-static int ivf_padded(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, int mode, const double* q_dev, int B,
-                      const int* k, const int* np, int ldo, int64_t* out_ids, double* out_d) {
+// One padded IVF search on st: the B real query rows are already in w.qpad
+// (copied there on the stream, outside the graph), results land in the first B
+// rows of w.pad_ids / w.pad_d.  The graph touches only workspace buffers, so
+// its key is (bucket, max k, max nprobe) whatever the caller's pointers are.
+static int ivf_padded(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, int B, const int* k, const int* np,
+                      int ldo) {
   const int Bc = bucket_of(B);
   const int kmax = *std::max_element(k, k + B), npmax = *std::max_element(np, np + B);
   TRY(upload_ragged(w, B, Bc, k, np, st));
-  TRY(ensure_padded(w, Bc, v->d, ldo));
   TRY(ensure_query_bufs(w, Bc, v->d, v->qld));
   std::vector<int> kprof(Bc, kmax), npprof(Bc, npmax);
-  TRY(graph_run(v, w, cw, st, mode, Bc, &kmax, &npmax, ldo, q_dev, out_ids, out_d, [&]() -> int {
+  TRY(graph_run(v, w, cw, st, 3, Bc, &kmax, &npmax, ldo, nullptr, nullptr, nullptr, [&]() -> int {
     const int* nB = w.rplan.as<int>();
-    CU(launch_pad_rows(q_dev ? q_dev : w.qpad.as<double>(), w.qpad.as<double>(), nB, Bc, v->d, st));
-    TRY(ivf_search_body(v, w, cw, w.qpad.as<double>(), Bc, kprof.data(), npprof.data(), ldo,
-                        w.pad_ids.as<int64_t>(), w.pad_d.as<double>(), st, nB));
-    if (out_ids)
-      CU(launch_copy_rows(w.pad_ids.as<long long>(), w.pad_d.as<double>(), reinterpret_cast<long long*>(out_ids),
-                          out_d, ldo, Bc, nB, st));
-    return TRI_OK;
+    CU(launch_pad_rows(w.qpad.as<double>(), w.qpad.as<double>(), nB, Bc, v->d, st));
+    return ivf_search_body(v, w, cw, w.qpad.as<double>(), Bc, kprof.data(), npprof.data(), ldo,
+                           w.pad_ids.as<int64_t>(), w.pad_d.as<double>(), st, nB);
   }, 1));
   w.last_B = B;  // introspection (probes, scan bytes, fix-ups) sees the real batch
   w.last_np.assign(np, np + B);
@@ -2294,24 +2300,31 @@ static int ivf_padded(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, 
 }
 
 // Padded brute force (uniform k): as ivf_padded.
-static int bf_padded(tri_store* s, Workspace& w, cudaStream_t st, int mode, const double* q_dev, int B, const int* k,
-                     int ldo, int64_t* out_ids, double* out_d) {
+static int bf_padded(tri_store* s, Workspace& w, cudaStream_t st, int B, const int* k, int ldo) {
   const int Bc = bucket_of(B);
   TRY(upload_ragged(w, B, Bc, k, nullptr, st));
-  TRY(ensure_padded(w, Bc, s->d, ldo));
   TRY(ensure_query_bufs(w, Bc, s->d, s->qld));
   std::vector<int> kk(Bc, k[0]);
-  TRY(graph_run(nullptr, w, nullptr, st, mode, Bc, k, k, ldo, q_dev, out_ids, out_d, [&]() -> int {
+  TRY(graph_run(nullptr, w, nullptr, st, 5, Bc, k, k, ldo, nullptr, nullptr, nullptr, [&]() -> int {
     const int* nB = w.rplan.as<int>();
-    CU(launch_pad_rows(q_dev ? q_dev : w.qpad.as<double>(), w.qpad.as<double>(), nB, Bc, s->d, st));
-    TRY(bruteforce_core(s, w, w, w.qpad.as<double>(), Bc, kk.data(), ldo, w.pad_ids.as<long long>(),
-                        w.pad_d.as<double>(), st, true));
-    if (out_ids)
-      CU(launch_copy_rows(w.pad_ids.as<long long>(), w.pad_d.as<double>(), reinterpret_cast<long long*>(out_ids),
-                          out_d, ldo, Bc, nB, st));
-    return TRI_OK;
+    CU(launch_pad_rows(w.qpad.as<double>(), w.qpad.as<double>(), nB, Bc, s->d, st));
+    return bruteforce_core(s, w, w, w.qpad.as<double>(), Bc, kk.data(), ldo, w.pad_ids.as<long long>(),
+                           w.pad_d.as<double>(), st, true);
   }, 1));
   w.pad_real = B;
+  return TRI_OK;
+}
+
+// Around a padded search: the B query rows in (any memory kind), the B result rows out.
+static int padded_in(Workspace& w, const double* q, int B, int Bc, int d, int ldo, cudaStream_t st) {
+  TRY(ensure_padded(w, Bc, d, ldo));
+  CU(cudaMemcpyAsync(w.qpad.p, q, (size_t)B * d * sizeof(double), cudaMemcpyDefault, st));
+  return TRI_OK;
+}
+
+static int padded_out(Workspace& w, int B, int ldo, int64_t* ids, double* dists, cudaStream_t st) {
+  CU(cudaMemcpyAsync(ids, w.pad_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDefault, st));
+  CU(cudaMemcpyAsync(dists, w.pad_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDefault, st));
   return TRI_OK;
 }
 
@@ -2339,7 +2352,9 @@ int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32
   Workspace* w = nullptr;
   TRY(s->lanes.get(st, &w));
   if (pad_bf(B, k)) {
-    TRY(bf_padded(s, *w, st, 5, q, B, k, ldo, ids, dists));
+    TRY(padded_in(*w, q, B, bucket_of(B), s->d, ldo, st));
+    TRY(bf_padded(s, *w, st, B, k, ldo));
+    TRY(padded_out(*w, B, ldo, ids, dists, st));
     return lane_done(*w, st);
   }
   TRY(ensure_query_bufs(*w, B, s->d, s->qld));
@@ -2361,9 +2376,11 @@ int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k,
   Workspace* cw = nullptr;
   TRY(v->lanes.get(st, &wp));
   TRY(v->cstore->lanes.get(st, &cw));
-  if (pad_ivf(B, k, nprobe, true))
-    TRY(ivf_padded(v, *wp, cw, st, 3, q, B, k, nprobe, ldo, ids, dists));
-  else {
+  if (pad_ivf(B, k, nprobe, true)) {
+    TRY(padded_in(*wp, q, B, bucket_of(B), v->d, ldo, st));
+    TRY(ivf_padded(v, *wp, cw, st, B, k, nprobe, ldo));
+    TRY(padded_out(*wp, B, ldo, ids, dists, st));
+  } else {
     wp->pad_real = cw->pad_real = -1;
     TRY(graph_run(v, *wp, cw, st, 0, B, k, nprobe, ldo, q, ids, dists,
                   [&] { return ivf_search_body(v, *wp, cw, q, B, k, nprobe, ldo, ids, dists, st); }));
@@ -2379,6 +2396,9 @@ int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, con
   TRY(check_queries(q, (long long)B * v->d));
   DeviceGuard g(v->device);
   cudaStream_t st = pick(stream, v->own);
+  const size_t ob = (size_t)B * ldo * sizeof(double);
+  void* stage_ids = nullptr;
+  void* stage_d = nullptr;
   {
     std::lock_guard<std::mutex> lk(v->mu);
     Workspace* wp = nullptr;
@@ -2389,16 +2409,22 @@ int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, con
     const bool pinned = host_pinned(q) && host_pinned(ids) && host_pinned(dists);
     if (pad_ivf(B, k, nprobe, pinned)) {
       // queries straight into the padded buffer, one graph launch, results back
-      TRY(ensure_padded(w, bucket_of(B), v->d, ldo));
-      CU(cudaMemcpyAsync(w.qpad.p, q, (size_t)B * v->d * sizeof(double), cudaMemcpyHostToDevice, st));
-      TRY(ivf_padded(v, w, cw, st, 4, nullptr, B, k, nprobe, ldo, nullptr, nullptr));
-      CU(cudaMemcpyAsync(ids, w.pad_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
-      CU(cudaMemcpyAsync(dists, w.pad_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+      // (through the lane's pinned buffers when the caller's are pageable, so
+      // the index lock is never held across a wait)
+      int64_t* oi = ids;
+      double* od = dists;
+      if (!(host_pinned(ids) && host_pinned(dists))) {
+        TRY(ensure_host(w.h_bids, ob));
+        TRY(ensure_host(w.h_bd, ob));
+        oi = static_cast<int64_t*>(stage_ids = w.h_bids.p);
+        od = static_cast<double*>(stage_d = w.h_bd.p);
+      }
+      TRY(padded_in(w, q, B, bucket_of(B), v->d, ldo, st));
+      TRY(ivf_padded(v, w, cw, st, B, k, nprobe, ldo));
+      TRY(padded_out(w, B, ldo, oi, od, st));
       TRY(lane_done(*cw, st));
       TRY(lane_done(w, st));
-      CU(cudaStreamSynchronize(st));
-      return TRI_OK;
-    }
+    } else {
     w.pad_real = cw->pad_real = -1;
     TRY(ensure(w.q64, (size_t)B * v->d * sizeof(double)));
     TRY(ensure(w.out_ids, (size_t)B * ldo * sizeof(long long)));
@@ -2419,8 +2445,13 @@ int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, con
     }
     TRY(lane_done(*cw, st));
     TRY(lane_done(w, st));
+    }
   }
   CU(cudaStreamSynchronize(st));
+  if (stage_ids) {
+    std::memcpy(ids, stage_ids, ob);
+    std::memcpy(dists, stage_d, ob);
+  }
   return TRI_OK;
 }
 

@@ -306,8 +306,6 @@ struct RaggedPlan {
 cudaError_t launch_ragged_plan(const RaggedPlan& r, cudaStream_t st);
 cudaError_t launch_fill_keys(unsigned long long* p, const long long* count, int grid, cudaStream_t st);
 cudaError_t launch_pad_rows(const double* src, double* dst, const int* nB, int Bc, int d, cudaStream_t st);
-cudaError_t launch_copy_rows(const long long* si, const double* sd, long long* di, double* dd, int ld, int Bc,
-                             const int* nB, cudaStream_t st);
 cudaError_t launch_pack(const PackLaunch& p, cudaStream_t st);
 
 // k-means / index layout --------------------------------------------------------

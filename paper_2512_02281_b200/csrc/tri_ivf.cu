@@ -260,25 +260,6 @@ cudaError_t launch_pad_rows(const double* src, double* dst, const int* nB, int B
   return cudaGetLastError();
 }
 
-// The first B rows (B read on the device) of a padded result into the caller's buffers.
-__global__ void copy_rows_kernel(const long long* __restrict__ si, const double* __restrict__ sd,
-                                 long long* __restrict__ di, double* __restrict__ dd, int ld, const int* __restrict__ nB) {
-  const long long total = (long long)(*nB) * ld;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    di[e] = si[e];
-    dd[e] = sd[e];
-  }
-}
-
-cudaError_t launch_copy_rows(const long long* si, const double* sd, long long* di, double* dd, int ld, int Bc,
-                             const int* nB, cudaStream_t st) {
-  const long long total = (long long)Bc * ld;
-  const int grid = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 592));
-  copy_rows_kernel<<<grid, 256, 0, st>>>(si, sd, di, dd, ld, nB);
-  return cudaGetLastError();
-}
-
 // ---------------------------------------------------------------------------
 
 __global__ void counts_kernel(const int* __restrict__ assign, long long n, int* counts) {
