@@ -179,6 +179,14 @@ int tri_engine_submit_batch(tri_engine* e, const double* q, int32_t B, const int
 int tri_engine_device_time(tri_engine* e, double* ms, int64_t* steps);
 /* active_count / pending_admissions (engine.py:347-353). */
 int tri_engine_counts(tri_engine* e, int32_t* active, int32_t* pending);
+/* One active request's state (white-box; synchronises the engine stream):
+ * found = 0 if rid is not active.  top_d / top_i / top_e (capacity m) get the
+ * top-M list in (dist, id) order with expanded flags, visited (capacity
+ * ceil(n / 32) words) the visited bitmap (bit i of word i / 32 = row i);
+ * any output may be NULL.  Replaces reading ContinuousBatchEngine._active
+ * (engine.py:330, SearchRequestState engine.py:70-83). */
+int tri_engine_request_state(tri_engine* e, int64_t rid, int32_t* found, int32_t* n_top, double* top_d,
+                             int32_t* top_i, uint8_t* top_e, uint32_t* visited, int32_t* extends, int32_t* streak);
 /* Up to max_steps steps (engine.py:369-411); step 0 admits the pending
  * requests.  until_idle != 0 stops after the first step that leaves no
  * active request (run_to_completion, engine.py:413-422).  Per-step outputs

@@ -62,6 +62,7 @@ _SIGS = {
     "tri_engine_destroy": [_vp],
     "tri_engine_submit": [_vp, _vp, _i32, _i64p],
     "tri_engine_counts": [_vp, _i32p, _i32p],
+    "tri_engine_request_state": [_vp, _i64, _i32p, _i32p, _vp, _vp, _vp, _vp, _i32p, _i32p],
     "tri_engine_submit_batch": [_vp, _vp, _i32, _vp, _vp],
     "tri_engine_device_time": [_vp, _f64p, _i64p],
     "tri_engine_run": [_vp, _i32, _i32, _i32p, _vp, _vp, _vp],

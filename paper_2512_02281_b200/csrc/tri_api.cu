@@ -2,6 +2,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -1822,7 +1823,14 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   const int npmax = *std::max_element(nprobe, nprobe + B);
   TRY(ensure_query_bufs(w, B, v->d, v->qld));
   const bool rec = v->prof && v->ev_used < kProfSearches;
+  // NVTX ranges per pipeline stage (host enqueue; the device work of an eager
+  // search follows them, a replayed graph shows as one tri.graph.replay range)
+  static const char* kStageNames[6] = {"tri.ivf.coarse", "tri.ivf.plan_pack", "tri.ivf.scan", "tri.ivf.merge",
+                                       "tri.ivf.rerank", "tri.ivf.fixup"};
+  nvtxRangePushA("tri.ivf.prep");
   auto mark = [&](int j) -> int {
+    nvtxRangePop();
+    if (j < 6) nvtxRangePushA(kStageNames[j]);
     if (!rec) return TRI_OK;
     if (w.capturing) {  // event node; the launch points it at the profiling ring
       CU(cudaEventRecordWithFlags(w.cap_ph[j], st, cudaEventRecordExternal));
@@ -2156,6 +2164,10 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
   }
   if (e->state == 1) {
     // capture the second sighting of this shape
+    nvtxRangePushA("tri.graph.capture");
+    struct PopOnExit {
+      ~PopOnExit() { nvtxRangePop(); }
+    } pop_capture;
     TRY(ensure_host(e->host, (size_t)B * (sizeof(QueryMeta) + sizeof(int)) + 64));
     if (prof)
       for (auto& ev : e->ph)
@@ -2224,7 +2236,10 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
     for (int j = 0; j < 7; ++j)
       CU(cudaGraphExecEventRecordNodeSetEvent(e->exec, e->evnode[j], v->ev[7 * v->ev_used + j]));
   }
-  CU(cudaGraphLaunch(e->exec, st));
+  nvtxRangePushA("tri.graph.replay");
+  const cudaError_t le = cudaGraphLaunch(e->exec, st);
+  nvtxRangePop();
+  CU(le);
   ++g_gr_replayed;
   if (prof) v->ev_used++;
   return TRI_OK;

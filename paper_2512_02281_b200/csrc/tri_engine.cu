@@ -721,6 +721,40 @@ int tri_engine_device_time(tri_engine* e, double* ms, int64_t* steps) {
   return TRI_OK;
 }
 
+// White-box read of one active request's state (the reference's
+// SearchRequestState, engine.py:70-83): top-M (dist, id, expanded) in list
+// order, the visited bitmap, extends and no-change streak.  Synchronises the
+// engine stream; introspection only (the reference's tests read
+// ContinuousBatchEngine._active, test_engine.py:304-332).
+int tri_engine_request_state(tri_engine* e, int64_t rid, int32_t* found, int32_t* n_top, double* top_d,
+                             int32_t* top_i, uint8_t* top_e, uint32_t* visited, int32_t* extends, int32_t* streak) {
+  if (!e || !found) return set_error(TRI_EINVAL, "NULL argument");
+  *found = 0;
+  Guard g(e->sv.device);
+  ECU(cudaStreamSynchronize(e->st));
+  if (e->hw <= 0) return TRI_OK;
+  std::vector<int> st(e->hw);
+  std::vector<long long> rids(e->hw);
+  ECU(cudaMemcpy(st.data(), e->status, e->hw * sizeof(int), cudaMemcpyDeviceToHost));
+  ECU(cudaMemcpy(rids.data(), e->rid, e->hw * sizeof(long long), cudaMemcpyDeviceToHost));
+  int s = -1;
+  for (int i = 0; i < e->hw; ++i)
+    if (st[i] == kActive && rids[i] == rid) s = i;
+  if (s < 0) return TRI_OK;
+  int n = 0;
+  ECU(cudaMemcpy(&n, e->cnt + s, sizeof(int), cudaMemcpyDeviceToHost));
+  const long long b = (long long)s * e->m;
+  if (top_d) ECU(cudaMemcpy(top_d, e->topd + b, n * sizeof(double), cudaMemcpyDeviceToHost));
+  if (top_i) ECU(cudaMemcpy(top_i, e->topi + b, n * sizeof(int), cudaMemcpyDeviceToHost));
+  if (top_e) ECU(cudaMemcpy(top_e, e->tope + b, n * sizeof(unsigned char), cudaMemcpyDeviceToHost));
+  if (visited) ECU(cudaMemcpy(visited, e->vis + (long long)s * e->vw, e->vw * sizeof(unsigned), cudaMemcpyDeviceToHost));
+  if (extends) ECU(cudaMemcpy(extends, e->ext + s, sizeof(int), cudaMemcpyDeviceToHost));
+  if (streak) ECU(cudaMemcpy(streak, e->streak + s, sizeof(int), cudaMemcpyDeviceToHost));
+  if (n_top) *n_top = n;
+  *found = 1;
+  return TRI_OK;
+}
+
 int tri_engine_counts(tri_engine* e, int32_t* active, int32_t* pending) {
   if (!e) return set_error(TRI_EINVAL, "engine is NULL");
   if (active) *active = e->n_active;
