@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/pytest.log
-cd baseline/ref_tests && PYTHONPATH=$GRAFT_REPO_ROOT/tests:$GRAFT_REPO_ROOT timeout 900 python -m pytest -p trinity_alias -p no:cacheprovider -rA --rootdir . -c /dev/null test_ann_graph.py test_engine.py test_scheduler.py test_workload.py test_acceptance.py > $GRAFT_REPO_ROOT/gpurun_out/refsuite_full.log 2>&1; echo "rc=$?" >> $GRAFT_REPO_ROOT/gpurun_out/refsuite_full.log
+timeout 900 python -m pytest tests/test_gpu_bruteforce.py tests/test_gpu_padded.py -q -x > gpurun_out/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/pytest.log
+start=$(date +%s)
+timeout 1200 python bench.py --steps 20 --warmup 5 --full-out gpurun_out/full.json > gpurun_out/bench.log 2> gpurun_out/bench.err; echo "bench rc=$? wall=$(( $(date +%s) - start ))s" >> gpurun_out/bench.err

@@ -40,7 +40,9 @@ extern "C" {
 #define TRI_EINTERNAL 2
 #define TRI_ECUDA 3
 
-#define TRI_MAX_K 1638 /* largest k (or nprobe) the device path accepts */
+#define TRI_MAX_K 1638 /* largest k of the candidate-scan path: IVF k and nprobe are capped at it; brute force
+                        * beyond it runs the exhaustive path (every exact distance + a device radix sort),
+                        * so tri_knn_bruteforce accepts any k <= n like brute_force_knn (ann_graph.py:131) */
 
 typedef struct tri_store tri_store;
 typedef struct tri_ivf tri_ivf;

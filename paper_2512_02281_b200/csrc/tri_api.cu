@@ -283,6 +283,7 @@ struct Workspace {
   // fixed-shape padded batches: uploaded plan input, device key total, padded
   // queries and results
   DevBuf rplan, rtot, qpad, pad_ids, pad_d;
+  DevBuf exh;  // exhaustive large-k path: distance keys, rows, sort scratch
   int pad_real = -1;  // real queries of the last search when it ran padded (-1: not padded)
   HostBuf h_plan;
   HostBuf h_stage[kStaging];
@@ -404,7 +405,7 @@ struct Workspace {
   Workspace() {
     for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat,
                       &probes, &probe_d, &counts, &fill, &mbase, &items, &members, &counters, &meta, &Qh, &qinv,
-                      &gthr, &fxs, &Ql, &seedb, &rplan, &rtot, &qpad, &pad_ids, &pad_d})
+                      &gthr, &fxs, &Ql, &seedb, &rplan, &rtot, &qpad, &pad_ids, &pad_d, &exh})
       b->owner = &epoch;
   }
   Workspace(const Workspace&) = delete;
@@ -417,7 +418,7 @@ struct Workspace {
     plan_cache.clear();
     for (DevBuf* b : {&q64, &Q32, &qn32, &qn64, &flags, &plan, &part, &merged, &exact, &out_ids, &out_d, &dmat,
                       &probes, &probe_d, &counts, &fill, &mbase, &items, &members, &counters, &meta, &Qh, &qinv,
-                      &gthr, &fxs, &Ql, &seedb, &rplan, &rtot, &qpad, &pad_ids, &pad_d})
+                      &gthr, &fxs, &Ql, &seedb, &rplan, &rtot, &qpad, &pad_ids, &pad_d, &exh})
       release(*b);
     for (HostBuf* b : {&h_plan, &h_bq, &h_bids, &h_bd}) {
       if (b->p) cudaFreeHost(b->p);
@@ -1119,10 +1120,10 @@ int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Wo
   return TRI_OK;
 }
 
-int validate_k(const int* k, int B, long long limit, const char* what) {
+int validate_k(const int* k, int B, long long limit, const char* what, bool capped = true) {
   for (int i = 0; i < B; ++i) {
     if (k[i] < 1 || k[i] > limit) return fail(TRI_EINVAL, "%s must be in [1, %lld], got %d", what, limit, k[i]);
-    if (k[i] > TRI_MAX_K) return fail(TRI_EINVAL, "%s=%d exceeds the device limit %d", what, k[i], TRI_MAX_K);
+    if (capped && k[i] > TRI_MAX_K) return fail(TRI_EINVAL, "%s=%d exceeds the device limit %d", what, k[i], TRI_MAX_K);
   }
   return TRI_OK;
 }
@@ -1245,6 +1246,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "rerank_smem_cap")) tri::g_rerank_smem_cap = value;
   else if (!std::strcmp(name, "rerank_f2f")) tri::g_rerank_f2f = value;
   else if (!std::strcmp(name, "rerank_skip")) tri::g_rerank_skip = value;
+  else if (!std::strcmp(name, "pdl")) tri::g_pdl = value;
   else if (!std::strcmp(name, "fx_slice_rows")) {
     if (value < 32) return fail(TRI_EINVAL, "fx_slice_rows must be >= 32");
     tri::g_fx_slice_rows = value;
@@ -1309,15 +1311,48 @@ int tri_store_set_id_offset(tri_store* s, int64_t id_offset) {
   return TRI_OK;
 }
 
+// k beyond the candidate-scan capacity (brute_force_knn takes any k <= N,
+// ann_graph.py:131-133): every row's exact distance + a stable radix sort
+// (tri_exhaustive.cu), eager.  q64 is on the device.
+static int bruteforce_exhaustive(tri_store* s, Workspace& w, const double* q64, int B, const int* k, int ldo,
+                                 int64_t* ids, double* dists, cudaStream_t st) {
+  StoreView sv;
+  TRY(tri::store_view(s, &sv));
+  TRY(ensure(w.exh, exhaustive_scratch_bytes(s->n)));
+  CU(launch_exhaustive_knn(sv, s->id_offset, q64, B, k, ldo, reinterpret_cast<long long*>(ids), dists, w.exh.p, st));
+  return TRI_OK;
+}
+
 int tri_knn_bruteforce(tri_store* s, const double* q, int32_t B, const int32_t* k, int32_t ldo, int64_t* ids,
                        double* dists, void* stream) {
   if (!s) return fail(TRI_EINVAL, "store is NULL");
   if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
   if (B == 0) return TRI_OK;
-  TRY(validate_k(k, B, s->n, "k"));
+  TRY(validate_k(k, B, s->n, "k", false));
   int km = *std::max_element(k, k + B);
   if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
   TRY(check_queries(q, (long long)B * s->d));
+  if (km > TRI_MAX_K) {
+    DeviceGuard g(s->device);
+    cudaStream_t st = pick(stream, s->own);
+    {
+      std::lock_guard<std::mutex> lk(s->mu);
+      Workspace* wp = nullptr;
+      TRY(s->lanes.get(st, &wp));
+      TRY(ensure(wp->q64, (size_t)B * s->d * sizeof(double)));
+      TRY(ensure(wp->out_ids, (size_t)B * ldo * sizeof(long long)));
+      TRY(ensure(wp->out_d, (size_t)B * ldo * sizeof(double)));
+      wp->pad_real = -1;
+      CU(cudaMemcpyAsync(wp->q64.p, q, (size_t)B * s->d * sizeof(double), cudaMemcpyHostToDevice, st));
+      TRY(bruteforce_exhaustive(s, *wp, wp->q64.as<double>(), B, k, ldo, wp->out_ids.as<int64_t>(),
+                                wp->out_d.as<double>(), st));
+      CU(cudaMemcpyAsync(ids, wp->out_ids.p, (size_t)B * ldo * sizeof(long long), cudaMemcpyDeviceToHost, st));
+      CU(cudaMemcpyAsync(dists, wp->out_d.p, (size_t)B * ldo * sizeof(double), cudaMemcpyDeviceToHost, st));
+      TRY(lane_done(*wp, st));
+    }
+    CU(cudaStreamSynchronize(st));
+    return TRI_OK;
+  }
   DeviceGuard g(s->device);
   cudaStream_t st = pick(stream, s->own);
   const size_t qb = (size_t)B * s->d * sizeof(double), ob = (size_t)B * ldo * sizeof(double);
@@ -2092,7 +2127,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
 
 long long graph_opts() {
   return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + g_bound_margin * 523 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_rerank_skip * 11 + tri::g_fx_slice_rows * 7919 +
-         g_scan_debug * 100003 + g_pack_mixed * 104729 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
+         g_scan_debug * 100003 + tri::g_pdl * 7907 + g_pack_mixed * 104729 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
 }
 
 
@@ -2358,7 +2393,7 @@ int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32
   if (!s) return fail(TRI_EINVAL, "store is NULL");
   if (B < 0) return fail(TRI_EINVAL, "batch size must be >= 0");
   if (B == 0) return TRI_OK;
-  TRY(validate_k(k, B, s->n, "k"));
+  TRY(validate_k(k, B, s->n, "k", false));
   int km = *std::max_element(k, k + B);
   if (ldo < km) return fail(TRI_EINVAL, "ldo=%d < max k=%d", ldo, km);
   std::lock_guard<std::mutex> lk(s->mu);
@@ -2366,6 +2401,11 @@ int tri_knn_bruteforce_dev(tri_store* s, const double* q, int32_t B, const int32
   cudaStream_t st = pick(stream, s->own);
   Workspace* w = nullptr;
   TRY(s->lanes.get(st, &w));
+  if (*std::max_element(k, k + B) > TRI_MAX_K) {
+    w->pad_real = -1;
+    TRY(bruteforce_exhaustive(s, *w, q, B, k, ldo, ids, dists, st));
+    return lane_done(*w, st);
+  }
   if (pad_bf(B, k)) {
     TRY(padded_in(*w, q, B, bucket_of(B), s->d, ldo, st));
     TRY(bf_padded(s, *w, st, B, k, ldo));

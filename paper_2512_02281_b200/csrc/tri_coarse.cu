@@ -86,6 +86,7 @@ struct CoSmem {
 __global__ void __launch_bounds__(kCoThreads, 1) coarse_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                                                                    const __grid_constant__ CUtensorMap map_l,
                                                                    CoarseLaunch a) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(1024) unsigned char co_raw[];
   __shared__ CoSmem sh;
   unsigned char* base = co_raw + ((1024u - (csu32(co_raw) & 1023u)) & 1023u);
@@ -260,7 +261,7 @@ cudaError_t launch_coarse_tc(const CoarseLaunch& a0, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(coarse_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.n + kCoRows - 1) / kCoRows), (unsigned)((a.B + kCoN - 1) / kCoN), (unsigned)S);
-  coarse_tc_kernel<<<grid, kCoThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(a.map_h),
+  (void)launch_pdl(coarse_tc_kernel, grid, kCoThreads, smem, st, *reinterpret_cast<const CUtensorMap*>(a.map_h),
                                                    *reinterpret_cast<const CUtensorMap*>(a.map_l), a);
   return cudaGetLastError();
 }

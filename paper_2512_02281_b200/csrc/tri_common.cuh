@@ -14,6 +14,16 @@
 
 namespace tri {
 
+// Programmatic dependent launch (launch_pdl): a kernel's CTAs may start while
+// the previous kernel on the stream is finishing; griddepcontrol.wait blocks
+// until that kernel has completed and its writes are visible, and
+// launch_dependents lets the NEXT kernel begin launching as soon as every CTA
+// of this one is running.  Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t f2ord(float f) {
   uint32_t b = __float_as_uint(f);
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kGThreads) dense_gemm_kernel(const float* __re
                                                                const float* __restrict__ X, long long ldx, long long n,
                                                                int dp, int kslice, float* __restrict__ P,
                                                                long long ldd) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   __shared__ __align__(16) float Qs[2][kGk][kGq];
   __shared__ __align__(16) float Xs[2][kGk][kGr];
   const int tid = threadIdx.x;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(kSelThreads) dense_select_kernel(const float* 
                                                                    const QueryMeta* __restrict__ meta,
                                                                    unsigned long long* __restrict__ merged,
                                                                    int ld_merged) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   __shared__ unsigned long long cand[kSelCap];
   __shared__ int red[2][kSelThreads / 32];
   __shared__ int s_cnt;
@@ -253,7 +255,7 @@ cudaError_t launch_dense(const float* Q, int qld, const float* qn, int B, const 
   const int kslice = ((dp + nsl - 1) / nsl + kGk - 1) / kGk * kGk;
   const int used = (dp + kslice - 1) / kslice;
   dim3 grid((B + kGq - 1) / kGq, (unsigned)((n + kGr - 1) / kGr), used);
-  dense_gemm_kernel<<<grid, kGThreads, 0, st>>>(Q, qld, B, X, ldx, n, dp, kslice, D, ldd);
+  (void)launch_pdl(dense_gemm_kernel, grid, kGThreads, 0, st, Q, qld, B, X, ldx, n, dp, kslice, D, ldd);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_dense_select(D, used, ldd, B, qn, xn, n, meta, merged, ld_merged, kp_max, st);
@@ -264,7 +266,7 @@ cudaError_t launch_dense_select(const float* D, int nsl, long long ldd, int B, c
                                 int kp_max, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
   if (n > (long long)kSelThreads * kSelPer || kp_max > kSelCap / 2) return cudaErrorInvalidValue;
-  dense_select_kernel<<<B, kSelThreads, 0, st>>>(D, nsl, ldd, B, qn, xn, n, meta, merged, ld_merged);
+  (void)launch_pdl(dense_select_kernel, B, kSelThreads, 0, st, D, nsl, ldd, B, qn, xn, n, meta, merged, ld_merged);
   return cudaGetLastError();
 }
 

@@ -4,7 +4,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace tri {
+
+// Hot-path kernels launch with programmatic stream serialization (option
+// "pdl", default on): the launch of kernel N+1 overlaps the tail of kernel N;
+// every such kernel starts with pdl_wait() (tri_common.cuh).
+extern long long g_pdl;
+template <typename... P, typename... A>
+inline cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
 
 // One unit of scan work: a contiguous row range of a (list-major) vector
 // matrix scanned against a group of <= gmax queries that share a candidate
@@ -334,5 +355,10 @@ struct StoreView {
 struct tri_store;
 namespace tri {
 int store_view(const tri_store* s, StoreView* v);
+// Exhaustive exact kNN for k > TRI_MAX_K (tri_exhaustive.cu): exact distances to
+// every row + a stable radix sort by (dist, id); q64 is B x d on the device.
+size_t exhaustive_scratch_bytes(long long n);
+cudaError_t launch_exhaustive_knn(const StoreView& sv, long long id_offset, const double* q64, int B, const int* k,
+                                  int ldo, long long* ids, double* dists, void* scratch, cudaStream_t st);
 int set_error(int code, const char* fmt, ...);
 }  // namespace tri

@@ -19,6 +19,7 @@ namespace tri {
 // whichever group position the query lands.
 
 __global__ void pack_hist_kernel(PackLaunch p) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   const int q = blockIdx.x;
   const int np = p.nprobe[q];
   const int cls = p.mixed ? 0 : p.meta[q].cls;
@@ -41,6 +42,7 @@ __global__ void pack_hist_kernel(PackLaunch p) {
 }
 
 __global__ void __launch_bounds__(1024) pack_items_kernel(PackLaunch p) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   __shared__ int s_mem[32], s_grp[32];
   __shared__ int carry_mem, carry_grp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -119,6 +121,7 @@ __global__ void __launch_bounds__(1024) pack_items_kernel(PackLaunch p) {
 }
 
 __global__ void pack_fill_kernel(PackLaunch p) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   const int q = blockIdx.x;
   const int np = p.nprobe[q];
   const QueryMeta m = p.meta[q];
@@ -142,9 +145,9 @@ cudaError_t launch_pack(const PackLaunch& p, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(p.counts, 0, cbytes, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(p.fill, 0, cbytes, st);
   if (e != cudaSuccess) return e;
-  pack_hist_kernel<<<p.B, 64, 0, st>>>(p);
-  pack_items_kernel<<<1, 1024, 0, st>>>(p);
-  pack_fill_kernel<<<p.B, 64, 0, st>>>(p);
+  (void)launch_pdl(pack_hist_kernel, p.B, 64, 0, st, p);
+  (void)launch_pdl(pack_items_kernel, 1, 1024, 0, st, p);
+  (void)launch_pdl(pack_fill_kernel, p.B, 64, 0, st, p);
   return cudaGetLastError();
 }
 
@@ -168,6 +171,7 @@ __device__ __forceinline__ int ragged_kp(int k, const RaggedPlan& r) {
 }
 
 __global__ void __launch_bounds__(1024) ragged_plan_kernel(RaggedPlan r) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   __shared__ long long s_warp[32];
   __shared__ long long s_carry;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -220,19 +224,20 @@ __global__ void __launch_bounds__(1024) ragged_plan_kernel(RaggedPlan r) {
 }
 
 cudaError_t launch_ragged_plan(const RaggedPlan& r, cudaStream_t st) {
-  ragged_plan_kernel<<<1, 1024, 0, st>>>(r);
+  (void)launch_pdl(ragged_plan_kernel, 1, 1024, 0, st, r);
   return cudaGetLastError();
 }
 
 // Every partial-list key starts as "empty" (all ones); the count comes from the plan.
 __global__ void fill_keys_kernel(unsigned long long* __restrict__ p, const long long* __restrict__ count) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   const long long n = *count;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = ~0ull;
 }
 
 cudaError_t launch_fill_keys(unsigned long long* p, const long long* count, int grid, cudaStream_t st) {
-  fill_keys_kernel<<<grid, 512, 0, st>>>(p, count);
+  (void)launch_pdl(fill_keys_kernel, grid, 512, 0, st, p, count);
   return cudaGetLastError();
 }
 
@@ -240,6 +245,7 @@ cudaError_t launch_fill_keys(unsigned long long* p, const long long* count, int 
 // src == dst pads in place.
 __global__ void pad_rows_kernel(const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ nB,
                                 int Bc, int d) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   const int B = *nB;
   const long long total = (long long)Bc * d;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -256,7 +262,7 @@ __global__ void pad_rows_kernel(const double* __restrict__ src, double* __restri
 cudaError_t launch_pad_rows(const double* src, double* dst, const int* nB, int Bc, int d, cudaStream_t st) {
   const long long total = (long long)Bc * d;
   const int grid = (int)std::min<long long>((total + 255) / 256, 1184);
-  pad_rows_kernel<<<grid, 256, 0, st>>>(src, dst, nB, Bc, d);
+  (void)launch_pdl(pad_rows_kernel, grid, 256, 0, st, src, dst, nB, Bc, d);
   return cudaGetLastError();
 }
 

@@ -330,6 +330,7 @@ __device__ void scan_consumers(const ScanLaunch& a, ScanSmem& sh, const float* s
 
 __global__ void __launch_bounds__(kThreadsScan, 1) scan_tma_kernel(const __grid_constant__ CUtensorMap map,
                                                                    ScanLaunch a) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ ScanSmem sh;
   // 1024-byte aligned stage ring (64B swizzle atoms), then queries, then selection buffers
@@ -365,7 +366,7 @@ cudaError_t launch_scan(const ScanLaunch& s, cudaStream_t st) {
   const size_t smem = scan_smem_bytes(s.gmax, s.qld, s.cap);
   cudaError_t e = cudaFuncSetAttribute(scan_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  scan_tma_kernel<<<s.grid, kThreadsScan, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(s.tmap), s);
+  (void)launch_pdl(scan_tma_kernel, s.grid, kThreadsScan, smem, st, *reinterpret_cast<const CUtensorMap*>(s.tmap), s);
   return cudaGetLastError();
 }
 

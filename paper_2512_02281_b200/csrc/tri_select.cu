@@ -22,6 +22,7 @@ constexpr int kThreads = 256;
 long long g_rerank_smem_cap = 0;
 long long g_rerank_f2f = 1;
 long long g_rerank_skip = 1;
+long long g_pdl = 0;  // programmatic dependent launch of the hot kernels (option "pdl")
 long long g_fx_slice_rows = 256;
 
 // ---------------------------------------------------------------------------
@@ -39,6 +40,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const double* __rest
                                                             __half* __restrict__ Qh, int ldh,
                                                             float* __restrict__ qinv, __half* __restrict__ Ql,
                                                             ClearList cl) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   const int q = blockIdx.x, tid = threadIdx.x;
   // per-search counters / buffers the later kernels expect filled (instead of
   // one cudaMemsetAsync each)
@@ -122,7 +124,7 @@ cudaError_t launch_prep(const double* q64, int B, int d, float* Q32, int qld, fl
   if (qld > kPrepThreads * kPrepMaxU || (Qh && ldh > kPrepThreads * kPrepMaxU)) return cudaErrorInvalidValue;
   ClearList cl{};
   if (clears) cl = *clears;
-  prep_kernel<<<B, kPrepThreads, 0, st>>>(q64, d, Q32, qld, qn32, qn64, bad, sx, static_cast<__half*>(Qh), ldh,
+  (void)launch_pdl(prep_kernel, B, kPrepThreads, 0, st, q64, d, Q32, qld, qn32, qn64, bad, sx, static_cast<__half*>(Qh), ldh,
                                           qinv, static_cast<__half*>(Ql), cl);
   return cudaGetLastError();
 }
@@ -202,6 +204,7 @@ cudaError_t launch_to_half(const float* X, long long n, int d, long long ldx, fl
 // them, so the exact fix-up answers them.  All-zero queries are exact (s_q = 1).
 __global__ void prep_half_kernel(const float* __restrict__ Q32, int qld, int d, float sx, __half* __restrict__ Qh,
                                  int ldh, float* __restrict__ qinv) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   const int q = blockIdx.x;
   const float* row = Q32 + (long long)q * qld;
   float m = 0.f;
@@ -227,7 +230,7 @@ __global__ void prep_half_kernel(const float* __restrict__ Q32, int qld, int d, 
 cudaError_t launch_prep_half(const float* Q32, int B, int qld, int d, float sx, void* Qh, int ldh, float* qinv,
                              cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  prep_half_kernel<<<B, 128, 0, st>>>(Q32, qld, d, sx, static_cast<__half*>(Qh), ldh, qinv);
+  (void)launch_pdl(prep_half_kernel, B, 128, 0, st, Q32, qld, d, sx, static_cast<__half*>(Qh), ldh, qinv);
   return cudaGetLastError();
 }
 
@@ -258,6 +261,7 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(const unsigned long lon
                                                          const QueryMeta* __restrict__ meta,
                                                          unsigned long long* __restrict__ merged, int ld_merged,
                                                          int buf_n) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ unsigned long long buf[];
   __shared__ int s_cnt;
   __shared__ unsigned long long s_thr;
@@ -365,6 +369,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_tree_kernel(const unsi
                                                                       const QueryMeta* __restrict__ meta,
                                                                       unsigned long long* __restrict__ merged,
                                                                       int ld_merged) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ unsigned long long msm[];
   const int q = blockIdx.x;
   const QueryMeta m = meta[q];
@@ -416,6 +421,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_compact_kernel(const u
                                                                          const QueryMeta* __restrict__ meta,
                                                                          unsigned long long* __restrict__ merged,
                                                                          int ld_merged) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ unsigned long long msm[];
   const int q = blockIdx.x;
   const QueryMeta m = meta[q];
@@ -437,7 +443,7 @@ cudaError_t launch_merge_compact(const unsigned long long* part, const int* cnt,
   const size_t smem = (size_t)kMergeWarps * kp_max * sizeof(unsigned long long);
   cudaError_t e = cudaFuncSetAttribute(merge_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  merge_compact_kernel<<<B, 32 * kMergeWarps, smem, st>>>(part, cnt, meta, merged, ld_merged);
+  (void)launch_pdl(merge_compact_kernel, B, 32 * kMergeWarps, smem, st, part, cnt, meta, merged, ld_merged);
   return cudaGetLastError();
 }
 
@@ -448,14 +454,14 @@ cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, 
     const size_t smem = (size_t)kMergeWarps * kp_max * sizeof(unsigned long long);
     cudaError_t e = cudaFuncSetAttribute(merge_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    merge_tree_kernel<<<B, 32 * kMergeWarps, smem, st>>>(part, meta, merged, ld_merged);
+    (void)launch_pdl(merge_tree_kernel, B, 32 * kMergeWarps, smem, st, part, meta, merged, ld_merged);
     return cudaGetLastError();
   }
   int buf_n = next_pow2(kp_max + kThreads * 4);
   size_t smem = (size_t)buf_n * sizeof(unsigned long long);
   cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  merge_kernel<<<B, kThreads, smem, st>>>(part, meta, merged, ld_merged, buf_n);
+  (void)launch_pdl(merge_kernel, B, kThreads, smem, st, part, meta, merged, ld_merged, buf_n);
   return cudaGetLastError();
 }
 
@@ -476,6 +482,7 @@ constexpr int kPairSlab = 1024;  // floats
 __device__ __forceinline__ uint32_t sel_su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
 __global__ void __launch_bounds__(2 * kPairCands) exact_pairs_kernel(RerankLaunch r, int row_stride) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(16) unsigned char pair_smem[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ long long pos_s[kPairCands];
@@ -647,6 +654,7 @@ __device__ __forceinline__ void finalize_query(const RerankLaunch& r, int q, int
 }
 
 __global__ void __launch_bounds__(128) finalize_warp_kernel(RerankLaunch r) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   const int q = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (q >= r.B) return;
   const int lane = threadIdx.x & 31;
@@ -659,6 +667,7 @@ __global__ void __launch_bounds__(128) finalize_warp_kernel(RerankLaunch r) {
 }
 
 __global__ void __launch_bounds__(128) finalize_kernel(RerankLaunch r) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ Exact ebuf[];
   const int q = blockIdx.x;
   const QueryMeta m = r.meta[q];
@@ -748,6 +757,7 @@ __device__ __forceinline__ double f2d_bits(float x, bool& sub) {
 
 template <bool F2F>
 __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(16) unsigned char rf_smem[];
   __shared__ double s_dk;
   __shared__ __align__(8) uint64_t bars[2];
@@ -900,11 +910,11 @@ cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
     if (g_rerank_f2f) {
       cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      rerank_fused_kernel<true><<<r.B, 2 * r.kp_max, smem, st>>>(r, S);
+      (void)launch_pdl(rerank_fused_kernel<true>, r.B, 2 * r.kp_max, smem, st, r, S);
     } else {
       cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      rerank_fused_kernel<false><<<r.B, 2 * r.kp_max, smem, st>>>(r, S);
+      (void)launch_pdl(rerank_fused_kernel<false>, r.B, 2 * r.kp_max, smem, st, r, S);
     }
     return cudaGetLastError();
   }
@@ -913,17 +923,17 @@ cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
   const size_t smem = (size_t)slab * sizeof(double) + (size_t)kPairCands * row_stride * sizeof(float);
   cudaError_t e = cudaFuncSetAttribute(exact_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  exact_pairs_kernel<<<(unsigned)(r.B * (r.ld_merged / kPairCands)), 2 * kPairCands, smem, st>>>(r, row_stride);
+  (void)launch_pdl(exact_pairs_kernel, (unsigned)(r.B * (r.ld_merged / kPairCands)), 2 * kPairCands, smem, st, r, row_stride);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (r.kp_max <= 256) {
-    finalize_warp_kernel<<<(r.B + 3) / 4, 128, 0, st>>>(r);
+    (void)launch_pdl(finalize_warp_kernel, (r.B + 3) / 4, 128, 0, st, r);
     return cudaGetLastError();
   }
   const size_t fsm = (size_t)r.kp_max * sizeof(Exact);
   e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
   if (e != cudaSuccess) return e;
-  finalize_kernel<<<r.B, 128, fsm, st>>>(r);
+  (void)launch_pdl(finalize_kernel, r.B, 128, fsm, st, r);
   return cudaGetLastError();
 }
 
@@ -1024,6 +1034,7 @@ __device__ void fixup_merge_all(const FixupLaunch& f, int S, const Exact* part, 
                                 int* s_cnt, long long* s_w);
 
 __global__ void __launch_bounds__(kThreads) fixup_part_kernel(FixupLaunch f, int cap, Exact* part, int ldp) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ Exact fbuf[];
   __shared__ int s_cnt;
   __shared__ Exact s_thr;
@@ -1277,7 +1288,7 @@ cudaError_t launch_fixup(const FixupLaunch& f, cudaStream_t st) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  fixup_part_kernel<<<4 * nsm, kThreads, smem, st>>>(f, cap, f.scratch, f.k_max);
+  (void)launch_pdl(fixup_part_kernel, 4 * nsm, kThreads, smem, st, f, cap, f.scratch, f.k_max);
   return cudaGetLastError();
 }
 
@@ -1355,6 +1366,7 @@ __global__ void __launch_bounds__(kThreads) merge_exact_kernel(const double* __r
                                                                int k_in, int k_out, double* __restrict__ out_d,
                                                                long long* __restrict__ out_ids, int n2, int ld_in,
                                                                int ld_out, long long g_stride) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ Exact mbuf[];
   const int q = blockIdx.x;
   const int n = G * k_in;
@@ -1390,7 +1402,7 @@ cudaError_t launch_merge_exact(const double* dists, const long long* ids, int G,
   cudaError_t e =
       cudaFuncSetAttribute(merge_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  merge_exact_kernel<<<B, kThreads, smem, st>>>(dists, ids, G, B, k_in, k_out, out_d, out_ids, n2, ld_in, ld_out,
+  (void)launch_pdl(merge_exact_kernel, B, kThreads, smem, st, dists, ids, G, B, k_in, k_out, out_d, out_ids, n2, ld_in, ld_out,
                                                    g_stride);
   return cudaGetLastError();
 }

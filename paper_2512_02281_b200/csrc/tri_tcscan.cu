@@ -939,6 +939,7 @@ template <bool H, int N>
 __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_constant__ CUtensorMap map,
                                                                 const __grid_constant__ CUtensorMap tail,
                                                                 const __grid_constant__ CUtensorMap qmap, ScanLaunch a) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   constexpr int kTmemCols = tc_acc<N>() * N;  // power of two >= 32
   extern __shared__ __align__(1024) unsigned char tsmem_raw[];
   __shared__ TcSmem<N> sh;
@@ -1003,7 +1004,7 @@ cudaError_t launch_tc(const ScanLaunch& s, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel<H, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const CUtensorMap* qm = reinterpret_cast<const CUtensorMap*>(s.q_tma ? s.tmap_q : s.tmap_tc);
-  scan_tc_kernel<H, N><<<s.grid, kTcThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(s.tmap_tc),
+  (void)launch_pdl(scan_tc_kernel<H, N>, s.grid, kTcThreads, smem, st, *reinterpret_cast<const CUtensorMap*>(s.tmap_tc),
                                                          *reinterpret_cast<const CUtensorMap*>(s.tmap_tc_tail), *qm, s);
   return cudaGetLastError();
 }

@@ -265,3 +265,38 @@ def test_device_path_non_finite_query_rows(scan_kernel):
     for i in (0, 1, 3, 7):
         oi, od = orc.exact_knn(data, qs[i], 10)
         assert np.array_equal(hi[i], oi) and np.array_equal(hd[i], od)
+
+
+@pytest.mark.gpu
+def test_large_k_exhaustive_path():
+    """k beyond the candidate-scan capacity (TRI_MAX_K) runs the exhaustive
+    sort path: brute_force_knn accepts any k <= N (ann_graph.py:131-133),
+    including k = N (test_ann_graph.py:77-79)."""
+    import torch
+
+    from paper_2512_02281_b200 import _lib
+    from paper_2512_02281_b200.ann_graph import VectorStore, brute_force_knn, brute_force_knn_batch
+
+    rng = np.random.Generator(np.random.Philox(41))
+    data = rng.standard_normal((5000, 24)).astype(np.float32)
+    store = VectorStore(data=data)
+    q = rng.standard_normal((3, 24))
+    res = brute_force_knn(store, q[0], 5000)
+    oi, od = orc.exact_knn(data, q[0], 5000)
+    assert [n.id for n in res] == oi.tolist() and [n.dist for n in res] == od.tolist()
+    assert sorted(n.id for n in res) == list(range(5000))
+    ks = np.array([2000, 10, 4096])
+    ids, d = brute_force_knn_batch(store, q, ks)
+    for i in range(3):
+        oi, od = orc.exact_knn(data, q[i], int(ks[i]))
+        assert np.array_equal(ids[i, :ks[i]], oi) and np.array_equal(d[i, :ks[i]], od)
+        assert (ids[i, ks[i]:] == -1).all()
+    # device-buffer entry point
+    dev = store.device()
+    qd = torch.from_numpy(q).cuda()
+    di = torch.empty((3, 4096), dtype=torch.int64, device="cuda")
+    dd = torch.empty((3, 4096), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.gpu().tri_knn_bruteforce_dev(dev.handle, _lib.ptr(qd), 3, ks.astype(np.int32).ctypes.data, 4096,
+                                                 _lib.ptr(di), _lib.ptr(dd), None))
+    torch.cuda.synchronize()
+    assert np.array_equal(di.cpu().numpy(), ids) and np.array_equal(dd.cpu().numpy(), d)
