@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_bruteforce.py tests/test_gpu_padded.py -q -x > gpurun_out/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/pytest.log
-start=$(date +%s)
-timeout 1200 python bench.py --steps 20 --warmup 5 --full-out gpurun_out/full.json > gpurun_out/bench.log 2> gpurun_out/bench.err; echo "bench rc=$? wall=$(( $(date +%s) - start ))s" >> gpurun_out/bench.err
+TRI_GRAPHS=0 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv python tools/c2_profile.py --steps 3 > gpurun_out/c2_launches.csv 2>&1
+TRI_GRAPHS=0 timeout 1200 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:scan_tc -c 1 -o gpurun_out/c2_scan python tools/c2_profile.py --steps 1 > gpurun_out/c2_ncu.log 2>&1
+TRI_GRAPHS=0 timeout 1200 ncu --profile-from-start off --set full --clock-control none -c 12 -o gpurun_out/c2_step python tools/c2_profile.py --steps 1 > gpurun_out/c2_ncu_step.log 2>&1
