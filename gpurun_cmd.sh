@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-TRI_GRAPHS=0 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv python tools/c2_profile.py --steps 3 > gpurun_out/c2_launches.csv 2>&1
-TRI_GRAPHS=0 timeout 1200 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:scan_tc -c 1 -o gpurun_out/c2_scan python tools/c2_profile.py --steps 1 > gpurun_out/c2_ncu.log 2>&1
-TRI_GRAPHS=0 timeout 1200 ncu --profile-from-start off --set full --clock-control none -c 12 -o gpurun_out/c2_step python tools/c2_profile.py --steps 1 > gpurun_out/c2_ncu_step.log 2>&1
+timeout 900 python tools/bench_engine.py --n 2000000 --d 128 --nq 4096 --reps 3 --graph random > gpurun_out/engine_hbm.json 2> gpurun_out/engine_hbm.err
+timeout 900 python tools/bench_engine.py --n 100000 --d 128 --nq 4096 --reps 3 --graph random > gpurun_out/engine_l2_random.json 2>> gpurun_out/engine_hbm.err
+TRI_GRAPHS=0 timeout 900 ncu --set full --clock-control none -k regex:engine_step -s 5 -c 1 -o gpurun_out/engine_hbm python tools/bench_engine.py --n 2000000 --d 128 --nq 4096 --reps 1 --graph random > gpurun_out/engine_ncu.log 2>&1
