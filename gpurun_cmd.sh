@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python tools/bench_engine.py --n 2000000 --d 128 --nq 4096 --reps 3 --graph random > gpurun_out/engine_hbm.json 2> gpurun_out/engine_hbm.err
-timeout 900 python tools/bench_engine.py --n 100000 --d 128 --nq 4096 --reps 3 --graph random > gpurun_out/engine_l2_random.json 2>> gpurun_out/engine_hbm.err
-TRI_GRAPHS=0 timeout 900 ncu --set full --clock-control none -k regex:engine_step -s 5 -c 1 -o gpurun_out/engine_hbm python tools/bench_engine.py --n 2000000 --d 128 --nq 4096 --reps 1 --graph random > gpurun_out/engine_ncu.log 2>&1
+timeout 300 python tools/c1_experiment.py "" "" > gpurun_out/c1.log 2>&1
+TRI_GRAPHS=0 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 300 -c 8 --csv python tools/c1_experiment.py > gpurun_out/c1_launches.csv 2>&1
+timeout 900 python -m pytest tests/test_gpu_bruteforce.py -q -x > gpurun_out/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/pytest.log

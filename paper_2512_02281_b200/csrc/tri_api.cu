@@ -909,7 +909,8 @@ int ensure_query_bufs(Workspace& w, int B, int d, int qld) {
 }
 
 int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Workspace& qw, const QueryMeta* meta,
-                      int B, int ldo, long long* ids, double* dists, int mode, cudaStream_t st);
+                      int B, int ldo, long long* ids, double* dists, int mode, cudaStream_t st,
+                      const unsigned long long* part = nullptr, const int* compact_cnt = nullptr);
 
 // Dense small-store brute force: distance matrix + warp select -> merged.
 int dense_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q64dev, int B, int ldo, long long* ids,
@@ -1037,18 +1038,18 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
                         : cudaMemsetAsync(cl.p[r], 0xff, (size_t)cl.words[r] * 4, st));
   }
   CU(w.tc ? launch_scan_tc(sl, st) : launch_scan(sl, st));
-  if (sl.compact_cnt)
-    CU(launch_merge_compact(w.part.as<unsigned long long>(), sl.compact_cnt, meta, w.merged.as<unsigned long long>(),
-                            w.kp_max, B, w.kp_max, st));
-  else
-    CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
-                    st));
+  if (sl.compact_cnt)  // the compact lists are merged by the re-rank kernel itself
+    return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, w.tc ? kTf32 : kSimt, st,
+                             w.part.as<unsigned long long>(), sl.compact_cnt);
+  CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
+                  st));
   return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, w.tc ? kTf32 : kSimt, st);
 }
 
 // Exact re-rank + certification + fix-up shared by the scan and dense paths.
 int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Workspace& qw, const QueryMeta* meta,
-                      int B, int ldo, long long* ids, double* dists, int mode, cudaStream_t st) {
+                      int B, int ldo, long long* ids, double* dists, int mode, cudaStream_t st,
+                      const unsigned long long* part, const int* compact_cnt) {
   int* n_flag = w.flags.as<int>();
   int* flag_list = n_flag + 64;
   RerankLaunch rr{};
@@ -1078,6 +1079,8 @@ int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Wo
   rr.flag_list = flag_list;
   rr.B = B;
   rr.kp_max = w.kp_max;
+  rr.part = part;
+  rr.compact_cnt = compact_cnt;
   CU(launch_rerank(rr, st));
   FixupLaunch fx;
   fx.n_flag = n_flag;

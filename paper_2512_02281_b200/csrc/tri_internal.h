@@ -234,6 +234,10 @@ struct RerankLaunch {
   int B;
   int kp_max;
   const float* qinv;        // fp16 scan: qinv[q] < 0 marks a query the scan could not scale (never certified)
+  // brute force with a cross-item seed: the scan's unsorted compact lists
+  // (cnt[q] keys at part + part_off); the re-rank merges them itself
+  const unsigned long long* part;
+  const int* compact_cnt;
 };
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st);
 extern long long g_rerank_smem_cap;  // bytes; 0 = no cap

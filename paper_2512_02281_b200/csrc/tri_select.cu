@@ -416,6 +416,52 @@ __device__ __forceinline__ void merge_compact(const unsigned long long* __restri
   }
 }
 
+// The same merge by the first `nw` warps of a CTA (nw a power of two, every
+// thread of the CTA calls it): the fused re-rank's prologue.
+template <int KL>
+__device__ __forceinline__ void merge_compact_nw(const unsigned long long* __restrict__ src, int n,
+                                                 unsigned long long* __restrict__ dst, unsigned long long* sm, int nw) {
+  constexpr int KP = 32 * KL;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long L[KL];
+#pragma unroll
+  for (int j = 0; j < KL; ++j) L[j] = TRI_KEY_MAX;
+  if (warp < nw) {
+    // every load of a round of 8 folds in flight before the first fold (the
+    // keys come from L2: one latency per round instead of one per fold)
+    constexpr int kPf = 8;
+    for (int b0 = warp * 32; b0 < n; b0 += kPf * 32 * nw) {
+      unsigned long long kb[kPf];
+#pragma unroll
+      for (int j = 0; j < kPf; ++j) {
+        const int b = b0 + j * 32 * nw + lane;
+        kb[j] = b < n ? __ldcg(src + b) : TRI_KEY_MAX;
+      }
+#pragma unroll
+      for (int j = 0; j < kPf; ++j)
+        if (b0 + j * 32 * nw < n) list_fold32<KL>(L, kb[j], lane);
+    }
+  }
+  for (int stride = 1; stride < nw; stride <<= 1) {
+    if (warp < nw && (warp & (2 * stride - 1)) == stride) {
+#pragma unroll
+      for (int j = 0; j < KL; ++j) sm[warp * KP + j * 32 + lane] = L[j];
+    }
+    __syncthreads();
+    if (warp < nw && (warp & (2 * stride - 1)) == 0 && warp + stride < nw && stride * 32 < n) {
+      unsigned long long R[KL];
+#pragma unroll
+      for (int j = 0; j < KL; ++j) R[j] = sm[(warp + stride) * KP + (KL - 1 - j) * 32 + (31 - lane)];
+      list_merge_rev<KL>(L, R, lane);
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+#pragma unroll
+    for (int j = 0; j < KL; ++j) dst[j * 32 + lane] = L[j];
+  }
+}
+
 __global__ void __launch_bounds__(32 * kMergeWarps) merge_compact_kernel(const unsigned long long* __restrict__ part,
                                                                          const int* __restrict__ cnt,
                                                                          const QueryMeta* __restrict__ meta,
@@ -768,10 +814,30 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
   double* qs = reinterpret_cast<double*>(rf_smem);       // dpad
   double* exd = qs + dpad;                               // kp_max
   long long* exi = reinterpret_cast<long long*>(exd + kpm);
-  float* ring = reinterpret_cast<float*>(exi + kpm);     // 2 x kp_max x (S + 4)
+  unsigned long long* mk = reinterpret_cast<unsigned long long*>(exi + kpm);  // kp_max (fused merge)
+  float* ring = reinterpret_cast<float*>(mk + kpm);      // 2 x kp_max x (S + 4)
   const int tid = threadIdx.x, nthr = blockDim.x, c = tid >> 1, ln = tid & 1;
+  // the query's sorted candidate list: the merge kernel's output, or (brute
+  // force with a cross-item seed) merged right here from the scan's compact
+  // region -- one launch and one global round trip less
+  const unsigned long long* mrow = r.merged + (long long)q * r.ld_merged;
+  if (r.compact_cnt) {
+    const int n = min(r.compact_cnt[q], m.n_slots * kp);
+    const unsigned long long* src = r.part + m.part_off;
+    unsigned long long* scratch = reinterpret_cast<unsigned long long*>(ring);  // free until the first slab
+    const int nw = min(nthr >> 5, 8);
+    switch (kp) {
+      case 32: merge_compact_nw<1>(src, n, mk, scratch, nw); break;
+      case 64: merge_compact_nw<2>(src, n, mk, scratch, nw); break;
+      case 128: merge_compact_nw<4>(src, n, mk, scratch, nw); break;
+      default: merge_compact_nw<8>(src, n, mk, scratch, nw); break;
+    }
+    __syncthreads();
+    for (int i = tid; i < kp; i += nthr) const_cast<unsigned long long*>(r.merged)[(long long)q * r.ld_merged + i] = mk[i];
+    mrow = mk;
+  }
   unsigned long long key = TRI_KEY_MAX;
-  if (c < kp) key = r.merged[(long long)q * r.ld_merged + c];
+  if (c < kp) key = mrow[c];
   bool active = key != TRI_KEY_MAX;
   // A candidate whose approx key exceeds the k-th approx key by more than 2E
   // cannot enter the exact top-k.  Its exact distance is > approx(k) + E >= D_k,
@@ -779,7 +845,7 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
   // row is neither loaded nor computed.  (merged is sorted; unscalable fp16
   // queries keep every candidate.)
   if (active && r.skip_far && m.k < kp && !(r.qinv && r.qinv[q] < 0.f)) {
-    const unsigned long long kk = r.merged[(long long)q * r.ld_merged + m.k - 1];
+    const unsigned long long kk = mrow[m.k - 1];
     const double sn = r.qn64[q] + r.xmax;
     const double E = (r.cdot * 2.0 * r.qn64[q] * r.xmax + r.csum * sn * sn) * 1.001 + 1e-30;
     if (kk != TRI_KEY_MAX && (double)key_dist(key) > (double)key_dist(kk) + 2.0 * E) active = false;
@@ -888,7 +954,7 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
   if (tid == 0) {
     bool cert = true;
     if (m.n_total > kp) {
-      cert = certified(r, q, s_dk, (double)key_dist(r.merged[(long long)q * r.ld_merged + kp - 1]));
+      cert = certified(r, q, s_dk, (double)key_dist(mrow[kp - 1]));
     }
     if (!cert || isnan(r.qn64[q])) flag_query(r, q, s_dk);
   }
@@ -903,20 +969,28 @@ cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
     const long long fit = (g_rerank_smem_cap - fixed) / (2LL * r.kp_max * 4) - 4;
     S = (int)std::max<long long>(32, std::min<long long>(S, fit / 16 * 16));
   }
-  const size_t rf_smem = (size_t)((r.d + 15) & ~15) * sizeof(double) + (size_t)r.kp_max * 16 +
-                         (size_t)2 * r.kp_max * (S + 4) * sizeof(float);
+  // a fused compact merge gets 8 warps (the distance phase uses 2 threads per candidate)
+  const int rf_threads = r.compact_cnt ? std::max(2 * r.kp_max, 256) : 2 * r.kp_max;
+  const size_t rf_smem = (size_t)((r.d + 15) & ~15) * sizeof(double) + (size_t)r.kp_max * 24 +
+                         std::max((size_t)2 * r.kp_max * (S + 4) * sizeof(float),
+                                  (size_t)std::min(8, rf_threads / 32) * r.kp_max * 8);
   if (r.kp_max <= 256 && rf_smem <= 200 * 1024) {
     const size_t smem = rf_smem;
     if (g_rerank_f2f) {
       cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      (void)launch_pdl(rerank_fused_kernel<true>, r.B, 2 * r.kp_max, smem, st, r, S);
+      (void)launch_pdl(rerank_fused_kernel<true>, r.B, rf_threads, smem, st, r, S);
     } else {
       cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      (void)launch_pdl(rerank_fused_kernel<false>, r.B, 2 * r.kp_max, smem, st, r, S);
+      (void)launch_pdl(rerank_fused_kernel<false>, r.B, rf_threads, smem, st, r, S);
     }
     return cudaGetLastError();
+  }
+  if (r.compact_cnt) {  // the pair kernels read merged lists: merge first
+    cudaError_t me = launch_merge_compact(r.part, r.compact_cnt, r.meta, const_cast<unsigned long long*>(r.merged),
+                                          r.ld_merged, r.B, r.kp_max, st);
+    if (me != cudaSuccess) return me;
   }
   const int slab = std::min(kPairSlab, (r.d + 15) & ~15);
   const int row_stride = slab + 4;  // floats; 16B-aligned rows, 2-way worst bank conflict

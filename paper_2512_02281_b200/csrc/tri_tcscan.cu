@@ -670,35 +670,51 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
       const float* mnb = reinterpret_cast<const float*>(sel);
       unsigned long long* sb = sel + 4096;
       const unsigned long long* thr_nv = sh.thr;  // fixed during this pass: loads may be hoisted
+      // four query columns at a time: one x4 TMEM load per resident chunk and
+      // ONE wait per group (a warp almost always has some lane passing a
+      // column's bound, so per-column loads serialised 32 waits per item)
 #pragma unroll 1
-      for (int j = 0; j < QPT; ++j) {
-        const int g = half * QPT + j;
-        const unsigned long long tk = thr_nv[g];
-        const bool hit = g < gc && !(mnb[j * 256 + e] > ord2f((uint32_t)(tk >> 32)));
-        if (!__any_sync(0xffffffffu, hit)) continue;
-        uint32_t col[kTcWideMaxChunks];
-        const uint32_t cbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * QPT + j);
+      for (int j0 = 0; j0 < QPT; j0 += 4) {
+        bool hit[4];
+        unsigned long long tk[4];
+        bool any = false;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int g = half * QPT + j0 + t;
+          tk[t] = thr_nv[g];
+          hit[t] = g < gc && !(mnb[(j0 + t) * 256 + e] > ord2f((uint32_t)(tk[t] >> 32)));
+          any |= hit[t];
+        }
+        if (!__any_sync(0xffffffffu, any)) continue;
+        uint32_t col[kTcWideMaxChunks][4];
+        const uint32_t cbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * QPT + j0);
 #pragma unroll
         for (int c = 0; c < kTcWideMaxChunks; ++c) {
-          col[c] = 0u;
+          col[c][0] = col[c][1] = col[c][2] = col[c][3] = 0u;
           if (c < nchunk)
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n"
-                         : "=r"(col[c])
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                         : "=r"(col[c][0]), "=r"(col[c][1]), "=r"(col[c][2]), "=r"(col[c][3])
                          : "r"(cbase + (uint32_t)(((acc + c) & (kTcWideMaxChunks - 1)) * N)));
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (!hit) continue;
-        const float qng = sh.qn[g];
-        const float qig = sh.qinv[g];
+        if (!any) continue;
 #pragma unroll
-        for (int c = 0; c < kTcWideMaxChunks; ++c) {
-          if (c < nchunk && c * kTcRows + row_in_chunk < w.row_count) {
-            const float dot = H ? __uint_as_float(col[c]) * qig : __uint_as_float(col[c]);
-            const float d = __fmaf_rn(-2.f, dot, __fadd_rn(qng, sh.xns[c * kTcRows + row_in_chunk]));
-            const unsigned long long key = make_key(d, (uint32_t)(w.row_begin + (long long)c * kTcRows + row_in_chunk));
-            if (key < tk) {
-              const int slot = atomicAdd(&sh.cnt[0][g], 1);
-              if (slot < kApp) sb[g * kApp + slot] = key;
+        for (int t = 0; t < 4; ++t) {
+          if (!hit[t]) continue;
+          const int g = half * QPT + j0 + t;
+          const float qng = sh.qn[g];
+          const float qig = sh.qinv[g];
+#pragma unroll
+          for (int c = 0; c < kTcWideMaxChunks; ++c) {
+            if (c < nchunk && c * kTcRows + row_in_chunk < w.row_count) {
+              const float dot = H ? __uint_as_float(col[c][t]) * qig : __uint_as_float(col[c][t]);
+              const float d = __fmaf_rn(-2.f, dot, __fadd_rn(qng, sh.xns[c * kTcRows + row_in_chunk]));
+              const unsigned long long key =
+                  make_key(d, (uint32_t)(w.row_begin + (long long)c * kTcRows + row_in_chunk));
+              if (key < tk[t]) {
+                const int slot = atomicAdd(&sh.cnt[0][g], 1);
+                if (slot < kApp) sb[g * kApp + slot] = key;
+              }
             }
           }
         }
