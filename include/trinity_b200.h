@@ -139,7 +139,11 @@ int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, con
                    int64_t* ids, double* dists, void* stream);
 int tri_ivf_search_dev(tri_ivf* v, const double* q, int32_t B, const int32_t* k, const int32_t* nprobe,
                        int32_t ldo, int64_t* ids, double* dists, void* stream);
-/* Probed list ids of the last search (B x ld, host), for inspection. */
+/* Probed list ids of the last search (B x ld, host), for inspection: the
+ * exact top-nprobe SET of centroids by (dist, id) (brute_force_knn over the
+ * centroids, ann_graph.py:124-137).  The fine step scans their union, so with
+ * option coarse_set (default) the set comes in approximate-distance order;
+ * coarse_set = 0 returns the exact (dist, id) order. */
 int tri_ivf_last_probes(tri_ivf* v, int64_t* probes, int32_t ld);
 /* Queries of the last search that needed the exact fix-up (host int). */
 int tri_ivf_last_fixups(tri_ivf* v, int32_t* n);

@@ -129,7 +129,8 @@ long long g_bf_wide = 1;      // brute force: 64-query groups (one row pass per 
 long long g_bf_seed = 2;      // ... with the TMEM seed pass (tri_tcscan.cu tc_seed_pass): 1 per item, 2 cross-item
 long long g_bf_qtma = 1;      // ... and TMA-loaded query tiles
 std::atomic<long long> g_gr_eager{0}, g_gr_captured{0}, g_gr_replayed{0};  // graph_run outcomes
-long long g_ragged_graphs = 1;  // ragged / odd-sized batches replay fixed-shape padded graphs (option "ragged_graphs")
+long long g_ragged_graphs = 1;
+long long g_coarse_set = 1;  // IVF coarse step: exact distances only where top-nprobe membership is open  // ragged / odd-sized batches replay fixed-shape padded graphs (option "ragged_graphs")
 
 
 // Candidate capacity: over-fetch so the certified re-rank almost never falls
@@ -910,11 +911,12 @@ int ensure_query_bufs(Workspace& w, int B, int d, int qld) {
 
 int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Workspace& qw, const QueryMeta* meta,
                       int B, int ldo, long long* ids, double* dists, int mode, cudaStream_t st,
-                      const unsigned long long* part = nullptr, const int* compact_cnt = nullptr);
+                      const unsigned long long* part = nullptr, const int* compact_cnt = nullptr,
+                      bool set_only = false);
 
 // Dense small-store brute force: distance matrix + warp select -> merged.
 int dense_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q64dev, int B, int ldo, long long* ids,
-               double* dists, cudaStream_t st) {
+               double* dists, cudaStream_t st, bool set_only) {
   const long long ldd = (s->n + 3) & ~3LL;
   TRY(ensure(w.dmat, (size_t)kDenseSlices * B * ldd * sizeof(float)));
   TRY(ensure(w.merged, (size_t)B * w.kp_max * sizeof(unsigned long long)));
@@ -939,11 +941,11 @@ int dense_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q6
     CU(launch_coarse_tc(c, st));
     CU(launch_dense_select(w.dmat.as<float>(), coarse_tc_slices(c.nslab), ldd, B, qw.qn32.as<float>(), s->xnorm, s->n, meta,
                            w.merged.as<unsigned long long>(), w.kp_max, w.kp_max, st));
-    return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, kSplit, st);
+    return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, kSplit, st, nullptr, nullptr, set_only);
   }
   CU(launch_dense(qw.Q32.as<float>(), s->qld, qw.qn32.as<float>(), B, s->X, s->dp, s->xnorm, s->n, s->dp,
                   w.dmat.as<float>(), ldd, meta, w.merged.as<unsigned long long>(), w.kp_max, w.kp_max, st));
-  return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, kSimt, st);
+  return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, kSimt, st, nullptr, nullptr, set_only);
 }
 
 int prep_queries(Workspace& w, const double* q64dev, int B, int d, int qld, cudaStream_t st);
@@ -952,11 +954,11 @@ int prep_queries(Workspace& w, const double* q64dev, int B, int d, int qld, cuda
 // q64dev into `w` first (w == qw), otherwise they are prepared in `qw`
 // (Q32/qn32/qn64).  Results to device ids/dists with row stride ldo.
 int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const double* q64dev, int B, const int* k,
-                    int ldo, long long* ids, double* dists, cudaStream_t st, bool prep) {
+                    int ldo, long long* ids, double* dists, cudaStream_t st, bool prep, bool set_only = false) {
   TRY(plan_bruteforce(s, w, B, k, st));
   if (w.dense) {
     if (prep) TRY(prep_queries(w, q64dev, B, s->d, s->qld, st));
-    return dense_core(s, w, qw, q64dev, B, ldo, ids, dists, st);
+    return dense_core(s, w, qw, q64dev, B, ldo, ids, dists, st, set_only);
   }
   TRY(ensure(w.part, (size_t)w.part_keys * sizeof(unsigned long long)));
   TRY(ensure(w.merged, (size_t)B * w.kp_max * sizeof(unsigned long long)));
@@ -1043,13 +1045,14 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
                              w.part.as<unsigned long long>(), sl.compact_cnt);
   CU(launch_merge(w.part.as<unsigned long long>(), meta, w.merged.as<unsigned long long>(), w.kp_max, B, w.kp_max,
                   st));
-  return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, w.tc ? kTf32 : kSimt, st);
+  return finish_bruteforce(s, w, q64dev, qw, meta, B, ldo, ids, dists, w.tc ? kTf32 : kSimt, st, nullptr, nullptr,
+                           set_only);
 }
 
 // Exact re-rank + certification + fix-up shared by the scan and dense paths.
 int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Workspace& qw, const QueryMeta* meta,
                       int B, int ldo, long long* ids, double* dists, int mode, cudaStream_t st,
-                      const unsigned long long* part, const int* compact_cnt) {
+                      const unsigned long long* part, const int* compact_cnt, bool set_only) {
   int* n_flag = w.flags.as<int>();
   int* flag_list = n_flag + 64;
   RerankLaunch rr{};
@@ -1081,7 +1084,12 @@ int finish_bruteforce(tri_store* s, Workspace& w, const double* q64dev, const Wo
   rr.kp_max = w.kp_max;
   rr.part = part;
   rr.compact_cnt = compact_cnt;
-  CU(launch_rerank(rr, st));
+  rr.xnorm = s->xnorm;
+  // the IVF coarse step needs only the top-nprobe SET (coarse_set_kernel)
+  if (set_only && g_coarse_set && !compact_cnt && w.kp_max <= 256 && s->d <= 1024)
+    CU(launch_coarse_set(rr, st));
+  else
+    CU(launch_rerank(rr, st));
   FixupLaunch fx;
   fx.n_flag = n_flag;
   fx.flag_list = flag_list;
@@ -1234,6 +1242,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "bf_seed")) g_bf_seed = value;
   else if (!std::strcmp(name, "bf_qtma")) g_bf_qtma = value;
   else if (!std::strcmp(name, "ragged_graphs")) g_ragged_graphs = value;
+  else if (!std::strcmp(name, "coarse_set")) g_coarse_set = value;
   else if (!std::strcmp(name, "dense_pow2")) g_dense_pow2 = value;
 
   else if (!std::strcmp(name, "coarse_split")) {
@@ -1915,7 +1924,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
   TRY(ensure(w.probes, (size_t)B * npmax * sizeof(long long)));
   TRY(ensure(w.probe_d, (size_t)B * npmax * sizeof(double)));
   TRY(bruteforce_core(v->cstore, *cw, w, q, B, nprobe, npmax, w.probes.as<long long>(), w.probe_d.as<double>(),
-                      st, false));
+                      st, false, /*set_only=*/true));
 
   // 2. per-query plan -> device
   long long part_keys = 0, members = 0;
@@ -2130,7 +2139,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
 
 long long graph_opts() {
   return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + g_bound_margin * 523 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_rerank_skip * 11 + tri::g_fx_slice_rows * 7919 +
-         g_scan_debug * 100003 + tri::g_pdl * 7907 + g_pack_mixed * 104729 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
+         g_scan_debug * 100003 + tri::g_pdl * 7907 + g_coarse_set * 7919 * 13 + g_pack_mixed * 104729 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
 }
 
 

@@ -238,8 +238,12 @@ struct RerankLaunch {
   // (cnt[q] keys at part + part_off); the re-rank merges them itself
   const unsigned long long* part;
   const int* compact_cnt;
+  const float* xnorm;  // squared row norms of X (coarse_set_kernel's per-candidate bound)
 };
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st);
+// IVF coarse step, set semantics: exact distances only for candidates whose top-k
+// membership the error bound leaves open (tri_select.cu coarse_set_kernel).
+cudaError_t launch_coarse_set(const RerankLaunch& r, cudaStream_t st);
 extern long long g_rerank_smem_cap;  // bytes; 0 = no cap
 extern long long g_rerank_f2f;
 extern long long g_rerank_skip;

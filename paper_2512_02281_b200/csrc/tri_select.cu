@@ -960,6 +960,283 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
   }
 }
 
+// IVF coarse step with set semantics.  The fine step scans the UNION of a
+// query's probed lists, so only WHICH nprobe centroids are the exact top-nprobe
+// by (dist, id) matters, not their order.  With the certificate's error bound
+// E (|D~ - D| <= E) and the merged candidates sorted by approximate distance
+// a_0 <= a_1 <= ...:
+//   * certified (no dropped centroid can enter): a_{kp-1} - E > a_{k-1} + E;
+//   * IN  (certainly in the top-k): #{j : a_j <= a_i + 2E} <= k -- fewer than
+//     k others can have an exact distance at or below i's;
+//   * OUT (certainly not): #{j : a_j < a_i - 2E} >= k -- k others are
+//     strictly closer;
+//   * the top-k = IN + the (k - |IN|) smallest of the rest by exact (dist, id).
+// Exact fp64 distances (reference order) are computed only for the uncertain
+// rest -- usually none or a few per query instead of every candidate.  Probes
+// come out in approximate order (IN exact-or-approx distances are not needed
+// downstream); an uncertified query goes to the fix-up, which writes the exact
+// ordered top-k.
+constexpr int kSetMax = 256;   // candidates per query (kp_max)
+constexpr int kSetMaxD = 1024; // dimensions (the query and the uncertain rows are staged in shared memory)
+constexpr int kSetRows = 16;   // uncertain rows computed at once (one lane pair each)
+constexpr int kSetWarps = 1;   // one query (warp) per CTA: its staged rows take up to 64 KB
+__global__ void __launch_bounds__(32 * kSetWarps) coarse_set_kernel(RerankLaunch r) {
+  pdl_wait();
+  __shared__ double sa[kSetWarps][kSetMax];
+  __shared__ double sx[kSetWarps][kSetMax];
+  __shared__ int su[kSetWarps][kSetMax];
+  extern __shared__ __align__(16) unsigned char cs_smem[];  // query (d doubles) + kSetRows rows (dpad floats)
+  __shared__ __align__(8) uint64_t cs_bar;
+  const int wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x * kSetWarps + wq;
+  if (q >= r.B) return;
+  const QueryMeta m = r.meta[q];
+  const int kp = m.kp, k = m.k, d = r.d;
+  const unsigned long long* mrow = r.merged + (long long)q * r.ld_merged;
+  double* a = sa[wq];
+  double* ex = sx[wq];
+  int* ul = su[wq];
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  for (int i = lane; i < kp; i += 32) {
+    const unsigned long long key = mrow[i];
+    a[i] = key != TRI_KEY_MAX ? (double)key_dist(key) : inf;
+    ex[i] = inf;
+  }
+  __syncwarp();
+  // per-candidate error bound E_i = E(|q|, |c_i|) from the candidate's own
+  // norm (singleton lists make a few centroids data-point sized, so the
+  // store-wide E_max is ~25x too wide for typical centroids); rows NOT among
+  // the candidates are bounded with E_max (their norm is unknown)
+  const double qn = r.qn64[q];
+  auto bound = [&](double xn) {
+    const double s = qn + xn;
+    return (r.cdot * 2.0 * qn * xn + r.csum * s * s) * 1.001 + 1e-30;
+  };
+  const double Emax = bound(r.xmax);
+  // [a_i - E_i, a_i + E_i] as fp32 rounded outward (a_i is an fp32 value):
+  // the counts below only get more conservative, and run on the fp32 pipe
+  float* lo = reinterpret_cast<float*>(ex);  // ex is free until the exact pass
+  float* hi = lo + kSetMax;
+  const float finf = __int_as_float(0x7f800000);
+  for (int i = lane; i < kp; i += 32) {
+    const unsigned long long key = mrow[i];
+    if (key != TRI_KEY_MAX) {
+      // |c|^2 is stored rounded to fp32: widen by 1e-6 relative to stay an upper bound
+      const float e = __double2float_ru(bound(sqrt((double)r.xnorm[key_pos(key)]) * (1.0 + 1e-6)));
+      const float af = key_dist(key);
+      const bool fin = af < finf && e < finf;  // else: could be anywhere
+      lo[i] = fin ? __fsub_rd(af, e) : -finf;
+      hi[i] = fin ? __fadd_ru(af, e) : finf;
+    } else {
+      lo[i] = finf;
+      hi[i] = finf;
+    }
+  }
+  __syncwarp();
+  const double ak = a[k - 1], akp = a[kp - 1];
+  bool cert = !isnan(qn) && ak < inf;
+  // U = an upper bound of the exact k-th distance: the k-th smallest a_j + E_j
+  float U = finf;
+  if (cert) {
+    for (int b = 0; b < kp; b += 32) {
+      const int i = b + lane;
+      float ui = finf;
+      if (i < kp && hi[i] < finf) {
+        ui = hi[i];
+        int below = 0;  // #{j : hi_j < ui} (ties: index order)
+        for (int j = 0; j < kp; ++j) {
+          const float uj = hi[j];
+          below += uj < ui || (uj == ui && j < i);
+        }
+        if (below != k - 1) ui = finf;
+      }
+      for (int o = 16; o > 0; o >>= 1) ui = fminf(ui, __shfl_xor_sync(0xffffffffu, ui, o));
+      U = fminf(U, ui);
+    }
+    if (m.n_total > kp) cert = akp < inf && !(r.qinv && r.qinv[q] < 0.f) && (double)U < akp - Emax;
+  }
+  long long* oid = r.out_ids + (long long)q * r.ldo;
+  double* od = r.out_d + (long long)q * r.ldo;
+  if (!cert) {  // the fix-up rewrites this query's exact ordered top-k; until then the
+    // approximate top-k (valid ids), or no lists at all for a non-finite query
+    const bool nq = isnan(qn);
+    for (int j = lane; j < k; j += 32) {
+      const unsigned long long key = mrow[j];
+      const bool ok = !nq && key != TRI_KEY_MAX;
+      oid[j] = ok ? (r.idmap ? r.idmap[key_pos(key)] : (long long)key_pos(key)) + r.id_offset : -1;
+      od[j] = ok ? a[j] : __longlong_as_double(0x7ff8000000000000ll);
+    }
+    pad_row(oid, od, k, r.ldo, lane, 32);
+    if (lane == 0) flag_query(r, q, U < finf ? (double)U : ak + Emax);
+    return;
+  }
+  // classify: IN if fewer than k others can be at or below it, OUT if k others
+  // are certainly strictly below it
+  int nin = 0, nun = 0;
+  unsigned injm = 0;  // bit b: this lane's entry of round b is IN
+  for (int b = 0, bi = 0; b < kp; b += 32, ++bi) {
+    const int i = b + lane;
+    bool in = false, out = true;
+    if (i < kp && mrow[i] != TRI_KEY_MAX) {  // (an infinite bound leaves the entry uncertain)
+      const float lo_i = lo[i], hi_i = hi[i];
+      int maybe = 0, sure = 0;
+      for (int j = 0; j < kp; ++j) {
+        const float lj = lo[j], hj = hi[j];
+        maybe += lj <= hi_i;  // j could be at or below i (i itself included)
+        sure += hj < lo_i;    // j is strictly below i
+      }
+      in = maybe <= k;  // fewer than k others
+      out = sure >= k;
+    }
+    injm |= (unsigned)in << bi;
+    const bool un = !in && !out;
+    const unsigned bin = __ballot_sync(0xffffffffu, in), bun = __ballot_sync(0xffffffffu, un);
+    const unsigned lt = (1u << lane) - 1u;
+    if (un) ul[nun + __popc(bun & lt)] = i;
+    nin += __popc(bin);
+    nun += __popc(bun);
+  }
+  __syncwarp();
+  for (int b = 0, bi = 0; b < kp; b += 32, ++bi) {
+    const int i = b + lane;
+    if (i < kp) ex[i] = ((injm >> bi) & 1u) ? -1.0 : inf;  // marker: -1 = IN
+  }
+  __syncwarp();
+  // exact distances of the uncertain candidates: the warp stages the query
+  // and one row at a time in shared memory (coalesced, one L2 latency per
+  // row), lanes 0 / 1 run numpy's two lanes in the reference order
+  if (nun > 0) {
+    // the query (fp64) and up to 16 uncertain rows at a time in shared memory
+    // (rows by 1-D bulk copies, one mbarrier: one L2 latency per 16 rows),
+    // then lane pair (2c, 2c+1) runs numpy's two lanes of candidate c
+    const int dpad = (d + 15) & ~15;
+    double* qs = reinterpret_cast<double*>(cs_smem);
+    float* rows = reinterpret_cast<float*>(qs + dpad);
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&cs_bar));
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    const double* qg = r.q64 + (long long)q * d;
+    {
+      constexpr int U = kSetMaxD / 32;
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int jj = u * 32 + lane;
+        v[u] = jj < d ? qg[jj] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int jj = u * 32 + lane;
+        if (jj < dpad) qs[jj] = v[u];
+      }
+    }
+    __syncwarp();
+    uint32_t phase = 0;
+    for (int t0 = 0; t0 < nun; t0 += kSetRows) {
+      const int nb = min(kSetRows, nun - t0);
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                     "r"((uint32_t)(nb * dpad * 4))
+                     : "memory");
+        for (int c = 0; c < nb; ++c) {
+          const long long pos = key_pos(mrow[ul[t0 + c]]);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                  static_cast<uint32_t>(__cvta_generic_to_shared(rows + c * dpad))),
+              "l"(r.X + pos * r.ldx), "r"((uint32_t)(dpad * 4)), "r"(bar)
+              : "memory");
+        }
+      }
+      asm volatile(
+          "{\n .reg .pred P;\n CSW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra CSW_%=;\n}\n" ::"r"(
+              bar),
+          "r"(phase)
+          : "memory");
+      phase ^= 1;
+      const int c = lane >> 1, ln = lane & 1;
+      double acc = 0.0;
+      if (c < nb) {
+        const float* xs = rows + c * dpad;
+        int jj = 0;
+        for (; jj + 32 <= d; jj += 32) {  // 16 independent squared differences, then the 16-step chain
+          double t2[16];
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+            for (int sub = 3; sub >= 0; --sub) {
+              const int e = jj + 8 * bb + 2 * sub + ln;
+              const double df = __dsub_rn(qs[e], (double)xs[e]);
+              t2[bb * 4 + (3 - sub)] = __dmul_rn(df, df);
+            }
+#pragma unroll
+          for (int t = 0; t < 16; ++t) acc = __dadd_rn(t2[t], acc);
+        }
+        for (; jj + 8 <= d; jj += 8)
+#pragma unroll
+          for (int sub = 3; sub >= 0; --sub) {
+            const int e = jj + 2 * sub + ln;
+            const double df = __dsub_rn(qs[e], (double)xs[e]);
+            acc = __dadd_rn(__dmul_rn(df, df), acc);
+          }
+        for (; jj < d; jj += 2) {
+          const int e = jj + ln;
+          if (e < d) {
+            const double df = __dsub_rn(qs[e], (double)xs[e]);
+            acc = __dadd_rn(__dmul_rn(df, df), acc);
+          }
+        }
+      }
+      const double other = __shfl_xor_sync(0xffffffffu, acc, 1);
+      if (ln == 0 && c < nb) ex[ul[t0 + c]] = __dadd_rn(acc, other);
+      __syncwarp();  // the row buffers are refilled by the next round
+    }
+  }
+  // the (k - nin) smallest uncertain by (exact, id) join the IN set
+  const int need = k - nin;
+  for (int t = lane; t < nun; t += 32) {
+    const int i = ul[t];
+    const double di = ex[i];
+    const long long ii = (long long)key_pos(mrow[i]);
+    int rank = 0;
+    for (int u = 0; u < nun; ++u) {
+      const int j = ul[u];
+      const double dj = ex[j];
+      const long long ij = (long long)key_pos(mrow[j]);
+      rank += dj < di || (dj == di && ij < ii);
+    }
+    if (rank < need) a[i] = -a[i] - 1.0;  // selected (approx distances are >= 0): mark by negation
+  }
+  __syncwarp();
+  // emit in approximate order: IN entries and the selected uncertain ones
+  int outn = 0;
+  for (int b = 0; b < kp; b += 32) {
+    const int i = b + lane;
+    const bool sel = i < kp && (ex[i] == -1.0 || a[i] < 0.0);
+    const unsigned bs = __ballot_sync(0xffffffffu, sel);
+    if (sel) {
+      const int o = outn + __popc(bs & ((1u << lane) - 1u));
+      const long long pos = key_pos(mrow[i]);
+      oid[o] = (r.idmap ? r.idmap[pos] : pos) + r.id_offset;
+      od[o] = ex[i] == -1.0 ? (double)key_dist(mrow[i]) : ex[i];
+    }
+    outn += __popc(bs);
+  }
+  pad_row(oid, od, k, r.ldo, lane, 32);
+}
+
+cudaError_t launch_coarse_set(const RerankLaunch& r, cudaStream_t st) {
+  if (r.B <= 0) return cudaSuccess;
+  if (r.kp_max > kSetMax || r.d > kSetMaxD) return cudaErrorInvalidValue;
+  const int dpad = (r.d + 15) & ~15;
+  const size_t smem = (size_t)dpad * 8 + (size_t)kSetRows * dpad * 4;
+  cudaError_t e = cudaFuncSetAttribute(coarse_set_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  (void)launch_pdl(coarse_set_kernel, (r.B + kSetWarps - 1) / kSetWarps, 32 * kSetWarps, smem, st, r);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
   if (r.B <= 0) return cudaSuccess;
   // slab width: 2 buffers x kp x (S+4) floats <= ~72 KB (several CTAs per SM)

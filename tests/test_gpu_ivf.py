@@ -52,6 +52,16 @@ def test_ivf_golden_ragged(small):
     ids, d = idx.search(qs, g["ks"], g["nprobes"])
     _check_rows(ids, d, g, g["ks"])
     probes = idx.last_probes(40, 16)
+    for i in range(40):  # the top-nprobe SET (coarse_set: approximate order)
+        npb = int(g["nprobes"][i])
+        assert sorted(probes[i, :npb].tolist()) == sorted(g["probes"][i, :npb].tolist())
+    _lib.set_option("coarse_set", 0)  # the full re-rank: exact (dist, id) order
+    try:
+        ids0, d0 = idx.search(qs, g["ks"], g["nprobes"])
+        probes = idx.last_probes(40, 16)
+    finally:
+        _lib.set_option("coarse_set", 1)
+    assert np.array_equal(ids0, ids) and np.array_equal(d0, d)
     for i in range(40):
         npb = int(g["nprobes"][i])
         assert probes[i, :npb].tolist() == g["probes"][i, :npb].tolist()
@@ -429,3 +439,23 @@ def test_device_path_non_finite_query_rows(small):
     _check_rows(hi[keep], hd[keep], {"ids": g["ids"][keep], "dists": g["dists"][keep]}, g["ks"][keep])
     with pytest.raises(ValueError):  # the host entry point rejects it up front
         idx.search(qs, g["ks"], g["nprobes"])
+
+
+@pytest.mark.gpu
+def test_coarse_set_semantics_on_tied_centroids():
+    """Duplicated centroids tie exactly: the coarse step's top-nprobe set must
+    still be the reference's (dist, id) prefix (nprobe splits tie pairs)."""
+    rng = np.random.Generator(np.random.Philox(23))
+    data = rng.standard_normal((4000, 16)).astype(np.float32)
+    cen = rng.standard_normal((32, 16)).astype(np.float32)
+    cen[16:] = cen[:16]  # exact duplicates: ids 16..31 tie with 0..15
+    idx = IVFFlatIndex.from_centroids(VectorStore(data=data), cen)
+    art = orc.IVFArtifact(cen, idx.export()[1])
+    qs = rng.standard_normal((24, 16))
+    for npb in (1, 5, 17):
+        ids, d = idx.search(qs, 10, npb)
+        probes = idx.last_probes(24, npb)
+        for i in range(24):
+            assert sorted(probes[i].tolist()) == sorted(orc.coarse_probe(art, qs[i], npb).tolist())
+            oi, od = orc.ivf_search(data, art, qs[i], 10, npb)
+            assert np.array_equal(ids[i, :oi.size], oi) and np.array_equal(d[i, :od.size], od)
