@@ -9,7 +9,7 @@
 namespace tri {
 
 // Hot-path kernels launch with programmatic stream serialization (option
-// "pdl", default on): the launch of kernel N+1 overlaps the tail of kernel N;
+// "pdl", default off: measured no gain): the launch of kernel N+1 may overlap the tail of kernel N;
 // every such kernel starts with pdl_wait() (tri_common.cuh).
 extern long long g_pdl;
 template <typename... P, typename... A>
