@@ -168,7 +168,7 @@ int tri_ivf_last_scan_kind(tri_ivf* v, int32_t* kind);
 /* Device-resident continuous-batching graph search: replaces
  * engine.ContinuousBatchEngine (engine.py:312-422).  adjacency: n x degree
  * uint32 (NeighborGraph, ann_graph.py:51-70); the config mirrors EngineConfig
- * (engine.py:39-66; m <= 256, p * degree <= 512).  Requests are seeded,
+ * (engine.py:39-66; m <= 4096, p * degree <= 8192).  Requests are seeded,
  * extended, merged and finalized on the device with the reference's exact
  * float64 distances; results and batch accounting are bit-identical. */
 typedef struct tri_engine tri_engine;

@@ -39,8 +39,9 @@
 namespace tri {
 namespace {
 
-constexpr int kEngMaxM = 256;     // top-M capacity per request
-constexpr int kEngMaxEmit = 512;  // p * degree per extend
+constexpr int kEngMaxM = 4096;     // top-M capacity per request
+constexpr int kEngMaxEmit = 8192;  // p * degree per extend
+constexpr size_t kEngSmemCap = 200 * 1024;  // per CTA: slots per CTA shrink (4 -> 2 -> 1) for big m, p * degree
 constexpr int kStats = 4;         // per-step counters: emissions, retired, active after, error
 constexpr int kMaxChunk = 64;     // steps launched between host read-backs
 
@@ -55,6 +56,7 @@ struct EngineLaunch {
   const unsigned* adj;
   int D;
   int m, p, E, stop_streak, max_extends;
+  int wpc;  // request slots (warps) per CTA
   int* status;
   const double* q64;
   const int* kq;
@@ -101,7 +103,7 @@ constexpr int kEngWarps = 4;
 __global__ void __launch_bounds__(32 * kEngWarps) engine_step_kernel(EngineLaunch L) {
   extern __shared__ __align__(16) unsigned char eng_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = blockIdx.x * kEngWarps + warp;
+  const int s = blockIdx.x * L.wpc + warp;
   if (s >= L.n_slots) return;
   const int st = L.status[s];
   if (st != kSeed && st != kActive) return;
@@ -307,10 +309,17 @@ __global__ void __launch_bounds__(32 * kEngWarps) engine_step_kernel(EngineLaunc
   }
 }
 
-size_t engine_smem(int m, int p, int D) {
+size_t engine_warp_smem(int m, int p, int D) {
   const size_t cap = (size_t)m + (size_t)p * D;
   const size_t per_warp = cap * 13 + (size_t)m * 13 + (size_t)p * 4 + 64;
-  return kEngWarps * ((per_warp + 15) & ~(size_t)15);
+  return (per_warp + 15) & ~(size_t)15;
+}
+
+// slots per CTA: kEngWarps unless the per-warp lists are too big for that
+int engine_wpc(int m, int p, int D) {
+  int w = kEngWarps;
+  while (w > 1 && (size_t)w * engine_warp_smem(m, p, D) > kEngSmemCap) w >>= 1;
+  return w;
 }
 
 // Admission: copy the staged queries into their slots, reset counters and the
@@ -358,6 +367,7 @@ using namespace tri;
 struct tri_engine {
   StoreView sv{};
   int D = 0, m = 0, p = 0, E = 0, C = 0, S = 0, maxext = 0;
+  int wpc = 4;  // request slots per CTA of the step kernel
   unsigned* adj = nullptr;
   long long vw = 0;
   cudaStream_t st = nullptr;
@@ -525,6 +535,7 @@ EngineLaunch launch_of(tri_engine* e) {
   L.E = e->E;
   L.stop_streak = e->S;
   L.max_extends = e->maxext;
+  L.wpc = e->wpc;
   L.status = e->status;
   L.q64 = e->q64;
   L.kq = e->kq;
@@ -655,7 +666,11 @@ int tri_engine_create(tri_store* s, const uint32_t* adjacency, int32_t degree, i
       cudaMallocHost(&e->h_stats, kMaxChunk * kStats * sizeof(int)) != cudaSuccess ||
       cudaEventCreate(&e->ev0) != cudaSuccess || cudaEventCreate(&e->ev1) != cudaSuccess)
     return bail(set_error(TRI_ECUDA, "engine allocation failed"));
-  e->smem = engine_smem(m, p, degree);
+  e->wpc = engine_wpc(m, p, degree);
+  e->smem = (size_t)e->wpc * engine_warp_smem(m, p, degree);
+  if (e->smem > kEngSmemCap)
+    return bail(set_error(TRI_EINVAL, "m=%d, p*degree=%lld need %zu bytes of shared memory per request (max %zu)", m,
+                          (long long)p * degree, e->smem, kEngSmemCap));
   if (e->smem > 48 * 1024 &&
       cudaFuncSetAttribute(engine_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem) != cudaSuccess)
     return bail(set_error(TRI_ECUDA, "engine shared memory %zu bytes not available", e->smem));
@@ -786,7 +801,7 @@ int tri_engine_run(tri_engine* e, int32_t max_steps, int32_t until_idle, int32_t
       L.stats = e->stats + i * kStats;
       L.step = done + i;
       if (e->hw > 0)
-        engine_step_kernel<<<(e->hw + kEngWarps - 1) / kEngWarps, 32 * kEngWarps, e->smem, e->st>>>(L);
+        engine_step_kernel<<<(e->hw + e->wpc - 1) / e->wpc, 32 * e->wpc, e->smem, e->st>>>(L);
     }
     ECU(cudaGetLastError());
     ECU(cudaEventRecord(e->ev1, e->st));

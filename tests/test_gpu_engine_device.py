@@ -52,6 +52,8 @@ def _check(eng, rids, ref):
         (3000, 16, 8, dict(m=16, p=1, entry_count=3, batch_capacity=7, stop_streak=2, max_extends=5)),
         # p > 32: parents beyond one warp's lanes must be marked expanded too
         (4000, 16, 8, dict(m=64, p=40, entry_count=8, batch_capacity=256, stop_streak=2, max_extends=12)),
+        # m beyond one warp's register reach and p * degree > 512 (round-1 caps lifted)
+        (3000, 16, 16, dict(m=1024, p=40, entry_count=16, batch_capacity=512, stop_streak=2, max_extends=8)),
     ],
 )
 def test_device_engine_matches_oracle(n, d, deg, cfg):
@@ -137,13 +139,29 @@ def test_device_engine_limits_and_bad_graph():
     store = VectorStore(data=gen_matrix(40, 4, 3))
     good = build_knn_graph(store, 4)
     with pytest.raises(ValueError):
-        ContinuousBatchEngine(store, good, EngineConfig(m=300, p=1, entry_count=2))
+        ContinuousBatchEngine(store, good, EngineConfig(m=5000, p=1, entry_count=2))
     wide = NeighborGraph(degree=4, adjacency=good.adjacency)
     with pytest.raises(ValueError):
-        ContinuousBatchEngine(store, wide, EngineConfig(m=256, p=200, entry_count=2))
+        ContinuousBatchEngine(store, wide, EngineConfig(m=256, p=3000, entry_count=2))
     bad_adj = good.adjacency.copy()
     bad_adj[:, 0] = 10_000
     eng = ContinuousBatchEngine(store, NeighborGraph(degree=4, adjacency=bad_adj), EngineConfig(m=8, p=1, entry_count=2))
     eng.submit(gen_matrix(1, 4, 5)[0], k=3)
     with pytest.raises(RuntimeError):
         eng.run_to_completion()
+
+
+def test_device_engine_one_slot_per_cta():
+    """m = 4096 with p * degree = 4096: the per-request lists need ~160 KB of
+    shared memory, so the step kernel runs one request slot per CTA."""
+    data = gen_matrix(5000, 8, 31)
+    store = VectorStore(data=data)
+    graph = build_knn_graph(store, 64)
+    cfg = dict(m=4096, p=64, entry_count=64, batch_capacity=1024, stop_streak=1, max_extends=3)
+    queries = gen_matrix(4, 8, 32).astype(np.float64)
+    ks = np.array([5, 50, 500, 17])
+    admit = np.zeros(4, np.int64)
+    ref = orc.engine_run(data, graph.adjacency, queries, ks, admit, **cfg)
+    eng = ContinuousBatchEngine(store, graph, EngineConfig(**cfg))
+    rids, steps = _drive(eng, queries, ks, admit)
+    _check(eng, rids, ref)
