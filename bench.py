@@ -77,6 +77,8 @@ def parse():
     ap.add_argument("--no-configs", action="store_true", help="skip the secondary configs (C1/C3/C4/C5/engine)")
     ap.add_argument("--configs", default="C1,C3,C4,C5,engine", help="secondary configs measured at N=1")
     ap.add_argument("--full-out", default=None, help="write every config's complete record to this JSON file")
+    ap.add_argument("--comm", default="torch", choices=["torch", "native"],
+                    help="N>1 gather: torch.distributed NCCL, or the library's own communicator (tri_comm_*)")
     ap.add_argument("--lanes", type=int, default=4,
                     help="independent batches in flight (one CUDA stream + library workspace each)")
     return ap.parse_args()
@@ -361,7 +363,7 @@ def run_ivf(cfg, args, ctx: Ctx, headline: bool = True, keep: bool = False):
     shard = None
     if ctx.world > 1:  # one process group per lane: each lane's gathers are ordered on its own communicator
         groups = [ctx.dist.new_group(list(range(ctx.world))) for _ in range(L)]
-        shard = [ShardedIVF(idx, K, group=g) for g in groups]
+        shard = [ShardedIVF(idx, K, group=g, transport=args.comm) for g in groups]
     torch.cuda.set_stream(stream)
     torch.cuda.synchronize()
     step_no = [0]
@@ -509,6 +511,7 @@ def run_ivf(cfg, args, ctx: Ctx, headline: bool = True, keep: bool = False):
             rec["artifact"] = orc.artifact_digest(art)
     if shard:
         for s in shard:
+            s.close()
             s._bufs.clear()
     if keep:
         return rec, b

@@ -238,12 +238,31 @@ int tri_merge_topk(const double* dists, const int64_t* ids, int32_t G, int32_t B
  * is at [g * g_stride + b * ld_in + j], output row b at [b * ld_out].  A rank
  * that writes its top-k ids and then its dists into ONE [2, B, k] block (ids
  * at p, dists at p + B*k, ldo = k) gathers a single tensor per batch and the
- * merge reads the gathered [G, 2, B, k] in place: ids = p, dists = p + B*k,
+ * merge reads the gathered [G, 2, B, k] in place (output columns [k_out, ld_out)
+ * get id -1 / +inf): ids = p, dists = p + B*k,
  * ld_in = k, g_stride = 2*B*k.  The per-shard merge SURVEY.md 8(e) adds (the
  * reference has none); tie rule of ann_graph.py:136. */
 int tri_merge_topk_ld(const double* dists, const int64_t* ids, int32_t G, int32_t B, int32_t k_in, int32_t ld_in,
                       int64_t g_stride, int32_t k_out, double* out_dists, int64_t* out_ids, int32_t ld_out,
                       void* stream);
+
+/* Native sharded search over NCCL (C4; the reference has no sharding,
+ * SPEC.md:536, and SURVEY.md 8(b) asks for tri_comm_init).  NCCL is loaded at
+ * run time (libnccl.so.2).  Rank 0 makes a 128-byte unique id, the caller
+ * distributes it (e.g. a torch.distributed broadcast), every rank calls
+ * tri_comm_init with it.  tri_ivf_search_sharded then runs one batch on
+ * `stream`: the rank's local search (global ids, shard offset folded in) into
+ * a packed [2, B, k] block, one ncclAllGather of B*k*16 bytes per rank, and
+ * the exact (dist, id) merge into ids / dists (device, row stride ldo) on every
+ * rank.  Stream-ordered and CUDA-graph capturable; one communicator per
+ * concurrently used stream is the caller's choice (collectives on one
+ * communicator must be issued in the same order on every rank). */
+typedef struct tri_comm tri_comm;
+int tri_comm_unique_id(uint8_t* id128);
+int tri_comm_init(const uint8_t* id128, int32_t world, int32_t rank, int32_t device, tri_comm** out);
+int tri_comm_destroy(tri_comm* c);
+int tri_ivf_search_sharded(tri_ivf* v, tri_comm* c, const double* q, int32_t B, int32_t k, const int32_t* nprobe,
+                           int32_t ldo, int64_t* ids, double* dists, void* stream);
 
 #ifdef __cplusplus
 }

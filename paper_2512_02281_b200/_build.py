@@ -10,7 +10,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtrinity_b200.so")
-SOURCES = ["tri_listscan.cu", "tri_tcscan.cu", "tri_dense.cu", "tri_select.cu", "tri_ivf.cu", "tri_engine.cu", "tri_coarse.cu", "tri_exhaustive.cu", "tri_api.cu"]
+SOURCES = ["tri_listscan.cu", "tri_tcscan.cu", "tri_dense.cu", "tri_select.cu", "tri_ivf.cu", "tri_engine.cu", "tri_coarse.cu", "tri_exhaustive.cu", "tri_comm.cu", "tri_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

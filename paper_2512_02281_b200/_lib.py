@@ -74,6 +74,10 @@ _SIGS = {
     "tri_debug_scan_ts": [_vp, _i32],
     "tri_merge_topk": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp],
     "tri_merge_topk_ld": [_vp, _vp, _i32, _i32, _i32, _i32, _i64, _i32, _vp, _vp, _i32, _vp],
+    "tri_comm_unique_id": [_vp],
+    "tri_comm_init": [_vp, _i32, _i32, _i32, C.POINTER(_vp)],
+    "tri_comm_destroy": [_vp],
+    "tri_ivf_search_sharded": [_vp, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp],
 }
 _RESTYPE = {"tri_last_error": C.c_char_p}
 

@@ -1736,11 +1736,11 @@ __global__ void __launch_bounds__(kThreads) merge_exact_kernel(const double* __r
   }
   __syncthreads();
   block_sort(mbuf, n2, ExactLess());
-  for (int j = threadIdx.x; j < k_out; j += kThreads) {
-    const Exact e = mbuf[j];
+  for (int j = threadIdx.x; j < ld_out; j += kThreads) {  // columns past k_out: id -1, distance +inf
+    const Exact e = j < k_out ? mbuf[j] : exact_max();
     const bool ok = e.id != 0x7fffffffffffffffll;
     out_ids[(long long)q * ld_out + j] = ok ? e.id : -1;
-    out_d[(long long)q * ld_out + j] = e.d;
+    out_d[(long long)q * ld_out + j] = ok ? e.d : __longlong_as_double(0x7ff0000000000000ll);
   }
 }
 

@@ -107,21 +107,59 @@ class ShardedIVF:
 
     No host round trip between the steps; every rank ends with the merged
     top-k.  k is one value for the batch (nprobe may vary per query).
+
+    ``transport="native"`` runs the same three steps inside the library
+    (``tri_ivf_search_sharded``: its own NCCL communicator, created from a
+    unique id that rank 0 broadcasts over ``group``); without an initialised
+    process group it is a world of one.
     """
 
-    def __init__(self, index, k: int, group=None):
+    def __init__(self, index, k: int, group=None, transport: str = "torch"):
+        import ctypes as C
+
         import torch.distributed as dist
 
+        from . import _lib
+
+        if transport not in ("torch", "native"):
+            raise ValueError(f"transport must be 'torch' or 'native', got {transport!r}")
         self.dist = dist
         self.group = group
         self.index = index
         self.k = int(k)
         if self.k < 1:
             raise ValueError(f"k must be >= 1, got {k}")
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        self.host_gather = dist.get_backend(group) == "gloo"  # test hook: gloo moves host tensors
+        self.transport = transport
+        ready = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if ready else 1
+        self.rank = dist.get_rank(group) if ready else 0
+        self.host_gather = ready and dist.get_backend(group) == "gloo"  # test hook: gloo moves host tensors
         self._bufs = {}
+        self._comm = None
+        if transport == "native":
+            uid = (C.c_uint8 * 128)()
+            if self.rank == 0:
+                _lib.check(_lib.gpu().tri_comm_unique_id(uid))
+            if self.world > 1:
+                box = [bytes(uid)]
+                dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+                uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+            h = C.c_void_p()
+            _lib.check(_lib.gpu().tri_comm_init(uid, self.world, self.rank, int(index.device), C.byref(h)))
+            self._comm = h
+
+    def close(self) -> None:
+        if self._comm:
+            from . import _lib
+
+            _lib.load_library().tri_comm_destroy(self._comm)
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def _lane(self, stream, B: int):
         import torch
@@ -154,6 +192,11 @@ class ShardedIVF:
         if int(out_ids.shape[1]) < self.k:
             raise ValueError(f"outputs hold {int(out_ids.shape[1])} columns, k={self.k}")
         ks, nps = self.index._ragged(B, self.k, nprobe)
+        if self._comm is not None:
+            _lib.check(_lib.gpu().tri_ivf_search_sharded(self.index.handle, self._comm, _lib.ptr(q_dev), B, self.k,
+                                                         nps.ctypes.data, int(out_ids.shape[1]), _lib.ptr(out_ids),
+                                                         _lib.ptr(out_dists), _stream_ptr(stream)))
+            return
         b = self._lane(stream, B)
         loc, k, st = b["local"], self.k, _stream_ptr(stream)
         lib = _lib.gpu()

@@ -459,3 +459,33 @@ def test_coarse_set_semantics_on_tied_centroids():
             assert sorted(probes[i].tolist()) == sorted(orc.coarse_probe(art, qs[i], npb).tolist())
             oi, od = orc.ivf_search(data, art, qs[i], 10, npb)
             assert np.array_equal(ids[i, :oi.size], oi) and np.array_equal(d[i, :od.size], od)
+
+
+@pytest.mark.gpu
+def test_native_comm_sharded_search_world_one():
+    """tri_comm_init / tri_ivf_search_sharded with a one-rank NCCL communicator:
+    local search -> packed all-gather -> device merge equals the plain search."""
+    import torch
+
+    from paper_2512_02281_b200.sharded import ShardedIVF
+
+    data = gen_matrix(20_000, 32, 41)
+    idx = IVFFlatIndex.train(VectorStore(data=data), nlist=64, iters=3, seed=2)
+    qs = torch.from_numpy(gen_matrix(40, 32, 42).astype(np.float64)).cuda()
+    st = torch.cuda.Stream()
+    ref_i = torch.empty((40, 10), dtype=torch.int64, device="cuda")
+    ref_d = torch.empty((40, 10), dtype=torch.float64, device="cuda")
+    idx.search_device(qs, 10, 8, ref_i, ref_d, st)
+    sh = ShardedIVF(idx, 10, transport="native")
+    try:
+        for _ in range(3):  # the second call captures a graph, the third replays it
+            out_i = torch.full((40, 12), 7, dtype=torch.int64, device="cuda")
+            out_d = torch.zeros((40, 12), dtype=torch.float64, device="cuda")
+            sh.search_device(qs, 8, out_i, out_d, st)
+            st.synchronize()
+            assert torch.equal(out_i[:, :10], ref_i) and torch.equal(out_d[:, :10], ref_d)
+            assert (out_i[:, 10:] == -1).all()
+    finally:
+        sh.close()
+    with pytest.raises(ValueError):
+        ShardedIVF(idx, 10, transport="mpi")
