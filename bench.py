@@ -483,15 +483,42 @@ def run_ivf(cfg, args, ctx: Ctx, headline: bool = True, keep: bool = False):
         t_end[j] = time.perf_counter()
 
     ctx.barrier()
-    ths = [threading.Thread(target=lane_loop, args=(j, len(range(j, args.steps, L)))) for j in range(L)]
-    for th in ths:
-        th.start()
-    gate.wait()
-    t0 = time.perf_counter()
-    for th in ths:
-        th.join()
-    torch.cuda.synchronize()
-    e2e_s = ctx.max_over_ranks(max(t_end) - t0)
+    if shard:
+        # sharded: ONE host thread keeps the lanes busy (search_async), so every
+        # rank issues its collectives in the same order -- NCCL kernels of
+        # different communicators may otherwise wait on each other across ranks
+        evs = [None] * L
+        t_issue = [0.0] * L
+        for i in range(3 * L):
+            j = i % L
+            if evs[j] is not None:
+                evs[j].synchronize()
+            evs[j] = shard[j].search_async(q_pin, NPROBE, *pins[j], stream=lanes[j])
+        torch.cuda.synchronize()
+        ctx.barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            j = i % L
+            if evs[j] is not None:
+                evs[j].synchronize()
+                call_ms[j].append((time.perf_counter() - t_issue[j]) * 1e3)
+            t_issue[j] = time.perf_counter()
+            evs[j] = shard[j].search_async(q_pin, NPROBE, *pins[j], stream=lanes[j])
+        for j in range(L):
+            if evs[j] is not None:
+                evs[j].synchronize()
+                call_ms[j].append((time.perf_counter() - t_issue[j]) * 1e3)
+        e2e_s = ctx.max_over_ranks(time.perf_counter() - t0)
+    else:
+        ths = [threading.Thread(target=lane_loop, args=(j, len(range(j, args.steps, L)))) for j in range(L)]
+        for th in ths:
+            th.start()
+        gate.wait()
+        t0 = time.perf_counter()
+        for th in ths:
+            th.join()
+        torch.cuda.synchronize()
+        e2e_s = ctx.max_over_ranks(max(t_end) - t0)
     lat = np.concatenate([np.asarray(c) for c in call_ms if c])
     rec["e2e"] = {"value": BATCH * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": BATCH * DIM * 8,
                   "d2h_bytes_per_step": BATCH * K * 16,

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-for G in 1 2 4 8; do timeout 900 python tools/bench_c4.py --shards $G --lanes 4 --check 8 --out gpurun_out/c4_G$G.json > gpurun_out/c4_G$G.log 2>&1; done
+timeout 900 python -m pytest tests/test_gpu_bench_sharded.py -q -x > gpurun_out/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/pytest.log

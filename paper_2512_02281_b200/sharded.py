@@ -213,9 +213,13 @@ class ShardedIVF:
         _lib.check(lib.tri_merge_topk_ld(allp.data_ptr() + 8 * B * k, allp.data_ptr(), self.world, B, k, k, 2 * B * k,
                                          k, _lib.ptr(out_dists), _lib.ptr(out_ids), int(out_ids.shape[1]), st))
 
-    def search_into(self, q_host, nprobe, ids_out, dists_out, stream) -> None:
-        """Host-buffer form (blocking): queries [B, d] float64 in (pinned for
-        asynchronous copies), merged top-k out, copies on ``stream``."""
+    def search_async(self, q_host, nprobe, ids_out, dists_out, stream):
+        """Host-buffer form, asynchronous: enqueues the H2D copy of the queries
+        [B, d] float64 (pinned host), the sharded search and the D2H copy of
+        the merged top-k into ``ids_out`` / ``dists_out`` (pinned) on
+        ``stream``; returns a CUDA event that completes with the copies.  One
+        host thread can keep several streams busy while every rank issues its
+        collectives in the same order (a requirement of NCCL)."""
         import torch
 
         B = int(q_host.shape[0])
@@ -226,7 +230,13 @@ class ShardedIVF:
         with torch.cuda.stream(stream):
             torch.as_tensor(ids_out)[:, :self.k].copy_(b["ids"], non_blocking=True)
             torch.as_tensor(dists_out)[:, :self.k].copy_(b["d"], non_blocking=True)
-        stream.synchronize()
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return ev
+
+    def search_into(self, q_host, nprobe, ids_out, dists_out, stream) -> None:
+        """Host-buffer form (blocking): ``search_async`` then wait."""
+        self.search_async(q_host, nprobe, ids_out, dists_out, stream).synchronize()
 
 def device_merge(dists, ids, k: int):
     """tri_merge_topk on device tensors [G, B, k] -> host (ids, dists)."""
