@@ -168,6 +168,14 @@ def queries_f64():
     return gen_matrix(BATCH, DIM, Q_SEED).astype(np.float64)
 
 
+def bench_config(cfg, artifact):
+    """The workload description both arms print (identical dicts: the driver
+    compares them); how the work is spread goes in the line's top level."""
+    return {"workload": cfg["workload"], "n_db": cfg["n"], "dim": DIM, "nlist": NLIST, "nprobe": NPROBE,
+            "global_batch": BATCH, "k": K, "db": cfg["db"], "queries": "gen_vectors(256, 768, seed=4) as f64",
+            "l2": "no flush: every batch streams > 1.5 GB of lists (> 126 MB L2)", "artifact": artifact}
+
+
 def pct(a):
     a = np.asarray(a, dtype=np.float64)
     return {"p50": float(np.percentile(a, 50)), "p95": float(np.percentile(a, 95)), "p99": float(np.percentile(a, 99))}
@@ -218,9 +226,8 @@ def run_reference(args):
         "impl": "reference", "metric": cfg["metric"], "value": qps, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": cfg["workload"], "n_db": cfg["n"], "dim": DIM, "nlist": NLIST,
-                                        "nprobe": NPROBE, "global_batch": BATCH, "k": K, "db": cfg["db"],
-                                        "parallelism": f"cpu x{cores}", "artifact": orc.artifact_digest(art)},
+        "data": "synthetic", "config": bench_config(cfg, orc.artifact_digest(art)),
+        "parallelism": f"cpu x{cores}",
         "cpu_baseline": {"value": qps, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{per_step} queries per step of the {name} batch ({per_step * args.steps} in "
                                    f"all), numpy oracle, one process per core ({cores} cores)"},
@@ -523,6 +530,13 @@ def run_ivf(cfg, args, ctx: Ctx, headline: bool = True, keep: bool = False):
     rec["e2e"] = {"value": BATCH * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": BATCH * DIM * 8,
                   "d2h_bytes_per_step": BATCH * K * 16,
                   "batch_latency_ms": {k: round(v, 4) for k, v in pct(lat).items()}}
+    if ctx.world > 1 and headline:  # the artifact digest over the whole database (what the reference arm prints)
+        from oracle import trinity_oracle as orc
+
+        parts = [None] * ctx.world if ctx.rank == 0 else None
+        ctx.dist.gather_object(b["asg"], parts, dst=0)
+        if ctx.rank == 0:
+            rec["artifact"] = orc.artifact_digest(orc.IVFArtifact(b["cen"], np.concatenate(parts)))
     if ctx.rank == 0 and (headline or ctx.world == 1):
         from oracle import trinity_oracle as orc
 
@@ -629,11 +643,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": f"{rec['scan_kind']} candidate scan (certified bound) + f64 exact re-rank",
         "data": "synthetic",
-        "config": {"workload": cfg["workload"], "n_db": cfg["n"], "dim": DIM, "nlist": NLIST, "nprobe": NPROBE,
-                   "global_batch": BATCH, "k": K, "db": cfg["db"], "queries": "gen_vectors(256, 768, seed=4) as f64",
-                   "l2": "no flush: every batch streams > 1.5 GB of lists (> 126 MB L2)",
-                   "parallelism": f"vector-shard x{world}" if world > 1 else "dp1", "lanes": args.lanes,
-                   "artifact": rec.get("artifact")},
+        "config": bench_config(cfg, rec.get("artifact")),
+        "parallelism": f"vector-shard x{world}" if world > 1 else "dp1", "lanes": args.lanes,
         "parity": rec["parity"],
         "roofline": rec["roofline"],
         "cpu_baseline": rec.get("cpu_baseline"),

@@ -37,7 +37,13 @@ def test_bench_sharded_step_two_ranks_full_parity():
     keep = [ln for ln in res.stderr.splitlines() if "[rank0]" in ln or "parity" in ln or "Error" in ln]
     assert res.returncode == 0, "\n".join(keep)[-4000:]
     line = json.loads(res.stdout.strip().splitlines()[-1])
-    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "vector-shard x2"
+    assert line["n_gpus"] == 2 and line["parallelism"] == "vector-shard x2"
     assert line["config"]["n_db"] == 300000 and line["config"]["workload"].startswith("C4")
     assert line["parity"].startswith("ok: 259 queries"), line["parity"]
     assert line["value"] > 0 and line["e2e"]["value"] > 0
+    # the reference arm (CPU oracle) builds the same index artifact on its own
+    ref = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "C4", "--steps", "1",
+                          "--warmup", "1"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
+    assert ref.returncode == 0, ref.stderr[-2000:]
+    rline = json.loads(ref.stdout.strip().splitlines()[-1])
+    assert rline["config"] == line["config"], (rline["config"], line["config"])
