@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests/test_gpu_bench_sharded.py -q -x > gpurun_out/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/pytest.log
-timeout 600 python bench.py --steps 20 --warmup 5 --no-configs > gpurun_out/bench.log 2>&1
+timeout 1800 python -m pytest tests/test_gpu_ivf.py -q -x -k "c4_scale" > gpurun_out/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/pytest.log

@@ -489,3 +489,36 @@ def test_native_comm_sharded_search_world_one():
         sh.close()
     with pytest.raises(ValueError):
         ShardedIVF(idx, 10, transport="mpi")
+
+
+@pytest.mark.slow
+@pytest.mark.gpu
+def test_c4_scale_parity(scan_kernel):
+    """BASELINE C4 (10M x 768): the whole database on one GPU and one rank's
+    share at G = 8 (rows [3.75M, 5M), global ids through id_offset), both
+    built like bench.py's C4 (centroids trained on rows [0, 1M), every row
+    listed under its exact nearest centroid); 64 queries of each compared with
+    the oracle over the same rows."""
+    if scan_kernel != "auto":
+        pytest.skip("one scan arithmetic is enough at this size")
+    from oracle.pool import assert_rows_equal, ivf_oracle_batch
+    from paper_2512_02281_b200.ann_graph import _DeviceStore
+    from paper_2512_02281_b200.sharded import shard_bounds
+    from paper_2512_02281_b200.workload import gen_rows_chunked
+
+    n, seed = 10_000_000, 100
+    tr = _DeviceStore(gen_rows_chunked(0, 1_000_000, 768, seed))
+    cen, _ = IVFFlatIndex.train(tr, nlist=1024, iters=5, seed=4).export()
+    tr.close()
+    qs = gen_matrix(256, 768, 4).astype(np.float64)[::4]
+    for lo, hi in [(0, n), shard_bounds(n, 8, 3)]:
+        data = gen_rows_chunked(lo, hi, 768, seed)
+        store = _DeviceStore(data)
+        idx = IVFFlatIndex.from_centroids(store, cen, id_offset=lo)
+        store.close()
+        ids, d = idx.search(qs, 10, 32)
+        art = orc.IVFArtifact(cen, idx.export()[1])
+        ref = [(i + lo, dd) for i, dd in ivf_oracle_batch(data, art, qs, 10, 32)]
+        assert_rows_equal(ids, d, ref)
+        idx.close()
+        del data
