@@ -2,10 +2,11 @@
 
 memcheck / racecheck / synccheck / initcheck over: the tensor-core brute force
 (TF32 tcgen05 scan, wide 64-query items with the TMEM seed pass, select, fp64
-re-rank), the IVF pipeline (split-fp16 tcgen05 coarse GEMM, dense select,
-device packer, fp16 tcgen05 list scan, merge, re-rank) on a ragged padded
-batch, the forced fix-up path, the graph engine step kernel and the shard
-merge.  Each result is checked against the CPU oracle; exit code 1 on a
+re-rank with the fused compact merge), the IVF pipeline (split-fp16 tcgen05
+coarse GEMM, dense select, coarse set kernel, device packer, fp16 tcgen05
+list scan, merge, re-rank) on a ragged padded batch (device-built plan), the
+forced fix-up path, the graph engine step kernel, the exhaustive large-k
+brute force, the native NCCL sharded search (one rank) and the shard merge.  Each result is checked against the CPU oracle; exit code 1 on a
 mismatch.  CUDA graphs are off (TRI_GRAPHS=0) so every kernel is launched
 directly under the tool.
 
@@ -76,6 +77,28 @@ def main():
         r = eng.result(int(rid))
         bad += [n.id for n in r.neighbors] != ref_ids[i].tolist()
     print("engine", "ok" if not bad else "MISMATCH", flush=True)
+    # 4b. exhaustive large-k brute force (k > TRI_MAX_K: exact distances + radix sort)
+    big = rng.standard_normal((3000, 16)).astype(np.float32)
+    bq = rng.standard_normal((2, 16))
+    ids, d = brute_force_knn_batch(VectorStore(data=big), bq, 2000)
+    for i in range(2):
+        oi, od = orc.exact_knn(big, bq[i], 2000)
+        bad += not (np.array_equal(ids[i], oi) and np.array_equal(d[i], od))
+    print("exhaustive", "ok" if not bad else "MISMATCH", flush=True)
+    # 4c. native sharded search (one-rank NCCL communicator): search, all-gather, strided merge
+    from paper_2512_02281_b200.sharded import ShardedIVF
+
+    sh = ShardedIVF(idx, 10, transport="native")
+    qd = torch.from_numpy(q).cuda()
+    si = torch.empty((24, 10), dtype=torch.int64, device="cuda")
+    sd = torch.empty((24, 10), dtype=torch.float64, device="cuda")
+    st = torch.cuda.Stream()
+    sh.search_device(qd, 8, si, sd, st)
+    st.synchronize()
+    ri, rd = idx.search(q, 10, 8)
+    bad += not (np.array_equal(si.cpu().numpy(), ri) and np.array_equal(sd.cpu().numpy(), rd))
+    sh.close()
+    print("native sharded", "ok" if not bad else "MISMATCH", flush=True)
     # 5. shard merge
     dd = torch.from_numpy(np.sort(rng.random((3, 5, 7)), axis=2)).cuda()
     ii = torch.from_numpy(rng.integers(0, 10_000, (3, 5, 7))).cuda()
