@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python -c "
-import sys, json; sys.path.insert(0,'.'); sys.path.insert(0,'tools')
-import bench, bench_configs as bc
-r = bc.c1(bench.load_peaks()[0]); print(json.dumps({k: r[k] for k in ('value','e2e','parity')}))
-" > gpurun_out/c1cfg.log 2>&1
+timeout 1800 python -m pytest tests/ -x -q -m gpu > gpurun_out/all_gpu.log 2>&1
+timeout 300 python tools/c1_experiment.py "" "" > gpurun_out/c1_exp.log 2>&1

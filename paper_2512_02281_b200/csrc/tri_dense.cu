@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kGThreads) dense_gemm_kernel(const float* __re
 // distances) the list is left empty: the re-rank cannot certify it and the
 // exact fix-up answers the query.
 constexpr int kSelThreads = 256, kSelPer = 16, kSelCap = 512;
+long long g_dense_fold = 1;  // warp-list selection instead of bisection (option "dense_fold")
 
 __global__ void __launch_bounds__(kSelThreads) dense_select_kernel(const float* __restrict__ P, int nsl,
                                                                    long long ldd, int B,
@@ -261,11 +262,98 @@ cudaError_t launch_dense(const float* Q, int qld, const float* qn, int B, const 
   return launch_dense_select(D, used, ldd, B, qn, xn, n, meta, merged, ld_merged, kp_max, st);
 }
 
+// The same selection by warp-resident sorted lists: every warp folds its rows'
+// keys 32 at a time into a KL x 32 list (list_fold32: insertion when few beat
+// the list's last key), then the 8 warp lists merge pairwise through shared
+// memory.  Keys (fp32 order bits << 32 | row) are unique, so the kp smallest
+// come out exactly as the bisection path produces them (option "dense_fold").
+template <int KL>
+__global__ void __launch_bounds__(kSelThreads) dense_select_fold_kernel(const float* __restrict__ P, int nsl,
+                                                                        long long ldd, int B,
+                                                                        const float* __restrict__ qn,
+                                                                        const float* __restrict__ xn, long long n,
+                                                                        const QueryMeta* __restrict__ meta,
+                                                                        unsigned long long* __restrict__ merged,
+                                                                        int ld_merged) {
+  pdl_wait();
+  constexpr int KP = 32 * KL, NW = kSelThreads / 32;
+  __shared__ unsigned long long sm[NW / 2][KP];
+  const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* row = P + (long long)q * ldd;
+  const long long slice_ld = (long long)B * ldd;
+  const float qv = qn[q];
+  const int kp = meta[q].kp;
+  unsigned long long L[KL];
+#pragma unroll
+  for (int j = 0; j < KL; ++j) L[j] = TRI_KEY_MAX;
+  // thread t owns rows 4t..4t+3 of every 1024-row block (float4 loads), slices summed in order
+#pragma unroll
+  for (int g = 0; g < kSelPer / 4; ++g) {
+    const long long i0 = (long long)g * 4 * kSelThreads + 4 * tid;
+    if ((long long)g * 4 * kSelThreads >= n) break;  // block-uniform
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i0 < n) {
+      for (int z = 0; z < nsl; ++z) {
+        const float4 v = *reinterpret_cast<const float4*>(row + z * slice_ld + i0);
+        acc.x = __fadd_rn(acc.x, v.x);
+        acc.y = __fadd_rn(acc.y, v.y);
+        acc.z = __fadd_rn(acc.z, v.z);
+        acc.w = __fadd_rn(acc.w, v.w);
+      }
+    }
+    const float av[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const long long i = i0 + j;
+      const unsigned long long key =
+          i < n ? ((unsigned long long)f2ord(__fmaf_rn(-2.f, av[j], __fadd_rn(qv, xn[i]))) << 32) | (unsigned long long)i
+                : TRI_KEY_MAX;
+      list_fold32<KL>(L, key, lane);
+    }
+  }
+  // pairwise merge of the warp lists: warp w + stride hands its list (reversed) to warp w
+  for (int stride = 1; stride < NW; stride <<= 1) {
+    if ((warp & (2 * stride - 1)) == stride) {
+#pragma unroll
+      for (int j = 0; j < KL; ++j) sm[warp >> 1][j * 32 + lane] = L[j];
+    }
+    __syncthreads();
+    if ((warp & (2 * stride - 1)) == 0) {
+      unsigned long long R[KL];
+#pragma unroll
+      for (int j = 0; j < KL; ++j) R[j] = sm[(warp + stride) >> 1][(KL - 1 - j) * 32 + (31 - lane)];
+      list_merge_rev<KL>(L, R, lane);
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+#pragma unroll
+    for (int j = 0; j < KL; ++j) {
+      const int e = j * 32 + lane;
+      if (e < kp) merged[(long long)q * ld_merged + e] = L[j];
+    }
+  }
+}
+
 cudaError_t launch_dense_select(const float* D, int nsl, long long ldd, int B, const float* qn, const float* xn,
                                 long long n, const QueryMeta* meta, unsigned long long* merged, int ld_merged,
                                 int kp_max, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
   if (n > (long long)kSelThreads * kSelPer || kp_max > kSelCap / 2) return cudaErrorInvalidValue;
+  if (g_dense_fold) {
+    const int kl = next_pow2((kp_max + 31) / 32);
+    switch (kl) {
+      case 1: (void)launch_pdl(dense_select_fold_kernel<1>, B, kSelThreads, 0, st, D, nsl, ldd, B, qn, xn, n, meta,
+                               merged, ld_merged); break;
+      case 2: (void)launch_pdl(dense_select_fold_kernel<2>, B, kSelThreads, 0, st, D, nsl, ldd, B, qn, xn, n, meta,
+                               merged, ld_merged); break;
+      case 4: (void)launch_pdl(dense_select_fold_kernel<4>, B, kSelThreads, 0, st, D, nsl, ldd, B, qn, xn, n, meta,
+                               merged, ld_merged); break;
+      default: (void)launch_pdl(dense_select_fold_kernel<8>, B, kSelThreads, 0, st, D, nsl, ldd, B, qn, xn, n, meta,
+                                merged, ld_merged); break;
+    }
+    return cudaGetLastError();
+  }
   (void)launch_pdl(dense_select_kernel, B, kSelThreads, 0, st, D, nsl, ldd, B, qn, xn, n, meta, merged, ld_merged);
   return cudaGetLastError();
 }

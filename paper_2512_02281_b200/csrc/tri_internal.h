@@ -197,6 +197,7 @@ cudaError_t launch_to_half_lo(const float* X, long long n, int d, long long ldx,
                               cudaStream_t st);
 
 // per-query top-kp of nsl summed dot slices (D: nsl x B x ldd fp32)
+extern long long g_dense_fold;  // dense select: warp-list folds (1) or bisection (0)
 cudaError_t launch_dense_select(const float* D, int nsl, long long ldd, int B, const float* qn, const float* xn,
                                 long long n, const QueryMeta* meta, unsigned long long* merged, int ld_merged,
                                 int kp_max, cudaStream_t st);

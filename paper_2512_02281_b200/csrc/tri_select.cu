@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
   pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(16) unsigned char rf_smem[];
   __shared__ double s_dk;
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[3];
   const int q = blockIdx.x;
   const QueryMeta m = r.meta[q];
   const int d = r.d, kpm = r.kp_max, kp = m.kp;
@@ -817,6 +817,26 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
   unsigned long long* mk = reinterpret_cast<unsigned long long*>(exi + kpm);  // kp_max (fused merge)
   float* ring = reinterpret_cast<float*>(mk + kpm);      // 2 x kp_max x (S + 4)
   const int tid = threadIdx.x, nthr = blockDim.x, c = tid >> 1, ln = tid & 1;
+  // the query row streams into shared memory (one bulk copy on bars[2]) while
+  // the candidate list is merged; an odd d (row not 16-byte aligned) is staged
+  // by the threads after the merge
+  const double* qg = r.q64 + (long long)q * d;
+  const bool qbulk = (d & 1) == 0 && (reinterpret_cast<uintptr_t>(qg) & 15) == 0;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bars[0]))));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bars[1]))));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bars[2]))));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    if (qbulk) {
+      const uint32_t b2 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[2]));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b2), "r"((uint32_t)(d * 8)) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(qs))),
+                   "l"(qg), "r"((uint32_t)(d * 8)), "r"(b2)
+                   : "memory");
+    }
+  }
+  const double qn64 = r.qn64[q];
   // the query's sorted candidate list: the merge kernel's output, or (brute
   // force with a cross-item seed) merged right here from the scan's compact
   // region -- one launch and one global round trip less
@@ -846,19 +866,23 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
   // queries keep every candidate.)
   if (active && r.skip_far && m.k < kp && !(r.qinv && r.qinv[q] < 0.f)) {
     const unsigned long long kk = mrow[m.k - 1];
-    const double sn = r.qn64[q] + r.xmax;
-    const double E = (r.cdot * 2.0 * r.qn64[q] * r.xmax + r.csum * sn * sn) * 1.001 + 1e-30;
+    const double sn = qn64 + r.xmax;
+    const double E = (r.cdot * 2.0 * qn64 * r.xmax + r.csum * sn * sn) * 1.001 + 1e-30;
     if (kk != TRI_KEY_MAX && (double)key_dist(key) > (double)key_dist(kk) + 2.0 * E) active = false;
   }
   const long long pos = active ? (long long)key_pos(key) : -1;
   const bool leader = ln == 0 && c < kp;
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bars[0]))));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bars[1]))));
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  if (qbulk) {
+    for (int j = d + tid; j < dpad; j += nthr) qs[j] = 0.0;
+  } else {
+    stage_query(qg, d, dpad, qs, tid, nthr);
   }
-  stage_query(r.q64 + (long long)q * d, d, dpad, qs, tid, nthr);
   const int nvalid = __syncthreads_count(leader && active);
+  if (qbulk)
+    asm volatile(
+        "{\n .reg .pred P;\n RFQ_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n @!P bra RFQ_%=;\n}\n" ::"r"(
+            static_cast<uint32_t>(__cvta_generic_to_shared(&bars[2])))
+        : "memory");
   const int nslab = (dpad + S - 1) / S;
   const int buf_floats = kpm * (S + 4);
   rf_issue(ring, &bars[0], S, c, pos, r.X, r.ldx, 0, dpad, nvalid, leader);

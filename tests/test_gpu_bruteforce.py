@@ -173,6 +173,29 @@ def test_ragged_k_mixed_groups(mixed):
         assert np.array_equal(d[i, : ks[i]], od), i
 
 
+@pytest.mark.parametrize("fold", [0, 1])
+def test_dense_select_variants(fold):
+    """Small stores (<= 4096 rows) take the dense path; its per-query top-kp
+    select by warp-list folds (dense_fold=1) or by bisection (0) keeps the same
+    keys, so both give the oracle's result, over ragged k up to kp 256 and
+    with exact ties."""
+    rng = np.random.Generator(np.random.Philox(41))
+    data = rng.standard_normal((4000, 48)).astype(np.float32)
+    data[3000:3100] = data[0]  # 101 identical rows: ties broken by id
+    store = VectorStore(data=data)
+    qs = np.concatenate([rng.standard_normal((30, 48)), data[:2].astype(np.float64)])
+    ks = np.array([1, 10, 100, 33, 120, 64, 7, 128] * 4)[: qs.shape[0]]
+    try:
+        _lib.set_option("dense_fold", fold)
+        ids, d = brute_force_knn_batch(store, qs, ks)
+    finally:
+        _lib.set_option("dense_fold", 1)
+    for i in range(qs.shape[0]):
+        oi, od = orc.exact_knn(data, qs[i], int(ks[i]))
+        assert np.array_equal(ids[i, : ks[i]], oi), i
+        assert np.array_equal(d[i, : ks[i]], od), i
+
+
 @pytest.mark.parametrize("dim", [1, 3, 5, 16, 17, 100, 768, 1000])
 def test_odd_dimensions(dim):
     rng = np.random.Generator(np.random.Philox(dim))
