@@ -22,6 +22,8 @@ constexpr int kThreads = 256;
 long long g_rerank_smem_cap = 0;
 long long g_rerank_f2f = 1;
 long long g_rerank_skip = 1;
+long long g_rerank_lpt = 1;  // fused re-rank in LPT query order when capacities mix (option "rerank_lpt")
+long long g_rerank_wide_slab = 80;  // slab width for kp >= 128 (option "rerank_wide_slab"; 0 = the 8192/kp rule)
 long long g_pdl = 0;  // programmatic dependent launch of the hot kernels (option "pdl")
 long long g_fx_slice_rows = 256;
 
@@ -801,13 +803,55 @@ __device__ __forceinline__ double f2d_bits(float x, bool& sub) {
                           (int)((u << 29) & nz));
 }
 
+// Longest-processing-time order for a mixed-capacity batch: CTA b takes the
+// b-th query in (capacity class descending, query ascending) order, so the
+// wide prefill lists start in the first wave and the short decode lists fill
+// in behind them.  Two block-wide passes over the classes in meta (L2-resident).
+__device__ __forceinline__ int lpt_query(const QueryMeta* __restrict__ meta, int B, int b) {
+  __shared__ int s_cnt[kNumCls];
+  __shared__ int s_w[16];
+  __shared__ int s_q;
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < kNumCls) s_cnt[tid] = 0;
+  if (tid == 0) s_q = b;
+  __syncthreads();
+  for (int i = tid; i < B; i += nthr) atomicAdd(&s_cnt[meta[i].cls], 1);
+  __syncthreads();
+  int acc = 0, c = kNumCls - 1;
+  for (; c > 0; --c) {
+    if (b < acc + s_cnt[c]) break;
+    acc += s_cnt[c];
+  }
+  int j = b - acc;  // rank of the wanted query inside class c
+  for (int base = 0; base < B; base += nthr) {
+    const int i = base + tid;
+    const bool m = i < B && meta[i].cls == c;
+    const unsigned bal = __ballot_sync(0xffffffffu, m);
+    if (lane == 0) s_w[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < (nthr >> 5); ++w) {
+      before += w < warp ? s_w[w] : 0;
+      total += s_w[w];
+    }
+    if (j < total) {
+      if (m && before + __popc(bal & ((1u << lane) - 1u)) == j) s_q = i;
+      __syncthreads();
+      break;
+    }
+    j -= total;
+    __syncthreads();
+  }
+  return s_q;
+}
+
 template <bool F2F>
 __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S) {
   pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
   extern __shared__ __align__(16) unsigned char rf_smem[];
   __shared__ double s_dk;
   __shared__ __align__(8) uint64_t bars[3];
-  const int q = blockIdx.x;
+  const int q = r.lpt ? lpt_query(r.meta, r.B, blockIdx.x) : blockIdx.x;
   const QueryMeta m = r.meta[q];
   const int d = r.d, kpm = r.kp_max, kp = m.kp;
   const int dpad = (d + 15) & ~15;
@@ -1265,6 +1309,14 @@ cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
   if (r.B <= 0) return cudaSuccess;
   // slab width: 2 buffers x kp x (S+4) floats <= ~72 KB (several CTAs per SM)
   int S = std::max(32, std::min(256, 8192 / r.kp_max)) / 16 * 16;  // slabs hold whole 8-element blocks, 16B rows
+  // wide candidate lists run 256-512 threads at ~100 registers: 1-2 CTAs per
+  // SM whatever the ring size, so the ring may grow to the SM's shared memory
+  // (fewer, larger bulk-copy rounds; option "rerank_wide_slab", 0 = off)
+  if (g_rerank_wide_slab > 0 && r.kp_max >= 128 && !g_rerank_smem_cap) {
+    const long long fixed = (long long)((r.d + 15) & ~15) * 8 + (long long)r.kp_max * 24;
+    const long long fit = (200 * 1024 - fixed) / (2LL * r.kp_max * 4) - 4;
+    S = (int)std::max<long long>(S, std::min<long long>({(long long)g_rerank_wide_slab, fit, 256LL}) / 16 * 16);
+  }
   if (g_rerank_smem_cap > 0) {  // leave room for co-resident CTAs (option "rerank_smem_cap")
     const long long fixed = (long long)((r.d + 15) & ~15) * 8 + (long long)r.kp_max * 16;
     const long long fit = (g_rerank_smem_cap - fixed) / (2LL * r.kp_max * 4) - 4;
@@ -1277,14 +1329,16 @@ cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
                                   (size_t)std::min(8, rf_threads / 32) * r.kp_max * 8);
   if (r.kp_max <= 256 && rf_smem <= 200 * 1024) {
     const size_t smem = rf_smem;
+    RerankLaunch rl = r;
+    rl.lpt = g_rerank_lpt && r.kp_max > kMinKp;  // one class only: the order is the identity anyway
     if (g_rerank_f2f) {
       cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      (void)launch_pdl(rerank_fused_kernel<true>, r.B, rf_threads, smem, st, r, S);
+      (void)launch_pdl(rerank_fused_kernel<true>, r.B, rf_threads, smem, st, rl, S);
     } else {
       cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      (void)launch_pdl(rerank_fused_kernel<false>, r.B, rf_threads, smem, st, r, S);
+      (void)launch_pdl(rerank_fused_kernel<false>, r.B, rf_threads, smem, st, rl, S);
     }
     return cudaGetLastError();
   }
