@@ -110,6 +110,13 @@ struct ScanLaunch {
   // front of the query's partial region (part + meta part_off), counted here
   // (B ints, zeroed before the launch); merged by launch_merge_compact
   int* compact_cnt;
+  // list scan, wide members (kp >= 128): at the end of each item the member's
+  // 32 smallest keys join the query's pool (pool + q * pool_cap), and the
+  // kp-th smallest key in the pool tightens the query's cross-item bound gthr
+  unsigned long long* pool;  // B x pool_cap keys, all ones = empty
+  int* pool_cnt;             // B: slots reserved so far
+  int pool_cap;              // multiple of 32, <= kPoolMax
+  int pool_pub;              // 32-key rows each finished item publishes (1 or 2)
   const QueryMeta* meta;
 };
 constexpr int kTcSeedItems = 160;

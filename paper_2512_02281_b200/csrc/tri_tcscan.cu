@@ -173,7 +173,8 @@ int tc_scan_stages(int row_bytes, int smem_limit, int want, int qbufs, int abufs
 constexpr int kTsCtas = 256, kTsSlots = 16;
 __device__ unsigned long long g_scan_ts[kTsCtas * kTsSlots];
 // dbg & 16: [0] candidates appended, [1] (chunk, query) folds with n > 0,
-// [2] seeds left open, [3] seeds set
+// [2] seeds left open, [3] seeds set (brute force) / [2] appended, [3] folds
+// of kp >= 128 members (list scan)
 __device__ unsigned long long g_scan_cnt[4];
 __device__ __forceinline__ void ts_mark(const ScanLaunch& a, int slot) {
   if ((a.dbg & 8) && blockIdx.x < kTsCtas) {
@@ -631,6 +632,75 @@ __device__ __forceinline__ void tc_seed_pass(const ScanLaunch& a, const WorkItem
   if (threadIdx.x == 64) ts_mark(a, 11);
 }
 
+// Cross-item bound from a pool of per-item winners (list scan, kp >= 128).
+// An item's local kp-th key bounds only its own list, and with lists of ~1000
+// rows a kp = 256 member admits about a quarter of every list it scans.  The
+// pool collects each finished item's 32 smallest keys for the query (distinct
+// rows: a row belongs to one list, a (query, list) pair to one item); the
+// kp-th smallest key in the pool is then a bound on the query's kp-th key (kp
+// real rows lie at or below it) that tightens with every finished list.
+// Unwritten slots read as all ones and are not counted.  Bisection on the
+// distance bits (the bound keeps every row id: low word all ones).
+constexpr int kPoolMax = 1024;
+template <int KL>
+__device__ __forceinline__ void pool_publish(const ScanLaunch& a, int q, int kp, const unsigned long long (&L)[KL],
+                                             int lane, uint32_t rmin) {
+  // the list's 32 smallest keys with row id >= rmin (a finished item skips its
+  // first chunk's rows, which it published when that chunk was folded)
+  unsigned m[KL];
+  int avail = 0;
+#pragma unroll
+  for (int j = 0; j < KL; ++j) {
+    m[j] = __ballot_sync(0xffffffffu, L[j] != TRI_KEY_MAX && (uint32_t)L[j] >= rmin);
+    avail += __popc(m[j]);
+  }
+  if (avail == 0) return;
+  int slot = 0;
+  if (lane == 0) slot = atomicAdd(a.pool_cnt + q, 32);
+  slot = __shfl_sync(0xffffffffu, slot, 0);
+  if (slot + 32 > a.pool_cap) return;  // full: later lists no longer tighten the bound
+  unsigned long long* P = a.pool + (long long)q * a.pool_cap;
+  int taken = 0;
+#pragma unroll
+  for (int j = 0; j < KL; ++j) {
+    const int r = taken + __popc(m[j] & ((1u << lane) - 1u));
+    if (((m[j] >> lane) & 1u) && r < 32) P[slot + r] = L[j];
+    taken += __popc(m[j]);
+  }
+  const int n = slot + 32;
+  if (n < kp) return;
+  __syncwarp();
+  constexpr int kPer = kPoolMax / 32;
+  uint32_t h[kPer];
+  uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int i = j * 32 + lane;
+    h[j] = i < n ? (uint32_t)(__ldcg(P + i) >> 32) : 0xffffffffu;
+    if (h[j] != 0xffffffffu) {
+      mn = min(mn, h[j]);
+      mx = max(mx, h[j]);
+    }
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) c += h[j] <= mx && h[j] != 0xffffffffu;
+  if ((int)__reduce_add_sync(0xffffffffu, (unsigned)c) < kp) return;  // fewer than kp written keys yet
+  // invariant: count(<= hi) >= kp, count(<= lo) < kp
+  long long lo = (long long)mn - 1, hi = mx;
+  for (int it = 0; it < 32 && hi - lo > (long long)(1u << 12); ++it) {
+    const uint32_t mid = (uint32_t)(lo + ((hi - lo) >> 1));
+    c = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) c += h[j] <= mid;
+    if ((int)__reduce_add_sync(0xffffffffu, (unsigned)c) >= kp) hi = mid;
+    else lo = mid;
+  }
+  if (lane == 0) atomicMin(a.gthr + q, ((unsigned long long)(uint32_t)hi << 32) | 0xffffffffull);
+}
+
 template <bool H, int N, int KL>
 __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& w, TcSmem<N>& sh,
                                            unsigned long long* sel, int ring) {
@@ -859,6 +929,10 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
         if ((a.dbg & 16) && lane == 0 && n > 0) {
           atomicAdd(&g_scan_cnt[0], (unsigned long long)n);
           atomicAdd(&g_scan_cnt[1], 1ull);
+          if (N != kTcGroupWide && sh.kpq[g] >= 128) {  // list scan: the wide (prefill) members' share
+            atomicAdd(&g_scan_cnt[2], (unsigned long long)n);
+            atomicAdd(&g_scan_cnt[3], 1ull);
+          }
         }
         const unsigned long long* sb = sel + (size_t)buf * N * kTcRows + g * kTcRows;
         for (int b = 0; b < n; b += 32) {
@@ -888,6 +962,10 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
         }
         __syncwarp();
         if (lane == 0) sh.cnt[buf][g] = 0;
+        // early pool entry: the first chunk's winners (published once; the
+        // item's end adds its best rows beyond this chunk)
+        if (N != kTcGroupWide && c == 0 && a.pool && a.pool_pub >= 2 && n > 0 && sh.kpq[g] >= 128)
+          pool_publish<KL>(a, sh.qid[g], sh.kpq[g], L[qi], lane, 0u);
       }
     }
     if (a.abufs == 1) epi_sync();  // single append buffer: drained before the next chunk appends
@@ -905,6 +983,9 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
 #pragma unroll
       for (int j = 0; j < KL; ++j)
         if (j * 32 < sh.kpq[g]) out[j * 32 + lane] = L[qi][j];  // the member's kp entries
+      if (N != kTcGroupWide && a.pool && sh.kpq[g] >= 128)
+        pool_publish<KL>(a, sh.qid[g], sh.kpq[g], L[qi], lane,
+                         a.pool_pub >= 2 ? (uint32_t)(w.row_begin + kTcRows) : 0u);
     }
   }
   return acc | (aphase << 8);

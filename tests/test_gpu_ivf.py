@@ -388,9 +388,11 @@ _SCAN_OPTS = [
     {"scan_reserve": 0},
     {"scan_qbufs": 1, "tc_stages": 4},
     {"pack_mixed": 0},
+    {"scan_pool": 0},
+    {"scan_pool_pub": 1},
 ]
 _SCAN_DEFAULTS = {"scan_abufs": 1, "scan_l2hint": 1, "scan_reserve": -1, "scan_qbufs": 2, "tc_stages": 0,
-                  "pack_mixed": 1}
+                  "pack_mixed": 1, "scan_pool": 1024, "scan_pool_pub": 2}
 
 
 @pytest.mark.parametrize("opts", _SCAN_OPTS, ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
@@ -414,6 +416,36 @@ def test_ivf_scan_options_parity(small, opts):
     finally:
         for k, v in _SCAN_DEFAULTS.items():
             _lib.set_option(k, v)
+
+
+@pytest.mark.parametrize("pool", [(1024, 2), (1024, 1), (64, 2), (0, 2)])
+def test_pooled_bound_wide_members(pool, scan_kernel):
+    """kp >= 128 members (k = 100 -> kp 256) tighten their cross-item bound
+    from a pool of finished items' (and first chunks') best keys; the bound
+    only prunes, so results equal the oracle with the pool on, off, one
+    publish per item, or too small to ever reach kp keys.  Rows are stored
+    twice (equal distances, distinct ids) so the pool's distinct-row count is
+    exercised on exact ties."""
+    base = gen_matrix(6000, 32, 41)
+    data = np.concatenate([base, base])
+    idx = IVFFlatIndex.train(VectorStore(data=data), nlist=48, iters=3, seed=5)
+    cen, asg = idx.export()
+    art = orc.IVFArtifact(cen, asg)
+    qs = np.concatenate([gen_matrix(20, 32, 42), base[:4].astype(np.float64)])
+    ks = np.array([100, 10, 150, 100, 30, 100] * 4)
+    nps = np.array([24, 8, 48, 12, 16, 6] * 4)
+    try:
+        _lib.set_option("scan_pool", pool[0])
+        _lib.set_option("scan_pool_pub", pool[1])
+        for _ in range(3):  # eager, captured, replayed
+            ids, dist = idx.search(qs, ks, nps)
+    finally:
+        _lib.set_option("scan_pool", 1024)
+        _lib.set_option("scan_pool_pub", 2)
+    for i in range(qs.shape[0]):
+        oi, od = orc.ivf_search(data, art, qs[i], int(ks[i]), int(nps[i]))
+        assert np.array_equal(ids[i, : oi.size], oi), i
+        assert np.array_equal(dist[i, : oi.size], od), i
 
 
 def test_device_path_non_finite_query_rows(small):

@@ -54,6 +54,16 @@ def main():
         idx.search_device(q, k, npb, ids, d, st)
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
+    if "scan_debug=16" in a.opt:
+        import ctypes as C
+
+        import numpy as np
+
+        cnt = np.zeros(4, np.uint64)
+        _lib.check(_lib.gpu().tri_debug_scan_ts(cnt.ctypes.data_as(C.c_void_p), 4))
+        mt = idx.meta_totals() if hasattr(idx, "meta_totals") else None
+        print(f"per step: appended {cnt[0] / (a.steps + 5):.0f} in {cnt[1] / (a.steps + 5):.0f} folds; "
+              f"kp>=128 members {cnt[2] / (a.steps + 5):.0f} in {cnt[3] / (a.steps + 5):.0f} folds", mt)
     print("done", a.steps, "steps of", a.config)
 
 

@@ -17,6 +17,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--option", default="dense_fold")
     ap.add_argument("--iters", type=int, default=200)
+    ap.add_argument("--values", default="0,1", help="two option values, alternated twice")
     a = ap.parse_args()
     import torch
 
@@ -29,7 +30,8 @@ def main():
     st = torch.cuda.Stream()
     out = {}
     res = {}
-    for val in (0, 1, 0, 1):
+    v0, v1 = (int(x) for x in a.values.split(","))
+    for val in (v0, v1, v0, v1):
         _lib.set_option(a.option, val)
         ids = torch.empty((256, 10), dtype=torch.int64, device="cuda")
         d = torch.empty((256, 10), dtype=torch.float64, device="cuda")
@@ -44,7 +46,7 @@ def main():
         torch.cuda.synchronize()
         out.setdefault(val, []).append(round(e0.elapsed_time(e1) * 1e3 / a.iters, 2))
         res[val] = (ids.cpu(), d.cpu())
-    same = bool(torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1]))
+    same = bool(torch.equal(res[v0][0], res[v1][0]) and torch.equal(res[v0][1], res[v1][1]))
     print(json.dumps({"option": a.option, "us_per_search": out, "identical": same}))
 
 
