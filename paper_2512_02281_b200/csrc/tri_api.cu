@@ -132,6 +132,7 @@ std::atomic<long long> g_gr_eager{0}, g_gr_captured{0}, g_gr_replayed{0};  // gr
 long long g_ragged_graphs = 1;
 long long g_scan_pool = 1024;  // list scan: pooled cross-item bound for kp >= 128 members, pool keys per query (option "scan_pool", 0 = off)
 long long g_scan_pool_pub = 2;  // 1: each finished item adds its 32 best keys; 2: also its first chunk's 32 best, when folded (option "scan_pool_pub")
+long long g_scan_pool_minkp = 128;  // ... for members with kp >= this (option "scan_pool_minkp")
 long long g_coarse_set = 1;  // IVF coarse step: exact distances only where top-nprobe membership is open  // ragged / odd-sized batches replay fixed-shape padded graphs (option "ragged_graphs")
 
 
@@ -1266,6 +1267,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "rerank_lpt")) tri::g_rerank_lpt = value;
   else if (!std::strcmp(name, "scan_pool")) g_scan_pool = value;
   else if (!std::strcmp(name, "scan_pool_pub")) g_scan_pool_pub = value;
+  else if (!std::strcmp(name, "scan_pool_minkp")) g_scan_pool_minkp = value;
   else if (!std::strcmp(name, "pdl")) tri::g_pdl = value;
   else if (!std::strcmp(name, "fx_slice_rows")) {
     if (value < 32) return fail(TRI_EINVAL, "fx_slice_rows must be >= 32");
@@ -2032,7 +2034,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
     TRY(ensure(w.gthr, (size_t)B * sizeof(unsigned long long)));
     CU(cudaMemsetAsync(w.gthr.p, 0xff, (size_t)B * sizeof(unsigned long long), st));
     sl.gthr = w.gthr.as<unsigned long long>();
-    if (g_scan_pool > 0 && kp_max >= 128) {  // wide members: the pooled cross-item bound
+    if (g_scan_pool > 0 && kp_max >= g_scan_pool_minkp) {  // wide members: the pooled cross-item bound
       const int cap = (int)std::min<long long>(1024, (g_scan_pool + 31) / 32 * 32);
       TRY(ensure(w.pool, (size_t)B * cap * sizeof(unsigned long long) + (size_t)B * sizeof(int)));
       CU(cudaMemsetAsync(w.pool.p, 0xff, (size_t)B * cap * sizeof(unsigned long long), st));
@@ -2041,6 +2043,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
       CU(cudaMemsetAsync(sl.pool_cnt, 0, (size_t)B * sizeof(int), st));
       sl.pool_cap = cap;
       sl.pool_pub = (int)g_scan_pool_pub;
+      sl.pool_minkp = (int)g_scan_pool_minkp;
     }
   }
   sl.X = v->Xl;
@@ -2156,7 +2159,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
 
 
 long long graph_opts() {
-  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + g_bound_margin * 523 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_rerank_skip * 11 + tri::g_dense_fold * 3001 + tri::g_rerank_wide_slab * 577 + tri::g_rerank_lpt * 1931 + g_scan_pool * 37 + g_scan_pool_pub * 41 + tri::g_fx_slice_rows * 7919 +
+  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + g_bound_margin * 523 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_rerank_skip * 11 + tri::g_dense_fold * 3001 + tri::g_rerank_wide_slab * 577 + tri::g_rerank_lpt * 1931 + g_scan_pool * 37 + g_scan_pool_pub * 41 + g_scan_pool_minkp * 47 + tri::g_fx_slice_rows * 7919 +
          g_scan_debug * 100003 + tri::g_pdl * 7907 + g_coarse_set * 7919 * 13 + g_pack_mixed * 104729 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
 }
 

@@ -116,7 +116,8 @@ struct ScanLaunch {
   unsigned long long* pool;  // B x pool_cap keys, all ones = empty
   int* pool_cnt;             // B: slots reserved so far
   int pool_cap;              // multiple of 32, <= kPoolMax
-  int pool_pub;              // 32-key rows each finished item publishes (1 or 2)
+  int pool_pub;              // 1: item ends publish; 2: first chunks too
+  int pool_minkp;            // members with kp >= this use the pool
   const QueryMeta* meta;
 };
 constexpr int kTcSeedItems = 160;

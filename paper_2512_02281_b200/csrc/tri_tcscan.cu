@@ -964,7 +964,7 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
         if (lane == 0) sh.cnt[buf][g] = 0;
         // early pool entry: the first chunk's winners (published once; the
         // item's end adds its best rows beyond this chunk)
-        if (N != kTcGroupWide && c == 0 && a.pool && a.pool_pub >= 2 && n > 0 && sh.kpq[g] >= 128)
+        if (N != kTcGroupWide && c == 0 && a.pool && a.pool_pub >= 2 && n > 0 && sh.kpq[g] >= a.pool_minkp)
           pool_publish<KL>(a, sh.qid[g], sh.kpq[g], L[qi], lane, 0u);
       }
     }
@@ -983,7 +983,7 @@ __device__ __forceinline__ int tc_epi_item(const ScanLaunch& a, const WorkItem& 
 #pragma unroll
       for (int j = 0; j < KL; ++j)
         if (j * 32 < sh.kpq[g]) out[j * 32 + lane] = L[qi][j];  // the member's kp entries
-      if (N != kTcGroupWide && a.pool && sh.kpq[g] >= 128)
+      if (N != kTcGroupWide && a.pool && sh.kpq[g] >= a.pool_minkp)
         pool_publish<KL>(a, sh.qid[g], sh.kpq[g], L[qi], lane,
                          a.pool_pub >= 2 ? (uint32_t)(w.row_begin + kTcRows) : 0u);
     }
