@@ -1,4 +1,2 @@
 mkdir -p gpurun_out
-for tool in memcheck racecheck synccheck initcheck; do
-  TRI_GRAPHS=0 timeout 1500 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize_smoke.py > gpurun_out/san_$tool.log 2>&1; echo "rc=$?" >> gpurun_out/san_$tool.log
-done
+timeout 600 python tools/engine_host_profile.py > gpurun_out/eng_host.log 2>&1
