@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 600 python tools/engine_host_profile.py > gpurun_out/eng_host.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_ivf.py -x -q -m gpu -k "scan_options" > gpurun_out/opt_tests.log 2>&1
