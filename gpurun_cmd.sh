@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_ivf.py -x -q -m gpu -k "scan_options" > gpurun_out/opt_tests.log 2>&1
+for o in 0 128; do
+TRI_GRAPHS=0 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c3_launch_rp$o.csv python tools/c2_profile.py --steps 3 --c3 --opt rerank_pairs_minkp=$o > gpurun_out/c3_ncu.log 2>&1
+done
