@@ -4,7 +4,8 @@ so `ncu --profile-from-start off` sees exactly those steps' kernels.
 ``--c3`` runs the first ragged C3 batch (prefill k100/np64 + decode k10/np16)
 over the same index instead.
 
-usage: TRI_GRAPHS=0 ncu --profile-from-start off ... python tools/c2_profile.py [--steps 3] [--c3]
+usage: TRI_GRAPHS=0 ncu --profile-from-start off ... python tools/c2_profile.py [--steps 3] [--c3] [--opt k=v,...]
+       python tools/c2_profile.py --c3 --opt scan_debug=16   (scan append / fold counters per step)
 """
 
 from __future__ import annotations
@@ -61,9 +62,8 @@ def main():
 
         cnt = np.zeros(4, np.uint64)
         _lib.check(_lib.gpu().tri_debug_scan_ts(cnt.ctypes.data_as(C.c_void_p), 4))
-        mt = idx.meta_totals() if hasattr(idx, "meta_totals") else None
         print(f"per step: appended {cnt[0] / (a.steps + 5):.0f} in {cnt[1] / (a.steps + 5):.0f} folds; "
-              f"kp>=128 members {cnt[2] / (a.steps + 5):.0f} in {cnt[3] / (a.steps + 5):.0f} folds", mt)
+              f"kp>=128 members {cnt[2] / (a.steps + 5):.0f} in {cnt[3] / (a.steps + 5):.0f} folds")
     print("done", a.steps, "steps of", a.config)
 
 
