@@ -133,6 +133,7 @@ long long g_ragged_graphs = 1;
 long long g_scan_pool = 1024;  // list scan: pooled cross-item bound for kp >= 128 members, pool keys per query (option "scan_pool", 0 = off)
 long long g_scan_pool_pub = 2;  // 1: each finished item adds its 32 best keys; 2: also its first chunk's 32 best, when folded (option "scan_pool_pub")
 long long g_scan_pool_minkp = 128;  // ... for members with kp >= this (option "scan_pool_minkp")
+long long g_scan_early = 1;  // wide brute force: scan launched as the prep's programmatic dependent (option "scan_early")
 long long g_coarse_set = 1;  // IVF coarse step: exact distances only where top-nprobe membership is open  // ragged / odd-sized batches replay fixed-shape padded graphs (option "ragged_graphs")
 
 
@@ -1038,6 +1039,9 @@ int bruteforce_core(tri_store* s, Workspace& w, const Workspace& qw, const doubl
   if (prep) {
     CU(launch_prep(q64dev, B, s->d, w.Q32.as<float>(), s->qld, w.qn32.as<float>(), w.qn64.as<double>(), nullptr, st,
                    1.f, nullptr, 0, nullptr, nullptr, &cl));
+    // the scan launches as the prep's programmatic dependent: its fixed
+    // per-CTA items start streaming rows while the prep runs
+    sl.early = (g_scan_early && w.tc && sl.seed == 2) ? 1 : 0;
   } else {
     for (int r = 0; r < cl.n; ++r)
       CU(cl.val[r] == 0 ? cudaMemsetAsync(cl.p[r], 0, (size_t)cl.words[r] * 4, st)
@@ -1266,6 +1270,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "rerank_wide_slab")) tri::g_rerank_wide_slab = value;
   else if (!std::strcmp(name, "rerank_lpt")) tri::g_rerank_lpt = value;
   else if (!std::strcmp(name, "scan_pool")) g_scan_pool = value;
+  else if (!std::strcmp(name, "scan_early")) g_scan_early = value;
   else if (!std::strcmp(name, "scan_pool_pub")) g_scan_pool_pub = value;
   else if (!std::strcmp(name, "scan_pool_minkp")) g_scan_pool_minkp = value;
   else if (!std::strcmp(name, "pdl")) tri::g_pdl = value;
@@ -2159,7 +2164,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
 
 
 long long graph_opts() {
-  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + g_bound_margin * 523 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_rerank_skip * 11 + tri::g_dense_fold * 3001 + tri::g_rerank_wide_slab * 577 + tri::g_rerank_lpt * 1931 + g_scan_pool * 37 + g_scan_pool_pub * 41 + g_scan_pool_minkp * 47 + tri::g_fx_slice_rows * 7919 +
+  return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + g_bound_margin * 523 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_rerank_skip * 11 + tri::g_dense_fold * 3001 + tri::g_rerank_wide_slab * 577 + tri::g_rerank_lpt * 1931 + g_scan_pool * 37 + g_scan_early * 67 + g_scan_pool_pub * 41 + g_scan_pool_minkp * 47 + tri::g_fx_slice_rows * 7919 +
          g_scan_debug * 100003 + tri::g_pdl * 7907 + g_coarse_set * 7919 * 13 + g_pack_mixed * 104729 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019;
 }
 
@@ -2249,6 +2254,11 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
     cudaError_t ce = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed);
     int rc = ce == cudaSuccess ? body() : TRI_ECUDA;
     if (ce == cudaSuccess) ce = cudaStreamEndCapture(st, &gr);
+    if (ce == cudaSuccess && gr && std::getenv("TRI_GRAPH_DOT")) {  // debugging: the captured graph's nodes
+      static int n_dot = 0;
+      const std::string path = std::string(std::getenv("TRI_GRAPH_DOT")) + "." + std::to_string(n_dot++) + ".dot";
+      cudaGraphDebugDotPrint(gr, path.c_str(), 0);
+    }
     w.capturing = false;
     if (cw) cw->capturing = false;
     w.cap_host = nullptr;

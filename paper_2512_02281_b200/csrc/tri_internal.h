@@ -103,6 +103,8 @@ struct ScanLaunch {
   int q_tma;
   const void* tmap_q;
   int seed;            // 1: per-item seed; 2: cross-item seed (one item per CTA, seed_items <= kTcSeedItems)
+  int early;           // launched as a programmatic dependent of the prep kernel: the row producer streams
+                       // before the prep's results are visible (fixed item assignment only), the other roles wait
   uint32_t* seed_min;  // seed 2: B x seed_items fp32 order bits of each item's smallest distance (0xff.. = none)
   int* seed_ctr;       // seed 2: items that published (zeroed before the launch)
   int seed_items;

@@ -1036,7 +1036,11 @@ template <bool H, int N>
 __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_constant__ CUtensorMap map,
                                                                 const __grid_constant__ CUtensorMap tail,
                                                                 const __grid_constant__ CUtensorMap qmap, ScanLaunch a) {
-  pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible
+  // programmatic dependent launch: the previous kernel's results are visible
+  // after griddepcontrol.wait.  An early launch (a.early) defers the wait to
+  // the roles that read them, so the setup and the row stream overlap the prep.
+  if (!a.early) pdl_wait();
+  else asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   constexpr int kTmemCols = tc_acc<N>() * N;  // power of two >= 32
   extern __shared__ __align__(1024) unsigned char tsmem_raw[];
   __shared__ TcSmem<N> sh;
@@ -1076,12 +1080,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   if (threadIdx.x == 0) ts_mark(a, 1);
   if (warp == 0) {
+    // rows and a fixed (host-uploaded) item assignment do not depend on the prep
+    if (a.early && a.seed != 2) asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if ((threadIdx.x & 31) == 0) tc_producer<H, N>(a, &map, &tail, sh, ring);
   } else if (warp == 1) {
     tc_mma<H, N>(a, sh, ring, qs, qtile_bytes);
   } else if (warp == 10) {
+    if (a.early) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the prepared query tile
     tc_qstage<H, N>(a, &qmap, sh, qs, qtile_bytes);
   } else {
+    if (a.early) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // norms, bounds, counters
     tc_epilogue<H, N>(a, sh, sel);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -1101,6 +1109,14 @@ cudaError_t launch_tc(const ScanLaunch& s, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel<H, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const CUtensorMap* qm = reinterpret_cast<const CUtensorMap*>(s.q_tma ? s.tmap_q : s.tmap_tc);
+  if (s.early) {
+    const long long saved = g_pdl;
+    g_pdl = 1;
+    (void)launch_pdl(scan_tc_kernel<H, N>, s.grid, kTcThreads, smem, st, *reinterpret_cast<const CUtensorMap*>(s.tmap_tc),
+                     *reinterpret_cast<const CUtensorMap*>(s.tmap_tc_tail), *qm, s);
+    g_pdl = saved;
+    return cudaGetLastError();
+  }
   (void)launch_pdl(scan_tc_kernel<H, N>, s.grid, kTcThreads, smem, st, *reinterpret_cast<const CUtensorMap*>(s.tmap_tc),
                                                          *reinterpret_cast<const CUtensorMap*>(s.tmap_tc_tail), *qm, s);
   return cudaGetLastError();

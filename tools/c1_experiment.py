@@ -1,6 +1,7 @@
 """C1 brute-force timing under library option sets (not a benchmark of record).
 
 python tools/c1_experiment.py "opt=v,opt2=v" ...   (options apply cumulatively; tc_box_rows needs a new store)
+C1_SAME_STORE=1 keeps one store for every spec (placement held fixed: the A/B of an option alone)
 """
 import ctypes as C
 import os
@@ -24,11 +25,13 @@ ks = np.full(64, 10, np.int32)
 ids = torch.empty((64, 10), dtype=torch.int64, device="cuda")
 d = torch.empty((64, 10), dtype=torch.float64, device="cuda")
 st = torch.cuda.Stream()
+same = os.environ.get("C1_SAME_STORE") == "1"
+shared = _DeviceStore(data) if same else None
 for spec in sys.argv[1:] or [""]:
     for kv in filter(None, spec.split(",")):
         k, v = kv.split("=")
         _lib.set_option(k, int(v))
-    store = _DeviceStore(data)
+    store = shared if same else _DeviceStore(data)
 
     def one():
         _lib.check(lib.tri_knn_bruteforce_dev(store.handle, _lib.ptr(q), 64, ks.ctypes.data, 10, _lib.ptr(ids),
@@ -52,4 +55,5 @@ for spec in sys.argv[1:] or [""]:
     reps.sort()
     print(f"[{spec or 'defaults'}] {reps[3]:.1f} us/batch (min {reps[0]:.1f}, max {reps[-1]:.1f}) "
           f"host enqueue {sorted(host)[3]:.1f} us/call parity={'ok' if ok else 'MISMATCH'}", flush=True)
-    store.close()
+    if not same:
+        store.close()
