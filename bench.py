@@ -385,7 +385,10 @@ def run_ivf(cfg, args, ctx: Ctx, headline: bool = True, keep: bool = False):
 
     # prime every lane (its workspace, plan and CUDA graph: a shape is captured
     # on its second sighting and replayed from the third), so a small --warmup
-    # cannot leave first-use work inside the timed region
+    # cannot leave first-use work inside the timed region.  Profiling is on
+    # while priming: the stage-timer event nodes are part of a graph's key, so
+    # graphs primed without them would be re-captured inside the timed region
+    idx.set_profiling(True)
     for _ in range(3 * L):
         step()
     torch.cuda.synchronize()
@@ -405,7 +408,8 @@ def run_ivf(cfg, args, ctx: Ctx, headline: bool = True, keep: bool = False):
     if ctx.rank == 0 and bad:
         raise SystemExit(f"parity failure: {bad} of {checked} checked queries differ from the oracle")
 
-    # timed region: device-resident inputs
+    # timed region: device-resident inputs (set_profiling resets the stage
+    # timers; the profiled graphs primed above replay from the first step)
     idx.set_profiling(True)
     sampler = ClockSampler(ctx.local)
     ctx.barrier()
@@ -449,6 +453,7 @@ def run_ivf(cfg, args, ctx: Ctx, headline: bool = True, keep: bool = False):
         n_iso = 50
         reserve_opt = dict(o.split("=", 1) for o in args.opt).get("scan_reserve")
         _lib.set_option("scan_reserve", 0)
+        idx.set_profiling(True)  # prime the profiled graph of this shape (see above)
         for _ in range(3):
             idx.search_device(q_dev, K, NPROBE, lane_ids[0], lane_d[0], lanes[0])
         torch.cuda.synchronize()

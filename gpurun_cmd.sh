@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 1800 python -m pytest tests/ -q -m gpu > gpurun_out/all_gpu.log 2>&1
-TRI_GRAPHS=0 timeout 1500 compute-sanitizer --tool racecheck --print-limit 50 python tools/sanitize_smoke.py > gpurun_out/san_racecheck.log 2>&1; echo "rc=$?" >> gpurun_out/san_racecheck.log
-TRI_GRAPHS=0 timeout 1500 compute-sanitizer --tool memcheck --print-limit 50 python tools/sanitize_smoke.py > gpurun_out/san_memcheck.log 2>&1; echo "rc=$?" >> gpurun_out/san_memcheck.log
-TRI_GRAPHS=0 timeout 1500 compute-sanitizer --tool synccheck --print-limit 50 python tools/sanitize_smoke.py > gpurun_out/san_synccheck.log 2>&1; echo "rc=$?" >> gpurun_out/san_synccheck.log
+for s in 20 20; do timeout 300 python bench.py --steps $s --warmup 5 --no-configs > gpurun_out/bench_s$s.log 2>&1; grep '^{' gpurun_out/bench_s$s.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($s, d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline']['frac'], d['roofline']['step_frac'], d['roofline']['isolated'], d['clocks'])" >> gpurun_out/bench_var.log; done
+timeout 900 python bench.py --steps 20 --warmup 5 --full-out gpurun_out/bench_full.json > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log

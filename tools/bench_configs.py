@@ -266,10 +266,13 @@ def c3(b: dict, peak_gbs: float, batch: int = 256, lanes: int = 4, cpu_sample: i
         idx.search_device(q_dev[s:e], ks[s:e], nps[s:e], ids[s:e], d[s:e], streams[0])
         streams[0].synchronize()
         scan_bytes += idx.last_scan_bytes()[0]
-    for _ in range(2):  # the shapes of every lane captured and replayed
+    # the shapes of every lane captured and replayed, with the stage-timer event
+    # nodes the timed pass uses (profiling is part of a graph's key)
+    idx.set_profiling(True)
+    for _ in range(2):
         run_all()
     torch.cuda.synchronize()
-    idx.set_profiling(True)
+    idx.set_profiling(True)  # reset the timers
     times = []
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
