@@ -245,6 +245,7 @@ struct RerankLaunch {
   int B;
   int kp_max;
   int lpt;                  // fused re-rank: CTAs take queries in descending capacity class (wide lists first)
+  int lpt_cls;              // fused re-rank split: 0 = every class, 1 = class 0 only (kp 32), 2 = classes >= 1
   const float* qinv;        // fp16 scan: qinv[q] < 0 marks a query the scan could not scale (never certified)
   // brute force with a cross-item seed: the scan's unsorted compact lists
   // (cnt[q] keys at part + part_off); the re-rank merges them itself
@@ -260,6 +261,7 @@ extern long long g_rerank_smem_cap;  // bytes; 0 = no cap
 extern long long g_rerank_f2f;
 extern long long g_rerank_skip;
 extern long long g_rerank_wide_slab;
+extern long long g_rerank_split;
 extern long long g_rerank_lpt;  // kp >= 128: ring up to the SM's shared memory
 extern long long g_fx_slice_rows;  // fix-up: minimum rows per slice       // 1: hardware F2F conversions in the re-rank (else integer bit moves)
 

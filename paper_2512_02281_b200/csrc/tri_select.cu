@@ -12,6 +12,9 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "tri_common.cuh"
 #include "tri_internal.h"
@@ -23,6 +26,10 @@ long long g_rerank_smem_cap = 0;
 long long g_rerank_f2f = 1;
 long long g_rerank_skip = 1;
 long long g_rerank_lpt = 1;  // fused re-rank in LPT query order when capacities mix (option "rerank_lpt")
+// mixed-capacity batches: the kp-32 queries re-rank in a second, narrow
+// launch (64-thread CTAs, several per SM) on a forked stream beside the wide
+// one, instead of each holding a 512-thread CTA (option "rerank_split")
+long long g_rerank_split = 1;
 long long g_rerank_wide_slab = 80;  // slab width for kp >= 128 (option "rerank_wide_slab"; 0 = the 8192/kp rule)
 long long g_pdl = 0;  // programmatic dependent launch of the hot kernels (option "pdl")
 long long g_fx_slice_rows = 256;
@@ -807,7 +814,8 @@ __device__ __forceinline__ double f2d_bits(float x, bool& sub) {
 // b-th query in (capacity class descending, query ascending) order, so the
 // wide prefill lists start in the first wave and the short decode lists fill
 // in behind them.  Two block-wide passes over the classes in meta (L2-resident).
-__device__ __forceinline__ int lpt_query(const QueryMeta* __restrict__ meta, int B, int b) {
+// Only classes lo..hi are taken (a split launch); a CTA past their count gets -1.
+__device__ __forceinline__ int lpt_query(const QueryMeta* __restrict__ meta, int B, int b, int lo, int hi) {
   __shared__ int s_cnt[kNumCls];
   __shared__ int s_w[16];
   __shared__ int s_q;
@@ -817,11 +825,12 @@ __device__ __forceinline__ int lpt_query(const QueryMeta* __restrict__ meta, int
   __syncthreads();
   for (int i = tid; i < B; i += nthr) atomicAdd(&s_cnt[meta[i].cls], 1);
   __syncthreads();
-  int acc = 0, c = kNumCls - 1;
-  for (; c > 0; --c) {
+  int acc = 0, c = hi;
+  for (; c >= lo; --c) {
     if (b < acc + s_cnt[c]) break;
     acc += s_cnt[c];
   }
+  if (c < lo) return -1;  // block-uniform (s_cnt, b)
   int j = b - acc;  // rank of the wanted query inside class c
   for (int base = 0; base < B; base += nthr) {
     const int i = base + tid;
@@ -851,7 +860,12 @@ __global__ void __launch_bounds__(512) rerank_fused_kernel(RerankLaunch r, int S
   extern __shared__ __align__(16) unsigned char rf_smem[];
   __shared__ double s_dk;
   __shared__ __align__(8) uint64_t bars[3];
-  const int q = r.lpt ? lpt_query(r.meta, r.B, blockIdx.x) : blockIdx.x;
+  int qb = blockIdx.x;
+  if (r.lpt) {
+    qb = lpt_query(r.meta, r.B, blockIdx.x, r.lpt_cls == 2 ? 1 : 0, r.lpt_cls == 1 ? 0 : kNumCls - 1);
+    if (qb < 0) return;  // split launch: this CTA's class range has fewer queries
+  }
+  const int q = qb;
   const QueryMeta m = r.meta[q];
   const int d = r.d, kpm = r.kp_max, kp = m.kp;
   const int dpad = (d + 15) & ~15;
@@ -1305,42 +1319,89 @@ cudaError_t launch_coarse_set(const RerankLaunch& r, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Forked stream per (caller stream, device) for the split re-rank: the narrow
+// launch runs on it between an event fork and join, so inside a captured
+// graph the two launches are sibling nodes.  Created on first use, kept.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static std::mutex g_side_mu;
+static std::map<std::pair<cudaStream_t, int>, SideStream> g_side;
+
+static cudaError_t side_stream(cudaStream_t st, SideStream** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  SideStream& sd = g_side[{st, dev}];
+  if (!sd.s) {
+    if ((e = cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  *out = &sd;
+  return cudaSuccess;
+}
+
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {
   if (r.B <= 0) return cudaSuccess;
-  // slab width: 2 buffers x kp x (S+4) floats <= ~72 KB (several CTAs per SM)
-  int S = std::max(32, std::min(256, 8192 / r.kp_max)) / 16 * 16;  // slabs hold whole 8-element blocks, 16B rows
-  // wide candidate lists run 256-512 threads at ~100 registers: 1-2 CTAs per
-  // SM whatever the ring size, so the ring may grow to the SM's shared memory
-  // (fewer, larger bulk-copy rounds; option "rerank_wide_slab", 0 = off)
-  if (g_rerank_wide_slab > 0 && r.kp_max >= 128 && !g_rerank_smem_cap) {
-    const long long fixed = (long long)((r.d + 15) & ~15) * 8 + (long long)r.kp_max * 24;
-    const long long fit = (200 * 1024 - fixed) / (2LL * r.kp_max * 4) - 4;
-    S = (int)std::max<long long>(S, std::min<long long>({(long long)g_rerank_wide_slab, fit, 256LL}) / 16 * 16);
-  }
-  if (g_rerank_smem_cap > 0) {  // leave room for co-resident CTAs (option "rerank_smem_cap")
-    const long long fixed = (long long)((r.d + 15) & ~15) * 8 + (long long)r.kp_max * 16;
-    const long long fit = (g_rerank_smem_cap - fixed) / (2LL * r.kp_max * 4) - 4;
-    S = (int)std::max<long long>(32, std::min<long long>(S, fit / 16 * 16));
-  }
-  // a fused compact merge gets 8 warps (the distance phase uses 2 threads per candidate)
-  const int rf_threads = r.compact_cnt ? std::max(2 * r.kp_max, 256) : 2 * r.kp_max;
-  const size_t rf_smem = (size_t)((r.d + 15) & ~15) * sizeof(double) + (size_t)r.kp_max * 24 +
-                         std::max((size_t)2 * r.kp_max * (S + 4) * sizeof(float),
-                                  (size_t)std::min(8, rf_threads / 32) * r.kp_max * 8);
-  if (r.kp_max <= 256 && rf_smem <= 200 * 1024) {
-    const size_t smem = rf_smem;
+  // fused re-rank geometry for a capacity kpm: slab width S, threads, smem
+  struct Geom {
+    int S, threads;
+    size_t smem;
+  };
+  auto geom = [&](int kpm) {
+    // slab width: 2 buffers x kp x (S+4) floats <= ~72 KB (several CTAs per SM)
+    int S = std::max(32, std::min(256, 8192 / kpm)) / 16 * 16;  // slabs hold whole 8-element blocks, 16B rows
+    // wide candidate lists run 256-512 threads at ~100 registers: 1-2 CTAs per
+    // SM whatever the ring size, so the ring may grow to the SM's shared memory
+    // (fewer, larger bulk-copy rounds; option "rerank_wide_slab", 0 = off)
+    if (g_rerank_wide_slab > 0 && kpm >= 128 && !g_rerank_smem_cap) {
+      const long long fixed = (long long)((r.d + 15) & ~15) * 8 + (long long)kpm * 24;
+      const long long fit = (200 * 1024 - fixed) / (2LL * kpm * 4) - 4;
+      S = (int)std::max<long long>(S, std::min<long long>({(long long)g_rerank_wide_slab, fit, 256LL}) / 16 * 16);
+    }
+    if (g_rerank_smem_cap > 0) {  // leave room for co-resident CTAs (option "rerank_smem_cap")
+      const long long fixed = (long long)((r.d + 15) & ~15) * 8 + (long long)kpm * 16;
+      const long long fit = (g_rerank_smem_cap - fixed) / (2LL * kpm * 4) - 4;
+      S = (int)std::max<long long>(32, std::min<long long>(S, fit / 16 * 16));
+    }
+    // a fused compact merge gets 8 warps (the distance phase uses 2 threads per candidate)
+    const int threads = r.compact_cnt ? std::max(2 * kpm, 256) : 2 * kpm;
+    const size_t smem = (size_t)((r.d + 15) & ~15) * sizeof(double) + (size_t)kpm * 24 +
+                        std::max((size_t)2 * kpm * (S + 4) * sizeof(float),
+                                 (size_t)std::min(8, threads / 32) * kpm * 8);
+    return Geom{S, threads, smem};
+  };
+  auto fused = [&](const RerankLaunch& rl, const Geom& g, cudaStream_t s) -> cudaError_t {
+    auto* kern = g_rerank_f2f ? rerank_fused_kernel<true> : rerank_fused_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    if (e != cudaSuccess) return e;
+    (void)launch_pdl(kern, r.B, g.threads, g.smem, s, rl, g.S);
+    return cudaGetLastError();
+  };
+  const Geom gw = geom(r.kp_max);
+  if (r.kp_max <= 256 && gw.smem <= 200 * 1024) {
     RerankLaunch rl = r;
     rl.lpt = g_rerank_lpt && r.kp_max > kMinKp;  // one class only: the order is the identity anyway
-    if (g_rerank_f2f) {
-      cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      (void)launch_pdl(rerank_fused_kernel<true>, r.B, rf_threads, smem, st, rl, S);
-    } else {
-      cudaError_t e = cudaFuncSetAttribute(rerank_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      (void)launch_pdl(rerank_fused_kernel<false>, r.B, rf_threads, smem, st, rl, S);
-    }
-    return cudaGetLastError();
+    rl.lpt_cls = 0;
+    if (!(rl.lpt && g_rerank_split && !g_pdl && !r.compact_cnt)) return fused(rl, gw, st);
+    // mixed capacities: the kp-32 class on the forked stream, the wider
+    // classes here; each grid has B CTAs, those past its class count exit
+    SideStream* sd = nullptr;
+    cudaError_t e = side_stream(st, &sd);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(sd->fork, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(sd->s, sd->fork, 0)) != cudaSuccess) return e;
+    RerankLaunch rn = rl;
+    rn.kp_max = kMinKp;
+    rn.lpt_cls = 1;
+    if ((e = fused(rn, geom(kMinKp), sd->s)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(sd->join, sd->s)) != cudaSuccess) return e;
+    rl.lpt_cls = 2;
+    if ((e = fused(rl, gw, st)) != cudaSuccess) return e;
+    return cudaStreamWaitEvent(st, sd->join, 0);
   }
   if (r.compact_cnt) {  // the pair kernels read merged lists: merge first
     cudaError_t me = launch_merge_compact(r.part, r.compact_cnt, r.meta, const_cast<unsigned long long*>(r.merged),
