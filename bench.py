@@ -72,7 +72,7 @@ def parse():
                     help="untimed oracle check: 3 queries per lane, or every query of lane 0 and the spot set")
     ap.add_argument("--tc-stages", type=int, default=0, help="tensor-core scan ring depth cap (0 = deepest)")
     ap.add_argument("--scan-reserve", type=int, default=-1,
-                    help="SMs the list scan leaves to other lanes (-1: the library's choice, 8 with > 1 lane)")
+                    help="SMs the list scan leaves to other lanes (-1: the library's choice, 24 with > 1 lane)")
     ap.add_argument("--opt", action="append", default=[], help="library option name=value (experiments)")
     ap.add_argument("--no-configs", action="store_true", help="skip the secondary configs (C1/C3/C4/C5/engine)")
     ap.add_argument("--configs", default="C1,C3,C4,C5,engine", help="secondary configs measured at N=1")

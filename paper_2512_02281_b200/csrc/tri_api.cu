@@ -572,10 +572,13 @@ struct tri_ivf {
 
 // SMs the IVF list scan leaves free: the option's value, or (-1, default)
 // kAutoReserve once batches run on more than one stream of the index, so the
-// other lanes' small kernels run beside the HBM-bound scan instead of in its
-// tail (measured at 4 lanes: +2.5% QPS with 8 SMs, same with 16; one lane
-// loses about 1% with any reservation, so it keeps every SM).
-constexpr int kAutoReserve = 8;
+// other lanes' small kernels -- and the next lane's scan -- start beside the
+// HBM-bound scan instead of in its tail.  The scan stays HBM-bound on 124 SMs,
+// so consecutive lanes' scans overlap on all 148 (measured at 4 lanes, 100
+// steps: 918K QPS with 8 SMs, 937-941K with 16, 946-949K with 24-28, 939K
+// with 40-48; C3 631-640K -> 659-665K at 24).  One lane loses about 1% with
+// any reservation, so it keeps every SM.
+constexpr int kAutoReserve = 24;
 int scan_reserve_for(const tri_ivf* v) {
   if (g_scan_reserve >= 0) return (int)g_scan_reserve;
   return v->lanes.used > 1 ? kAutoReserve : 0;
