@@ -68,7 +68,7 @@ def compact(r: dict) -> dict:
 # C1
 
 
-def c1(peak_gbs: float, steps: int = 200, cpu_sample: int = 16) -> dict:
+def c1(peak_gbs: float, steps: int = 200, cpu_sample: int = 16, lanes: int = 4) -> dict:
     """Brute force 100K x 128, 64 queries, k=10 (store L2-resident: 51 MB)."""
     import ctypes as C
 
@@ -87,7 +87,7 @@ def c1(peak_gbs: float, steps: int = 200, cpu_sample: int = 16) -> dict:
     lib = _lib.gpu()
     q = torch.from_numpy(qs).cuda()
     ks = np.full(B, K, np.int32)
-    L = 4  # batches in flight (one stream + library workspace each), as C2
+    L = lanes  # batches in flight (one stream + library workspace each), as C2
     ids = [torch.empty((B, K), dtype=torch.int64, device="cuda") for _ in range(L)]
     d = [torch.empty((B, K), dtype=torch.float64, device="cuda") for _ in range(L)]
     sts = [torch.cuda.Stream() for _ in range(L)]
@@ -133,7 +133,7 @@ def c1(peak_gbs: float, steps: int = 200, cpu_sample: int = 16) -> dict:
         brute_force_knn_batch(vs, qs, K)
     single_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
     dev = vs.device()
-    lanes = 4
+    # (lanes: the host threads, one per device lane)
     qp = torch.from_numpy(qs).pin_memory()
     outs = [(torch.empty((B, K), dtype=torch.int64).pin_memory(), torch.empty((B, K), dtype=torch.float64).pin_memory())
             for _ in range(lanes)]
