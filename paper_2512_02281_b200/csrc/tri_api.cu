@@ -561,6 +561,7 @@ struct tri_ivf {
   cudaStream_t own = nullptr;
   Lanes lanes;
   std::mutex mu;  // enqueue is serialised per handle; waits happen outside it
+  int reserve_now = 0;  // automatic scan reserve of the search being enqueued (set_reserve_now)
   bool prof = false;
   // profiling: a ring of (start, stop) event pairs around the list-scan kernel,
   // read back lazily so the timed loop never synchronises.
@@ -578,10 +579,24 @@ struct tri_ivf {
 // steps: 918K QPS with 8 SMs, 937-941K with 16, 946-949K with 24-28, 939K
 // with 40-48; C3 631-640K -> 659-665K at 24).  One lane loses about 1% with
 // any reservation, so it keeps every SM.
+// "More than one stream" means another lane of the index still has a search
+// in flight when this one is enqueued (its done event not yet reached): a
+// single-stream caller of an index that once served several lanes keeps
+// every SM.  Decided once per search (set_reserve_now, under the handle's
+// lock), so the graph key and the captured grid agree.
 constexpr int kAutoReserve = 24;
+void set_reserve_now(tri_ivf* v, cudaStream_t st) {
+  int r = 0;
+  if (g_scan_reserve < 0 && v->lanes.used > 1)
+    for (int i = 0; i < v->lanes.used && !r; ++i)
+      if (v->lanes.st[i] != st && v->lanes.w[i].done_live && cudaEventQuery(v->lanes.w[i].done) == cudaErrorNotReady)
+        r = kAutoReserve;
+  cudaGetLastError();  // cudaEventQuery's not-ready status is not an error
+  v->reserve_now = r;
+}
 int scan_reserve_for(const tri_ivf* v) {
   if (g_scan_reserve >= 0) return (int)g_scan_reserve;
-  return v->lanes.used > 1 ? kAutoReserve : 0;
+  return v->reserve_now;
 }
 
 namespace {
@@ -2191,6 +2206,7 @@ static int graph_run(tri_ivf* v, Workspace& w, Workspace* cw, cudaStream_t st, i
   // plus the epochs of the workspaces it reads; all only grow, so the sum
   // changes exactly when one of them does
   auto stamp = [&]() { return g_epoch + w.epoch + (cw ? cw->epoch : 0); };
+  if (v) set_reserve_now(v, st);
   if (!g_graphs) {
     ++g_gr_eager;
     return body();
@@ -2543,6 +2559,7 @@ int tri_ivf_search(tri_ivf* v, const double* q, int32_t B, const int32_t* k, con
     if (pinned) {
       TRY(graph_run(v, w, cw, st, 1, B, k, nprobe, ldo, q, ids, dists, body));
     } else {
+      set_reserve_now(v, st);
       TRY(body());
     }
     TRY(lane_done(*cw, st));
