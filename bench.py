@@ -453,6 +453,9 @@ def run_ivf(cfg, args, ctx: Ctx, headline: bool = True, keep: bool = False):
         "algorithmic_bytes_per_launch": scan_bytes, "scan_ms_per_launch": avg_scan_ms,
         "step_frac": scan_bytes / (total_ms / args.steps / 1e3) / 1e9 / peak,
         "query_vector_pairs_per_launch": pairs,
+        "note": "achieved = bytes / mean scan launch duration with the lanes' scans overlapping (the next lane's "
+                "scan starts on the SMs the running one leaves free, and the two share the HBM); step_frac = the "
+                "batch's scan bytes / the step time; isolated = one scan alone on all 148 SMs",
     }
     if headline and ctx.world == 1:
         # the same scan with no other lane beside it (one stream, all 148 SMs)
