@@ -85,6 +85,7 @@ class GpuBackend:
         self.cd = torch.empty((slots, 1), dtype=torch.float64).pin_memory()
         self.ones = np.ones(slots, dtype=np.int32)
         self.kmax = kmax
+        self._s2 = None  # second stream for the cache lookups (search_and_cache), made on first use
 
     def search(self, queries: np.ndarray, ks, nps) -> np.ndarray:
         B = queries.shape[0]
@@ -97,6 +98,35 @@ class GpuBackend:
         self.cq.numpy()[:B] = queries
         self.cache_store.knn_into(self.cq[:B], self.ones[:B], self.cids[:B], self.cd[:B], stream=self.stream)
         return self.cids.numpy()[:B]
+
+    def search_and_cache(self, queries: np.ndarray, ks, nps, cqueries: np.ndarray):
+        """One batch's IVF search and prompt-cache lookups side by side: the
+        lookups are enqueued on a second stream (H2D, exact kNN on the device
+        store, D2H), the IVF search runs blocking on the first, then the second
+        is awaited -- the batch takes the longer of the two, not their sum."""
+        import torch
+
+        from . import _lib
+
+        if self._s2 is None:
+            self._s2 = torch.cuda.Stream()
+            n, d = self.cq.shape
+            self._cq_dev = torch.empty((n, d), dtype=torch.float64, device="cuda")
+            self._cids_dev = torch.empty((n, 1), dtype=torch.int64, device="cuda")
+            self._cd_dev = torch.empty((n, 1), dtype=torch.float64, device="cuda")
+            self._ev = torch.cuda.Event()
+        Bc = cqueries.shape[0]
+        self.cq.numpy()[:Bc] = cqueries
+        with torch.cuda.stream(self._s2):
+            self._cq_dev[:Bc].copy_(self.cq[:Bc], non_blocking=True)
+            _lib.check(_lib.gpu().tri_knn_bruteforce_dev(
+                self.cache_store.handle, _lib.ptr(self._cq_dev), Bc, self.ones.ctypes.data, 1,
+                _lib.ptr(self._cids_dev), _lib.ptr(self._cd_dev), _lib.C.c_void_p(self._s2.cuda_stream)))
+            self.cids[:Bc].copy_(self._cids_dev[:Bc], non_blocking=True)
+            self._ev.record(self._s2)
+        ids = self.search(queries, ks, nps)
+        self._ev.synchronize()
+        return ids, self.cids.numpy()[:Bc]
 
 
 class RealtimePool:
@@ -148,12 +178,18 @@ class RealtimePool:
             qs = np.stack([e.payload[0].queries[e.payload[1]] for e in ivf]).astype(np.float64)
             ks = np.array([self.stage_knp[e.stage][0] for e in ivf], np.int32)
             nps = np.array([self.stage_knp[e.stage][1] for e in ivf], np.int32)
-            ids = self.backend.search(qs, ks, nps)
-            res.launches += 1
         if cch:
             cq = np.stack([e.payload[0].queries[0] for e in cch]).astype(np.float64)
-            cids = self.backend.cache(cq)
-            res.launches += 1
+        if ivf and cch and hasattr(self.backend, "search_and_cache"):
+            ids, cids = self.backend.search_and_cache(qs, ks, nps, cq)  # both on the device at once
+            res.launches += 2
+        else:
+            if ivf:
+                ids = self.backend.search(qs, ks, nps)
+                res.launches += 1
+            if cch:
+                cids = self.backend.cache(cq)
+                res.launches += 1
         t_done = self._clock()
         dt = time.perf_counter() - t0
         res.busy_s += dt
