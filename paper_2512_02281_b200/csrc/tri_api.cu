@@ -5,6 +5,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -481,11 +482,16 @@ struct Lanes {
   static constexpr int kMax = 8;
   Workspace w[kMax];
   cudaStream_t st[kMax] = {};
+  double t_get[kMax] = {};  // host time (s) of each lane's last search
   int used = 0, next_victim = 0, last = 0;
+  static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
   int get(cudaStream_t s, Workspace** out) {
     for (int i = 0; i < used; ++i)
       if (st[i] == s) {
         last = i;
+        t_get[i] = now_s();
         *out = &w[i];
         return TRI_OK;
       }
@@ -495,8 +501,16 @@ struct Lanes {
     w[i].done_live = false;
     st[i] = s;
     last = i;
+    t_get[i] = now_s();
     *out = &w[i];
     return TRI_OK;
+  }
+  // another lane searched within the last `window` seconds
+  bool others_active(cudaStream_t s, double window) const {
+    const double t = now_s();
+    for (int i = 0; i < used; ++i)
+      if (st[i] != s && t - t_get[i] < window) return true;
+    return false;
   }
   Workspace& recent() { return w[last]; }
   void free_all() {
@@ -579,20 +593,19 @@ struct tri_ivf {
 // steps: 918K QPS with 8 SMs, 937-941K with 16, 946-949K with 24-28, 939K
 // with 40-48; C3 631-640K -> 659-665K at 24).  One lane loses about 1% with
 // any reservation, so it keeps every SM.
-// "More than one stream" means another lane of the index still has a search
-// in flight when this one is enqueued (its done event not yet reached): a
-// single-stream caller of an index that once served several lanes keeps
-// every SM.  Decided once per search (set_reserve_now, under the handle's
-// lock), so the graph key and the captured grid agree.
+// "More than one stream" means another lane of the index enqueued a search
+// within the last kActiveWindow seconds: a single-stream caller of an index
+// that once served several lanes keeps every SM, while lanes that keep each
+// other busy reserve from their first search on.  (Deciding by whether
+// another lane's work is still in flight instead cost 7% at 20 bench steps:
+// the first search after an idle moment took the whole GPU.)  Decided once
+// per search (set_reserve_now, under the handle's lock), so the graph key and
+// the captured grid agree.
 constexpr int kAutoReserve = 24;
+constexpr double kActiveWindow = 0.25;
 void set_reserve_now(tri_ivf* v, cudaStream_t st) {
-  int r = 0;
-  if (g_scan_reserve < 0 && v->lanes.used > 1)
-    for (int i = 0; i < v->lanes.used && !r; ++i)
-      if (v->lanes.st[i] != st && v->lanes.w[i].done_live && cudaEventQuery(v->lanes.w[i].done) == cudaErrorNotReady)
-        r = kAutoReserve;
-  cudaGetLastError();  // cudaEventQuery's not-ready status is not an error
-  v->reserve_now = r;
+  v->reserve_now = (g_scan_reserve < 0 && v->lanes.used > 1 && v->lanes.others_active(st, kActiveWindow))
+                       ? kAutoReserve : 0;
 }
 int scan_reserve_for(const tri_ivf* v) {
   if (g_scan_reserve >= 0) return (int)g_scan_reserve;
