@@ -1,13 +1,4 @@
 mkdir -p gpurun_out
-cat > /tmp/eng_ab.py <<'PY'
-import sys, json
-sys.path.insert(0, '.'); sys.path.insert(0, 'tools')
-from bench_engine import run
-from paper_2512_02281_b200 import _lib
-for n, kind in [(100_000, "knn"), (2_000_000, "random")]:
-    for v in [0, 1, 0, 1]:
-        _lib.set_option("eng_prefetch", v)
-        r = run(n=n, graph_kind=kind, reps=3, cpu_sample=2)
-        print(n, kind, "prefetch", v, {k: r[k] for k in r if k in ("value", "parity")}, json.dumps(r.get("roofline", {}))[:160], flush=True)
-PY
-timeout 1200 python /tmp/eng_ab.py > gpurun_out/eng_ab.log 2>&1; echo "rc=$?" >> gpurun_out/eng_ab.log
+timeout 900 python tools/c3_stages.py "merge_split=0" "merge_split=1" "merge_split=0" "merge_split=1" > gpurun_out/c3_ms.log 2>&1
+TRI_GRAPHS=0 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c3_launches.csv python tools/c2_profile.py --steps 3 --c3 > gpurun_out/c3_ncu.log 2>&1
+timeout 1800 python -m pytest tests/test_gpu_ivf.py tests/test_gpu_padded.py tests/test_gpu_pool.py tests/test_gpu_stress.py tests/test_gpu_bruteforce.py -q -x > gpurun_out/ms_tests.log 2>&1; echo "rc=$?" >> gpurun_out/ms_tests.log

@@ -1300,6 +1300,7 @@ int tri_set_option(const char* name, int64_t value) {
   else if (!std::strcmp(name, "dense_fold")) tri::g_dense_fold = value;
   else if (!std::strcmp(name, "rerank_wide_slab")) tri::g_rerank_wide_slab = value;
   else if (!std::strcmp(name, "rerank_split")) tri::g_rerank_split = value;
+  else if (!std::strcmp(name, "merge_split")) tri::g_merge_split = value;
   else if (!std::strcmp(name, "rerank_lpt")) tri::g_rerank_lpt = value;
   else if (!std::strcmp(name, "scan_pool")) g_scan_pool = value;
   else if (!std::strcmp(name, "scan_early")) g_scan_early = value;
@@ -2197,7 +2198,7 @@ static int ivf_search_body(tri_ivf* v, Workspace& w, Workspace* cw, const double
 
 long long graph_opts() {
   return ((plan_opts() * 7 + g_tc_stages) * 1009 + g_scan_reserve) * 31 + g_force_fixup * 3 + g_gthr * 7 + g_scan_qbufs * 37 + g_coarse_tc * 13 + tri::g_coarse_split * 29 + g_f16_div * 131 + g_bound_margin * 523 + tri::g_dense_slices * 17 + tri::g_rerank_smem_cap * 3 + tri::g_rerank_f2f * 5 + tri::g_rerank_skip * 11 + tri::g_dense_fold * 3001 + tri::g_rerank_wide_slab * 577 + tri::g_rerank_lpt * 1931 + g_scan_pool * 37 + g_scan_early * 67 + g_scan_pool_pub * 41 + g_scan_pool_minkp * 47 + tri::g_fx_slice_rows * 7919 +
-         g_scan_debug * 100003 + tri::g_pdl * 7907 + g_coarse_set * 7919 * 13 + g_pack_mixed * 104729 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019 + tri::g_rerank_split * 7;
+         g_scan_debug * 100003 + tri::g_pdl * 7907 + g_coarse_set * 7919 * 13 + g_pack_mixed * 104729 + g_scan_l2hint * 1000003 + g_scan_abufs * 10000019 + tri::g_rerank_split * 7 + tri::g_merge_split * 100019;
 }
 
 

@@ -262,6 +262,7 @@ extern long long g_rerank_f2f;
 extern long long g_rerank_skip;
 extern long long g_rerank_wide_slab;
 extern long long g_rerank_split;
+extern long long g_merge_split;
 extern long long g_rerank_lpt;  // kp >= 128: ring up to the SM's shared memory
 extern long long g_fx_slice_rows;  // fix-up: minimum rows per slice       // 1: hardware F2F conversions in the re-rank (else integer bit moves)
 

@@ -21,6 +21,33 @@
 
 namespace tri {
 
+// Forked stream per (caller stream, device) for the split merge /
+// re-rank: the narrow
+// launch runs on it between an event fork and join, so inside a captured
+// graph the two launches are sibling nodes.  Created on first use, kept.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static std::mutex g_side_mu;
+static std::map<std::pair<cudaStream_t, int>, SideStream> g_side;
+
+static cudaError_t side_stream(cudaStream_t st, SideStream** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  SideStream& sd = g_side[{st, dev}];
+  if (!sd.s) {
+    if ((e = cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  *out = &sd;
+  return cudaSuccess;
+}
+
+
 constexpr int kThreads = 256;
 long long g_rerank_smem_cap = 0;
 long long g_rerank_f2f = 1;
@@ -30,6 +57,8 @@ long long g_rerank_lpt = 1;  // fused re-rank in LPT query order when capacities
 // launch (64-thread CTAs, several per SM) on a forked stream beside the wide
 // one, instead of each holding a 512-thread CTA (option "rerank_split")
 long long g_rerank_split = 1;
+// the same split for the partial-list merge (option "merge_split")
+long long g_merge_split = 1;
 long long g_rerank_wide_slab = 80;  // slab width for kp >= 128 (option "rerank_wide_slab"; 0 = the 8192/kp rule)
 long long g_pdl = 0;  // programmatic dependent launch of the hot kernels (option "pdl")
 long long g_fx_slice_rows = 256;
@@ -325,7 +354,7 @@ __global__ void __launch_bounds__(kThreads) merge_kernel(const unsigned long lon
 // skipped), then the 8 lists are merged pairwise through shared memory.
 constexpr int kMergeWarps = 8;
 
-template <int KL>
+template <int KL, int W = kMergeWarps>
 __device__ __forceinline__ void merge_tree(const unsigned long long* __restrict__ src, int n_slots,
                                            unsigned long long* __restrict__ dst, unsigned long long* sm) {
   constexpr int KP = 32 * KL;
@@ -334,10 +363,10 @@ __device__ __forceinline__ void merge_tree(const unsigned long long* __restrict_
 #pragma unroll
   for (int j = 0; j < KL; ++j) L[j] = TRI_KEY_MAX;
   unsigned long long thr = TRI_KEY_MAX;
-  for (int s0 = warp; s0 < n_slots; s0 += 2 * kMergeWarps) {
+  for (int s0 = warp; s0 < n_slots; s0 += 2 * W) {
     // two slots in flight per warp: both loads issue before either merge
     unsigned long long P0[KL], P1[KL];
-    const int s1 = s0 + kMergeWarps;
+    const int s1 = s0 + W;
     const unsigned long long* a0 = src + (long long)s0 * KP;
     const unsigned long long* a1 = src + (long long)s1 * KP;
 #pragma unroll
@@ -354,7 +383,7 @@ __device__ __forceinline__ void merge_tree(const unsigned long long* __restrict_
       thr = __shfl_sync(0xffffffffu, L[KL - 1], 31);
     }
   }
-  for (int stride = 1; stride < kMergeWarps; stride <<= 1) {
+  for (int stride = 1; stride < W; stride <<= 1) {
     if ((warp & (2 * stride - 1)) == stride) {
 #pragma unroll
       for (int j = 0; j < KL; ++j) sm[warp * KP + j * 32 + lane] = L[j];
@@ -389,6 +418,32 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_tree_kernel(const unsi
     case 64: merge_tree<2>(src, m.n_slots, dst, msm); break;
     case 128: merge_tree<4>(src, m.n_slots, dst, msm); break;
     default: merge_tree<8>(src, m.n_slots, dst, msm); break;
+  }
+}
+
+// Split merge of a mixed-capacity batch (option "merge_split"): W warps per
+// query over the classes lo..hi only, CTA b taking the b-th query of those
+// classes in descending class order (lpt_query; CTAs past their count exit).
+// The kp-32 class runs 8-warp CTAs on a forked stream, the wide classes
+// 16-warp CTAs (half the slots folded per warp) beside it.
+__device__ __forceinline__ int lpt_query(const QueryMeta* __restrict__ meta, int B, int b, int lo, int hi);
+template <int W>
+__global__ void __launch_bounds__(32 * W) merge_tree_split_kernel(const unsigned long long* __restrict__ part,
+                                                                  const QueryMeta* __restrict__ meta,
+                                                                  unsigned long long* __restrict__ merged,
+                                                                  int ld_merged, int B, int lo, int hi) {
+  pdl_wait();
+  extern __shared__ unsigned long long msm[];
+  const int q = lpt_query(meta, B, blockIdx.x, lo, hi);
+  if (q < 0) return;
+  const QueryMeta m = meta[q];
+  const unsigned long long* src = part + m.part_off;
+  unsigned long long* dst = merged + (long long)q * ld_merged;
+  switch (m.kp) {
+    case 32: merge_tree<1, W>(src, m.n_slots, dst, msm); break;
+    case 64: merge_tree<2, W>(src, m.n_slots, dst, msm); break;
+    case 128: merge_tree<4, W>(src, m.n_slots, dst, msm); break;
+    default: merge_tree<8, W>(src, m.n_slots, dst, msm); break;
   }
 }
 
@@ -505,6 +560,25 @@ cudaError_t launch_merge_compact(const unsigned long long* part, const int* cnt,
 cudaError_t launch_merge(const unsigned long long* part, const QueryMeta* meta, unsigned long long* merged,
                          int ld_merged, int B, int kp_max, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
+  if (kp_max <= 256 && kp_max > kMinKp && g_merge_split && !g_pdl) {
+    // mixed capacities: kp-32 queries (8 warps) on a forked stream, wider ones
+    // (16 warps) here; each grid has B CTAs, those past its class count exit
+    SideStream* sd = nullptr;
+    cudaError_t e = side_stream(st, &sd);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(sd->fork, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(sd->s, sd->fork, 0)) != cudaSuccess) return e;
+    const size_t sn = (size_t)8 * kMinKp * sizeof(unsigned long long);
+    (void)launch_pdl(merge_tree_split_kernel<8>, B, 256, sn, sd->s, part, meta, merged, ld_merged, B, 0, 0);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(sd->join, sd->s)) != cudaSuccess) return e;
+    const size_t sw = (size_t)16 * kp_max * sizeof(unsigned long long);
+    e = cudaFuncSetAttribute(merge_tree_split_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sw);
+    if (e != cudaSuccess) return e;
+    (void)launch_pdl(merge_tree_split_kernel<16>, B, 512, sw, st, part, meta, merged, ld_merged, B, 1, kNumCls - 1);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaStreamWaitEvent(st, sd->join, 0);
+  }
   if (kp_max <= 256) {
     const size_t smem = (size_t)kMergeWarps * kp_max * sizeof(unsigned long long);
     cudaError_t e = cudaFuncSetAttribute(merge_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1317,31 +1391,6 @@ cudaError_t launch_coarse_set(const RerankLaunch& r, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   (void)launch_pdl(coarse_set_kernel, (r.B + kSetWarps - 1) / kSetWarps, 32 * kSetWarps, smem, st, r);
   return cudaGetLastError();
-}
-
-// Forked stream per (caller stream, device) for the split re-rank: the narrow
-// launch runs on it between an event fork and join, so inside a captured
-// graph the two launches are sibling nodes.  Created on first use, kept.
-struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-static std::mutex g_side_mu;
-static std::map<std::pair<cudaStream_t, int>, SideStream> g_side;
-
-static cudaError_t side_stream(cudaStream_t st, SideStream** out) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  std::lock_guard<std::mutex> lk(g_side_mu);
-  SideStream& sd = g_side[{st, dev}];
-  if (!sd.s) {
-    if ((e = cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming)) != cudaSuccess) return e;
-  }
-  *out = &sd;
-  return cudaSuccess;
 }
 
 cudaError_t launch_rerank(const RerankLaunch& r, cudaStream_t st) {

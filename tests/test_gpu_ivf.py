@@ -392,11 +392,12 @@ _SCAN_OPTS = [
     {"scan_pool_pub": 1},
     {"rerank_wide_slab": 0, "rerank_lpt": 0},
     {"rerank_split": 0},
+    {"merge_split": 0},
     {"dense_fold": 0},
 ]
 _SCAN_DEFAULTS = {"scan_abufs": 1, "scan_l2hint": 1, "scan_reserve": -1, "scan_qbufs": 2, "tc_stages": 0,
                   "pack_mixed": 1, "scan_pool": 1024, "scan_pool_pub": 2, "rerank_wide_slab": 80, "rerank_lpt": 1,
-                  "rerank_split": 1, "dense_fold": 1}
+                  "rerank_split": 1, "merge_split": 1, "dense_fold": 1}
 
 
 @pytest.mark.parametrize("opts", _SCAN_OPTS, ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
