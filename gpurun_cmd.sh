@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python tools/c3_stages.py "merge_split=0" "merge_split=1" "merge_split=0" "merge_split=1" > gpurun_out/c3_ms.log 2>&1
-TRI_GRAPHS=0 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c3_launches.csv python tools/c2_profile.py --steps 3 --c3 > gpurun_out/c3_ncu.log 2>&1
-timeout 1800 python -m pytest tests/test_gpu_ivf.py tests/test_gpu_padded.py tests/test_gpu_pool.py tests/test_gpu_stress.py tests/test_gpu_bruteforce.py -q -x > gpurun_out/ms_tests.log 2>&1; echo "rc=$?" >> gpurun_out/ms_tests.log
+timeout 2400 python -m pytest tests/ -q -m gpu > gpurun_out/all_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/all_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py --steps 20 --warmup 5 --full-out gpurun_out/bench_full.json > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ref.log 2>&1; echo "rc=$?" >> gpurun_out/ref.log
