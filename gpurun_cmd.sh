@@ -1,5 +1,2 @@
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests/ -q -m gpu > gpurun_out/all_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/all_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py --steps 20 --warmup 5 --full-out gpurun_out/bench_full.json > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ref.log 2>&1; echo "rc=$?" >> gpurun_out/ref.log
+timeout 900 python tools/c3_stages.py "" "" "" "" > gpurun_out/c3_e2e.log 2>&1
