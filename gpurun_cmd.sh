@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py --steps 20 --warmup 5 --full-out gpurun_out/bench_full.json > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
+timeout 600 python tools/dense_ab.py --option scan_qbufs --values 2,3 > gpurun_out/qb3_ab.log 2>&1
+timeout 900 python tools/c3_stages.py "scan_qbufs=2" "scan_qbufs=3" "scan_qbufs=2" "scan_qbufs=3" > gpurun_out/c3_qb3.log 2>&1
