@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 600 python tools/dense_ab.py --option scan_qbufs --values 2,3 > gpurun_out/qb3_ab.log 2>&1
-timeout 900 python tools/c3_stages.py "scan_qbufs=2" "scan_qbufs=3" "scan_qbufs=2" "scan_qbufs=3" > gpurun_out/c3_qb3.log 2>&1
+for i in 1 2; do timeout 900 python bench.py --steps 20 --warmup 5 --configs C3,C5 --full-out gpurun_out/bf$i.json > gpurun_out/b$i.log 2>&1; done

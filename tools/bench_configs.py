@@ -398,7 +398,7 @@ def _orc_cache(q):
     return orc.exact_knn(_ORC[2], q, 1)[0]
 
 
-def c5(b: dict, peak_gbs: float, rates=(5_000.0, 10_000.0), seconds: float = 1.0, repeats: int = 1,
+def c5(b: dict, peak_gbs: float, rates=(5_000.0, 10_000.0), seconds: float = 1.0, repeats: int = 3,
        cpu_rate: float = 10.0, cpu_requests: int = 40) -> dict:
     """Stage-aware scheduled trace on the wall clock (pool.py): RAG retrievals
     (prefill k=100 nprobe=64, decode k=10 nprobe=16) + one prompt-cache lookup
@@ -407,6 +407,7 @@ def c5(b: dict, peak_gbs: float, rates=(5_000.0, 10_000.0), seconds: float = 1.0
     import torch
 
     from oracle import trinity_oracle as orc
+    from paper_2512_02281_b200 import _lib
     from paper_2512_02281_b200.ann_graph import VectorStore
     from paper_2512_02281_b200.pool import GpuBackend, RealtimePool
     from paper_2512_02281_b200.scheduler import SchedulerConfig
@@ -436,10 +437,12 @@ def c5(b: dict, peak_gbs: float, rates=(5_000.0, 10_000.0), seconds: float = 1.0
         for policy, chunk in policies.items():
             reps = []
             for _ in range(repeats):
+                g0 = _lib.graph_counters()
                 r = RealtimePool(be, cfg(policy), tpot=tpot, prefill_chunk=chunk).run(trace)
+                g1 = _lib.graph_counters()
                 reps.append({"latency": r.percentiles(), "batches": r.batches, "launches": r.launches,
                              "preemptions": r.preemptions, "retrievals": r.retrievals, "wall_s": r.wall_s,
-                             "busy_s": r.busy_s})
+                             "busy_s": r.busy_s, "graphs": {k: g1[k] - g0[k] for k in g1}})
             out["runs"][f"{policy}@{rate:g}/s"] = reps if repeats > 1 else reps[0]
     # CPU reference (scheduler + oracle) in the same real-time loop, bounded
     art = orc.IVFArtifact(b["cen"], b["asg"])
@@ -452,8 +455,13 @@ def c5(b: dict, peak_gbs: float, rates=(5_000.0, 10_000.0), seconds: float = 1.0
     finally:
         ob.close()
     cpu_lat = cr.percentiles()
+    # the headline run: with repeats, the one with the median prefill p99 (every
+    # run's latencies stay in "runs"; at 10K requests/s the pool is ~97% busy,
+    # so a single run's p99 can jump on a host hiccup)
     hi = out["runs"][f"decode_priority@{rates[-1]:g}/s"]
-    hi = hi[0] if isinstance(hi, list) else hi
+    if isinstance(hi, list):
+        hi = sorted(hi, key=lambda x: x["latency"]["prefill"]["p99_ms"])[len(hi) // 2]
+    out["headline_run"] = "median prefill p99 of the repeats" if repeats > 1 else "single run"
     out["value"] = hi["retrievals"] / hi["wall_s"]
     out["unit"] = "retrievals/s served"
     out["latency_ms"] = hi["latency"]
