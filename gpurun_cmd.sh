@@ -1,2 +1,5 @@
 mkdir -p gpurun_out
-for i in 1 2; do timeout 900 python bench.py --steps 20 --warmup 5 --configs C3,C5 --full-out gpurun_out/bf$i.json > gpurun_out/b$i.log 2>&1; done
+timeout 2400 python -m pytest tests/ -q -m gpu > gpurun_out/all_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/all_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py --steps 20 --warmup 5 --full-out gpurun_out/bench_full.json > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ref.log 2>&1; echo "rc=$?" >> gpurun_out/ref.log
